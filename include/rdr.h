@@ -1,0 +1,131 @@
+/* rdr.h — C ABI of the B200 Riesz-map PCG library (arXiv 2506.17406 hot path).
+ *
+ * Problem (Eq. 2.9): find u in X^k_{p,D} with
+ *     a^k(u, v) = (u, beta v) + (d^k u, alpha d^k v) = F(v)  for all v,
+ * k = 0 (H(grad), CG_p) or k = 1 (H(curl), first-kind Nedelec Ned1_p,
+ * P:288-299 Eq. 2.4), piecewise-constant alpha > 0, beta >= 0 per cell, on an
+ * affine tetrahedral mesh, in the paper's basis (dofs = moments against
+ * doubly-orthogonal bubble eigenbases, Eq. 3.8-3.10, §3.4.1-3.4.2
+ * P:725-807; basis = Ciarlet dual).
+ *
+ * Vectors: full length n_total in the canonical global numbering of DESIGN.md
+ * R-A9 (dimension-major: vertices by id, edges sorted lexicographically,
+ * faces sorted, cells in input order; inside an entity R-A8). Constrained
+ * (Dirichlet) entries of inputs are ignored (read as 0);
+ * constrained entries of outputs are written as 0.
+ *
+ * Ownership: the library copies everything it needs during rdr_setup and
+ * retains no caller pointer. The handle owns all device buffers; rdr_destroy
+ * frees them (safe on NULL). A handle must not be used from two host threads
+ * at once.
+ *
+ * Streams: all device work is enqueued on the stream argument (a cudaStream_t
+ * passed as void*, NULL = legacy default stream). rdr_apply and rdr_precond
+ * never synchronize. rdr_setup and rdr_solve synchronize the stream.
+ *
+ * Errors: every function returns an rdr status and never aborts. On error the
+ * outputs are unspecified, except that rdr_solve returning RDR_ENOCONV still
+ * writes x and sets *iters = maxit.
+ */
+#ifndef RDR_H
+#define RDR_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct rdr_handle rdr_handle;
+
+enum { RDR_HGRAD = 0, RDR_HCURL = 1 };
+
+enum {
+  RDR_OK = 0,
+  RDR_EINVAL = -1,   /* bad p / space / sizes / alpha <= 0 / beta < 0 / NULL pointer */
+  RDR_EMESH = -2,    /* |det J| <= 1e-12 h^3, non-manifold face, mask bit on an interior face */
+  RDR_ENOTSPD = -3,  /* a patch Cholesky pivot <= 0 (e.g. beta = 0 with H(curl)) */
+  RDR_ENOMEM = -4,   /* device or host allocation failed */
+  RDR_ECUDA = -5,    /* any other CUDA runtime error */
+  RDR_ENOCONV = -6   /* PCG reached maxit */
+};
+
+struct rdr_info {
+  int64_t n_total;       /* vector length (all dofs, constrained included) */
+  int64_t n_free;        /* unconstrained dofs */
+  int64_t n_interior;    /* cell-interior dofs (point-Jacobi block, Thm 5.1) */
+  int64_t n_cells;
+  int32_t n_loc;         /* local dofs per cell */
+  int32_t n_mat;         /* reference matrices: 7 (H(grad)) or 12 (H(curl)) */
+  int64_t n_patches;     /* star patches (Eq. 5.4 P:1763-1774 / Eq. 5.12) */
+  int32_t max_patch;     /* largest patch dimension */
+  int64_t patch_bytes;   /* device bytes of the stored patch inverses (with tile padding) */
+  double flops_apply;    /* algorithmic flops of one rdr_apply: 2 n_loc^2 n_mat n_cells */
+  double bytes_apply;    /* algorithmic HBM bytes of one rdr_apply */
+  double bytes_precond;  /* algorithmic HBM bytes of one rdr_precond: 8 sum n_m(n_m+1)/2 + 24 N_int */
+  double setup_seconds;  /* wall time of rdr_setup */
+};
+
+/* Build the operator and the preconditioner (host setup once, then upload).
+ *   vertices [nv][3] float64 row-major; tets [nt][4] int32 (any vertex order);
+ *   alpha, beta [nt] float64; dirichlet_mask [nt][4] uint8: bit (t,i) = 1 iff
+ *   the face opposite INPUT vertex i of tet t lies on Gamma_D.
+ *   Each of these five pointers may be host or device memory (detected).
+ *   1 <= p <= 12 for H(grad), 1 <= p <= 10 for H(curl).
+ *   Reference element: DESIGN.md readings R-A1..A8, R-A24 (extended precision,
+ *   P:595-619). Patches: R-A13. Inverses stored per patch (R-A15). */
+int rdr_setup(rdr_handle** h, const double* vertices, int64_t nv, const int32_t* tets, int64_t nt,
+              int p, int space, const double* alpha, const double* beta,
+              const uint8_t* dirichlet_mask, void* stream);
+
+int rdr_ndofs(const rdr_handle* h, int64_t* n_total);
+int rdr_get_info(const rdr_handle* h, struct rdr_info* out);
+
+/* y = A x (device pointers, length n_total): gather, per-cell contraction
+ * y_e = sum_s c_{e,s} R_s x_e with the shared reference matrices, scatter-add
+ * (north_star; matrix-free action P:2267-2275). */
+int rdr_apply(rdr_handle* h, const double* x, double* y, void* stream);
+
+/* z = P^-1 r (device pointers): interior point-Jacobi + additive star patches
+ * (DESIGN.md R-A13..A17). */
+int rdr_precond(rdr_handle* h, const double* r, double* z, void* stream);
+
+/* PCG (DESIGN.md R-A16) from x0 = 0 on device vectors b -> x.
+ * *iters (host) receives the iteration count; synchronizes `stream`. */
+int rdr_solve(rdr_handle* h, const double* b, double* x, double rtol, int maxit, int* iters, void* stream);
+
+/* Same as rdr_solve with HOST b and x (pinned or pageable): H2D copy of b,
+ * PCG, D2H copy of x, all on `stream` (the end-to-end path). */
+int rdr_solve_host(rdr_handle* h, const double* b_host, double* x_host, double rtol, int maxit,
+                   int* iters, void* stream);
+
+/* Per-kernel launch accounting of the last rdr_solve: number of library kernel
+ * launches (graph nodes included). */
+int rdr_last_launches(const rdr_handle* h, int64_t* launches);
+
+/* Measurement helper (bench.py roofline): launch each hot-path kernel `reps`
+ * times back to back on `stream` between CUDA events and return the average
+ * device time per launch in ms: ms[0] operator apply (gather-contract-scatter),
+ * ms[1] interior Jacobi + zeroing, ms[2] patch solves, ms[3] discrete-gradient
+ * kernels (H(curl), else 0). x, r: device input vectors, y, z: outputs
+ * (contents overwritten). Synchronizes `stream`. */
+int rdr_time_kernels(rdr_handle* h, const double* x, double* y, const double* r, double* z, int reps, double* ms,
+                     void* stream);
+
+void rdr_destroy(rdr_handle* h);
+const char* rdr_strerror(int code);
+
+/* Host-only debug entry points (no device needed).
+ * rdr_reference_matrices: the n_mat reference matrices of (space, p) in
+ * float64, layout [n_mat][n_loc][n_loc]; pass out = NULL to query *n_loc and
+ * *n_mat. Order: H(grad) M, Kxx, Kyy, Kzz, Kxy+Kyx, Kxz+Kzx, Kyz+Kzy;
+ * H(curl) Mxx, Myy, Mzz, Mxy+Myx, Mxz+Mzx, Myz+Mzy, then the same for K (curl).
+ * Local dof order: DESIGN.md R-A8. */
+int rdr_reference_matrices(int space, int p, double* out, int32_t* n_loc, int32_t* n_mat);
+/* Bubble eigenvalues lambda_j (Eq. 3.8) on the canonical l-simplex: kind 0 = CG, 1 = Ned1. */
+int rdr_bubble_eigenvalues(int kind, int l, int p, double* out, int32_t* n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -69,17 +69,23 @@ class Assembler:
         det = np.linalg.det(J)
         vol = np.abs(det) * self.vol_hat
         wq = self.w
+        sw = np.sqrt(wq)
+
+        def gram(F):  # sum_q w_q F[c,q,i,:].F[c,q,j,:] as a batched matmul
+            G = np.transpose(F * sw[None, :, None, None], (0, 2, 1, 3)).reshape(F.shape[0], F.shape[2], -1)
+            return G @ np.transpose(G, (0, 2, 1))
+
         if self.space == "hgrad":
             Jit = np.linalg.inv(np.transpose(J, (0, 2, 1)))   # J^-T
             g = np.einsum("cab,qnb->cqna", Jit, self.der)     # physical gradients
             Mm = np.einsum("q,qi,qj->ij", wq, self.val, self.val)
-            Kk = np.einsum("q,cqia,cqja->cij", wq, g, g)
+            Kk = gram(g)
             return vol[:, None, None] * (beta[:, None, None] * Mm[None] + alpha[:, None, None] * Kk)
         Jit = np.linalg.inv(np.transpose(J, (0, 2, 1)))
         ph = np.einsum("cab,qnb->cqna", Jit, self.val)
         cu = np.einsum("cab,qnb->cqna", J, self.der) / det[:, None, None, None]
-        Mm = np.einsum("q,cqia,cqja->cij", wq, ph, ph)
-        Kk = np.einsum("q,cqia,cqja->cij", wq, cu, cu)
+        Mm = gram(ph)
+        Kk = gram(cu)
         return vol[:, None, None] * (beta[:, None, None] * Mm + alpha[:, None, None] * Kk)
 
     def assemble(self, alpha, beta, chunk: int = 256):

@@ -167,25 +167,42 @@ class Oracle:
         self.G = sp.csr_matrix((vals, (rows, cols)), shape=(ned.n_total, cg.n_total))
         return self.G
 
-    def build_preconditioner(self):
-        A = self.A
-        d = A.diagonal()
+    def _potential_operator(self):
+        """(grad phi_i, beta grad phi_j) on CG_p (Eq. 5.11), free CG dofs only."""
+        if getattr(self, "_Apot", None) is None:
+            self._build_gradient()
+            asm = Assembler("hgrad", self.p, self.topo, self.cg_num)
+            K = asm.assemble(self.beta, np.zeros_like(self.beta))
+            f = sp.diags((~self.cg_num.constrained).astype(np.float64))
+            self._Apot = (f @ K @ f).tocsr()
+        return self._Apot
+
+    def build_preconditioner(self, kappa: bool = True):
+        """Factor every patch matrix; kappa=True also records max kappa(A_m)
+        (the oracle reports it next to the 1e-11 parity bar)."""
+        Ar = self.A
+        d = Ar.diagonal()
         self.int_idx = np.nonzero(self.num.interior & self.free)[0]
         self.dinv = 1.0 / d[self.int_idx]
         self.factors = []
         self.kappa_max = 0.0
         for kind, idx in self.patch_sets():
             if kind == "dof":
-                Am = A[idx][:, idx].toarray()
+                Am = Ar[idx][:, idx].toarray()
                 emb = None
             else:
+                # Eq. 5.11 (P:1916-1920): the local potential problem is
+                # (d phi, beta d psi) on the star, i.e. the beta-weighted CG_p
+                # stiffness (= G_V^T A G_V since curl grad = 0, pinned in
+                # test_hcurl_gradients), assembled by physical quadrature.
                 Gv = self.G[:, idx]
-                Am = (Gv.T @ A @ Gv).toarray()
+                Am = self._potential_operator()[idx][:, idx].toarray()
                 emb = Gv.tocsr()
-            ev = np.linalg.eigvalsh(Am)
-            if ev[0] <= 0:
-                raise np.linalg.LinAlgError("patch matrix not SPD")
-            self.kappa_max = max(self.kappa_max, ev[-1] / ev[0])
+            if kappa:
+                ev = np.linalg.eigvalsh(Am)
+                if ev[0] <= 0:
+                    raise np.linalg.LinAlgError("patch matrix not SPD")
+                self.kappa_max = max(self.kappa_max, ev[-1] / ev[0])
             self.factors.append((kind, idx, emb, sla.cho_factor(Am, lower=True)))
         return self
 

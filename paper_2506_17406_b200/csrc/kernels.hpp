@@ -1,0 +1,76 @@
+// Launch wrappers of the sm_100a kernels (kernels.cu). Host code never sees
+// device code; every wrapper enqueues on the given stream and returns the
+// cudaError_t of the launch.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace rdr {
+
+struct PcgScalars {
+  double rz;       // r.z of the current iterate
+  double rz_new;   // accumulator for the next r.z
+  double pq;       // accumulator for p.Aq
+  double zz;       // accumulator for ||z||^2
+  double z0;       // ||z_0||
+  double rtol;
+  double beta;
+  int32_t iters;
+  int32_t maxit;
+  int32_t done;
+  int32_t converged;
+  uint32_t ticket;  // last-block counter of the reduction kernel
+  int32_t pad;
+};
+
+struct DevOperator {
+  int n_loc, n_mat, n_pad;      // n_pad: row stride of the reference matrices
+  int64_t n_cells, n_total;
+  const int32_t* dofmap_m;      // [n_cells][n_loc], -1 for constrained dofs
+  const double* coef;           // [n_cells][n_mat]
+  const double* R;              // [n_mat][n_loc][n_pad]
+};
+
+struct DevPrecond {
+  int64_t n_total, off3;        // interior dofs are [off3, n_total)
+  const double* dinv;           // [n_total - off3]
+  int64_t n_patches;
+  int32_t max_n;                // largest patch dimension
+  const int32_t* pn;            // [np]
+  const int64_t* idx_off;       // [np+1]
+  const int32_t* idx;
+  const int64_t* tile_off;      // [np+1]
+  const double* tiles;
+  const uint8_t* pkind;         // 0 own numbering, 1 CG potential
+  // H(curl) potential space
+  int64_t n_cg_iface;           // CG dofs [0, n_cg_iface) used by patches
+  const int64_t* g_ptr;
+  const int32_t* g_col;
+  const double* g_val;
+  double* gbuf;                 // G^T r (CG numbering)
+  double* ubuf;                 // patch corrections in the CG numbering
+};
+
+cudaError_t launch_apply(const DevOperator& op, const double* x, double* y, double* pq_acc,
+                         const PcgScalars* guard, cudaStream_t s);
+cudaError_t launch_precond(const DevPrecond& pc, const double* r, double* z, double* rz_acc,
+                           const PcgScalars* guard, cudaStream_t s);
+// one piece of the preconditioner: 0 interior Jacobi + zeroing, 1 G^T r (H(curl)),
+// 2 patch solves, 3 z += G u (H(curl))
+cudaError_t launch_precond_part(int part, const DevPrecond& pc, const double* r, double* z, double* rz_acc,
+                                const PcgScalars* guard, cudaStream_t s);
+
+// PCG pieces (DESIGN.md R-A16)
+cudaError_t launch_pcg_init(const double* b, const uint8_t* constrained, int64_t n, double* x, double* r,
+                            double* q, cudaStream_t s);
+cudaError_t launch_pcg_start(PcgScalars* sc, const double* z, double* p, int64_t n, double rtol, int maxit,
+                             cudaStream_t s);
+cudaError_t launch_pcg_update(PcgScalars* sc, const double* p, const double* q, double* x, double* r, int64_t n,
+                              cudaStream_t s);
+cudaError_t launch_pcg_finish(PcgScalars* sc, const double* z, int64_t n, cudaStream_t s);
+cudaError_t launch_pcg_direction(PcgScalars* sc, const double* z, double* p, double* q, int64_t n, cudaStream_t s);
+
+int count_precond_launches(const DevPrecond& pc);  // kernels per rdr_precond
+void configure_kernels();                            // shared-memory opt-ins (call once, outside capture)
+
+}  // namespace rdr

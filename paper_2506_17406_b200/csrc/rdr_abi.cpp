@@ -1,0 +1,466 @@
+// C ABI of the library (include/rdr.h): host setup once, then device-resident
+// operator, preconditioner and PCG.
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <cstdio>
+#include <cstring>
+#include <exception>
+#include <new>
+#include <vector>
+
+#include "../../include/rdr.h"
+#include "kernels.hpp"
+#include "refelem.hpp"
+#include "setup.hpp"
+
+using namespace rdr;
+
+namespace {
+
+int cuda_status(cudaError_t e) {
+  if (e == cudaSuccess) return RDR_OK;
+  if (e == cudaErrorMemoryAllocation) return RDR_ENOMEM;
+  return RDR_ECUDA;
+}
+
+#define CK(call)                              \
+  do {                                        \
+    cudaError_t e_ = (call);                  \
+    if (e_ != cudaSuccess) return cuda_status(e_); \
+  } while (0)
+
+template <class T>
+int upload(T** dptr, const std::vector<T>& h) {
+  *dptr = nullptr;
+  if (h.empty()) return RDR_OK;
+  CK(cudaMalloc((void**)dptr, sizeof(T) * h.size()));
+  CK(cudaMemcpy(*dptr, h.data(), sizeof(T) * h.size(), cudaMemcpyHostToDevice));
+  return RDR_OK;
+}
+
+// copy a caller array (host or device) into a host vector
+template <class T>
+int fetch(const T* p, size_t count, std::vector<T>& out) {
+  out.resize(count);
+  if (count == 0) return RDR_OK;
+  cudaPointerAttributes a;
+  cudaError_t e = cudaPointerGetAttributes(&a, p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    a.type = cudaMemoryTypeUnregistered;
+  }
+  if (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) {
+    CK(cudaMemcpy(out.data(), p, sizeof(T) * count, cudaMemcpyDeviceToHost));
+  } else {
+    std::memcpy(out.data(), p, sizeof(T) * count);
+  }
+  return RDR_OK;
+}
+
+struct DeviceTiles : PatchSink {
+  double* d = nullptr;
+  int reserve(int64_t total) override {
+    if (total == 0) return RDR_OK;
+    cudaError_t e = cudaMalloc((void**)&d, sizeof(double) * total);
+    return cuda_status(e);
+  }
+  int put(int64_t begin, const double* tiles, int64_t count) override {
+    cudaError_t e = cudaMemcpy(d + begin, tiles, sizeof(double) * count, cudaMemcpyHostToDevice);
+    return cuda_status(e);
+  }
+};
+
+}  // namespace
+
+struct rdr_handle {
+  int space = 0, p = 0;
+  int64_t n_total = 0;
+  rdr_info info{};
+  DevOperator op{};
+  DevPrecond pc{};
+  // owned device memory
+  std::vector<void*> owned;
+  uint8_t* d_cons = nullptr;
+  double *d_x = nullptr, *d_r = nullptr, *d_z = nullptr, *d_p = nullptr, *d_q = nullptr, *d_b = nullptr;
+  PcgScalars* d_sc = nullptr;
+  PcgScalars* h_sc = nullptr;  // pinned
+  cudaStream_t cap_stream = nullptr;
+  cudaGraphExec_t graph = nullptr;
+  int graph_iters = 0;
+  int launches_per_iter = 0;
+  int64_t last_launches = 0;
+
+  template <class T>
+  int own_upload(T** d, const std::vector<T>& h) {
+    int st = upload(d, h);
+    if (*d) owned.push_back((void*)*d);
+    return st;
+  }
+  int own_alloc(void** d, size_t bytes) {
+    CK(cudaMalloc(d, bytes));
+    owned.push_back(*d);
+    return RDR_OK;
+  }
+  ~rdr_handle() {
+    if (graph) cudaGraphExecDestroy(graph);
+    if (cap_stream) cudaStreamDestroy(cap_stream);
+    for (void* p : owned) cudaFree(p);
+    if (h_sc) cudaFreeHost(h_sc);
+  }
+};
+
+static int setup_impl(rdr_handle* h, const double* vertices, int64_t nv, const int32_t* tets, int64_t nt, int p,
+                      int space, const double* alpha, const double* beta, const uint8_t* mask, cudaStream_t stream) {
+  auto t0 = std::chrono::steady_clock::now();
+  if (stream) CK(cudaStreamSynchronize(stream));
+  configure_kernels();
+  std::vector<double> hx, ha, hb;
+  std::vector<int32_t> ht;
+  std::vector<uint8_t> hm;
+  int st;
+  if ((st = fetch(vertices, (size_t)nv * 3, hx))) return st;
+  if ((st = fetch(tets, (size_t)nt * 4, ht))) return st;
+  if ((st = fetch(alpha, (size_t)nt, ha))) return st;
+  if ((st = fetch(beta, (size_t)nt, hb))) return st;
+  if ((st = fetch(mask, (size_t)nt * 4, hm))) return st;
+  for (int64_t t = 0; t < nt; ++t)
+    if (!(ha[t] > 0) || !(hb[t] >= 0)) return RDR_EINVAL;
+
+  Mesh m;
+  if ((st = build_mesh(hx.data(), nv, ht.data(), nt, hm.data(), m))) return st;
+  const RefElement& el = reference_element(space, p);
+  Numbering num;
+  build_numbering(m, el, num);
+  std::vector<double> coef;
+  cell_coefficients(m, space, ha.data(), hb.data(), coef);
+  h->space = space;
+  h->p = p;
+  h->n_total = num.n_total;
+
+  // ---- operator
+  std::vector<int32_t> dm = num.dofmap;
+  for (auto& g : dm)
+    if (num.constrained[g]) g = -1;
+  DevOperator& op = h->op;
+  op.n_loc = el.n;
+  op.n_mat = el.n_mat;
+  op.n_pad = el.n;
+  op.n_cells = nt;
+  op.n_total = num.n_total;
+  int32_t* d_dm;
+  double *d_coef, *d_R;
+  if ((st = h->own_upload(&d_dm, dm))) return st;
+  if ((st = h->own_upload(&d_coef, coef))) return st;
+  if ((st = h->own_upload(&d_R, el.R))) return st;
+  op.dofmap_m = d_dm;
+  op.coef = d_coef;
+  op.R = d_R;
+  if ((st = h->own_upload(&h->d_cons, num.constrained))) return st;
+
+  // ---- preconditioner
+  DevPrecond& pc = h->pc;
+  pc.n_total = num.n_total;
+  pc.off3 = num.off[3];
+  std::vector<double> dinv;
+  interior_inverse_diagonal(m, num, el, coef, dinv);
+  double* d_dinv;
+  if ((st = h->own_upload(&d_dinv, dinv))) return st;
+  pc.dinv = d_dinv;
+  Numbering cg_num;
+  std::vector<double> cg_coef;
+  const RefElement* cg_el = nullptr;
+  if (space == RDR_HCURL) {
+    cg_el = &reference_element(RDR_HGRAD, p);
+    build_numbering(m, *cg_el, cg_num);
+    // potential patches: A_V = G_V^T A G_V = CG stiffness weighted by beta (curl grad = 0)
+    std::vector<double> zero(nt, 0.0);
+    cell_coefficients(m, RDR_HGRAD, hb.data(), zero.data(), cg_coef);
+    Gradient G;
+    build_gradient(m, num, cg_num, G);
+    pc.n_cg_iface = cg_num.off[3];
+    G.ptr.resize(pc.n_cg_iface + 1);
+    G.col.resize(G.ptr.back());
+    G.val.resize(G.ptr.back());
+    int64_t* d_gp;
+    int32_t* d_gc;
+    double* d_gv;
+    if ((st = h->own_upload(&d_gp, G.ptr))) return st;
+    if ((st = h->own_upload(&d_gc, G.col))) return st;
+    if ((st = h->own_upload(&d_gv, G.val))) return st;
+    pc.g_ptr = d_gp;
+    pc.g_col = d_gc;
+    pc.g_val = d_gv;
+    if ((st = h->own_alloc((void**)&pc.gbuf, sizeof(double) * std::max<int64_t>(1, pc.n_cg_iface)))) return st;
+    if ((st = h->own_alloc((void**)&pc.ubuf, sizeof(double) * std::max<int64_t>(1, pc.n_cg_iface)))) return st;
+  }
+  Patches P;
+  DeviceTiles sink;
+  st = build_patches(m, num, el, coef, space == RDR_HCURL ? &cg_num : nullptr, cg_el,
+                     space == RDR_HCURL ? &cg_coef : nullptr, P, sink);
+  if (sink.d) h->owned.push_back(sink.d);
+  if (st) return st;
+  pc.n_patches = (int64_t)P.n.size();
+  pc.max_n = P.max_n;
+  int32_t *d_pn, *d_idx;
+  int64_t *d_io, *d_to;
+  uint8_t* d_pk;
+  if ((st = h->own_upload(&d_pn, P.n))) return st;
+  if ((st = h->own_upload(&d_io, P.idx_off))) return st;
+  if ((st = h->own_upload(&d_idx, P.idx))) return st;
+  if ((st = h->own_upload(&d_to, P.tile_off))) return st;
+  if ((st = h->own_upload(&d_pk, P.kind))) return st;
+  pc.pn = d_pn;
+  pc.idx_off = d_io;
+  pc.idx = d_idx;
+  pc.tile_off = d_to;
+  pc.tiles = sink.d;
+  pc.pkind = d_pk;
+
+  // ---- PCG workspace
+  const size_t vb = sizeof(double) * std::max<int64_t>(1, num.n_total);
+  for (double** v : {&h->d_x, &h->d_r, &h->d_z, &h->d_p, &h->d_q, &h->d_b})
+    if ((st = h->own_alloc((void**)v, vb))) return st;
+  if ((st = h->own_alloc((void**)&h->d_sc, sizeof(PcgScalars)))) return st;
+  CK(cudaMallocHost((void**)&h->h_sc, sizeof(PcgScalars)));
+  CK(cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
+  h->launches_per_iter = 4 + count_precond_launches(pc);
+
+  // ---- info
+  rdr_info& in = h->info;
+  in.n_total = num.n_total;
+  int64_t nfree = 0;
+  for (uint8_t c : num.constrained) nfree += !c;
+  in.n_free = nfree;
+  in.n_interior = num.n_total - num.off[3];
+  in.n_cells = nt;
+  in.n_loc = el.n;
+  in.n_mat = el.n_mat;
+  in.n_patches = pc.n_patches;
+  in.max_patch = P.max_n;
+  in.patch_bytes = P.total_doubles * 8;
+  in.flops_apply = 2.0 * el.n * (double)el.n * el.n_mat * (double)nt;
+  in.bytes_apply = 24.0 * num.n_total + (double)nt * (4.0 * el.n + 8.0 * el.n_mat);
+  in.bytes_precond = P.alg_bytes + 24.0 * in.n_interior;
+  CK(cudaDeviceSynchronize());
+  in.setup_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return RDR_OK;
+}
+
+extern "C" {
+
+int rdr_setup(rdr_handle** hp, const double* vertices, int64_t nv, const int32_t* tets, int64_t nt, int p, int space,
+              const double* alpha, const double* beta, const uint8_t* dirichlet_mask, void* stream) {
+  if (!hp) return RDR_EINVAL;
+  *hp = nullptr;
+  if (!vertices || !tets || !alpha || !beta || !dirichlet_mask || nv < 4 || nt < 1) return RDR_EINVAL;
+  if (space != RDR_HGRAD && space != RDR_HCURL) return RDR_EINVAL;
+  if (p < 1 || (space == RDR_HGRAD && p > 12) || (space == RDR_HCURL && p > 10)) return RDR_EINVAL;
+  if (nv > 0x7fffffff || nt > 0x7fffffff) return RDR_EINVAL;
+  rdr_handle* h = new (std::nothrow) rdr_handle();
+  if (!h) return RDR_ENOMEM;
+  int st;
+  try {
+    st = setup_impl(h, vertices, nv, tets, nt, p, space, alpha, beta, dirichlet_mask, (cudaStream_t)stream);
+  } catch (const std::bad_alloc&) {
+    st = RDR_ENOMEM;
+  } catch (const std::exception& e) {
+    std::fprintf(stderr, "rdr_setup: %s\n", e.what());
+    st = RDR_EINVAL;
+  }
+  if (st) {
+    delete h;
+    return st;
+  }
+  *hp = h;
+  return RDR_OK;
+}
+
+int rdr_ndofs(const rdr_handle* h, int64_t* n_total) {
+  if (!h || !n_total) return RDR_EINVAL;
+  *n_total = h->n_total;
+  return RDR_OK;
+}
+
+int rdr_get_info(const rdr_handle* h, rdr_info* out) {
+  if (!h || !out) return RDR_EINVAL;
+  *out = h->info;
+  return RDR_OK;
+}
+
+int rdr_apply(rdr_handle* h, const double* x, double* y, void* stream) {
+  if (!h || !x || !y) return RDR_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  CK(cudaMemsetAsync(y, 0, sizeof(double) * h->n_total, s));
+  CK(launch_apply(h->op, x, y, nullptr, nullptr, s));
+  return RDR_OK;
+}
+
+int rdr_precond(rdr_handle* h, const double* r, double* z, void* stream) {
+  if (!h || !r || !z) return RDR_EINVAL;
+  CK(launch_precond(h->pc, r, z, nullptr, nullptr, (cudaStream_t)stream));
+  return RDR_OK;
+}
+
+static int enqueue_iteration(rdr_handle* h, cudaStream_t s) {
+  const int64_t n = h->n_total;
+  CK(launch_apply(h->op, h->d_p, h->d_q, &h->d_sc->pq, h->d_sc, s));
+  CK(launch_pcg_update(h->d_sc, h->d_p, h->d_q, h->d_x, h->d_r, n, s));
+  CK(launch_precond(h->pc, h->d_r, h->d_z, &h->d_sc->rz_new, h->d_sc, s));
+  CK(launch_pcg_finish(h->d_sc, h->d_z, n, s));
+  CK(launch_pcg_direction(h->d_sc, h->d_z, h->d_p, h->d_q, n, s));
+  return RDR_OK;
+}
+
+static int build_graph(rdr_handle* h, int iters) {
+  if (h->graph) return RDR_OK;
+  cudaGraph_t g;
+  CK(cudaStreamBeginCapture(h->cap_stream, cudaStreamCaptureModeThreadLocal));
+  int st = RDR_OK;
+  for (int k = 0; k < iters && st == RDR_OK; ++k) st = enqueue_iteration(h, h->cap_stream);
+  cudaError_t e = cudaStreamEndCapture(h->cap_stream, &g);
+  if (st) return st;
+  CK(e);
+  e = cudaGraphInstantiate(&h->graph, g, 0);
+  cudaGraphDestroy(g);
+  CK(e);
+  h->graph_iters = iters;
+  return RDR_OK;
+}
+
+static int solve_device(rdr_handle* h, const double* b, double rtol, int maxit, int* iters, cudaStream_t s) {
+  const int64_t n = h->n_total;
+  int st;
+  if ((st = build_graph(h, 8))) return st;
+  int64_t launches = 0;
+  CK(cudaMemsetAsync(h->d_sc, 0, sizeof(PcgScalars), s));
+  CK(launch_pcg_init(b, h->d_cons, n, h->d_x, h->d_r, h->d_q, s));
+  CK(launch_precond(h->pc, h->d_r, h->d_z, &h->d_sc->rz_new, nullptr, s));
+  CK(launch_pcg_start(h->d_sc, h->d_z, h->d_p, n, rtol, maxit, s));
+  launches += 2 + count_precond_launches(h->pc);
+  for (;;) {
+    CK(cudaMemcpyAsync(h->h_sc, h->d_sc, sizeof(PcgScalars), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (h->h_sc->done) break;
+    CK(cudaGraphLaunch(h->graph, s));
+    launches += (int64_t)h->graph_iters * h->launches_per_iter;
+  }
+  h->last_launches = launches;
+  *iters = h->h_sc->iters;
+  return h->h_sc->converged ? RDR_OK : RDR_ENOCONV;
+}
+
+int rdr_solve(rdr_handle* h, const double* b, double* x, double rtol, int maxit, int* iters, void* stream) {
+  if (!h || !b || !x || !iters || !(rtol >= 0)) return RDR_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  int st = solve_device(h, b, rtol, maxit, iters, s);
+  if (st != RDR_OK && st != RDR_ENOCONV) return st;
+  CK(cudaMemcpyAsync(x, h->d_x, sizeof(double) * h->n_total, cudaMemcpyDeviceToDevice, s));
+  CK(cudaStreamSynchronize(s));
+  return st;
+}
+
+int rdr_solve_host(rdr_handle* h, const double* b_host, double* x_host, double rtol, int maxit, int* iters,
+                   void* stream) {
+  if (!h || !b_host || !x_host || !iters || !(rtol >= 0)) return RDR_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  CK(cudaMemcpyAsync(h->d_b, b_host, sizeof(double) * h->n_total, cudaMemcpyHostToDevice, s));
+  int st = solve_device(h, h->d_b, rtol, maxit, iters, s);
+  if (st != RDR_OK && st != RDR_ENOCONV) return st;
+  CK(cudaMemcpyAsync(x_host, h->d_x, sizeof(double) * h->n_total, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return st;
+}
+
+int rdr_last_launches(const rdr_handle* h, int64_t* launches) {
+  if (!h || !launches) return RDR_EINVAL;
+  *launches = h->last_launches;
+  return RDR_OK;
+}
+
+int rdr_time_kernels(rdr_handle* h, const double* x, double* y, const double* r, double* z, int reps, double* ms,
+                     void* stream) {
+  if (!h || !x || !y || !r || !z || !ms || reps < 1) return RDR_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  auto timed = [&](auto launch, double* out) -> int {
+    CK(launch());  // warm-up
+    CK(cudaEventRecord(e0, s));
+    for (int k = 0; k < reps; ++k) CK(launch());
+    CK(cudaEventRecord(e1, s));
+    CK(cudaEventSynchronize(e1));
+    float t = 0;
+    CK(cudaEventElapsedTime(&t, e0, e1));
+    *out = (double)t / reps;
+    return RDR_OK;
+  };
+  int st = timed([&] { return launch_apply(h->op, x, y, nullptr, nullptr, s); }, &ms[0]);
+  if (!st) st = timed([&] { return launch_precond_part(0, h->pc, r, z, nullptr, nullptr, s); }, &ms[1]);
+  if (!st) st = timed([&] { return launch_precond_part(2, h->pc, r, z, nullptr, nullptr, s); }, &ms[2]);
+  if (!st) {
+    if (h->pc.gbuf) {
+      st = timed([&] {
+        cudaError_t e = launch_precond_part(1, h->pc, r, z, nullptr, nullptr, s);
+        return e != cudaSuccess ? e : launch_precond_part(3, h->pc, r, z, nullptr, nullptr, s);
+      }, &ms[3]);
+    } else {
+      ms[3] = 0;
+    }
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return st;
+}
+
+void rdr_destroy(rdr_handle* h) {
+  if (h) {
+    cudaDeviceSynchronize();
+    delete h;
+  }
+}
+
+const char* rdr_strerror(int code) {
+  switch (code) {
+    case RDR_OK: return "ok";
+    case RDR_EINVAL: return "invalid argument";
+    case RDR_EMESH: return "invalid mesh (degenerate cell, non-manifold face or mask on an interior face)";
+    case RDR_ENOTSPD: return "patch matrix not SPD";
+    case RDR_ENOMEM: return "out of memory";
+    case RDR_ECUDA: return "CUDA error";
+    case RDR_ENOCONV: return "PCG did not converge within maxit";
+    default: return "unknown error";
+  }
+}
+
+int rdr_reference_matrices(int space, int p, double* out, int32_t* n_loc, int32_t* n_mat) {
+  if (!n_loc || !n_mat) return RDR_EINVAL;
+  if (space != RDR_HGRAD && space != RDR_HCURL) return RDR_EINVAL;
+  if (p < 1 || (space == RDR_HGRAD && p > 12) || (space == RDR_HCURL && p > 10)) return RDR_EINVAL;
+  try {
+    const RefElement& el = reference_element(space, p);
+    *n_loc = el.n;
+    *n_mat = el.n_mat;
+    if (out) std::memcpy(out, el.R.data(), sizeof(double) * el.R.size());
+  } catch (const std::exception& e) {
+    std::fprintf(stderr, "rdr_reference_matrices: %s\n", e.what());
+    return RDR_EINVAL;
+  }
+  return RDR_OK;
+}
+
+int rdr_bubble_eigenvalues(int kind, int l, int p, double* out, int32_t* n) {
+  if (!n || (kind != 0 && kind != 1) || l < 1 || l > 3 || p < 1 || p > 12 || (kind == 1 && l < 2)) return RDR_EINVAL;
+  try {
+    std::vector<double> v = bubble_eigenvalues(kind, l, p);
+    *n = (int32_t)v.size();
+    if (out) std::memcpy(out, v.data(), sizeof(double) * v.size());
+  } catch (const std::exception& e) {
+    std::fprintf(stderr, "rdr_bubble_eigenvalues: %s\n", e.what());
+    return RDR_EINVAL;
+  }
+  return RDR_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,33 @@
+// Reference element of the paper's basis, built on the host in x87 extended
+// precision (long double) and rounded to FP64 once (DESIGN.md R-A24).
+#pragma once
+#include <array>
+#include <string>
+#include <vector>
+
+namespace rdr {
+
+struct LocalDof {
+  int dim;    // 0 vertex, 1 edge, 2 face, 3 cell
+  int ent;    // local entity index on T-hat (R-A8 order)
+  int j;      // index inside the entity's family
+  int type;   // 0 = type-I / vertex / H(grad) bubble, 1 = type-II, 2 = Whitney
+};
+
+struct RefElement {
+  int space = 0;                 // 0 H(grad), 1 H(curl)
+  int p = 0;
+  int n = 0;                     // local dofs
+  int n_mat = 0;                 // 7 or 12
+  std::vector<LocalDof> dofs;    // R-A8 order
+  std::vector<double> R;         // [n_mat][n][n] symmetric reference matrices (FP64)
+  std::vector<double> lam_cell;  // interior type-I eigenvalues
+};
+
+// Cached per (space, p). Throws std::runtime_error on internal failure.
+const RefElement& reference_element(int space, int p);
+
+// Bubble eigenvalues on the canonical l-simplex; kind 0 = CG_p, 1 = Ned1_p.
+std::vector<double> bubble_eigenvalues(int kind, int l, int p);
+
+}  // namespace rdr

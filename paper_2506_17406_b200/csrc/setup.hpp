@@ -1,0 +1,78 @@
+// Host-side setup of the Riesz-map operator and preconditioner (SURVEY §8(a)
+// S0/S1 and the patch factorisation of P:2284-2288).
+#pragma once
+#include <cstdint>
+#include <vector>
+
+#include "refelem.hpp"
+
+namespace rdr {
+
+struct Mesh {
+  int64_t nv = 0, nt = 0, ne = 0, nf = 0;
+  std::vector<double> x;             // [nv][3]
+  std::vector<int32_t> cells;        // [nt][4], sorted vertex ids (R-A3)
+  std::vector<int32_t> cell_edges;   // [nt][6] local edge order (01,02,03,12,13,23)
+  std::vector<int32_t> cell_faces;   // [nt][4] local face order (012,013,023,123)
+  std::vector<int32_t> edges;        // [ne][2] lexicographic (R-A9)
+  std::vector<int32_t> faces;        // [nf][3] lexicographic
+  std::vector<uint8_t> dir_v, dir_e, dir_f;  // Dirichlet closure (R-A11)
+};
+
+// Returns 0 or an rdr error code (RDR_EMESH).
+int build_mesh(const double* x, int64_t nv, const int32_t* tets, int64_t nt, const uint8_t* mask, Mesh& m);
+
+struct Numbering {
+  int space = 0, p = 0;
+  int64_t per[4] = {0, 0, 0, 0};
+  int64_t off[4] = {0, 0, 0, 0};
+  int64_t n_total = 0;
+  std::vector<int32_t> dofmap;       // [nt][n_loc] global ids
+  std::vector<uint8_t> constrained;  // [n_total]
+};
+
+void build_numbering(const Mesh& m, const RefElement& el, Numbering& num);
+
+// Per-cell coefficients c_{e,s} (7 for H(grad), 12 for H(curl)), see setup.cpp.
+void cell_coefficients(const Mesh& m, int space, const double* alpha, const double* beta, std::vector<double>& c);
+
+struct Patches {
+  // patches sorted by decreasing size; indices are global ids in `space_of_idx`
+  // (0 = the problem's own numbering, 1 = the CG_p potential numbering)
+  std::vector<int32_t> n;            // [np] patch dimension
+  std::vector<int64_t> idx_off;      // [np+1] offsets into idx
+  std::vector<int32_t> idx;          // patch dof ids (padded to a multiple of 32 with -1)
+  std::vector<int64_t> tile_off;     // [np+1] offsets (in doubles) into the packed inverse store
+  std::vector<uint8_t> kind;         // [np] 0 = direct dofs, 1 = potential (through G)
+  int64_t total_doubles = 0;
+  int32_t max_n = 0;
+  double alg_bytes = 0;              // 8 sum n(n+1)/2
+};
+
+// Builds the patch index sets (R-A13), assembles and inverts each patch
+// matrix (R-A15), and hands the packed tiles to `sink(first_patch, last_patch,
+// host_tiles)` in chunks so that the full inverse store never lives on the host.
+// Returns 0 or RDR_ENOTSPD.
+struct PatchSink {
+  virtual int reserve(int64_t total_doubles) = 0;
+  virtual int put(int64_t tile_begin, const double* tiles, int64_t count) = 0;
+  virtual ~PatchSink() {}
+};
+int build_patches(const Mesh& m, const Numbering& num, const RefElement& el, const std::vector<double>& coef,
+                  const Numbering* cg_num, const RefElement* cg_el, const std::vector<double>* cg_coef,
+                  Patches& P, PatchSink& sink);
+
+// Interior point-Jacobi (R-A17): 1/A_ll for the cell-interior dofs [off[3], n_total).
+void interior_inverse_diagonal(const Mesh& m, const Numbering& num, const RefElement& el,
+                               const std::vector<double>& coef, std::vector<double>& dinv);
+
+// Discrete gradient rows for the H(curl) potential space (R-A12), CSR over the
+// CG_p dofs: g_c = sum_k G[k][c] r_k.
+struct Gradient {
+  std::vector<int64_t> ptr;   // [n_cg + 1]
+  std::vector<int32_t> col;   // Ned1 dof ids
+  std::vector<double> val;    // +-1
+};
+void build_gradient(const Mesh& m, const Numbering& ned, const Numbering& cg, Gradient& G);
+
+}  // namespace rdr

@@ -1,0 +1,196 @@
+"""Thin ctypes binding of librdr.so (include/rdr.h). Argument marshalling only:
+every step of the hot path runs in the library's CUDA kernels. There is no
+CPU fallback: if the extension is missing, importing this module fails."""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "librdr.so")
+
+HGRAD, HCURL = 0, 1
+RDR_OK, RDR_ENOCONV = 0, -6
+
+
+class RdrError(RuntimeError):
+    def __init__(self, code: int, what: str):
+        self.code = code
+        super().__init__(f"{what}: {_lib.rdr_strerror(code).decode()} ({code})")
+
+
+class Info(ctypes.Structure):
+    _fields_ = [("n_total", ctypes.c_int64), ("n_free", ctypes.c_int64), ("n_interior", ctypes.c_int64),
+                ("n_cells", ctypes.c_int64), ("n_loc", ctypes.c_int32), ("n_mat", ctypes.c_int32),
+                ("n_patches", ctypes.c_int64), ("max_patch", ctypes.c_int32), ("patch_bytes", ctypes.c_int64),
+                ("flops_apply", ctypes.c_double), ("bytes_apply", ctypes.c_double),
+                ("bytes_precond", ctypes.c_double), ("setup_seconds", ctypes.c_double)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_2506_17406_b200.build` "
+                          "(there is no CPU fallback)")
+    lib = ctypes.CDLL(LIB_PATH)
+    P, I64, I32, D = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_double
+    sig = {
+        "rdr_setup": (ctypes.c_int, [ctypes.POINTER(P), P, I64, P, I64, ctypes.c_int, ctypes.c_int, P, P, P, P]),
+        "rdr_ndofs": (ctypes.c_int, [P, ctypes.POINTER(I64)]),
+        "rdr_get_info": (ctypes.c_int, [P, ctypes.POINTER(Info)]),
+        "rdr_apply": (ctypes.c_int, [P, P, P, P]),
+        "rdr_precond": (ctypes.c_int, [P, P, P, P]),
+        "rdr_solve": (ctypes.c_int, [P, P, P, D, ctypes.c_int, ctypes.POINTER(ctypes.c_int), P]),
+        "rdr_solve_host": (ctypes.c_int, [P, P, P, D, ctypes.c_int, ctypes.POINTER(ctypes.c_int), P]),
+        "rdr_last_launches": (ctypes.c_int, [P, ctypes.POINTER(I64)]),
+        "rdr_time_kernels": (ctypes.c_int, [P, P, P, P, P, ctypes.c_int, P, P]),
+        "rdr_destroy": (None, [P]),
+        "rdr_strerror": (ctypes.c_char_p, [ctypes.c_int]),
+        "rdr_reference_matrices": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, P, ctypes.POINTER(I32),
+                                                  ctypes.POINTER(I32)]),
+        "rdr_bubble_eigenvalues": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, P,
+                                                  ctypes.POINTER(I32)]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    return lib
+
+
+_lib = _load()
+
+
+def _ptr(a):
+    """Raw address of a torch tensor or numpy array (contiguous)."""
+    if hasattr(a, "data_ptr"):
+        assert a.is_contiguous()
+        return ctypes.c_void_p(a.data_ptr())
+    assert a.flags["C_CONTIGUOUS"]
+    return ctypes.c_void_p(a.ctypes.data)
+
+
+def _stream(stream):
+    if stream is None:
+        import torch
+        return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    if isinstance(stream, int):
+        return ctypes.c_void_p(stream)
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _check(code, what):
+    if code != RDR_OK:
+        raise RdrError(code, what)
+
+
+def reference_matrices(space: int, p: int) -> np.ndarray:
+    """[n_mat, n_loc, n_loc] FP64 reference matrices (host-only entry point)."""
+    n, m = ctypes.c_int32(), ctypes.c_int32()
+    _check(_lib.rdr_reference_matrices(space, p, None, ctypes.byref(n), ctypes.byref(m)), "rdr_reference_matrices")
+    out = np.zeros((m.value, n.value, n.value))
+    _check(_lib.rdr_reference_matrices(space, p, _ptr(out), ctypes.byref(n), ctypes.byref(m)),
+           "rdr_reference_matrices")
+    return out
+
+
+def bubble_eigenvalues(kind: int, l: int, p: int) -> np.ndarray:
+    n = ctypes.c_int32()
+    _check(_lib.rdr_bubble_eigenvalues(kind, l, p, None, ctypes.byref(n)), "rdr_bubble_eigenvalues")
+    out = np.zeros(n.value)
+    _check(_lib.rdr_bubble_eigenvalues(kind, l, p, _ptr(out), ctypes.byref(n)), "rdr_bubble_eigenvalues")
+    return out
+
+
+class Solver:
+    """rdr.Solver(vertices, tets, p, space, alpha, beta, mask): torch CUDA tensors
+    (float64 / int32 / uint8) or host numpy arrays; vectors are torch float64
+    CUDA tensors of length n_total."""
+
+    def __init__(self, vertices, tets, p, space, alpha, beta, mask, stream=None):
+        import torch
+        self._keep = [np.ascontiguousarray(vertices, dtype=np.float64) if isinstance(vertices, np.ndarray) else vertices,
+                      np.ascontiguousarray(tets, dtype=np.int32) if isinstance(tets, np.ndarray) else tets,
+                      np.ascontiguousarray(alpha, dtype=np.float64) if isinstance(alpha, np.ndarray) else alpha,
+                      np.ascontiguousarray(beta, dtype=np.float64) if isinstance(beta, np.ndarray) else beta,
+                      np.ascontiguousarray(mask, dtype=np.uint8) if isinstance(mask, np.ndarray) else mask]
+        v, t, a, b, m = self._keep
+        self._h = ctypes.c_void_p()
+        nv, nt = v.shape[0], t.shape[0]
+        _check(_lib.rdr_setup(ctypes.byref(self._h), _ptr(v), nv, _ptr(t), nt, int(p), int(space), _ptr(a), _ptr(b),
+                              _ptr(m), _stream(stream)), "rdr_setup")
+        self._keep = None
+        n = ctypes.c_int64()
+        _check(_lib.rdr_ndofs(self._h, ctypes.byref(n)), "rdr_ndofs")
+        self.n_total = n.value
+        self.p, self.space = p, space
+        self.device = torch.device("cuda", torch.cuda.current_device())
+
+    @property
+    def info(self) -> dict:
+        i = Info()
+        _check(_lib.rdr_get_info(self._h, ctypes.byref(i)), "rdr_get_info")
+        return i.as_dict()
+
+    def _vec(self, v):
+        import torch
+        return torch.empty(self.n_total, dtype=torch.float64, device=self.device) if v is None else v
+
+    def apply(self, x, y=None, stream=None):
+        y = self._vec(y)
+        _check(_lib.rdr_apply(self._h, _ptr(x), _ptr(y), _stream(stream)), "rdr_apply")
+        return y
+
+    def precond(self, r, z=None, stream=None):
+        z = self._vec(z)
+        _check(_lib.rdr_precond(self._h, _ptr(r), _ptr(z), _stream(stream)), "rdr_precond")
+        return z
+
+    def solve(self, b, x=None, rtol=1e-8, maxit=10000, stream=None):
+        """PCG from x0 = 0; returns (x, iters). Raises RdrError on failure,
+        except non-convergence which returns iters == maxit and sets .converged False."""
+        x = self._vec(x)
+        it = ctypes.c_int()
+        code = _lib.rdr_solve(self._h, _ptr(b), _ptr(x), float(rtol), int(maxit), ctypes.byref(it), _stream(stream))
+        if code not in (RDR_OK, RDR_ENOCONV):
+            _check(code, "rdr_solve")
+        self.converged = code == RDR_OK
+        return x, it.value
+
+    def solve_host(self, b_host, x_host, rtol=1e-8, maxit=10000, stream=None):
+        """End-to-end path: host b -> device -> PCG -> host x (copies inside)."""
+        it = ctypes.c_int()
+        code = _lib.rdr_solve_host(self._h, _ptr(b_host), _ptr(x_host), float(rtol), int(maxit), ctypes.byref(it),
+                                   _stream(stream))
+        if code not in (RDR_OK, RDR_ENOCONV):
+            _check(code, "rdr_solve_host")
+        self.converged = code == RDR_OK
+        return it.value
+
+    def time_kernels(self, x, r, reps=20, stream=None):
+        """Average device ms per launch: (apply, jacobi, patches, gradient)."""
+        y, z = self._vec(None), self._vec(None)
+        ms = np.zeros(4)
+        _check(_lib.rdr_time_kernels(self._h, _ptr(x), _ptr(y), _ptr(r), _ptr(z), int(reps), _ptr(ms),
+                                     _stream(stream)), "rdr_time_kernels")
+        return ms
+
+    def last_launches(self) -> int:
+        n = ctypes.c_int64()
+        _check(_lib.rdr_last_launches(self._h, ctypes.byref(n)), "rdr_last_launches")
+        return n.value
+
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value:
+            _lib.rdr_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

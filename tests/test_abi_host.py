@@ -1,0 +1,72 @@
+"""C-ABI library checks that need no GPU: it loads, exports every symbol that
+include/rdr.h declares, and its HOST-side reference element (DESIGN.md R-A24,
+built independently in C++) agrees with the oracle's and with the paper's
+closed forms."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+LIB = os.path.join(ROOT, "paper_2506_17406_b200", "librdr.so")
+
+
+def _lib():
+    if not os.path.exists(LIB):
+        import __graft_entry__
+        __graft_entry__.build()
+    return ctypes.CDLL(LIB)
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _lib()
+    hdr = open(os.path.join(ROOT, "include", "rdr.h")).read()
+    names = set(re.findall(r"\b(rdr_[a-z_]+)\s*\(", hdr))
+    assert {"rdr_setup", "rdr_apply", "rdr_precond", "rdr_solve", "rdr_destroy"} <= names
+    for n in names:
+        assert hasattr(lib, n), n
+
+
+def test_strerror_and_argument_errors():
+    from paper_2506_17406_b200 import rdr
+    lib = rdr._lib
+    assert lib.rdr_strerror(0) == b"ok"
+    assert b"SPD" in lib.rdr_strerror(-3)
+    h = ctypes.c_void_p()
+    # NULL pointers and bad p/space are rejected before any device work
+    assert lib.rdr_setup(ctypes.byref(h), None, 8, None, 1, 3, 0, None, None, None, None) == -1
+    n, m = ctypes.c_int32(), ctypes.c_int32()
+    assert lib.rdr_reference_matrices(0, 13, None, ctypes.byref(n), ctypes.byref(m)) == -1
+    assert lib.rdr_reference_matrices(1, 11, None, ctypes.byref(n), ctypes.byref(m)) == -1
+    assert lib.rdr_reference_matrices(2, 3, None, ctypes.byref(n), ctypes.byref(m)) == -1
+
+
+@pytest.mark.parametrize("kind,l,p,lams", [
+    (0, 1, 3, [2 / 5, 2 / 21]), (0, 2, 3, [1 / 14]), (0, 3, 4, [4 / 165]),
+    (1, 2, 2, [2 / 9, 2 / 9]), (1, 3, 3, [7 / 144] * 3),
+])
+def test_library_eigenvalues_closed_forms(kind, l, p, lams):
+    from paper_2506_17406_b200 import rdr
+    assert np.allclose(rdr.bubble_eigenvalues(kind, l, p), lams, rtol=1e-14)
+
+
+@pytest.mark.parametrize("space,p", [(0, 1), (0, 2), (0, 3), (0, 4), (0, 6), (1, 1), (1, 2), (1, 3), (1, 4)])
+def test_library_reference_matrices_match_oracle(space, p):
+    """The C++ reference element (pivoted Cholesky + Jacobi + Gauss-Jordan) and the
+    oracle's (Gram eigendecomposition + Ogita-Aishima + GEPP) agree to rounding."""
+    from paper_2506_17406_b200 import rdr
+    from oracle.refelem import element, reference_matrices
+    R = rdr.reference_matrices(space, p)
+    M, K = reference_matrices(element("hgrad" if space == 0 else "hcurl", p))
+    M, K = M.astype(float), K.astype(float)
+    if space == 0:
+        ref = [M, K[0, 0], K[1, 1], K[2, 2], K[0, 1] + K[1, 0], K[0, 2] + K[2, 0], K[1, 2] + K[2, 1]]
+    else:
+        ref = [M[0, 0], M[1, 1], M[2, 2], M[0, 1] + M[1, 0], M[0, 2] + M[2, 0], M[1, 2] + M[2, 1],
+               K[0, 0], K[1, 1], K[2, 2], K[0, 1] + K[1, 0], K[0, 2] + K[2, 0], K[1, 2] + K[2, 1]]
+    assert R.shape[0] == len(ref)
+    scale = max(np.abs(r).max() for r in ref)
+    for s, r in enumerate(ref):
+        assert np.abs(R[s] - r).max() <= 1e-14 * scale, s

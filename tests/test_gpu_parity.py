@@ -1,0 +1,178 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the
+same seeded inputs. Bars (BASELINE.json north_star): operator and
+preconditioner applies within 1e-11 relative l2, PCG iteration counts within
++-1 at rtol 1e-8."""
+import numpy as np
+import pytest
+
+from rdr_inputs import make_config, HGRAD, HCURL
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-11
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+def rel(a, b):
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
+
+
+def _pair(torch, cfg, **kw):
+    from paper_2506_17406_b200 import rdr
+    from oracle.solver import Oracle
+    c = make_config(cfg, **kw)
+    S = rdr.Solver(c.vertices, c.tets, c.p, c.space, c.alpha, c.beta, c.mask)
+    O = Oracle(c.vertices, c.tets, c.p, c.space, c.alpha, c.beta, c.mask)
+    assert S.n_total == O.n_total
+    return c, S, O
+
+
+def _check_apply_precond(torch, c, S, O, nvec=2):
+    for _ in range(nvec):
+        x = c.draw_vector(O.n_total)            # constrained entries NOT zeroed: must be ignored
+        xt = torch.from_numpy(x).cuda()
+        y = S.apply(xt).cpu().numpy()
+        z = S.precond(xt).cpu().numpy()
+        ya, za = O.apply(x), O.precond(x)
+        assert rel(y, ya) <= TOL, rel(y, ya)
+        assert rel(z, za) <= TOL, rel(z, za)
+        assert np.all(y[~O.free] == 0) and np.all(z[~O.free] == 0)
+
+
+def _check_pcg(torch, c, S, O):
+    b = c.draw_vector(O.n_total)
+    x, it = S.solve(torch.from_numpy(b).cuda(), rtol=1e-8)
+    xo, ito, res = O.solve(b, rtol=1e-8)
+    assert abs(it - ito) <= 1, (it, ito)
+    xg = x.cpu().numpy()
+    bm = O.mask(b)
+    assert np.linalg.norm(bm - O.apply(xg)) / np.linalg.norm(bm) <= 1e-5
+    assert rel(xg, xo) <= 1e-6
+    return it, ito
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 5, 6, 7, 8])
+@pytest.mark.parametrize("perturb", [False, True])
+def test_hgrad_small(torch_cuda, p, perturb):
+    c, S, O = _pair(torch_cuda, 0, n=2, p=p, space=HGRAD, perturb=perturb, bc="all")
+    _check_apply_precond(torch_cuda, c, S, O)
+    _check_pcg(torch_cuda, c, S, O)
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 5])
+@pytest.mark.parametrize("perturb", [False, True])
+def test_hcurl_small(torch_cuda, p, perturb):
+    c, S, O = _pair(torch_cuda, 0, n=2, p=p, space=HCURL, perturb=perturb, bc="all")
+    _check_apply_precond(torch_cuda, c, S, O)
+    _check_pcg(torch_cuda, c, S, O)
+
+
+@pytest.mark.parametrize("space,bc,coeffs", [(HGRAD, "x0", "loguniform"), (HCURL, "x0", "loguniform"),
+                                             (HGRAD, "none", "one")])
+def test_partial_dirichlet_and_contrast(torch_cuda, space, bc, coeffs):
+    c, S, O = _pair(torch_cuda, 0, n=3, p=3, space=space, perturb=True, bc=bc, coeffs=coeffs)
+    _check_apply_precond(torch_cuda, c, S, O)
+    _check_pcg(torch_cuda, c, S, O)
+
+
+def test_config1(torch_cuda):
+    c, S, O = _pair(torch_cuda, 1)
+    b = c.draw_vector(O.n_total)   # the config's rhs (first draw)
+    x, it = S.solve(torch_cuda.from_numpy(b).cuda(), rtol=1e-8)
+    xo, ito, _ = O.solve(b)
+    assert abs(it - ito) <= 1
+    _check_apply_precond(torch_cuda, c, S, O)
+
+
+def test_config2(torch_cuda):
+    """BASELINE configs[1] (the bench workload) at full size."""
+    c, S, O = _pair(torch_cuda, 2)
+    O.build_preconditioner(kappa=False)
+    _check_apply_precond(torch_cuda, c, S, O, nvec=1)
+    _check_pcg(torch_cuda, c, S, O)
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 4])
+def test_config5_sweep_small_p(torch_cuda, p):
+    c, S, O = _pair(torch_cuda, 5, p=p)
+    O.build_preconditioner(kappa=False)
+    _check_apply_precond(torch_cuda, c, S, O, nvec=1)
+    _check_pcg(torch_cuda, c, S, O)
+
+
+def test_symmetry_and_gradient_kernel(torch_cuda):
+    """x^T A y = y^T A x, x^T P^-1 y = y^T P^-1 x through the library; K1 G = 0:
+    A(G u) does not depend on alpha (H(curl), no Dirichlet)."""
+    from paper_2506_17406_b200 import rdr
+    torch = torch_cuda
+    c = make_config(0, n=2, p=3, space=HCURL, perturb=True, bc="none")
+    S = rdr.Solver(c.vertices, c.tets, 3, HCURL, c.alpha, c.beta, c.mask)
+    rng = np.random.default_rng(0)
+    x, y = (torch.from_numpy(rng.standard_normal(S.n_total)).cuda() for _ in range(2))
+    assert abs(float(x @ S.apply(y) - y @ S.apply(x))) <= 1e-12 * float(x.norm() * S.apply(x).norm())
+    assert abs(float(x @ S.precond(y) - y @ S.precond(x))) <= 1e-12 * float(x.norm() * S.precond(x).norm())
+    from oracle.solver import Oracle
+    O = Oracle(c.vertices, c.tets, 3, HCURL, c.alpha, c.beta, c.mask, assemble=False)
+    G = O._build_gradient()
+    u = G @ rng.standard_normal(G.shape[1])
+    ut = torch.from_numpy(u).cuda()
+    S2 = rdr.Solver(c.vertices, c.tets, 3, HCURL, 1e3 * c.alpha, c.beta, c.mask)
+    a1, a2 = S.apply(ut).cpu().numpy(), S2.apply(ut).cpu().numpy()
+    assert rel(a2, a1) <= 1e-10
+
+
+def test_error_codes(torch_cuda):
+    from paper_2506_17406_b200 import rdr
+    c = make_config(0, n=1, p=2, space=HGRAD, bc="all")
+    bad = c.mask.copy()
+    # a mask bit on an interior face
+    from oracle.mesh import Topology
+    T = Topology(c.vertices, c.tets, np.zeros_like(c.mask))
+    t0 = 0
+    for i in range(4):
+        f = tuple(sorted(np.delete(c.tets[t0], i)))
+        fi = {tuple(x): k for k, x in enumerate(T.faces)}[f]
+        if not T.boundary_face[fi]:
+            bad[t0, i] = 1
+            break
+    with pytest.raises(rdr.RdrError) as e:
+        rdr.Solver(c.vertices, c.tets, 2, HGRAD, c.alpha, c.beta, bad)
+    assert e.value.code == -2
+    with pytest.raises(rdr.RdrError) as e:
+        rdr.Solver(c.vertices, c.tets, 2, HGRAD, -c.alpha, c.beta, c.mask)
+    assert e.value.code == -1
+    with pytest.raises(rdr.RdrError) as e:
+        rdr.Solver(c.vertices, c.tets, 13, HGRAD, c.alpha, c.beta, c.mask)
+    assert e.value.code == -1
+    v = c.vertices.copy()
+    v[c.tets[0, 1]] = v[c.tets[0, 0]]  # collapse an edge
+    with pytest.raises(rdr.RdrError) as e:
+        rdr.Solver(v, c.tets, 2, HGRAD, c.alpha, c.beta, c.mask)
+    assert e.value.code == -2
+    with pytest.raises(rdr.RdrError) as e:  # beta = 0: singular potential patches
+        rdr.Solver(c.vertices, c.tets, 2, HCURL, c.alpha, 0 * c.beta, np.zeros_like(c.mask))
+    assert e.value.code == -3
+
+
+def test_degenerate_sizes(torch_cuda):
+    """n=1 full Dirichlet at p=1: no free dof -> y = 0, z = 0, PCG 0 iterations;
+    p=12 H(grad) on one cube (largest supported element)."""
+    from paper_2506_17406_b200 import rdr
+    torch = torch_cuda
+    c = make_config(0, n=1, p=1, space=HGRAD, bc="all")
+    S = rdr.Solver(c.vertices, c.tets, 1, HGRAD, c.alpha, c.beta, c.mask)
+    b = torch.ones(S.n_total, dtype=torch.float64, device="cuda")
+    assert float(S.apply(b).abs().max()) == 0.0 and float(S.precond(b).abs().max()) == 0.0
+    x, it = S.solve(b)
+    assert it == 0 and float(x.abs().max()) == 0.0
+    c = make_config(0, n=1, p=12, space=HGRAD, bc="none")
+    S = rdr.Solver(c.vertices, c.tets, 12, HGRAD, c.alpha, c.beta, c.mask)
+    assert S.info["n_loc"] == 455

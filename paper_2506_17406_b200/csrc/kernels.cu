@@ -117,6 +117,122 @@ __global__ void __launch_bounds__(128) apply_kernel(DevOperator op, const double
   }
 }
 
+// ---------------------------------------------------------------- operator apply on FP64 tensor cores
+// Y[c][i] = sum_s sum_j (c_{c,s} X[c][j]) R_s[j][i]: one GEMM with M = cells,
+// N = n_loc, K = n_mat * n_loc, on DMMA (mma.sync.m8n8k4.f64 -> SASS DMMA.8x8x4;
+// sm_100a has no tcgen05 kind::f64). CTA = TM cells (TM/8 m-tiles),
+// 4 warps split the n8-tiles of N; the A fragment (X scaled by c_s in registers)
+// comes from shared memory, the B fragment (R_s, zero-padded [KP][LDN], L2/L1
+// resident and shared by all CTAs) straight from global memory.
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+template <int TM, int NTW>
+__global__ void __launch_bounds__(128) apply_dmma_kernel(DevOperator op, const double* __restrict__ x,
+                                                         double* __restrict__ y, double* pq_acc,
+                                                         const PcgScalars* guard) {
+  if (stopped(guard)) return;
+  constexpr int MT = TM / 8;
+  extern __shared__ double smem[];
+  const int n = op.n_loc, nm = op.n_mat, KP = op.kp, LDN = op.ldn;
+  double* X = smem;                              // [TM][KP], zero padded
+  double* C = X + TM * KP;                       // [TM][nm]
+  int* D = reinterpret_cast<int*>(C + TM * nm);  // [TM][n]
+  const int64_t c0 = (int64_t)blockIdx.x * TM;
+  const int64_t rem = op.n_cells - c0;
+  const int nc = rem < TM ? (int)rem : TM;
+  for (int k = threadIdx.x; k < TM * KP; k += blockDim.x) {
+    const int c = k / KP, j = k - c * KP;
+    int g = (c < nc && j < n) ? op.dofmap_m[(c0 + c) * n + j] : -1;
+    if (j < n) D[c * n + j] = g;
+    X[k] = (g >= 0) ? x[g] : 0.0;
+  }
+  for (int k = threadIdx.x; k < TM * nm; k += blockDim.x) {
+    const int c = k / nm;
+    C[k] = (c < nc) ? op.coef[(c0 + c) * nm + (k - c * nm)] : 0.0;
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int NT = LDN / 8;
+  double acc[MT][NTW][2];
+#pragma unroll
+  for (int m = 0; m < MT; ++m)
+#pragma unroll
+    for (int q = 0; q < NTW; ++q) acc[m][q][0] = acc[m][q][1] = 0.0;
+  int ncol[NTW];
+#pragma unroll
+  for (int q = 0; q < NTW; ++q) {
+    const int tile = warp + 4 * q;
+    ncol[q] = (tile < NT) ? tile * 8 + g : -1;
+  }
+  for (int s = 0; s < nm; ++s) {
+    double cs[MT];
+#pragma unroll
+    for (int m = 0; m < MT; ++m) cs[m] = C[(m * 8 + g) * nm + s];
+    const double* __restrict__ Rs = op.Rt + (size_t)s * KP * LDN;
+#pragma unroll 4
+    for (int k0 = 0; k0 < KP; k0 += 4) {
+      const int kk = k0 + t;
+      double b[NTW];
+#pragma unroll
+      for (int q = 0; q < NTW; ++q) b[q] = (ncol[q] >= 0) ? __ldg(Rs + (size_t)kk * LDN + ncol[q]) : 0.0;
+      double a[MT];
+#pragma unroll
+      for (int m = 0; m < MT; ++m) a[m] = cs[m] * X[(m * 8 + g) * KP + kk];
+#pragma unroll
+      for (int m = 0; m < MT; ++m)
+#pragma unroll
+        for (int q = 0; q < NTW; ++q)
+          if (warp + 4 * q < NT) dmma884(acc[m][q][0], acc[m][q][1], a[m], b[q]);
+    }
+  }
+  // epilogue: C fragment (row g, cols 2t, 2t+1) -> scatter-add, fused p.(Ap)
+  double pq = 0;
+#pragma unroll
+  for (int m = 0; m < MT; ++m)
+#pragma unroll
+    for (int q = 0; q < NTW; ++q) {
+      const int tile = warp + 4 * q;
+      if (tile >= NT) continue;
+      const int cell = m * 8 + g;
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int col = tile * 8 + 2 * t + i;
+        if (col < n && cell < nc) {
+          const int gd = D[cell * n + col];
+          if (gd >= 0) {
+            atomicAdd(y + gd, acc[m][q][i]);
+            pq = fma(X[cell * KP + col], acc[m][q][i], pq);
+          }
+        }
+      }
+    }
+  if (pq_acc) {
+    __shared__ double sh[32];
+    double sum = block_sum(pq, sh);
+    if (threadIdx.x == 0) atomicAdd(pq_acc, sum);
+  }
+}
+
+template <int TM, int NTW>
+cudaError_t launch_apply_dmma(const DevOperator& op, const double* x, double* y, double* pq_acc,
+                              const PcgScalars* guard, cudaStream_t s) {
+  size_t sm = (size_t)TM * op.kp * sizeof(double) + (size_t)TM * op.n_mat * sizeof(double) +
+              (size_t)TM * op.n_loc * sizeof(int);
+  static bool configured = false;  // first call happens in rdr_setup (outside stream capture)
+  if (!configured) {
+    cudaFuncSetAttribute(apply_dmma_kernel<TM, NTW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    configured = true;
+  }
+  unsigned grid = (unsigned)((op.n_cells + TM - 1) / TM);
+  apply_dmma_kernel<TM, NTW><<<grid, 128, sm, s>>>(op, x, y, pq_acc, guard);
+  return cudaGetLastError();
+}
+
 template <int TC>
 cudaError_t launch_apply_tc(const DevOperator& op, const double* x, double* y, double* pq_acc,
                             const PcgScalars* guard, cudaStream_t s) {
@@ -384,9 +500,32 @@ unsigned vec_grid(int64_t n) {
 
 cudaError_t launch_apply(const DevOperator& op, const double* x, double* y, double* pq_acc,
                          const PcgScalars* guard, cudaStream_t s) {
-  if (op.n_loc <= 64) return launch_apply_tc<16>(op, x, y, pq_acc, guard, s);
-  if (op.n_loc <= 400) return launch_apply_tc<8>(op, x, y, pq_acc, guard, s);
-  return launch_apply_tc<4>(op, x, y, pq_acc, guard, s);
+  if (!op.Rt) {  // CUDA-core reference kernel (RDR_KERNEL=simple)
+    if (op.n_loc <= 64) return launch_apply_tc<16>(op, x, y, pq_acc, guard, s);
+    if (op.n_loc <= 400) return launch_apply_tc<8>(op, x, y, pq_acc, guard, s);
+    return launch_apply_tc<4>(op, x, y, pq_acc, guard, s);
+  }
+  const int nt = (op.ldn / 8 + 3) / 4;  // n8-tiles per warp
+  const int64_t cells = op.n_cells;
+#define RDR_DMMA_CASE(NTW)                                                                     \
+  if (nt <= NTW) {                                                                             \
+    if (NTW <= 6 && cells >= 32 * 296) return launch_apply_dmma<32, NTW>(op, x, y, pq_acc, guard, s); \
+    if (NTW <= 12 && cells >= 16 * 296) return launch_apply_dmma<16, NTW>(op, x, y, pq_acc, guard, s); \
+    return launch_apply_dmma<8, NTW>(op, x, y, pq_acc, guard, s);                              \
+  }
+  RDR_DMMA_CASE(1)
+  RDR_DMMA_CASE(2)
+  RDR_DMMA_CASE(3)
+  RDR_DMMA_CASE(4)
+  RDR_DMMA_CASE(6)
+  RDR_DMMA_CASE(8)
+  RDR_DMMA_CASE(10)
+  RDR_DMMA_CASE(12)
+  RDR_DMMA_CASE(15)
+  RDR_DMMA_CASE(19)
+  RDR_DMMA_CASE(25)
+#undef RDR_DMMA_CASE
+  return cudaErrorInvalidValue;
 }
 
 int count_precond_launches(const DevPrecond& pc) {

@@ -29,6 +29,8 @@ struct DevOperator {
   const int32_t* dofmap_m;      // [n_cells][n_loc], -1 for constrained dofs
   const double* coef;           // [n_cells][n_mat]
   const double* R;              // [n_mat][n_loc][n_pad]
+  int kp, ldn;                  // n_loc rounded up to 4 (K) and to 8 (N)
+  const double* Rt;             // [n_mat][kp][ldn] zero-padded copy for the DMMA kernel (NULL: CUDA-core kernel)
 };
 
 struct DevPrecond {

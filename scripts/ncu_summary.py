@@ -1,0 +1,62 @@
+"""Summarise ncu outputs brought back in gpurun_out/ into profiles/ (tracked).
+
+    python scripts/ncu_summary.py launches gpurun_out/launches_r1.csv > profiles/r1_launches.txt
+    python scripts/ncu_summary.py full gpurun_out/prof_patch_r1.ncu-rep > profiles/r1_patch_kernel.txt
+"""
+import collections
+import csv
+import io
+import subprocess
+import sys
+
+KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+        "launch__registers_per_thread", "launch__occupancy_limit_registers", "launch__grid_size",
+        "launch__block_size", "sm__warps_active.avg.pct_of_peak_sustained_active",
+        "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
+        "smsp__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
+        "sm__pipe_tensor_op_dmma_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_tensor_op_dmma.avg.pct_of_peak_sustained_active",
+        "lts__t_bytes.sum", "l1tex__t_bytes.sum", "sm__cycles_elapsed.avg.per_second",
+        "dram__cycles_elapsed.avg.per_second", "smsp__average_warp_latency_issue_stalled"]
+
+
+def launches(path):
+    rows = list(csv.reader(open(path)))
+    hdr = None
+    data = collections.defaultdict(list)
+    for r in rows:
+        if "Kernel Name" in r:
+            hdr = r
+            continue
+        if hdr and len(r) == len(hdr):
+            d = dict(zip(hdr, r))
+            if d.get("Metric Name") == "gpu__time_duration.sum":
+                name = d["Kernel Name"].split("(")[0].split("<")[0].split("::")[-1]
+                unit = d.get("Metric Unit", "ns")
+                v = float(d["Metric Value"].replace(",", ""))
+                v *= {"ns": 1e-3, "us": 1.0, "usecond": 1.0, "nsecond": 1e-3, "ms": 1e3, "msecond": 1e3}.get(unit, 1e-3)
+                data[name].append(v)
+    tot = sum(sum(v) for v in data.values())
+    print(f"# ncu launch list {path} (cold-cache, serialised: compare shares, not absolutes)")
+    print(f"{'kernel':28s} {'launches':>8s} {'mean_us':>9s} {'share':>7s}")
+    for k, v in sorted(data.items(), key=lambda kv: -sum(kv[1])):
+        print(f"{k:28s} {len(v):8d} {sum(v) / len(v):9.2f} {100 * sum(v) / tot:6.1f}%")
+
+
+def full(path):
+    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    h, units = rows[0], rows[1]
+    print(f"# ncu --set full summary of {path}")
+    for r in rows[2:]:
+        name = r[h.index("Kernel Name")] if "Kernel Name" in h else "?"
+        print(f"## {name[:120]}")
+        for i, k in enumerate(h):
+            if any(k.startswith(w) for w in KEYS):
+                print(f"{k:75s} {r[i]:>16s} {units[i]}")
+
+
+if __name__ == "__main__":
+    {"launches": launches, "full": full}[sys.argv[1]](sys.argv[2])

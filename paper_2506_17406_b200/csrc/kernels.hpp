@@ -20,7 +20,10 @@ struct PcgScalars {
   int32_t done;
   int32_t converged;
   uint32_t ticket;  // last-block counter of the reduction kernel
-  int32_t pad;
+  int32_t k;        // fused path: iteration index of the next fused apply
+  double rz_acc;    // fused path: r.z accumulated by the preconditioner
+  double rz_old;    // fused path: r.z of the z used by the current direction
+  double pq2[2];    // fused path: p.Ap, double-buffered by iteration parity
 };
 
 struct DevOperator {
@@ -31,6 +34,7 @@ struct DevOperator {
   const double* R;              // [n_mat][n_loc][n_pad]
   int kp, ldn;                  // n_loc rounded up to 4 (K) and to 8 (N)
   const double* Rt;             // [n_mat][kp][ldn] zero-padded copy for the DMMA kernel (NULL: CUDA-core kernel)
+  const uint8_t* owner;         // [n_cells][n_loc] 1 at the first (cell, local) occurrence of each free dof
 };
 
 struct DevPrecond {
@@ -71,6 +75,14 @@ cudaError_t launch_pcg_update(PcgScalars* sc, const double* p, const double* q, 
                               cudaStream_t s);
 cudaError_t launch_pcg_finish(PcgScalars* sc, const double* z, int64_t n, cudaStream_t s);
 cudaError_t launch_pcg_direction(PcgScalars* sc, const double* z, double* p, double* q, int64_t n, cudaStream_t s);
+
+// Fused PCG step (3 kernels per iteration for H(grad)): fused apply (direction
+// update + A p + ||z||^2 + stopping test), update + interior Jacobi, patches.
+bool fused_pcg_supported(const DevOperator& op);
+cudaError_t launch_pcg_fused_apply(const DevOperator& op, PcgScalars* sc, const double* z, double* p0, double* p1,
+                                   double* q, cudaStream_t s);
+cudaError_t launch_pcg_update_jacobi(PcgScalars* sc, const DevPrecond& pc, const double* p0, const double* p1,
+                                     double* q, double* x, double* r, double* z, cudaStream_t s);
 
 int count_precond_launches(const DevPrecond& pc);  // kernels per rdr_precond
 void configure_kernels();                            // shared-memory opt-ins (call once, outside capture)

@@ -84,6 +84,8 @@ struct rdr_handle {
   std::vector<void*> owned;
   uint8_t* d_cons = nullptr;
   double *d_x = nullptr, *d_r = nullptr, *d_z = nullptr, *d_p = nullptr, *d_q = nullptr, *d_b = nullptr;
+  double* d_p2 = nullptr;  // second search-direction buffer of the fused path
+  bool fused = false;
   PcgScalars* d_sc = nullptr;
   PcgScalars* h_sc = nullptr;  // pinned
   cudaStream_t cap_stream = nullptr;
@@ -172,6 +174,19 @@ static int setup_impl(rdr_handle* h, const double* vertices, int64_t nv, const i
     op.Rt = d_Rt;
   }
   if ((st = h->own_upload(&h->d_cons, num.constrained))) return st;
+  {  // owner flags: first (cell, local) occurrence of every free dof (fused PCG reductions)
+    std::vector<uint8_t> owner((size_t)nt * el.n, 0), seen(num.n_total, 0);
+    for (size_t k = 0; k < owner.size(); ++k) {
+      const int32_t g = num.dofmap[k];
+      if (!num.constrained[g] && !seen[g]) {
+        seen[g] = 1;
+        owner[k] = 1;
+      }
+    }
+    uint8_t* d_owner;
+    if ((st = h->own_upload(&d_owner, owner))) return st;
+    op.owner = d_owner;
+  }
 
   // ---- preconditioner
   DevPrecond& pc = h->pc;
@@ -234,12 +249,13 @@ static int setup_impl(rdr_handle* h, const double* vertices, int64_t nv, const i
 
   // ---- PCG workspace
   const size_t vb = sizeof(double) * std::max<int64_t>(1, num.n_total);
-  for (double** v : {&h->d_x, &h->d_r, &h->d_z, &h->d_p, &h->d_q, &h->d_b})
+  for (double** v : {&h->d_x, &h->d_r, &h->d_z, &h->d_p, &h->d_q, &h->d_b, &h->d_p2})
     if ((st = h->own_alloc((void**)v, vb))) return st;
+  h->fused = fused_pcg_supported(op);
   if ((st = h->own_alloc((void**)&h->d_sc, sizeof(PcgScalars)))) return st;
   CK(cudaMallocHost((void**)&h->h_sc, sizeof(PcgScalars)));
   CK(cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
-  h->launches_per_iter = 4 + count_precond_launches(pc);
+  h->launches_per_iter = h->fused ? 1 + count_precond_launches(pc) : 4 + count_precond_launches(pc);
   // one warm-up apply/precond on zero vectors: kernel attributes get configured
   // here, outside any later stream capture
   CK(cudaMemset(h->d_p, 0, vb));
@@ -324,6 +340,13 @@ int rdr_precond(rdr_handle* h, const double* r, double* z, void* stream) {
 
 static int enqueue_iteration(rdr_handle* h, cudaStream_t s) {
   const int64_t n = h->n_total;
+  if (h->fused) {  // 3 kernels (+2 for the H(curl) discrete gradient) per PCG iteration
+    CK(launch_pcg_fused_apply(h->op, h->d_sc, h->d_z, h->d_p, h->d_p2, h->d_q, s));
+    CK(launch_pcg_update_jacobi(h->d_sc, h->pc, h->d_p, h->d_p2, h->d_q, h->d_x, h->d_r, h->d_z, s));
+    for (int part = 1; part < 4; ++part)
+      CK(launch_precond_part(part, h->pc, h->d_r, h->d_z, &h->d_sc->rz_acc, h->d_sc, s));
+    return RDR_OK;
+  }
   CK(launch_apply(h->op, h->d_p, h->d_q, &h->d_sc->pq, h->d_sc, s));
   CK(launch_pcg_update(h->d_sc, h->d_p, h->d_q, h->d_x, h->d_r, n, s));
   CK(launch_precond(h->pc, h->d_r, h->d_z, &h->d_sc->rz_new, h->d_sc, s));
@@ -353,17 +376,37 @@ static int solve_device(rdr_handle* h, const double* b, double rtol, int maxit, 
   int st;
   if ((st = build_graph(h, 8))) return st;
   int64_t launches = 0;
-  CK(cudaMemsetAsync(h->d_sc, 0, sizeof(PcgScalars), s));
-  CK(launch_pcg_init(b, h->d_cons, n, h->d_x, h->d_r, h->d_q, s));
-  CK(launch_precond(h->pc, h->d_r, h->d_z, &h->d_sc->rz_new, nullptr, s));
-  CK(launch_pcg_start(h->d_sc, h->d_z, h->d_p, n, rtol, maxit, s));
-  launches += 2 + count_precond_launches(h->pc);
-  for (;;) {
-    CK(cudaMemcpyAsync(h->h_sc, h->d_sc, sizeof(PcgScalars), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    if (h->h_sc->done) break;
-    CK(cudaGraphLaunch(h->graph, s));
-    launches += (int64_t)h->graph_iters * h->launches_per_iter;
+  if (h->fused) {
+    CK(cudaStreamSynchronize(s));  // h_sc (pinned) is reused as the H2D template
+    std::memset(h->h_sc, 0, sizeof(PcgScalars));
+    h->h_sc->rtol = rtol;
+    h->h_sc->maxit = maxit;
+    CK(cudaMemcpyAsync(h->d_sc, h->h_sc, sizeof(PcgScalars), cudaMemcpyHostToDevice, s));
+    CK(cudaMemsetAsync(h->d_p, 0, sizeof(double) * n, s));
+    CK(cudaMemsetAsync(h->d_p2, 0, sizeof(double) * n, s));
+    CK(launch_pcg_init(b, h->d_cons, n, h->d_x, h->d_r, h->d_q, s));
+    CK(launch_precond(h->pc, h->d_r, h->d_z, &h->d_sc->rz_acc, nullptr, s));
+    launches += 1 + count_precond_launches(h->pc);
+    for (;;) {  // the fused apply of each iteration performs the stopping test
+      CK(cudaGraphLaunch(h->graph, s));
+      launches += (int64_t)h->graph_iters * h->launches_per_iter;
+      CK(cudaMemcpyAsync(h->h_sc, h->d_sc, sizeof(PcgScalars), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      if (h->h_sc->done) break;
+    }
+  } else {
+    CK(cudaMemsetAsync(h->d_sc, 0, sizeof(PcgScalars), s));
+    CK(launch_pcg_init(b, h->d_cons, n, h->d_x, h->d_r, h->d_q, s));
+    CK(launch_precond(h->pc, h->d_r, h->d_z, &h->d_sc->rz_new, nullptr, s));
+    CK(launch_pcg_start(h->d_sc, h->d_z, h->d_p, n, rtol, maxit, s));
+    launches += 2 + count_precond_launches(h->pc);
+    for (;;) {
+      CK(cudaMemcpyAsync(h->h_sc, h->d_sc, sizeof(PcgScalars), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      if (h->h_sc->done) break;
+      CK(cudaGraphLaunch(h->graph, s));
+      launches += (int64_t)h->graph_iters * h->launches_per_iter;
+    }
   }
   h->last_launches = launches;
   *iters = h->h_sc->iters;

@@ -474,7 +474,8 @@ int build_patches(const Mesh& m, const Numbering& num, const RefElement& el, con
     P.n[k] = n;
     P.kind[k] = (uint8_t)d.numbering;
     P.idx_off[k + 1] = P.idx_off[k] + (int64_t)nb * 32;
-    P.tile_off[k + 1] = P.tile_off[k] + (int64_t)nb * (nb + 1) / 2 * 1024;
+    (void)nb;
+    P.tile_off[k + 1] = P.tile_off[k] + patch_stored_doubles(n);
     P.max_n = std::max(P.max_n, n);
     P.alg_bytes += 8.0 * n * (n + 1) / 2;
   }
@@ -533,22 +534,24 @@ int build_patches(const Mesh& m, const Numbering& num, const RefElement& el, con
         W1.resize((size_t)n * n);
         W2.resize((size_t)n * n);
         chol_inverse(A.data(), n, W1.data(), W2.data());
-        // pack lower tiles: tile (I,J), I >= J, t = I(I+1)/2 + J; element (i,k) at ((k>>2)*32 + i)*4 + (k&3)
-        const int nbk = (n + 31) / 32;
+        // exact packed lower triangle in 32-row block rows (see patch_layout)
         double* out = buf.data() + (P.tile_off[k] - base);
-        for (int I = 0; I < nbk; ++I)
+        const int nbk = (n + 31) / 32;
+        for (int I = 0; I < nbk; ++I) {
+          const int rows = std::min(32, n - 32 * I);
           for (int J = 0; J <= I; ++J) {
-            double* tile = out + ((size_t)I * (I + 1) / 2 + J) * 1024;
-            for (int i = 0; i < 32; ++i) {
-              int r = I * 32 + i;
-              if (r >= n) continue;
-              for (int kk = 0; kk < 32; ++kk) {
-                int cc = J * 32 + kk;
-                if (cc >= n) continue;
-                tile[((kk >> 2) * 32 + i) * 4 + (kk & 3)] = W2[(size_t)r * n + cc];
-              }
+            double* tile = out + patch_tile_offset(n, I, J);
+            if (J < I) {  // full-width tile, `rows` rows: (i,k) at ((k>>2)*rows + i)*4 + (k&3)
+              for (int i = 0; i < rows; ++i)
+                for (int kk = 0; kk < 32; ++kk)
+                  tile[((kk >> 2) * rows + i) * 4 + (kk & 3)] = W2[(size_t)(I * 32 + i) * n + J * 32 + kk];
+            } else {      // diagonal: packed lower triangle by columns, (i,k), k<=i at k*rows - k(k-1)/2 + (i-k)
+              for (int kk = 0; kk < rows; ++kk)
+                for (int i = kk; i < rows; ++i)
+                  tile[kk * rows - kk * (kk - 1) / 2 + (i - kk)] = W2[(size_t)(I * 32 + i) * n + I * 32 + kk];
             }
           }
+        }
       }
     }
     if (status) break;

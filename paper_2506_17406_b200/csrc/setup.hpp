@@ -49,6 +49,25 @@ struct Patches {
   double alg_bytes = 0;              // 8 sum n(n+1)/2
 };
 
+// Stored layout of one patch inverse A_m^{-1} (n x n, symmetric): the lower
+// triangle in 32-row block rows I = 0..nb-1 (rows = min(32, n - 32 I)); block
+// row I holds I full-width tiles J < I ((i,k) at ((k>>2)*rows + i)*4 + (k&3),
+// i.e. 32-byte groups of 4 consecutive columns, one group per row and lane)
+// followed by the diagonal tile packed by columns ((i,k), k <= i, at
+// k*rows - k(k-1)/2 + (i-k)). Exactly n(n+1)/2 doubles, padded to 16.
+inline int64_t patch_block_row_start(int n, int I) {
+  (void)n;
+  return 512LL * I * I + 16LL * I;  // sum_{I'<I} (1024 I' + 528), all earlier rows are full
+}
+inline int64_t patch_tile_offset(int n, int I, int J) {
+  const int rows = (n - 32 * I) < 32 ? (n - 32 * I) : 32;
+  return patch_block_row_start(n, I) + (int64_t)J * 32 * rows;
+}
+inline int64_t patch_stored_doubles(int n) {
+  const int64_t exact = (int64_t)n * (n + 1) / 2;
+  return (exact + 15) / 16 * 16;
+}
+
 // Builds the patch index sets (R-A13), assembles and inverts each patch
 // matrix (R-A15), and hands the packed tiles to `sink(first_patch, last_patch,
 // host_tiles)` in chunks so that the full inverse store never lives on the host.

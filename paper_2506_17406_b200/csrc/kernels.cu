@@ -126,173 +126,114 @@ __global__ void __launch_bounds__(128) apply_kernel(DevOperator op, const double
 }
 
 // ---------------------------------------------------------------- operator apply on FP64 tensor cores
-// Y[c][i] = sum_s sum_j (c_{c,s} X[c][j]) R_s[j][i]: one GEMM with M = cells,
-// N = n_loc, K = n_mat * n_loc, on DMMA (mma.sync.m8n8k4.f64 -> SASS DMMA.8x8x4;
-// sm_100a has no tcgen05 kind::f64). CTA = TM cells (TM/8 m-tiles),
-// 4 warps split the n8-tiles of N; the A fragment (X scaled by c_s in registers)
-// comes from shared memory, the B fragment (R_s, zero-padded [KP][LDN], L2/L1
-// resident and shared by all CTAs) straight from global memory.
+// Y[c][i] = sum_s c_{c,s} sum_j X[c][j] R_s[j][i]: one GEMM with M = cells,
+// N = n_loc, K = n_mat * kp (the stacked reference matrices), on DMMA
+// (mma.sync.m8n8k4.f64 -> SASS DMMA.8x8x4; sm_100a has no tcgen05 kind::f64,
+// SURVEY F1/F2).
+//
+// CTA = BM cells x one 32-column group of N. The CTA's B operand (the group's
+// K x 32 slice of the stack, stored swizzled in HBM/L2) streams through an
+// 8-slot shared-memory ring by cp.async.bulk (TMA bulk copies) completing on
+// mbarriers; a dedicated producer warp refills slots as consumers release them.
+// Consumer warps own 16 cells x 32 columns (2 x 4 DMMA tiles, 16 FP64
+// accumulators per lane: every A fragment is reused 4x and every B fragment
+// 2x from registers) and split K in KS groups (chunk c -> group c % KS); the
+// groups' partial sums are reduced through shared memory. A = c_s X is scaled
+// in registers (c_s changes every kp/4 k-steps). The gathered X tile (BM x kp)
+// stays in shared memory for the whole K loop; the epilogue scatter-adds with
+// red.global.add.f64 and accumulates p.(Ap) (or, in PCG mode, runs the fused
+// direction update and stopping test).
 __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
                : "+d"(c0), "+d"(c1)
                : "d"(a), "d"(b));
 }
 
-__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
-  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(gmem_src));
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
+__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      " .reg .pred P;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+      " @!P bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// TMA bulk copy global -> shared (bytes % 16 == 0, both addresses 16-byte aligned)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
 
-// smem row strides chosen so a warp's 8x4 fragment reads hit each bank pair at most twice
+constexpr int kApplyKC = 16;     // K rows per ring slot (16 x 32 doubles = 4 KB)
+constexpr int kApplySlots = 8;   // ring depth
+constexpr int kApplyCols = 32;   // N columns per CTA (4 n8-tiles)
+constexpr int kApplyWarps = 8;   // consumer warps (+1 producer warp)
+
+// smem row stride of X: == 4 (mod 16) doubles, so a warp's 8x4 A-fragment read is conflict-free
 __host__ __device__ __forceinline__ int apply_x_stride(int kp) { return kp + ((4 - kp % 16) + 16) % 16; }
-__host__ __device__ __forceinline__ int apply_b_stride(int ncol) { return ncol + 8; }
 
-constexpr int kApplyKC = 16;      // K rows per pipeline stage
-constexpr int kApplyStages = 3;   // cp.async ring depth
-
-template <int TM, int NTW>
-__global__ void __launch_bounds__(128) apply_dmma_kernel(DevOperator op, const double* __restrict__ x,
-                                                         double* __restrict__ y, double* pq_acc,
-                                                         const PcgScalars* guard) {
-  if (stopped(guard)) return;
-  constexpr int MT = TM / 8;
-  constexpr int NCOL = 32 * NTW;  // columns of this CTA's group: 4 warps x NTW n8-tiles
-  extern __shared__ double smem[];
-  const int n = op.n_loc, nm = op.n_mat, KP = op.kp, LDN = op.ldn;
-  const int XS = apply_x_stride(KP), BS = apply_b_stride(NCOL);
-  double* Bs = smem;                               // [stages][KC][BS]
-  double* X = Bs + kApplyStages * kApplyKC * BS;   // [TM][XS], zero padded
-  double* C = X + TM * XS;                         // [TM][nm]
-  int* D = reinterpret_cast<int*>(C + TM * nm);    // [TM][n]
-  const int col0 = blockIdx.y * NCOL;
-  const int ncols = min(NCOL, LDN - col0);         // multiple of 8
-  const int ktot = nm * KP;                        // rows of the concatenated [R_0; ...; R_{nm-1}]
-  const int nchunks = (ktot + kApplyKC - 1) / kApplyKC;
-  const double* __restrict__ Rcat = op.Rt;
-
-  auto issue = [&](int c) {
-    if (c < nchunks) {
-      double* dst = Bs + (c % kApplyStages) * kApplyKC * BS;
-      const int pieces_per_row = ncols / 2;  // 16-byte pieces
-      for (int p = threadIdx.x; p < kApplyKC * pieces_per_row; p += blockDim.x) {
-        const int r = p / pieces_per_row, q = p - r * pieces_per_row;
-        const int krow = c * kApplyKC + r;
-        if (krow < ktot) cp_async16(dst + r * BS + 2 * q, Rcat + (size_t)krow * LDN + col0 + 2 * q);
-      }
-    }
-    cp_async_commit();
-  };
-  issue(0);
-  issue(1);
-
-  const int64_t c0 = (int64_t)blockIdx.x * TM;
-  const int64_t rem = op.n_cells - c0;
-  const int nc = rem < TM ? (int)rem : TM;
-  for (int k = threadIdx.x; k < TM * XS; k += blockDim.x) {
-    const int c = k / XS, j = k - c * XS;
-    const int gd = (c < nc && j < n) ? op.dofmap_m[(c0 + c) * n + j] : -1;
-    if (j < n) D[c * n + j] = gd;
-    X[k] = (gd >= 0) ? x[gd] : 0.0;
-  }
-  for (int k = threadIdx.x; k < TM * nm; k += blockDim.x) {
-    const int c = k / nm;
-    C[k] = (c < nc) ? op.coef[(c0 + c) * nm + (k - c * nm)] : 0.0;
-  }
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int g = lane >> 2, t = lane & 3;
-  double acc[MT][NTW][2];
-#pragma unroll
-  for (int m = 0; m < MT; ++m)
-#pragma unroll
-    for (int q = 0; q < NTW; ++q) acc[m][q][0] = acc[m][q][1] = 0.0;
-  bool live[NTW];
-#pragma unroll
-  for (int q = 0; q < NTW; ++q) live[q] = (warp + 4 * q) * 8 < ncols;
-
-  for (int c = 0; c < nchunks; ++c) {
-    cp_async_wait<kApplyStages - 2>();
-    __syncthreads();  // chunk c landed for everyone; slot (c+2)%3 is free again
-    issue(c + kApplyStages - 1);
-    const double* Bc = Bs + (c % kApplyStages) * kApplyKC * BS;
-#pragma unroll
-    for (int k4 = 0; k4 < kApplyKC / 4; ++k4) {
-      const int kg = c * kApplyKC + k4 * 4;  // first K row of this k-step (KP is a multiple of 4)
-      if (kg >= ktot) break;
-      const int s = kg / KP, j = kg - s * KP + t;
-      double a[MT];
-#pragma unroll
-      for (int m = 0; m < MT; ++m) a[m] = C[(m * 8 + g) * nm + s] * X[(m * 8 + g) * XS + j];
-      double b[NTW];
-#pragma unroll
-      for (int q = 0; q < NTW; ++q) b[q] = Bc[(k4 * 4 + t) * BS + (warp + 4 * q) * 8 + g];
-#pragma unroll
-      for (int m = 0; m < MT; ++m)
-#pragma unroll
-        for (int q = 0; q < NTW; ++q)
-          if (live[q]) dmma884(acc[m][q][0], acc[m][q][1], a[m], b[q]);
-    }
-  }
-  cp_async_wait<0>();
-
-  // epilogue: C fragment (row g, cols 2t, 2t+1) -> scatter-add, fused p.(Ap)
-  double pq = 0;
-#pragma unroll
-  for (int m = 0; m < MT; ++m)
-#pragma unroll
-    for (int q = 0; q < NTW; ++q) {
-      if (!live[q]) continue;
-      const int cell = m * 8 + g;
-#pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const int col = col0 + (warp + 4 * q) * 8 + 2 * t + i;
-        if (col < n && cell < nc) {
-          const int gd = D[cell * n + col];
-          if (gd >= 0) {
-            atomicAdd(y + gd, acc[m][q][i]);
-            pq = fma(X[cell * XS + col], acc[m][q][i], pq);
-          }
-        }
-      }
-    }
-  if (pq_acc) {
-    __shared__ double sh[32];
-    double sum = block_sum(pq, sh);
-    if (threadIdx.x == 0) atomicAdd(pq_acc, sum);
-  }
+template <int BM>
+__host__ __device__ __forceinline__ size_t apply_smem_bytes(int kp, int nm) {
+  return sizeof(uint64_t) * 2 * kApplySlots + sizeof(double) * kApplySlots * kApplyKC * kApplyCols +
+         sizeof(double) * (size_t)BM * apply_x_stride(kp) + sizeof(double) * (size_t)BM * nm +
+         sizeof(int) * (size_t)BM * kApplyCols;
 }
 
-// B-stationary variant for n_mat * n_loc * 8 columns that fit in shared memory:
-// a CTA owns NTC n8-tiles (8*NTC output columns) and keeps the matching slice
-// of the stacked reference matrices [R_0; ...; R_{nm-1}] resident in smem for
-// its whole range of cells; each warp loops over m-tiles of 8 cells: gather x
-// (8 x n), K-loop of DMMA.8x8x4 with A = c_s X (scaled in registers) and B from
-// the resident slice, scatter-add. R is read from L2 once per CTA.
-constexpr int kBstStride = 8;  // smem row stride (doubles) of the B slice: 4 K rows x 8 cols -> 2 wavefronts
-__host__ __device__ __forceinline__ int bst_x_stride(int kp) { return kp + ((4 - kp % 16) + 16) % 16; }
-
-// B-stationary apply: a CTA owns one n8-tile (8 output columns) and keeps the
-// matching K x 8 slice of the stacked reference matrices [R_0; ...; R_{nm-1}]
-// resident in shared memory for its whole range of cells (R read from L2 once
-// per CTA). Per m-tile of 8 cells: cooperative gather of x (8 x n), split-K
-// DMMA.8x8x4 over the 4 warps (A = c_s X scaled in registers, B from the
-// resident slice), cross-warp reduction in smem, scatter-add.
-//
-// PCG mode (fused PCG step): the gathered vector is the new search
-// direction p_k = z_k + beta_k p_{k-1} (beta_k = (r_k.z_k)/(r_{k-1}.z_{k-1}),
-// beta_0 = 0), written once per dof by its owner cell; ||z_k||^2 (owners) and
-// p_k.A p_k are reduced, and the last CTA applies the stopping test of R-A16 to
-// z_k and advances the iteration counter.
-template <bool PCG>
-__global__ void __launch_bounds__(128) apply_bst_kernel(DevOperator op, const double* __restrict__ x,
-                                                        double* __restrict__ y, double* pq_acc,
-                                                        const PcgScalars* guard, int cells_per_cta,
-                                                        PcgScalars* sc, double* pbuf0, double* pbuf1) {
+template <int BM, bool PCG>
+__global__ void __launch_bounds__((kApplyWarps + 1) * 32, 2)
+    apply_tc_kernel(DevOperator op, const double* __restrict__ x, double* __restrict__ y, double* pq_acc,
+                    const PcgScalars* guard, PcgScalars* sc, double* pbuf0, double* pbuf1) {
   if (stopped(guard)) return;
-  extern __shared__ double smem[];
+  constexpr int MW = BM / 16;             // warps along M (16 cells each)
+  constexpr int KS = kApplyWarps / MW;    // K-split groups
+  static_assert(MW * KS == kApplyWarps && kApplySlots % KS == 0, "warp layout");
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
+  uint64_t* empty = full + kApplySlots;
+  double* ring = reinterpret_cast<double*>(empty + kApplySlots);      // [slots][KC][32] swizzled
+  const int n = op.n_loc, nm = op.n_mat, kp = op.kp;
+  const int XS = apply_x_stride(kp);
+  double* X = ring + kApplySlots * kApplyKC * kApplyCols;              // [BM][XS]
+  double* C = X + BM * XS;                                             // [BM][nm]
+  int* D = reinterpret_cast<int*>(C + BM * nm);                        // [BM][32] dofs of this CTA's columns
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int cg = blockIdx.y, col0 = cg * kApplyCols;
+  const int nchunks = op.kpad / kApplyKC;
+  const double* __restrict__ Bg = op.Bsw + (size_t)cg * op.kpad * kApplyCols;
+  constexpr uint32_t kChunkBytes = kApplyKC * kApplyCols * sizeof(double);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kApplySlots; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], MW);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  const bool producer = warp == kApplyWarps;
+  if (producer && lane == 0) {  // fill the ring while everyone gathers
+    for (int c = 0; c < nchunks && c < kApplySlots; ++c) {
+      mbar_expect_tx(&full[c], kChunkBytes);
+      bulk_g2s(ring + c * kApplyKC * kApplyCols, Bg + (size_t)c * kApplyKC * kApplyCols, kChunkBytes, &full[c]);
+    }
+  }
+
+  // ---- PCG mode: direction update p_k = z_k + beta_k p_{k-1} folded into the gather
   double beta = 0.0;
   const double* p_old = nullptr;
   double* p_new = nullptr;
@@ -305,113 +246,153 @@ __global__ void __launch_bounds__(128) apply_bst_kernel(DevOperator op, const do
     p_new = (kit & 1) ? pbuf1 : pbuf0;
   }
   double zz = 0.0;
-  const int n = op.n_loc, nm = op.n_mat, KP = op.kp, LDN = op.ldn;
-  const int XS = bst_x_stride(KP);
-  const int ktot = nm * KP;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int g = lane >> 2, t = lane & 3;
-  double* Bst = smem;                              // [ktot][8]
-  double* X = Bst + (size_t)ktot * kBstStride;     // [8][XS]
-  double* C = X + 8 * XS;                          // [8][nm]
-  double* red = C + 8 * nm;                        // [4 warps][32 lanes][2]
-  int* D = reinterpret_cast<int*>(red + 4 * 64);   // [8][8] dofs of this CTA's columns
-  const int col0 = blockIdx.y * 8;
-  for (int e = threadIdx.x; e < ktot * 4; e += blockDim.x) {
-    const int k = e >> 2, c2 = e & 3;
-    const double2 v = __ldg(reinterpret_cast<const double2*>(op.Rt + (size_t)k * LDN + col0 + 2 * c2));
-    Bst[k * kBstStride + 2 * c2] = v.x;
-    Bst[k * kBstStride + 2 * c2 + 1] = v.y;
-  }
-  // split-K: warp w owns k-steps [ks0, ks1) of the ktot/4 steps
-  const int nsteps = ktot / 4;
-  const int ks0 = (warp * nsteps) / 4, ks1 = ((warp + 1) * nsteps) / 4;
-  const int64_t cbeg = (int64_t)blockIdx.x * cells_per_cta;
-  const int64_t cend = min((int64_t)op.n_cells, cbeg + cells_per_cta);
-  double pq = 0;
-  for (int64_t cb = cbeg; cb < cend; cb += 8) {
-    const int nc = (int)min((int64_t)8, cend - cb);
-    __syncthreads();  // previous m-tile fully consumed (and the B slice loaded)
-    // gather in batches of 8 elements per thread: all dof-map loads, then all
-    // vector loads, then the smem stores (8 independent loads in flight per thread)
+
+  // ---- gather X (BM x XS, zero padded), coefficients and this CTA's dof columns
+  const int64_t c0 = (int64_t)blockIdx.x * BM;
+  const int nc = (int)min((int64_t)BM, op.n_cells - c0);
+  {
     constexpr int GB = 8;
-    for (int e0 = 0; e0 < 8 * XS; e0 += GB * 128) {
-      int gd[GB], cc[GB], jj[GB];
+    const int nthr = blockDim.x;
+    for (int e0 = 0; e0 < BM * XS; e0 += GB * nthr) {
+      int gd[GB];
 #pragma unroll
       for (int i = 0; i < GB; ++i) {
-        const int e = e0 + i * 128 + threadIdx.x;
+        const int e = e0 + i * nthr + threadIdx.x;
         const int c = e / XS, j = e - c * XS;
-        cc[i] = c;
-        jj[i] = j;
-        gd[i] = (e < 8 * XS && c < nc && j < n) ? op.dofmap_m[(cb + c) * n + j] : -1;
+        gd[i] = (e < BM * XS && c < nc && j < n) ? op.dofmap_m[(c0 + c) * n + j] : -1;
       }
-      double val[GB], zv[GB];
+      double xv[GB], pv[GB];
 #pragma unroll
       for (int i = 0; i < GB; ++i) {
-        zv[i] = gd[i] >= 0 ? x[gd[i]] : 0.0;
-        val[i] = (PCG && gd[i] >= 0) ? p_old[gd[i]] : 0.0;
+        xv[i] = gd[i] >= 0 ? x[gd[i]] : 0.0;
+        pv[i] = (PCG && gd[i] >= 0) ? p_old[gd[i]] : 0.0;
       }
 #pragma unroll
       for (int i = 0; i < GB; ++i) {
-        const int e = e0 + i * 128 + threadIdx.x;
-        if (e >= 8 * XS) continue;
-        double v = zv[i];
+        const int e = e0 + i * nthr + threadIdx.x;
+        if (e >= BM * XS) continue;
+        const int c = e / XS, j = e - c * XS;
+        double v = xv[i];
         if (PCG && gd[i] >= 0) {
-          v = fma(beta, val[i], zv[i]);
-          if (blockIdx.y == 0 && op.owner[(cb + cc[i]) * n + jj[i]]) {
+          v = fma(beta, pv[i], xv[i]);
+          if (cg == 0 && op.owner[(c0 + c) * n + j]) {
             p_new[gd[i]] = v;
-            zz = fma(zv[i], zv[i], zz);
+            zz = fma(xv[i], xv[i], zz);
           }
         }
         X[e] = v;
-        const int j = jj[i];
-        if (j >= col0 && j < col0 + 8) D[cc[i] * 8 + (j - col0)] = (j < n) ? gd[i] : -1;
+        if (j >= col0 && j < col0 + kApplyCols) D[c * kApplyCols + (j - col0)] = (j < n) ? gd[i] : -1;
       }
     }
-    for (int e = threadIdx.x; e < 8 * nm; e += blockDim.x) {
+    for (int e = threadIdx.x; e < BM * nm; e += nthr) {
       const int c = e / nm;
-      C[e] = (c < nc) ? op.coef[(cb + c) * nm + (e - c * nm)] : 0.0;
+      C[e] = (c < nc) ? op.coef[(c0 + c) * nm + (e - c * nm)] : 0.0;
     }
-    __syncthreads();
-    // two independent accumulator chains (even / odd k-steps) hide the DMMA latency
-    double c0 = 0.0, c1 = 0.0, d0 = 0.0, d1 = 0.0;
-    int s = (ks0 * 4) / KP, j = ks0 * 4 - s * KP;
-    double cs = C[g * nm + s];
-    const double* xr = X + g * XS + t;
-    const double* br = Bst + (size_t)(ks0 * 4 + t) * kBstStride + g;
-    auto advance = [&]() {
-      br += 4 * kBstStride;
-      j += 4;
-      if (j >= KP) {
-        j = 0;
-        ++s;
-        cs = (s < nm) ? C[g * nm + s] : 0.0;
-      }
-    };
-    int ks = ks0;
-#pragma unroll 2
-    for (; ks + 1 < ks1; ks += 2) {
-      dmma884(c0, c1, cs * xr[j], *br);
-      advance();
-      dmma884(d0, d1, cs * xr[j], *br);
-      advance();
-    }
-    if (ks < ks1) dmma884(c0, c1, cs * xr[j], *br);
-    red[(warp * 32 + lane) * 2] = c0 + d0;
-    red[(warp * 32 + lane) * 2 + 1] = c1 + d1;
-    __syncthreads();
-    if (warp == 0) {
+    // columns past n_loc (n not a multiple of 32): never written by the loop above
+    for (int e = threadIdx.x; e < BM * kApplyCols; e += nthr)
+      if (col0 + (e % kApplyCols) >= n) D[e] = -1;
+  }
+  __syncthreads();
+
+  const int g = lane >> 2, t = lane & 3;
+  const int mw = warp % MW, kg = warp / MW;
+  double acc[2][4][2];
 #pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        double v = red[lane * 2 + i] + red[(32 + lane) * 2 + i] + red[(64 + lane) * 2 + i] + red[(96 + lane) * 2 + i];
-        const int col = 2 * t + i;  // row g = cell, column col0 + col
-        const int gd = (g < nc && col0 + col < n) ? D[g * 8 + col] : -1;
-        if (gd >= 0) {
-          atomicAdd(y + gd, v);
-          pq = fma(X[g * XS + col0 + col], v, pq);
+  for (int m = 0; m < 2; ++m)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[m][q][0] = acc[m][q][1] = 0.0;
+
+  if (producer) {
+    if (lane == 0) {
+      for (int c = kApplySlots; c < nchunks; ++c) {
+        const int slot = c % kApplySlots;
+        mbar_wait(&empty[slot], ((c / kApplySlots) - 1) & 1);
+        mbar_expect_tx(&full[slot], kChunkBytes);
+        bulk_g2s(ring + slot * kApplyKC * kApplyCols, Bg + (size_t)c * kApplyKC * kApplyCols, kChunkBytes,
+                 &full[slot]);
+      }
+    }
+  } else {
+    // per-lane B offsets inside a 4-row k-step: (k, col) stored at k*32 + (col ^ ((k & 3) << 2))
+    int boff[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) boff[q] = t * kApplyCols + ((q * 8 + g) ^ (t << 2));
+    const double* xr0 = X + (mw * 16 + g) * XS + t;
+    const double* xr1 = xr0 + 8 * XS;
+    const double* cr0 = C + (mw * 16 + g) * nm;
+    const double* cr1 = cr0 + 8 * nm;
+    for (int c = kg; c < nchunks; c += KS) {
+      const int slot = c % kApplySlots;
+      mbar_wait(&full[slot], (c / kApplySlots) & 1);
+      const double* Bs = ring + slot * kApplyKC * kApplyCols;
+      int krow = c * kApplyKC;
+      int s = krow / kp, j = krow - s * kp;
+      double cs0 = s < nm ? cr0[s] : 0.0, cs1 = s < nm ? cr1[s] : 0.0;
+#pragma unroll
+      for (int k4 = 0; k4 < kApplyKC / 4; ++k4) {
+        const double a0 = cs0 * xr0[j], a1 = cs1 * xr1[j];
+        double b[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) b[q] = Bs[k4 * 4 * kApplyCols + boff[q]];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          dmma884(acc[0][q][0], acc[0][q][1], a0, b[q]);
+          dmma884(acc[1][q][0], acc[1][q][1], a1, b[q]);
+        }
+        j += 4;
+        if (j >= kp) {
+          j = 0;
+          ++s;
+          cs0 = s < nm ? cr0[s] : 0.0;
+          cs1 = s < nm ? cr1[s] : 0.0;
         }
       }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[slot]);
     }
   }
+  __syncthreads();  // every chunk consumed (all bulk copies complete): the ring is free
+
+  // ---- K-split reduction through the ring, then scatter-add from group 0
+  double* red = ring;  // [(KS-1)][MW][16][32]
+  if (!producer && kg > 0) {
+    double* dst = red + (((kg - 1) * MW + mw) * 16) * 32 + lane;
+#pragma unroll
+    for (int m = 0; m < 2; ++m)
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int i = 0; i < 2; ++i) dst[((m * 4 + q) * 2 + i) * 32] = acc[m][q][i];
+  }
+  __syncthreads();
+  double pq = 0.0;
+  if (!producer && kg == 0) {
+    for (int h = 1; h < KS; ++h) {
+      const double* src = red + (((h - 1) * MW + mw) * 16) * 32 + lane;
+#pragma unroll
+      for (int m = 0; m < 2; ++m)
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+          for (int i = 0; i < 2; ++i) acc[m][q][i] += src[((m * 4 + q) * 2 + i) * 32];
+    }
+#pragma unroll
+    for (int m = 0; m < 2; ++m) {
+      const int row = mw * 16 + m * 8 + g;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int cl = q * 8 + 2 * t + i;
+          const int gd = D[row * kApplyCols + cl];
+          if (gd >= 0) {
+            atomicAdd(y + gd, acc[m][q][i]);
+            pq = fma(X[row * XS + col0 + cl], acc[m][q][i], pq);
+          }
+        }
+    }
+  }
+
   if (PCG) {
     __shared__ double sh[32];
     __shared__ bool last;
@@ -456,55 +437,48 @@ __global__ void __launch_bounds__(128) apply_bst_kernel(DevOperator op, const do
     }
   } else if (pq_acc) {
     __shared__ double sh[32];
-    double sum = block_sum(pq, sh);
+    const double sum = block_sum(pq, sh);
     if (threadIdx.x == 0) atomicAdd(pq_acc, sum);
   }
 }
 
-size_t bst_smem_bytes(const DevOperator& op) {
-  return sizeof(double) * ((size_t)op.n_mat * op.kp * kBstStride + 8 * (size_t)bst_x_stride(op.kp) + 8 * op.n_mat + 256) +
-         sizeof(int) * 64;
+constexpr size_t kMaxSmem = 226 * 1024;  // 227 KB opt-in minus the static reduction scratch
+
+size_t apply_smem(int bm, const DevOperator& op) {
+  return bm == 64 ? apply_smem_bytes<64>(op.kp, op.n_mat)
+                  : bm == 32 ? apply_smem_bytes<32>(op.kp, op.n_mat) : apply_smem_bytes<16>(op.kp, op.n_mat);
+}
+
+// cells per CTA: the largest of 64/32/16 whose tile fits in shared memory and
+// still gives two CTAs per SM (else one), so small meshes fill the 148 SMs
+int apply_bm(const DevOperator& op) {
+  for (int want : {2 * 148, 148})
+    for (int bm : {64, 32})
+      if (apply_smem(bm, op) <= kMaxSmem && (op.n_cells + bm - 1) / bm * op.ngroups >= want) return bm;
+  return apply_smem(32, op) <= kMaxSmem ? 32 : 16;
+}
+
+template <int BM, bool PCG>
+cudaError_t launch_apply_tc_bm(const DevOperator& op, const double* x, double* y, double* pq_acc,
+                               const PcgScalars* guard, cudaStream_t s, PcgScalars* sc, double* p0, double* p1) {
+  const size_t sm = apply_smem_bytes<BM>(op.kp, op.n_mat);
+  dim3 grid((unsigned)((op.n_cells + BM - 1) / BM), (unsigned)op.ngroups);
+  apply_tc_kernel<BM, PCG><<<grid, (kApplyWarps + 1) * 32, sm, s>>>(op, x, y, pq_acc, guard, sc, p0, p1);
+  return cudaGetLastError();
 }
 
 template <bool PCG>
-cudaError_t launch_apply_bst(const DevOperator& op, const double* x, double* y, double* pq_acc,
-                             const PcgScalars* guard, cudaStream_t s, PcgScalars* sc = nullptr,
-                             double* pbuf0 = nullptr, double* pbuf1 = nullptr) {
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(apply_bst_kernel<PCG>, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 * 1024);
-    configured = true;
-  }
-  const size_t sm = bst_smem_bytes(op);
-  const int groups = op.ldn / 8;
-  const int per_sm = (int)std::min<size_t>(4, (220 * 1024) / (sm + 1024));
-  int64_t gx = (148 * std::max(1, per_sm) + groups - 1) / groups;
-  int64_t cpc = (op.n_cells + gx - 1) / gx;
-  cpc = (cpc + 7) / 8 * 8;
-  gx = (op.n_cells + cpc - 1) / cpc;
-  dim3 grid((unsigned)gx, (unsigned)groups);
-  apply_bst_kernel<PCG><<<grid, 128, sm, s>>>(op, x, y, pq_acc, guard, (int)cpc, sc, pbuf0, pbuf1);
-  return cudaGetLastError();
-}
-template <int TM, int NTW>
-cudaError_t launch_apply_dmma(const DevOperator& op, const double* x, double* y, double* pq_acc,
-                              const PcgScalars* guard, cudaStream_t s) {
-  const int ncol = 32 * NTW;
-  size_t sm = sizeof(double) * ((size_t)kApplyStages * kApplyKC * apply_b_stride(ncol) +
-                                (size_t)TM * apply_x_stride(op.kp) + (size_t)TM * op.n_mat) +
-              sizeof(int) * (size_t)TM * op.n_loc;
-  static bool configured = false;  // first call happens in rdr_setup (outside stream capture)
-  if (!configured) {
-    cudaFuncSetAttribute(apply_dmma_kernel<TM, NTW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    configured = true;
-  }
-  dim3 grid((unsigned)((op.n_cells + TM - 1) / TM), (unsigned)((op.ldn + ncol - 1) / ncol));
-  apply_dmma_kernel<TM, NTW><<<grid, 128, sm, s>>>(op, x, y, pq_acc, guard);
-  return cudaGetLastError();
+cudaError_t launch_apply_tc(const DevOperator& op, const double* x, double* y, double* pq_acc,
+                            const PcgScalars* guard, cudaStream_t s, PcgScalars* sc = nullptr,
+                            double* p0 = nullptr, double* p1 = nullptr) {
+  const int bm = apply_bm(op);
+  if (bm == 64) return launch_apply_tc_bm<64, PCG>(op, x, y, pq_acc, guard, s, sc, p0, p1);
+  if (bm == 32) return launch_apply_tc_bm<32, PCG>(op, x, y, pq_acc, guard, s, sc, p0, p1);
+  return launch_apply_tc_bm<16, PCG>(op, x, y, pq_acc, guard, s, sc, p0, p1);
 }
 
 template <int TC>
-cudaError_t launch_apply_tc(const DevOperator& op, const double* x, double* y, double* pq_acc,
+cudaError_t launch_apply_simple(const DevOperator& op, const double* x, double* y, double* pq_acc,
                             const PcgScalars* guard, cudaStream_t s) {
   size_t sm = (size_t)TC * op.n_loc * (sizeof(double) + sizeof(int)) + (size_t)TC * op.n_mat * sizeof(double);
   static bool configured = false;
@@ -821,28 +795,12 @@ unsigned vec_grid(int64_t n) {
 
 cudaError_t launch_apply(const DevOperator& op, const double* x, double* y, double* pq_acc,
                          const PcgScalars* guard, cudaStream_t s) {
-  if (!op.Rt) {  // CUDA-core reference kernel (RDR_KERNEL=simple)
-    if (op.n_loc <= 64) return launch_apply_tc<16>(op, x, y, pq_acc, guard, s);
-    if (op.n_loc <= 400) return launch_apply_tc<8>(op, x, y, pq_acc, guard, s);
-    return launch_apply_tc<4>(op, x, y, pq_acc, guard, s);
+  if (!op.Bsw) {  // CUDA-core reference kernel (RDR_KERNEL=simple)
+    if (op.n_loc <= 64) return launch_apply_simple<16>(op, x, y, pq_acc, guard, s);
+    if (op.n_loc <= 400) return launch_apply_simple<8>(op, x, y, pq_acc, guard, s);
+    return launch_apply_simple<4>(op, x, y, pq_acc, guard, s);
   }
-  // B-stationary kernel when the stacked reference-matrix slice fits in shared memory
-  static const bool force_stream = std::getenv("RDR_APPLY_STREAM") != nullptr;
-  if (bst_smem_bytes(op) <= 220 * 1024 && !force_stream) return launch_apply_bst<false>(op, x, y, pq_acc, guard, s);
-  // n8-tiles per warp (column groups of 4*NTW tiles go to gridDim.y); cells per CTA
-  // chosen so the grid covers the 148 SMs about twice
-  const int per_warp = (op.ldn / 8 + 3) / 4;
-  const int ntw = per_warp <= 1 ? 1 : per_warp <= 2 ? 2 : per_warp <= 3 ? 3 : 4;
-  const int64_t groups = (op.ldn / 8 + 4 * ntw - 1) / (4 * ntw);
-  const int64_t ctas32 = (op.n_cells + 31) / 32 * groups, ctas16 = (op.n_cells + 15) / 16 * groups;
-  const int tm = ctas32 >= 296 ? 32 : (ctas16 >= 296 ? 16 : 8);
-#define RDR_DMMA_CASE(TM, NTW) \
-  if (tm == TM && ntw == NTW) return launch_apply_dmma<TM, NTW>(op, x, y, pq_acc, guard, s);
-  RDR_DMMA_CASE(8, 1) RDR_DMMA_CASE(8, 2) RDR_DMMA_CASE(8, 3) RDR_DMMA_CASE(8, 4)
-  RDR_DMMA_CASE(16, 1) RDR_DMMA_CASE(16, 2) RDR_DMMA_CASE(16, 3) RDR_DMMA_CASE(16, 4)
-  RDR_DMMA_CASE(32, 1) RDR_DMMA_CASE(32, 2) RDR_DMMA_CASE(32, 3) RDR_DMMA_CASE(32, 4)
-#undef RDR_DMMA_CASE
-  return cudaErrorInvalidValue;
+  return launch_apply_tc<false>(op, x, y, pq_acc, guard, s);
 }
 
 int count_precond_launches(const DevPrecond& pc) {
@@ -906,13 +864,13 @@ cudaError_t launch_pcg_direction(PcgScalars* sc, const double* z, double* p, dou
 }
 
 bool fused_pcg_supported(const DevOperator& op) {
-  static const bool off = std::getenv("RDR_PCG_UNFUSED") != nullptr || std::getenv("RDR_APPLY_STREAM") != nullptr;
-  return op.Rt && op.owner && !off && bst_smem_bytes(op) <= 220 * 1024;
+  static const bool off = std::getenv("RDR_PCG_UNFUSED") != nullptr;
+  return op.Bsw && op.owner && !off;
 }
 
 cudaError_t launch_pcg_fused_apply(const DevOperator& op, PcgScalars* sc, const double* z, double* p0, double* p1,
                                    double* q, cudaStream_t s) {
-  return launch_apply_bst<true>(op, z, q, nullptr, sc, s, sc, p0, p1);
+  return launch_apply_tc<true>(op, z, q, nullptr, sc, s, sc, p0, p1);
 }
 
 cudaError_t launch_pcg_update_jacobi(PcgScalars* sc, const DevPrecond& pc, const double* p0, const double* p1,
@@ -924,10 +882,17 @@ cudaError_t launch_pcg_update_jacobi(PcgScalars* sc, const DevPrecond& pc, const
 }  // namespace rdr
 
 namespace rdr {
-void configure_kernels() {
+void configure_kernels() {  // errors here would surface as a later launch's cudaGetLastError
   cudaFuncSetAttribute(apply_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(apply_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(apply_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(patch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  cudaFuncSetAttribute(apply_tc_kernel<64, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
+  cudaFuncSetAttribute(apply_tc_kernel<64, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
+  cudaFuncSetAttribute(apply_tc_kernel<32, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
+  cudaFuncSetAttribute(apply_tc_kernel<32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
+  cudaFuncSetAttribute(apply_tc_kernel<16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
+  cudaFuncSetAttribute(apply_tc_kernel<16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
+  cudaGetLastError();
 }
 }  // namespace rdr

@@ -32,8 +32,11 @@ struct DevOperator {
   const int32_t* dofmap_m;      // [n_cells][n_loc], -1 for constrained dofs
   const double* coef;           // [n_cells][n_mat]
   const double* R;              // [n_mat][n_loc][n_pad]
-  int kp, ldn;                  // n_loc rounded up to 4 (K) and to 8 (N)
-  const double* Rt;             // [n_mat][kp][ldn] zero-padded copy for the DMMA kernel (NULL: CUDA-core kernel)
+  int kp;                       // n_loc rounded up to 4: rows per reference matrix in the K stack
+  int kpad;                     // n_mat * kp rounded up to 16 (K rows of the stack)
+  int ngroups;                  // ceil(n_loc / 32) column groups
+  const double* Bsw;            // [ngroups][kpad][32] stacked reference matrices, swizzled (kernels.cu
+                                // apply_tc_kernel); NULL selects the CUDA-core kernel (RDR_KERNEL=simple)
   const uint8_t* owner;         // [n_cells][n_loc] 1 at the first (cell, local) occurrence of each free dof
 };
 

@@ -25,10 +25,13 @@ int cuda_status(cudaError_t e) {
   return RDR_ECUDA;
 }
 
-#define CK(call)                              \
-  do {                                        \
-    cudaError_t e_ = (call);                  \
-    if (e_ != cudaSuccess) return cuda_status(e_); \
+#define CK(call)                                                                              \
+  do {                                                                                        \
+    cudaError_t e_ = (call);                                                                  \
+    if (e_ != cudaSuccess) {                                                                  \
+      std::fprintf(stderr, "rdr: %s (%s:%d)\n", cudaGetErrorString(e_), __FILE__, __LINE__); \
+      return cuda_status(e_);                                                                 \
+    }                                                                                         \
   } while (0)
 
 template <class T>
@@ -160,18 +163,28 @@ static int setup_impl(rdr_handle* h, const double* vertices, int64_t nv, const i
   op.coef = d_coef;
   op.R = d_R;
   op.kp = (el.n + 3) / 4 * 4;
-  op.ldn = (el.n + 7) / 8 * 8;
-  op.Rt = nullptr;
+  op.kpad = (el.n_mat * op.kp + 15) / 16 * 16;
+  op.ngroups = (el.n + 31) / 32;
+  op.Bsw = nullptr;
   const char* kern = std::getenv("RDR_KERNEL");
   if (!(kern && std::strcmp(kern, "simple") == 0)) {
-    std::vector<double> Rt((size_t)el.n_mat * op.kp * op.ldn, 0.0);
-    for (int s = 0; s < el.n_mat; ++s)
-      for (int i = 0; i < el.n; ++i)
-        for (int j = 0; j < el.n; ++j)
-          Rt[((size_t)s * op.kp + i) * op.ldn + j] = el.R[((size_t)s * el.n + i) * el.n + j];
-    double* d_Rt;
-    if ((st = h->own_upload(&d_Rt, Rt))) return st;
-    op.Rt = d_Rt;
+    // stacked reference matrices [R_0; ...; R_{nm-1}] (kp rows each), split in
+    // 32-column groups, element (k, col) of a group at k*32 + (col ^ ((k & 3) << 2))
+    // (the shared-memory swizzle of apply_tc_kernel's B fragments)
+    std::vector<double> B((size_t)op.ngroups * op.kpad * 32, 0.0);
+    for (int g = 0; g < op.ngroups; ++g)
+      for (int k = 0; k < el.n_mat * op.kp; ++k) {
+        const int s = k / op.kp, j = k % op.kp;
+        if (j >= el.n) continue;
+        for (int c = 0; c < 32; ++c) {
+          const int col = 32 * g + c;
+          if (col >= el.n) continue;
+          B[((size_t)g * op.kpad + k) * 32 + (c ^ ((k & 3) << 2))] = el.R[((size_t)s * el.n + j) * el.n + col];
+        }
+      }
+    double* d_B;
+    if ((st = h->own_upload(&d_B, B))) return st;
+    op.Bsw = d_B;
   }
   if ((st = h->own_upload(&h->d_cons, num.constrained))) return st;
   {  // owner flags: first (cell, local) occurrence of every free dof (fused PCG reductions)

@@ -1,10 +1,12 @@
 // sm_100a kernels of the Riesz-map PCG hot path.
 //
-//  * apply_kernel      : gather x_e -> y_e = sum_s c_{e,s} R_s x_e -> scatter-add
+//  * apply_tc_kernel   : gather x_e -> y_e = sum_s c_{e,s} R_s x_e on DMMA -> scatter-add
 //                        (north_star operator apply; matrix-free action P:2267-2275)
+//  * apply_kernel      : the same on CUDA cores (RDR_KERNEL=simple, parity bring-up)
 //  * precond_init      : interior point-Jacobi z_I = r_I / A_II (Thm 5.1)
-//  * patch_kernel      : additive star patches z += E_m A_m^{-1} E_m^T r with the
-//                        stored packed inverses streamed from HBM (Eq. 5.4 / 5.12)
+//  * patch_stream_kernel: additive star patches z += E_m A_m^{-1} E_m^T r with the
+//                        stored packed inverses streamed from HBM by TMA bulk
+//                        copies (Eq. 5.4 / 5.12)
 //  * gather_grad / scatter_grad : the discrete gradient of the H(curl) potential
 //                        patches (R-A12, Lemma 4.3)
 //  * pcg_*             : fused PCG vector updates and reductions (R-A16)
@@ -45,21 +47,6 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
   }
   __syncthreads();
   return s;
-}
-
-// 32-byte streaming load (sm_100: LDG.E.NA.EFL2.256): no L1 allocation, L2 evict-first
-__device__ __forceinline__ double4 ld_stream4(const double4* p) {
-  double4 v;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v4.f64 {%0, %1, %2, %3}, [%4];"
-               : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w)
-               : "l"(p));
-  return v;
-}
-
-__device__ __forceinline__ double ld_stream1(const double* p) {
-  double v;
-  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
-  return v;
 }
 
 // ---------------------------------------------------------------- operator apply
@@ -536,26 +523,331 @@ __global__ void scatter_grad_kernel(DevPrecond pc, double* __restrict__ z, const
   }
 }
 
-// Sum over the 32 lanes of v[lane'][k], delivered to lane k (recursive halving, 31 shuffles).
-template <int S>
-__device__ __forceinline__ void transpose_reduce_stage(double (&v)[32], int lane) {
-  const bool upper = (lane & S) != 0;
-#pragma unroll
-  for (int k = 0; k < S; ++k) {
-    double send = upper ? v[k] : v[k + S];
-    double keep = upper ? v[k + S] : v[k];
-    v[k] = keep + __shfl_xor_sync(0xffffffffu, send, S);
+// Persistent star-patch kernel (Eq. 5.4 P:1763-1774 / Eq. 5.12 P:1956-1970 with
+// exact local solvers, R-A15): z += E_m A_m^{-1} E_m^T r for every patch m.
+// The packed lower tiles of A_m^{-1} (setup.hpp patch layout) are the only
+// HBM stream of the kernel. A CTA owns a list of patches (LPT schedule from
+// setup, sched_off/sched_ids); its tile sequence (patch by patch, tiles in
+// order I(I+1)/2 + J) is dealt round-robin to the 8 warps. Every warp streams
+// its own tiles with cp.async.bulk (TMA) into its own K-slot ring, each slot
+// completing on an mbarrier, issuing tile j+K as soon as tile j is consumed:
+// no producer warp and no cross-warp slot hand-off, so a slow warp never
+// stalls the stream of another. For an off-diagonal tile (I,J) lane l forms
+// the row product sum_k A[l][k] r_J[k] (-> z_I) and the column product
+// sum_i A[i][l] r_I[i] (-> z_J) straight from the swizzled tile in shared
+// memory, without shuffles or atomics: each warp accumulates into a private
+// copy of the patch's z (double-buffered by patch parity when it fits). At a
+// patch boundary (CTA barrier) the copies are summed and scatter-added to
+// global memory and the r buffer is refilled with r of the patch two ahead.
+constexpr int kPatchWarps = 8;
+
+struct PatchView {
+  int n, nb, kind;
+  int64_t idx_off, tile_off;
+};
+__device__ __forceinline__ PatchView patch_view(const DevPrecond& pc, int pid) {
+  PatchView v;
+  v.n = pc.pn[pid];
+  v.nb = (v.n + 31) >> 5;
+  v.kind = pc.pkind[pid];
+  v.idx_off = pc.idx_off[pid];
+  v.tile_off = pc.tile_off[pid];
+  return v;
+}
+
+// gather r of patch `pid` into rb (npad entries, zero padded)
+__device__ __forceinline__ void patch_gather(const DevPrecond& pc, int pid, const double* __restrict__ r,
+                                             double* rb) {
+  if (pid < 0) return;
+  const PatchView v = patch_view(pc, pid);
+  const double* __restrict__ rin = v.kind ? pc.gbuf : r;
+  const int32_t* id = pc.idx + v.idx_off;
+  const int npad = v.nb * 32;
+  for (int i = threadIdx.x; i < npad; i += kPatchWarps * 32) {
+    const int gi = id[i];
+    rb[i] = gi >= 0 ? rin[gi] : 0.0;
   }
 }
 
-// One CTA per patch (patches sorted by decreasing size). The packed lower
-// tiles of A_m^{-1} (32x32, element (i,k) at ((k>>2)*32+i)*4+(k&3)) are
-// streamed once with 32-byte non-allocating loads; a warp owns a tile: row
-// products go to z_I, the transposed products (off-diagonal tiles) to z_J.
-constexpr int kPatchThreads = 256;
-__global__ void __launch_bounds__(kPatchThreads) patch_kernel(DevPrecond pc, const double* __restrict__ r,
-                                                             double* __restrict__ z, double* rz_acc,
-                                                             const PcgScalars* guard) {
+// Dynamic patch queue: CTAs claim patches (sorted by decreasing size at setup,
+// so the claim order is longest-first) from a global counter. The j-th patch
+// a CTA processes is recorded in a 64-entry shared ring so that the warps'
+// tile cursors, which run ahead independently, agree on it.
+constexpr int kClaimRing = 64;
+constexpr int kUnclaimed = -2, kClaiming = -1, kQueueEnd = -3;
+
+__device__ __forceinline__ int get_patch(const DevPrecond& pc, int* claim, int j) {
+  volatile int* c = claim + (j & (kClaimRing - 1));
+  int v = *c;
+  if (v == kUnclaimed) {
+    if ((threadIdx.x & 31) == 0 && atomicCAS(claim + (j & (kClaimRing - 1)), kUnclaimed, kClaiming) == kUnclaimed) {
+      const int pid = atomicAdd(pc.queue, 1);
+      *c = pid < pc.n_patches ? pid : kQueueEnd;
+    }
+    __syncwarp();
+    do {
+      v = *c;
+    } while (v == kUnclaimed || v == kClaiming);
+  } else {
+    while (v == kClaiming) v = *c;
+  }
+  return v == kQueueEnd ? -1 : v;
+}
+
+// A warp's cursor over its tiles t = w, w+8, ... of the CTA's tile sequence.
+struct TileCursor {
+  int k, pid, I, J;  // sequence index of the patch (pid < 0: past the end), tile (I, J)
+  PatchView v;
+  __device__ __forceinline__ void settle(const DevPrecond& pc, int* claim) {
+    // normalise (I, J) in tile order, moving on to later patches as needed
+    while (pid >= 0) {
+      while (J > I) {
+        J -= I + 1;
+        ++I;
+      }
+      if (I < v.nb) return;
+      const int over = J + I * (I + 1) / 2 - v.nb * (v.nb + 1) / 2;  // tiles past the end of the patch
+      pid = get_patch(pc, claim, ++k);
+      if (pid >= 0) v = patch_view(pc, pid);
+      I = 0;
+      J = over;
+    }
+  }
+  __device__ __forceinline__ bool valid() const { return pid >= 0; }
+};
+
+__device__ __forceinline__ void issue_tile(const DevPrecond& pc, const TileCursor& c, double* dst, uint64_t* bar) {
+  const int rows = min(32, c.v.n - 32 * c.I);
+  const double* src = pc.tiles + c.v.tile_off + 512LL * c.I * c.I + 16LL * c.I + (int64_t)c.J * 32 * rows;
+  // full tile rows*32 doubles; diagonal rows(rows+1)/2 rounded up to 2 (16 bytes)
+  const uint32_t nd = c.J < c.I ? 32u * rows : (uint32_t)((rows * (rows + 1) / 2 + 1) & ~1);
+  mbar_expect_tx(bar, nd * 8u);
+  bulk_g2s(dst, src, nd * 8u, bar);
+}
+
+__global__ void __launch_bounds__(kPatchWarps * 32, 2)
+    patch_stream_kernel(DevPrecond pc, const double* __restrict__ r, double* __restrict__ z, double* rz_acc,
+                        const PcgScalars* guard) {
+  if (stopped(guard)) return;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int K = pc.ring_slots / kPatchWarps;  // slots per warp
+  const int NP = pc.npad_max;
+  const int ZB = pc.zbufs;                    // private z copies per warp (1 or 2)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw) + warp * K;
+  double* ring = reinterpret_cast<double*>(smem_raw + 8 * pc.ring_slots) + (size_t)warp * K * 1024;  // [K][1024]
+  double* rbuf = reinterpret_cast<double*>(smem_raw + 8 * pc.ring_slots) + (size_t)pc.ring_slots * 1024;  // [2][NP]
+  double* zw = rbuf + 2 * NP;                                            // [ZB][8 warps][NP]
+  __shared__ int claim[kClaimRing];
+  for (int i = threadIdx.x; i < kClaimRing; i += blockDim.x) claim[i] = kUnclaimed;
+  if (lane == 0) {
+    for (int s = 0; s < K; ++s) mbar_init(&full[s], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  // consumer cursor and prefetch cursor start at this warp's first tile
+  TileCursor cur;
+  cur.k = 0;
+  cur.pid = get_patch(pc, claim, 0);
+  if (cur.pid >= 0) cur.v = patch_view(pc, cur.pid);
+  cur.I = 0;
+  cur.J = warp;
+  cur.settle(pc, claim);
+  TileCursor pre = cur;
+  for (int s = 0; s < K && pre.valid(); ++s) {
+    if (lane == 0) issue_tile(pc, pre, ring + (size_t)s * 1024, &full[s]);
+    pre.J += kPatchWarps;
+    pre.settle(pc, claim);
+  }
+
+  for (int i = threadIdx.x; i < ZB * kPatchWarps * NP; i += kPatchWarps * 32) zw[i] = 0.0;
+  patch_gather(pc, get_patch(pc, claim, 0), r, rbuf);
+  patch_gather(pc, get_patch(pc, claim, 1), r, rbuf + NP);
+  __syncthreads();
+  double part = 0.0;
+  int slot = 0;
+  uint32_t phase = 0;
+  for (int k = 0;; ++k) {
+    const int pid = get_patch(pc, claim, k);
+    if (pid < 0) break;
+    const PatchView v = patch_view(pc, pid);
+    double* rl = rbuf + (k & 1) * NP;
+    double* zmine = zw + ((size_t)(ZB == 2 ? (k & 1) : 0) * kPatchWarps + warp) * NP;
+    while (cur.valid() && cur.k == k) {
+      const int I = cur.I, J = cur.J;
+      mbar_wait(&full[slot], phase);
+      const double* tb = ring + (size_t)slot * 1024;
+      const int rows = min(32, v.n - 32 * I);
+      const double* rI = rl + I * 32;
+      double acc_i, acc_j = 0.0;
+      if (J < I) {
+        // row product (lane = row l): chunk c of row l at l*32 + 2*(c ^ (l&7));
+        // column product (lane = column l): (i, l) at i*32 + 2*((l>>1) ^ (i&7)) + (l&1)
+        const double2* rJ2 = reinterpret_cast<const double2*>(rl + J * 32);
+        const double2* trow = reinterpret_cast<const double2*>(tb + lane * 32);
+        const double* tcol = tb + (lane & 1);
+        double ar[4] = {0.0, 0.0, 0.0, 0.0}, ac[4] = {0.0, 0.0, 0.0, 0.0};
+        if (lane < rows) {
+#pragma unroll
+          for (int c = 0; c < 16; ++c) {
+            const double2 a = trow[c ^ (lane & 7)];
+            const double2 x = rJ2[c];
+            ar[c & 3] = fma(a.x, x.x, ar[c & 3]);
+            ar[c & 3] = fma(a.y, x.y, ar[c & 3]);
+          }
+        }
+        if (rows == 32) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            ac[i & 3] = fma(tcol[i * 32 + 2 * ((lane >> 1) ^ (i & 7))], rI[i], ac[i & 3]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (i < rows) ac[i & 3] = fma(tcol[i * 32 + 2 * ((lane >> 1) ^ (i & 7))], rI[i], ac[i & 3]);
+        }
+        acc_i = (ar[0] + ar[1]) + (ar[2] + ar[3]);
+        acc_j = (ac[0] + ac[1]) + (ac[2] + ac[3]);
+      } else {
+        // diagonal tile, lower triangle packed by columns: (i,q), q <= i at q*rows - q(q-1)/2 + i - q;
+        // lane l: sum_{q<=l} L(l,q) r_q + sum_{q>l} L(q,l) r_q
+        double ad[4] = {0.0, 0.0, 0.0, 0.0};
+        if (lane < rows) {
+          const int colbase = lane * rows - lane * (lane - 1) / 2 - lane;  // L(q,l) at colbase + q
+#pragma unroll
+          for (int q = 0; q < 32; ++q) {
+            if (q < rows) {
+              const int off = q <= lane ? q * rows - q * (q - 1) / 2 + (lane - q) : colbase + q;
+              ad[q & 3] = fma(tb[off], rI[q], ad[q & 3]);
+            }
+          }
+        }
+        acc_i = (ad[0] + ad[1]) + (ad[2] + ad[3]);
+      }
+      // slot consumed: refill it with this warp's tile K ahead (generic reads
+      // ordered before the async-proxy write by the fence)
+      __syncwarp();
+      if (pre.valid()) {
+        if (lane == 0) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          issue_tile(pc, pre, ring + (size_t)slot * 1024, &full[slot]);
+        }
+        pre.J += kPatchWarps;
+        pre.settle(pc, claim);
+      }
+      if (++slot == K) {
+        slot = 0;
+        phase ^= 1u;
+      }
+      zmine[I * 32 + lane] += acc_i;
+      if (J < I) zmine[J * 32 + lane] += acc_j;
+      cur.J += kPatchWarps;
+      cur.settle(pc, claim);
+    }
+    __syncthreads();  // every warp's z copy of patch k complete
+    // sum the copies, scatter-add z of patch k, r.z partial, refill this r
+    // buffer with r of patch k+2 (a thread refills exactly the entries it read)
+    {
+      double* __restrict__ zout = v.kind ? pc.ubuf : z;
+      const int32_t* id = pc.idx + v.idx_off;
+      const double* zk = zw + (size_t)(ZB == 2 ? (k & 1) : 0) * kPatchWarps * NP;
+      for (int i = threadIdx.x; i < v.n; i += kPatchWarps * 32) {
+        double zi = 0.0;
+#pragma unroll
+        for (int w = 0; w < kPatchWarps; ++w) zi += zk[(size_t)w * NP + i];
+        atomicAdd(zout + id[i], zi);
+        part = fma(rl[i], zi, part);
+      }
+      patch_gather(pc, get_patch(pc, claim, k + 2), r, rl);
+      // every warp is past patch k-1: its claim entry can be reused (the
+      // cursors run at most a few patches ahead, far less than the ring)
+      if (threadIdx.x == 0 && k >= 1) claim[(k - 1) & (kClaimRing - 1)] = kUnclaimed;
+    }
+    if (ZB == 2) {
+      // patch k+1 accumulates into the copies of parity (k+1)&1, last summed at
+      // boundary k-1, i.e. before the barrier above: each warp clears its own
+      {
+        double* znext = zw + ((size_t)((k + 1) & 1) * kPatchWarps + warp) * NP;
+        for (int i = lane; i < NP; i += 32) znext[i] = 0.0;
+        __syncwarp();
+      }
+    } else {
+      __syncthreads();  // every copy summed before it is cleared
+      double* zmine0 = zw + (size_t)warp * NP;
+      for (int i = lane; i < NP; i += 32) zmine0[i] = 0.0;
+      __syncwarp();
+    }
+  }
+  __shared__ double sh[kPatchWarps];
+  part = warp_sum(part);
+  if (lane == 0) sh[warp] = part;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (rz_acc) {
+      double s = 0;
+      for (int w = 0; w < kPatchWarps; ++w) s += sh[w];
+      atomicAdd(rz_acc, s);
+    }
+    // the last CTA out resets the queue for the next launch
+    __threadfence();
+    if (atomicAdd(pc.queue + 1, 1) == (int)gridDim.x - 1) {
+      pc.queue[0] = 0;
+      pc.queue[1] = 0;
+      __threadfence();
+    }
+  }
+}
+
+size_t patch_smem_bytes(int slots, int npad_max, int zbufs) {
+  return sizeof(uint64_t) * slots +
+         sizeof(double) * ((size_t)slots * 1024 + (2 + (size_t)zbufs * kPatchWarps) * (size_t)npad_max);
+}
+
+// Direct-load star-patch kernel (the default; RDR_PATCH_KERNEL=tma selects
+// patch_stream_kernel above). One CTA per patch, patches in decreasing size
+// order, so the hardware block scheduler hands out the work longest-first.
+// Full tiles are stored row-major in 32-byte groups ((i,k) at
+// ((k>>2)*rows + i)*4 + (k&3)): a warp owns a tile and reads it in two
+// 16-column halves with coalesced 32-byte non-allocating loads, lane = row.
+// Half-tiles keep the kernel at <= 64 registers, i.e. 4 CTAs = 32 warps per
+// SM streaming. Row products (-> z_I) are dot products with r_J; transposed
+// products (-> z_J) are a 16-value transpose reduction across the warp.
+constexpr int kLdgWarps = 8;
+
+__device__ __forceinline__ double4 ld_stream4(const double4* p) {
+  double4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v4.f64 {%0, %1, %2, %3}, [%4];"
+               : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w)
+               : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double ld_stream1(const double* p) {
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+
+// v[k] over 32 lanes -> lane l holds sum_{lanes} v[l & 15] (16-value transpose reduction)
+template <int S>
+__device__ __forceinline__ void treduce_stage(double (&v)[16], int lane) {
+  const bool upper = (lane & S) != 0;
+#pragma unroll
+  for (int k = 0; k < S; ++k) {
+    const double send = upper ? v[k] : v[k + S];
+    const double keep = upper ? v[k + S] : v[k];
+    v[k] = keep + __shfl_xor_sync(0xffffffffu, send, S);
+  }
+}
+__device__ __forceinline__ double treduce16(double (&v)[16], int lane) {
+  treduce_stage<8>(v, lane);
+  treduce_stage<4>(v, lane);
+  treduce_stage<2>(v, lane);
+  treduce_stage<1>(v, lane);
+  return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 16);
+}
+
+__global__ void __launch_bounds__(kLdgWarps * 32, 4)
+    patch_ldg_kernel(DevPrecond pc, const double* __restrict__ r, double* __restrict__ z, double* rz_acc,
+                     const PcgScalars* guard) {
   if (stopped(guard)) return;
   extern __shared__ double smem[];
   const int pid = blockIdx.x;
@@ -568,7 +860,7 @@ __global__ void __launch_bounds__(kPatchThreads) patch_kernel(DevPrecond pc, con
   double* zl = smem + npad;
   const int32_t* id = pc.idx + pc.idx_off[pid];
   for (int i = threadIdx.x; i < npad; i += blockDim.x) {
-    int g = id[i];
+    const int g = id[i];
     rl[i] = (g >= 0) ? rin[g] : 0.0;
     zl[i] = 0.0;
   }
@@ -576,70 +868,72 @@ __global__ void __launch_bounds__(kPatchThreads) patch_kernel(DevPrecond pc, con
   const double* T = pc.tiles + pc.tile_off[pid];
   const int ntiles = nb * (nb + 1) / 2;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nwarps = blockDim.x >> 5;
-  int I = 0, J = 0, tcur = 0;
-  for (int t = warp; t < ntiles; t += nwarps) {
-    while (tcur < t) {  // advance (I,J) in tile order I(I+1)/2 + J
-      ++J;
-      if (J > I) { ++I; J = 0; }
-      ++tcur;
-    }
-    // exact packed layout (setup.hpp: patch_tile_offset): rows valid rows in block row I
+  int I = 0, J = warp;
+  while (J > I) {
+    J -= I + 1;
+    ++I;
+  }
+  for (int t = warp; t < ntiles; t += kLdgWarps) {
     const int rows = min(32, n - 32 * I);
     const double* tb = T + 512LL * I * I + 16LL * I + (int64_t)J * 32 * rows;
-    double a[32];
     const double ri = rl[I * 32 + lane];
-    double row = 0;
-    if (J < I) {
-      if (lane < rows) {
-        const double4* tp = reinterpret_cast<const double4*>(tb) + lane;
+    double row = 0.0;
+#pragma unroll 1
+    for (int h = 0; h < 2; ++h) {
+      double a[16];
+      if (J < I) {
+        if (lane < rows) {
+          const double4* tp = reinterpret_cast<const double4*>(tb) + lane + 4 * h * rows;
 #pragma unroll
-        for (int k4 = 0; k4 < 8; ++k4) {
-          double4 v = ld_stream4(tp + k4 * rows);
-          a[4 * k4] = v.x;
-          a[4 * k4 + 1] = v.y;
-          a[4 * k4 + 2] = v.z;
-          a[4 * k4 + 3] = v.w;
+          for (int k4 = 0; k4 < 4; ++k4) {
+            const double4 v = ld_stream4(tp + k4 * rows);
+            a[4 * k4] = v.x;
+            a[4 * k4 + 1] = v.y;
+            a[4 * k4 + 2] = v.z;
+            a[4 * k4 + 3] = v.w;
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < 16; ++q) a[q] = 0.0;
         }
+        const double* rJ = rl + J * 32 + 16 * h;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) row = fma(a[q], rJ[q], row);
+#pragma unroll
+        for (int q = 0; q < 16; ++q) a[q] *= ri;
       } else {
+        // diagonal tile, lower triangle packed by columns: (i,k), k <= i at k*rows - k(k-1)/2 + i - k
 #pragma unroll
-        for (int k = 0; k < 32; ++k) a[k] = 0.0;
+        for (int q = 0; q < 16; ++q) {
+          const int k = 16 * h + q;
+          a[q] = (k <= lane && lane < rows) ? ld_stream1(tb + k * rows - k * (k - 1) / 2 + (lane - k)) : 0.0;
+        }
+        const double* rI = rl + I * 32 + 16 * h;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) row = fma(a[q], rI[q], row);
+#pragma unroll
+        for (int q = 0; q < 16; ++q) a[q] = (16 * h + q < lane) ? a[q] * ri : 0.0;  // strict lower, transposed
       }
-      const double* rJ = rl + J * 32;
-#pragma unroll
-      for (int k = 0; k < 32; ++k) row = fma(a[k], rJ[k], row);
-#pragma unroll
-      for (int k = 0; k < 32; ++k) a[k] *= ri;
-    } else {
-      // diagonal tile, lower triangle packed by columns: (i,k), k <= i, at k*rows - k(k-1)/2 + i - k
-#pragma unroll
-      for (int k = 0; k < 32; ++k)
-        a[k] = (k <= lane && lane < rows) ? ld_stream1(tb + k * rows - k * (k - 1) / 2 + (lane - k)) : 0.0;
-      const double* rI = rl + I * 32;
-#pragma unroll
-      for (int k = 0; k < 32; ++k) row = fma(a[k], rI[k], row);
-#pragma unroll
-      for (int k = 0; k < 32; ++k) a[k] = (k < lane) ? a[k] * ri : 0.0;  // strict lower part, transposed
+      const double col = treduce16(a, lane);
+      if (lane < 16) atomicAdd(zl + J * 32 + 16 * h + lane, col);
     }
     atomicAdd(zl + I * 32 + lane, row);
-    transpose_reduce_stage<16>(a, lane);
-    transpose_reduce_stage<8>(a, lane);
-    transpose_reduce_stage<4>(a, lane);
-    transpose_reduce_stage<2>(a, lane);
-    transpose_reduce_stage<1>(a, lane);
-    atomicAdd(zl + J * 32 + lane, a[0]);
+    J += kLdgWarps;
+    while (J > I) {
+      J -= I + 1;
+      ++I;
+    }
   }
   __syncthreads();
-  double part = 0;
+  double part = 0.0;
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    int g = id[i];
-    double zi = zl[i];
-    atomicAdd(zout + g, zi);
+    const double zi = zl[i];
+    atomicAdd(zout + id[i], zi);
     part = fma(rl[i], zi, part);
   }
   if (rz_acc) {
     __shared__ double sh[32];
-    double s = block_sum(part, sh);
+    const double s = block_sum(part, sh);
     if (threadIdx.x == 0) atomicAdd(rz_acc, s);
   }
 }
@@ -803,6 +1097,9 @@ cudaError_t launch_apply(const DevOperator& op, const double* x, double* y, doub
   return launch_apply_tc<false>(op, x, y, pq_acc, guard, s);
 }
 
+size_t patch_kernel_smem(int slots, int npad_max, int zbufs) { return patch_smem_bytes(slots, npad_max, zbufs); }
+size_t max_kernel_smem() { return kMaxSmem; }
+
 int count_precond_launches(const DevPrecond& pc) {
   return 1 + (pc.n_patches > 0 ? 1 : 0) + (pc.gbuf ? 2 : 0);
 }
@@ -818,9 +1115,12 @@ cudaError_t launch_precond_part(int part, const DevPrecond& pc, const double* r,
       break;
     case 2:
       if (pc.n_patches > 0) {
-        const int npad = ((pc.max_n + 31) / 32) * 32;  // the largest patch (grid sorted by size)
-        const size_t sm = (size_t)2 * npad * sizeof(double);
-        patch_kernel<<<(unsigned)pc.n_patches, kPatchThreads, sm, s>>>(pc, r, z, rz_acc, guard);
+        if (pc.kernel == 1)
+          patch_stream_kernel<<<(unsigned)pc.n_ctas, kPatchWarps * 32,
+                                patch_smem_bytes(pc.ring_slots, pc.npad_max, pc.zbufs), s>>>(pc, r, z, rz_acc, guard);
+        else
+          patch_ldg_kernel<<<(unsigned)pc.n_patches, kLdgWarps * 32, 2 * sizeof(double) * pc.npad_max, s>>>(
+              pc, r, z, rz_acc, guard);
       }
       break;
     case 3:
@@ -886,7 +1186,8 @@ void configure_kernels() {  // errors here would surface as a later launch's cud
   cudaFuncSetAttribute(apply_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(apply_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(apply_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  cudaFuncSetAttribute(patch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  cudaFuncSetAttribute(patch_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
+  cudaFuncSetAttribute(patch_ldg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
   cudaFuncSetAttribute(apply_tc_kernel<64, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
   cudaFuncSetAttribute(apply_tc_kernel<64, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
   cudaFuncSetAttribute(apply_tc_kernel<32, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);

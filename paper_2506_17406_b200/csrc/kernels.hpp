@@ -51,6 +51,13 @@ struct DevPrecond {
   const int64_t* tile_off;      // [np+1]
   const double* tiles;
   const uint8_t* pkind;         // 0 own numbering, 1 CG potential
+  int32_t kernel;               // 0: patch_ldg_kernel (tile layout "groups"), 1: patch_stream_kernel ("swizzled")
+  // persistent patch kernel: n_ctas CTAs claim patches from a queue
+  int32_t n_ctas;
+  int32_t* queue;               // [2] claim counter, finished-CTA counter (zero between launches)
+  int32_t ring_slots;           // shared-memory tile slots of 8 KB: 8 warps x K
+  int32_t zbufs;                // private z copies per warp: 2 (by patch parity) or 1
+  int32_t npad_max;             // largest patch dimension rounded up to 32
   // H(curl) potential space
   int64_t n_cg_iface;           // CG dofs [0, n_cg_iface) used by patches
   const int64_t* g_ptr;
@@ -88,6 +95,8 @@ cudaError_t launch_pcg_update_jacobi(PcgScalars* sc, const DevPrecond& pc, const
                                      double* q, double* x, double* r, double* z, cudaStream_t s);
 
 int count_precond_launches(const DevPrecond& pc);  // kernels per rdr_precond
+size_t patch_kernel_smem(int slots, int npad_max, int zbufs);  // dynamic shared memory of the patch kernel
+size_t max_kernel_smem();                           // per-CTA dynamic shared-memory opt-in used
 void configure_kernels();                            // shared-memory opt-ins (call once, outside capture)
 
 }  // namespace rdr

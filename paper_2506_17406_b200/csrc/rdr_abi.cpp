@@ -239,8 +239,12 @@ static int setup_impl(rdr_handle* h, const double* vertices, int64_t nv, const i
   }
   Patches P;
   DeviceTiles sink;
+  {
+    const char* pk = std::getenv("RDR_PATCH_KERNEL");
+    pc.kernel = (pk && std::strcmp(pk, "tma") == 0) ? 1 : 0;
+  }
   st = build_patches(m, num, el, coef, space == RDR_HCURL ? &cg_num : nullptr, cg_el,
-                     space == RDR_HCURL ? &cg_coef : nullptr, P, sink);
+                     space == RDR_HCURL ? &cg_coef : nullptr, P, sink, pc.kernel == 1 ? kTileSwizzled : kTileGroups);
   if (sink.d) h->owned.push_back(sink.d);
   if (st) return st;
   pc.n_patches = (int64_t)P.n.size();
@@ -259,6 +263,37 @@ static int setup_impl(rdr_handle* h, const double* vertices, int64_t nv, const i
   pc.tile_off = d_to;
   pc.tiles = sink.d;
   pc.pkind = d_pk;
+  {  // persistent patch kernel: tile slots, CTAs per SM, claim queue
+    int dev = 0, sms = 148;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    pc.npad_max = std::max(32, (P.max_n + 31) / 32 * 32);
+    const size_t per_sm = 228 * 1024;
+    // 8 warps x K tile slots of 8 KB and private z copies per warp: two CTAs
+    // per SM (16 consumer warps) with K = 1 when they fit -- measured faster
+    // than deeper per-warp prefetch with 8 warps per SM -- else one CTA with
+    // the deepest K that fits (RDR_PATCH_CTAS / RDR_PATCH_K / RDR_PATCH_ZB override)
+    const size_t cap1 = max_kernel_smem(), cap2 = per_sm / 2 - 1024;
+    auto fits = [&](int c, int k, int zb) { return patch_kernel_smem(8 * k, pc.npad_max, zb) <= (c == 2 ? cap2 : cap1); };
+    int per_cta_sm = 2, K = 1, ZB = 1;
+    if (!fits(2, 1, 1)) {
+      per_cta_sm = 1;
+      while (K < 3 && fits(1, K + 1, 1)) ++K;
+    }
+    if (const char* e = std::getenv("RDR_PATCH_K")) K = std::max(1, std::atoi(e));
+    if (const char* e = std::getenv("RDR_PATCH_ZB")) ZB = std::atoi(e) == 2 ? 2 : 1;
+    if (const char* e = std::getenv("RDR_PATCH_CTAS")) per_cta_sm = std::atoi(e) == 2 ? 2 : 1;
+    if (!fits(1, K, ZB)) return RDR_EINVAL;
+    pc.ring_slots = 8 * K;
+    pc.zbufs = ZB;
+    const int64_t np = (int64_t)P.n.size();
+    const int G = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * per_cta_sm, np));
+    pc.n_ctas = G;
+    // patches are claimed dynamically in decreasing size order (the order of P)
+    if ((st = h->own_alloc((void**)&pc.queue, 2 * sizeof(int32_t)))) return st;
+    CK(cudaMemset(pc.queue, 0, 2 * sizeof(int32_t)));
+
+  }
 
   // ---- PCG workspace
   const size_t vb = sizeof(double) * std::max<int64_t>(1, num.n_total);

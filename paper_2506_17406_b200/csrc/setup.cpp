@@ -392,7 +392,7 @@ void chol_inverse(const double* L, int n, double* U, double* Ainv) {
 
 int build_patches(const Mesh& m, const Numbering& num, const RefElement& el, const std::vector<double>& coef,
                   const Numbering* cg_num, const RefElement* cg_el, const std::vector<double>* cg_coef,
-                  Patches& P, PatchSink& sink) {
+                  Patches& P, PatchSink& sink, PatchLayout layout) {
   CSR v_cells = invert_incidence(m.nt, m.nv, 4, m.cells);
   CSR v_edges = invert_incidence(m.ne, m.nv, 2, m.edges);
   CSR v_faces = invert_incidence(m.nf, m.nv, 3, m.faces);
@@ -541,10 +541,12 @@ int build_patches(const Mesh& m, const Numbering& num, const RefElement& el, con
           const int rows = std::min(32, n - 32 * I);
           for (int J = 0; J <= I; ++J) {
             double* tile = out + patch_tile_offset(n, I, J);
-            if (J < I) {  // full-width tile, `rows` rows: (i,k) at ((k>>2)*rows + i)*4 + (k&3)
+            if (J < I) {  // full-width tile, `rows` rows (setup.hpp layouts)
               for (int i = 0; i < rows; ++i)
                 for (int kk = 0; kk < 32; ++kk)
-                  tile[((kk >> 2) * rows + i) * 4 + (kk & 3)] = W2[(size_t)(I * 32 + i) * n + J * 32 + kk];
+                  tile[layout == kTileGroups ? ((kk >> 2) * rows + i) * 4 + (kk & 3)
+                                             : i * 32 + 2 * ((kk >> 1) ^ (i & 7)) + (kk & 1)] =
+                      W2[(size_t)(I * 32 + i) * n + J * 32 + kk];
             } else {      // diagonal: packed lower triangle by columns, (i,k), k<=i at k*rows - k(k-1)/2 + (i-k)
               for (int kk = 0; kk < rows; ++kk)
                 for (int i = kk; i < rows; ++i)

@@ -51,8 +51,13 @@ struct Patches {
 
 // Stored layout of one patch inverse A_m^{-1} (n x n, symmetric): the lower
 // triangle in 32-row block rows I = 0..nb-1 (rows = min(32, n - 32 I)); block
-// row I holds I full-width tiles J < I ((i,k) at ((k>>2)*rows + i)*4 + (k&3),
-// i.e. 32-byte groups of 4 consecutive columns, one group per row and lane)
+// row I holds I full-width tiles J < I, in one of two layouts: kTileGroups
+// (i,k) at ((k>>2)*rows + i)*4 + (k&3) -- 32-byte groups of 4 columns, one per
+// row, for coalesced direct loads with lane = row (patch_ldg_kernel) -- or
+// kTileSwizzled (i,k) at i*32 + 2*((k>>1) ^ (i&7)) + (k&1) -- 16-byte chunks
+// XOR-swizzled by row, so that lane-per-row 16-byte and lane-per-column
+// 8-byte reads of the tile in shared memory are both bank-conflict free
+// (patch_stream_kernel)
 // followed by the diagonal tile packed by columns ((i,k), k <= i, at
 // k*rows - k(k-1)/2 + (i-k)). Exactly n(n+1)/2 doubles, padded to 16.
 inline int64_t patch_block_row_start(int n, int I) {
@@ -77,9 +82,10 @@ struct PatchSink {
   virtual int put(int64_t tile_begin, const double* tiles, int64_t count) = 0;
   virtual ~PatchSink() {}
 };
+enum PatchLayout { kTileGroups = 0, kTileSwizzled = 1 };
 int build_patches(const Mesh& m, const Numbering& num, const RefElement& el, const std::vector<double>& coef,
                   const Numbering* cg_num, const RefElement* cg_el, const std::vector<double>* cg_coef,
-                  Patches& P, PatchSink& sink);
+                  Patches& P, PatchSink& sink, PatchLayout layout);
 
 // Interior point-Jacobi (R-A17): 1/A_ll for the cell-interior dofs [off[3], n_total).
 void interior_inverse_diagonal(const Mesh& m, const Numbering& num, const RefElement& el,

@@ -1,28 +1,29 @@
 """Benchmark of the B200 Riesz-map PCG hot path (arXiv 2506.17406).
 
-Workload (BASELINE.json configs[1], "cfg2"): H(grad) Riesz map, p=6, 8x8x8 cubes
-x 6 = 3072 tets with interior vertices displaced by up to 0.2h (seed 0),
-per-cell alpha, beta log-uniform in [1e-2, 1e2], Dirichlet on x=0, seeded
-uniform[-1,1] rhs, PCG rtol 1e-8 from x0 = 0.
+Workload (BASELINE.json configs[1], "cfg2", the default): H(grad) Riesz map,
+p=6, 8x8x8 cubes x 6 = 3072 tets with interior vertices displaced by up to
+0.2h (seed 0), per-cell alpha, beta log-uniform in [1e-2, 1e2], Dirichlet on
+x=0, seeded uniform[-1,1] rhs, PCG rtol 1e-8 from x0 = 0. Other configs:
+--config 1..5 (--p for the config-5 sweep point).
 
 A step = one full PCG solve (every hot-path row of SURVEY §8(a): operator
 apply, interior Jacobi, star-patch solves, PCG vector ops) on a fresh rhs
 already resident in HBM. value = PCG iterations/s over the whole job.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--config 2]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--config 2] [--p 6]
 
-Multi-GPU: the path does not shard within one solve (single-GPU north_star);
-N ranks run N independent problems (replicas, weak scaling, no collective on
-the data path; torch.distributed only for the barrier and the max-over-ranks
-time).
+Multi-GPU: the north_star path is one GPU and does not shard within a solve
+("replicas only"): under torchrun every rank solves its own
+problem (seed = rank), with no collective on the data path; torch.distributed
+only provides the barrier, the max-over-ranks time and the sum of iterations.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
-import subprocess
 import sys
+import threading
 import time
 
 import numpy as np
@@ -38,66 +39,93 @@ WORKLOADS = {
     4: "cfg4: H(curl) Ned1_6, 12^3x6 tets, alpha=beta=1, full tangential Dirichlet",
     5: "cfg5: H(grad) p-sweep point, 8^3x6 perturbed tets, alpha=beta=1, full Dirichlet",
 }
+KERNELS = ("apply_tc_kernel", "patch_ldg_kernel")
 
 
-def _peaks():
+def hbm_peak():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            d = json.load(f)
-        return float(d["hbm_gbs"]), "measured"
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
     except Exception:
-        return 6650.0, "fallback"
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def committed_traffic(workload_key, kernel):
+    """DRAM bytes per launch of `kernel` on this workload from the committed
+    `ncu --set full` capture (profiles/traffic.json), else None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            e = json.load(f)[workload_key][kernel]
+        return float(e["dram_bytes_per_launch"]), e["source"]
+    except Exception:
+        return None, None
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled (NVML, every 5 ms) during the
+    timed region."""
 
-    def __init__(self, index=0):
-        self.index = index
-        self.proc = None
-        self.path = f"/tmp/rdr_clocks_{os.getpid()}.csv"
+    NAMES = {"hw_slowdown": "nvmlClocksEventReasonHwSlowdown",
+             "hw_thermal_slowdown": "nvmlClocksEventReasonHwThermalSlowdown",
+             "sw_thermal_slowdown": "nvmlClocksEventReasonSwThermalSlowdown",
+             "sw_power_cap": "nvmlClocksEventReasonSwPowerCap",
+             "hw_power_brake": "nvmlClocksEventReasonHwPowerBrakeSlowdown"}
+
+    def __init__(self, index=0, period=0.005):
+        self.index, self.period = index, period
+        self.sm, self.reasons, self.max = [], set(), None
+        self._stop = threading.Event()
+
+    def _loop(self):
+        import pynvml as nv
+        h = nv.nvmlDeviceGetHandleByIndex(self.index)
+        self.max = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        while not self._stop.is_set():
+            self.sm.append(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+            bits = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+            for name, attr in self.NAMES.items():
+                if bits & getattr(nv, attr, 0):
+                    self.reasons.add(name)
+            time.sleep(self.period)
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index),
-                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+            import pynvml as nv
+            nv.nvmlInit()
+            self._t = threading.Thread(target=self._loop, daemon=True)
+            self._t.start()
         except Exception:
-            self.proc = None
+            self._t = None
         return self
 
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=2)
 
     def summary(self):
-        try:
-            rows = [l.split(", ") for l in open(self.path).read().strip().splitlines() if l.strip()]
-        except Exception:
-            rows = []
-        if not rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for r in rows for k in range(4) if len(r) > 4 + k and r[4 + k].strip() == "Active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(rows)}
+        if not self.sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": float(np.median(self.sm)), "sm_max_mhz": self.max, "reasons": sorted(self.reasons),
+                "samples": len(self.sm)}
 
 
-def _dist():
-    ws = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return ws, rank, local
+def dist_env():
+    return int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), int(os.environ.get("LOCAL_RANK", "0"))
+
+
+def reduce_over_ranks(ms, units, device=None):
+    """(max over ranks of the device time, sum over ranks of the work units):
+    the whole-job throughput is sum(units) / max(ms)."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return float(ms), float(units)
+    t = torch.tensor([float(ms)], dtype=torch.float64, device=device)
+    u = torch.tensor([float(units)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dist.all_reduce(u, op=dist.ReduceOp.SUM)
+    return float(t.item()), float(u.item())
 
 
 def oracle_sample(cfg, p, iters_per_step, steps, warmup):
@@ -118,22 +146,22 @@ def oracle_sample(cfg, p, iters_per_step, steps, warmup):
         if k >= warmup:
             times.append(dt)
     cores = len(os.sched_getaffinity(0))
-    return iters_per_step * steps / sum(times), sum(times), cores, O.n_total
+    return iters_per_step * steps / sum(times), sum(times), cores
 
 
 def run_reference(args):
-    ws, rank, _ = _dist()
+    ws, rank, _ = dist_env()
     if rank != 0:
         return
-    ips, tot, cores, n_total = oracle_sample(args.config, args.p, args.ref_iters, args.steps, args.warmup)
+    ips, tot, cores = oracle_sample(args.config, args.p, args.ref_iters, args.steps, args.warmup)
+    sample = (f"{args.ref_iters} oracle PCG iterations per step (scipy CSR apply + cho_solve patches, "
+              f"setup untimed) on {WORKLOADS[args.config]}")
     line = {
         "impl": "reference", "metric": METRIC, "value": ips, "unit": "PCG iters/s", "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": WORKLOADS[args.config], "rtol": 1e-8},
-        "cpu_baseline": {"value": ips, "unit": "PCG iters/s", "cores": cores, "kind": "oracle",
-                         "sample": f"{args.ref_iters} oracle PCG iterations per step (scipy CSR apply + "
-                                   f"cho_solve patches), setup untimed"},
+        "cpu_baseline": {"value": ips, "unit": "PCG iters/s", "cores": cores, "kind": "oracle", "sample": sample},
         "e2e": {"value": ips, "unit": "PCG iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -141,20 +169,20 @@ def run_reference(args):
 
 def run(args):
     import torch
-    ws, rank, local = _dist()
+    ws, rank, local = dist_env()
     torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
     if ws > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist.init_process_group("nccl", device_id=dev)
     from rdr_inputs import make_config
     from paper_2506_17406_b200 import rdr
 
     cfg = args.config
-    c = make_config(cfg, p=args.p) if cfg == 5 else make_config(cfg, seed=rank)
+    c = make_config(cfg, p=args.p, seed=rank) if cfg == 5 else make_config(cfg, seed=rank)
     S = rdr.Solver(c.vertices, c.tets, c.p, c.space, c.alpha, c.beta, c.mask)
     info = S.info
     n = S.n_total
-    dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream()
     rhs = [torch.from_numpy(c.draw_vector(n)).to(dev) for _ in range(args.steps + args.warmup)]
     x = torch.empty(n, dtype=torch.float64, device=dev)
@@ -165,12 +193,11 @@ def run(args):
             torch.distributed.barrier()
         torch.cuda.synchronize()
 
-    iters = []
     for k in range(args.warmup):
-        _, it = S.solve(rhs[k], x, rtol=1e-8)
+        S.solve(rhs[k], x, rtol=1e-8)
     barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    launches = 0
+    iters, launches = [], 0
     with ClockSampler(local) as clk:
         ev0.record(stream)
         for k in range(args.steps):
@@ -179,22 +206,15 @@ def run(args):
             launches += S.last_launches()
         ev1.record(stream)
         ev1.synchronize()
-    ms = ev0.elapsed_time(ev1)
+    ms_local = ev0.elapsed_time(ev1)
     barrier()
-    tot_iters = float(sum(iters))
-    if ws > 1:
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms = float(t.item())
-        it_t = torch.tensor([tot_iters], device=dev, dtype=torch.float64)
-        torch.distributed.all_reduce(it_t)
-        tot_iters = float(it_t.item())
+    ms, tot_iters = reduce_over_ranks(ms_local, sum(iters), dev)
     value = tot_iters / (ms / 1e3)
 
-    # ---- end to end: host (pinned) b -> device -> PCG -> host x, per step
+    # ---- end to end through the public API: pinned host b -> device -> PCG -> host x, every step
     bh = torch.from_numpy(c.draw_vector(n)).pin_memory()
     xh = torch.empty(n, dtype=torch.float64).pin_memory()
-    S.solve_host(bh, xh)  # warm
+    S.solve_host(bh, xh)
     barrier()
     e_iters = 0
     ev0.record(stream)
@@ -202,26 +222,17 @@ def run(args):
         e_iters += S.solve_host(bh, xh)
     ev1.record(stream)
     ev1.synchronize()
-    e_ms = ev0.elapsed_time(ev1)
-    if ws > 1:
-        t = torch.tensor([e_ms], device=dev, dtype=torch.float64)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        e_ms = float(t.item())
-        t = torch.tensor([float(e_iters)], device=dev, dtype=torch.float64)
-        torch.distributed.all_reduce(t)
-        e_iters = float(t.item())
+    e_ms, e_iters = reduce_over_ranks(ev0.elapsed_time(ev1), e_iters, dev)
 
-    # ---- per-kernel device times (roofline of the dominant kernel)
+    # ---- per-kernel device times (CUDA events on this stream) and the roofline of the dominant kernel
     kms = S.time_kernels(rhs[0], rhs[0], reps=args.kernel_reps)
-    hbm, peak_kind = _peaks()
-    patch_alg = info["bytes_precond"] - 24.0 * info["n_interior"]
-    it_ms = ms / max(1.0, sum(iters))
     if rank != 0:
         if ws > 1:
             torch.distributed.destroy_process_group()
         return
-    result = None
-    fp64 = None
+    hbm, hbm_src = hbm_peak()
+    fp64_peak = rdr.measure_fp64_peak()
+    dgemm = None
     if not args.no_dgemm:
         a = torch.randn(4096, 4096, dtype=torch.float64, device=dev)
         for _ in range(2):
@@ -233,8 +244,24 @@ def run(args):
             a @ a
         e1.record()
         e1.synchronize()
-        fp64 = 5 * 2 * 4096 ** 3 / (e0.elapsed_time(e1) / 1e3) / 1e12
-    apply_flops = info["flops_apply"] / (kms[0] / 1e3) / 1e12
+        dgemm = 5 * 2 * 4096 ** 3 / (e0.elapsed_time(e1) / 1e3) / 1e12
+    patch_alg = info["bytes_precond"] - 24.0 * info["n_interior"]
+    apply_tf = info["flops_apply"] / (kms[0] / 1e3) / 1e12
+    patch_gbs = patch_alg / (kms[2] / 1e3) / 1e9
+    key = f"cfg{cfg}" + (f"_p{c.p}" if cfg == 5 else "")
+    apply_roof = {"bound": "tensor", "kernel": "apply_tc_kernel (gather, DMMA contraction, scatter-add)",
+                  "achieved": apply_tf, "peak": fp64_peak, "unit": "TFLOP/s", "frac": apply_tf / fp64_peak,
+                  "peak_source": "measured in this run: DMMA.8x8x4 issue-bound loop (rdr_measure_fp64_peak)",
+                  "alg_flops_per_launch": info["flops_apply"],
+                  "traffic": committed_traffic(key, "apply_tc_kernel")[0]}
+    patch_roof = {"bound": "hbm", "kernel": "patch_ldg_kernel (star-patch solves, packed FP64 inverses)",
+                  "achieved": patch_gbs, "peak": hbm, "unit": "GB/s", "frac": patch_gbs / hbm, "peak_source": hbm_src,
+                  "alg_bytes_per_launch": patch_alg, "stored_bytes_per_launch": info["patch_bytes"],
+                  "traffic": committed_traffic(key, "patch_ldg_kernel")[0]}
+    dominant, other = (patch_roof, apply_roof) if kms[2] >= kms[0] else (apply_roof, patch_roof)
+    tsrc = committed_traffic(key, dominant["kernel"].split()[0])[1]
+    if tsrc:
+        dominant["traffic_source"] = tsrc
     line = {
         "metric": METRIC, "value": value, "unit": "PCG iters/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
@@ -242,19 +269,14 @@ def run(args):
         "config": {"workload": WORKLOADS[cfg] + (f" (p={c.p})" if cfg == 5 else ""),
                    "n_free": info["n_free"], "n_total": n, "n_cells": info["n_cells"], "n_loc": info["n_loc"],
                    "n_patches": info["n_patches"], "max_patch": info["max_patch"], "rtol": 1e-8,
-                   "parallelism": f"replicas x{ws}",
+                   "parallelism": f"replicas x{ws} (one independent solve per GPU)",
                    "l2": f"inputs larger than L2: {info['patch_bytes'] / 1e9:.2f} GB of patch inverses streamed "
                          f"every iteration (> 126 MB L2)"},
-        "iters_per_solve": float(np.mean(iters)), "ms_per_iter": it_ms,
-        "apply": {"dofs_per_s": info["n_free"] / (kms[0] / 1e3), "ms": kms[0], "tflops": apply_flops,
-                  "fp64_dgemm_tflops_measured": fp64,
-                  "frac_of_dgemm": (apply_flops / fp64) if fp64 else None},
+        "iters_per_solve": float(np.mean(iters)), "ms_per_iter": ms_local / max(1.0, sum(iters)),
+        "dofs_per_s_per_apply": info["n_free"] / (kms[0] / 1e3),
         "kernel_ms": {"apply": kms[0], "jacobi": kms[1], "patches": kms[2], "gradient": kms[3]},
-        "roofline": {"bound": "hbm", "kernel": "patch_kernel (star-patch solves, packed FP64 inverses)",
-                     "achieved": patch_alg / (kms[2] / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
-                     "frac": patch_alg / (kms[2] / 1e3) / 1e9 / hbm, "peak_source": peak_kind,
-                     "alg_bytes_per_launch": patch_alg, "stored_bytes_per_launch": info["patch_bytes"],
-                     "traffic": None},
+        "roofline": dominant, "roofline_other": other,
+        "fp64_dgemm_tflops_cublas": dgemm,
         "e2e": {"value": e_iters / (e_ms / 1e3), "unit": "PCG iters/s", "h2d_bytes_per_step": 8 * n,
                 "d2h_bytes_per_step": 8 * n},
         "gpu_launches": int(launches),
@@ -262,7 +284,7 @@ def run(args):
         "setup_s": info["setup_seconds"],
     }
     if not args.no_cpu:
-        ips, tot, cores, _ = oracle_sample(cfg, c.p, args.ref_iters, 1, 0)
+        ips, tot, cores = oracle_sample(cfg, c.p, args.ref_iters, 1, 0)
         line["cpu_baseline"] = {"value": ips, "unit": "PCG iters/s", "cores": cores, "kind": "oracle",
                                 "sample": f"{args.ref_iters} oracle PCG iterations on the same workload "
                                           f"(scipy CSR apply + cho_solve patches), setup untimed"}
@@ -274,11 +296,11 @@ def run(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=2)
-    ap.add_argument("--p", type=int, default=6, help="degree for the config-5 sweep point")
+    ap.add_argument("--p", type=int, default=6, help="degree of the config-5 sweep point")
     ap.add_argument("--ref-iters", type=int, default=20)
     ap.add_argument("--kernel-reps", type=int, default=50)
     ap.add_argument("--no-cpu", action="store_true")

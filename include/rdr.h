@@ -112,6 +112,11 @@ int rdr_last_launches(const rdr_handle* h, int64_t* launches);
 int rdr_time_kernels(rdr_handle* h, const double* x, double* y, const double* r, double* z, int reps, double* ms,
                      void* stream);
 
+/* Measurement helper (bench.py roofline denominator of the apply): FP64
+ * tensor-core (DMMA.8x8x4) throughput of an issue-bound loop over all SMs, in
+ * TFLOP/s, timed with CUDA events on `stream` (synchronizes it). */
+int rdr_measure_fp64_peak(double* tflops, void* stream);
+
 void rdr_destroy(rdr_handle* h);
 const char* rdr_strerror(int code);
 

@@ -72,53 +72,67 @@ class Oracle:
         return self.A @ self.mask(x)
 
     # ------------------------------------------------------------ patches
+    def _incidence(self):
+        """vertex -> incident edges / faces, edge -> incident faces (cached)."""
+        if getattr(self, "_inc", None) is None:
+            t = self.topo
+            v_edges = [[] for _ in range(t.nv)]
+            for e, (a, b) in enumerate(t.edges):
+                v_edges[a].append(e)
+                v_edges[b].append(e)
+            v_faces = [[] for _ in range(t.nv)]
+            for f, tri in enumerate(t.faces):
+                for a in tri:
+                    v_faces[a].append(f)
+            e_faces = [[] for _ in range(t.ne)]
+            for f, tri in enumerate(t.faces):
+                for a, b in ((0, 1), (0, 2), (1, 2)):
+                    e_faces[t.edge_index[(tri[a], tri[b])]].append(f)
+            self._inc = (v_edges, v_faces, e_faces)
+        return self._inc
+
+    def vertex_patch(self, v):
+        """(kind, idx) of the star patch of vertex v (R-A13): the free interface
+        dofs of v, the edges and the faces containing v -- in the problem's own
+        numbering for H(grad) ('dof'), in the CG_p potential numbering for
+        H(curl) ('pot', embedded by G[:, idx]). Empty idx: no patch."""
+        v_edges, v_faces, _ = self._incidence()
+        if self.space == "hgrad":
+            idx = self._entity_dofs(self.num, v, v_edges[v], v_faces[v], kinds=None)
+            return "dof", idx[self.free[idx]]
+        self._build_gradient()
+        cg = self.cg_num
+        idx = self._entity_dofs(cg, v, v_edges[v], v_faces[v], kinds=None)
+        return "pot", idx[~cg.constrained[idx]]
+
+    def edge_patch(self, e):
+        """('dof', idx) of the type-I edge patch of E (H(curl), R-A13): the free
+        Whitney dof of E and the type-I dofs of the faces containing E."""
+        _, _, e_faces = self._incidence()
+        num = self.num
+        nI_face = num.per[2] - (self.p - 1) * (self.p - 2) // 2
+        idx = [num.offsets[1] + e * num.per[1]]       # Whitney dof of E
+        for f in e_faces[e]:
+            base = num.offsets[2] + f * num.per[2]
+            idx.extend(range(base, base + nI_face))  # type-I face dofs
+        idx = np.array(sorted(idx), dtype=np.int64)
+        return "dof", idx[self.free[idx]]
+
     def patch_sets(self):
         """List of (kind, idx) with idx global dof ids; for kind 'pot' idx are
         CG_p dof ids of the potential space and the embedding is G[:, idx]."""
         if self._patches is not None:
             return self._patches
-        t = self.topo
         out = []
-        # vertex -> incident edges / faces
-        v_edges = [[] for _ in range(t.nv)]
-        for e, (a, b) in enumerate(t.edges):
-            v_edges[a].append(e)
-            v_edges[b].append(e)
-        v_faces = [[] for _ in range(t.nv)]
-        for f, tri in enumerate(t.faces):
-            for a in tri:
-                v_faces[a].append(f)
-        if self.space == "hgrad":
-            num = self.num
-            for v in range(t.nv):
-                idx = self._entity_dofs(num, v, v_edges[v], v_faces[v], kinds=None)
-                idx = idx[self.free[idx]]
+        for v in range(self.topo.nv):
+            kind, idx = self.vertex_patch(v)
+            if len(idx):
+                out.append((kind, idx))
+        if self.space == "hcurl":
+            for e in range(self.topo.ne):
+                kind, idx = self.edge_patch(e)
                 if len(idx):
-                    out.append(("dof", idx))
-        else:
-            self._build_gradient()
-            cg = self.cg_num
-            cg_free = ~cg.constrained
-            for v in range(t.nv):
-                idx = self._entity_dofs(cg, v, v_edges[v], v_faces[v], kinds=None)
-                idx = idx[cg_free[idx]]
-                if len(idx):
-                    out.append(("pot", idx))
-            e_faces = [[] for _ in range(t.ne)]
-            for f, tri in enumerate(t.faces):
-                for a, b in ((0, 1), (0, 2), (1, 2)):
-                    e_faces[t.edge_index[(tri[a], tri[b])]].append(f)
-            num = self.num
-            nI_face = num.per[2] - (self.p - 1) * (self.p - 2) // 2
-            for e in range(t.ne):
-                idx = [num.offsets[1] + e * num.per[1]]       # Whitney dof of E
-                for f in e_faces[e]:
-                    base = num.offsets[2] + f * num.per[2]
-                    idx.extend(range(base, base + nI_face))  # type-I face dofs
-                idx = np.array(sorted(idx), dtype=np.int64)
-                idx = idx[self.free[idx]]
-                if len(idx):
-                    out.append(("dof", idx))
+                    out.append((kind, idx))
         self._patches = out
         return out
 

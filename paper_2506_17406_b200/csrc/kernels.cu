@@ -1179,6 +1179,25 @@ cudaError_t launch_pcg_update_jacobi(PcgScalars* sc, const DevPrecond& pc, const
   return cudaGetLastError();
 }
 
+// FP64 tensor-core peak microbenchmark (roofline denominator of the apply,
+// bench.py): 4 independent DMMA.8x8x4 chains per warp, issue-bound.
+__global__ void dmma_peak_kernel(double* out, int n) {
+  double c0 = 0, c1 = 0, d0 = 0, d1 = 0, e0 = 0, e1 = 0, f0 = 0, f1 = 0;
+  const double a = threadIdx.x * 1e-3, b = 1.0;
+  for (int i = 0; i < n; ++i) {
+    dmma884(c0, c1, a, b);
+    dmma884(d0, d1, a, b);
+    dmma884(e0, e1, a, b);
+    dmma884(f0, f1, a, b);
+  }
+  if (c0 + d0 + e0 + f0 + c1 + d1 + e1 + f1 == 1.2345) out[0] = 1.0;
+}
+
+cudaError_t launch_dmma_peak(double* out, int n, int blocks, int threads, cudaStream_t s) {
+  dmma_peak_kernel<<<blocks, threads, 0, s>>>(out, n);
+  return cudaGetLastError();
+}
+
 }  // namespace rdr
 
 namespace rdr {

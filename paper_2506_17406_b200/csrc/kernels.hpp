@@ -98,5 +98,7 @@ int count_precond_launches(const DevPrecond& pc);  // kernels per rdr_precond
 size_t patch_kernel_smem(int slots, int npad_max, int zbufs);  // dynamic shared memory of the patch kernel
 size_t max_kernel_smem();                           // per-CTA dynamic shared-memory opt-in used
 void configure_kernels();                            // shared-memory opt-ins (call once, outside capture)
+// DMMA.8x8x4 issue-bound loop: n iterations x 4 chains x 512 flop per warp
+cudaError_t launch_dmma_peak(double* out, int n, int blocks, int threads, cudaStream_t s);
 
 }  // namespace rdr

@@ -525,6 +525,32 @@ int rdr_time_kernels(rdr_handle* h, const double* x, double* y, const double* r,
   return st;
 }
 
+int rdr_measure_fp64_peak(double* tflops, void* stream) {
+  if (!tflops) return RDR_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  int dev = 0, sms = 148;
+  CK(cudaGetDevice(&dev));
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  double* d;
+  CK(cudaMalloc((void**)&d, sizeof(double)));
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  const int n = 1 << 15, threads = 512;
+  CK(launch_dmma_peak(d, n, sms, threads, s));  // warm-up
+  CK(cudaEventRecord(e0, s));
+  CK(launch_dmma_peak(d, n, sms, threads, s));
+  CK(cudaEventRecord(e1, s));
+  CK(cudaEventSynchronize(e1));
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  *tflops = 512.0 * 4.0 * n * (double)sms * (threads / 32) / (ms * 1e-3) / 1e12;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(d);
+  return RDR_OK;
+}
+
 void rdr_destroy(rdr_handle* h) {
   if (h) {
     cudaDeviceSynchronize();

@@ -48,6 +48,7 @@ def _load():
         "rdr_solve_host": (ctypes.c_int, [P, P, P, D, ctypes.c_int, ctypes.POINTER(ctypes.c_int), P]),
         "rdr_last_launches": (ctypes.c_int, [P, ctypes.POINTER(I64)]),
         "rdr_time_kernels": (ctypes.c_int, [P, P, P, P, P, ctypes.c_int, P, P]),
+        "rdr_measure_fp64_peak": (ctypes.c_int, [ctypes.POINTER(D), P]),
         "rdr_destroy": (None, [P]),
         "rdr_strerror": (ctypes.c_char_p, [ctypes.c_int]),
         "rdr_reference_matrices": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, P, ctypes.POINTER(I32),
@@ -104,6 +105,13 @@ def bubble_eigenvalues(kind: int, l: int, p: int) -> np.ndarray:
     out = np.zeros(n.value)
     _check(_lib.rdr_bubble_eigenvalues(kind, l, p, _ptr(out), ctypes.byref(n)), "rdr_bubble_eigenvalues")
     return out
+
+
+def measure_fp64_peak(stream=None) -> float:
+    """FP64 tensor-core (DMMA) TFLOP/s of an issue-bound loop (roofline denominator)."""
+    t = ctypes.c_double()
+    _check(_lib.rdr_measure_fp64_peak(ctypes.byref(t), _stream(stream)), "rdr_measure_fp64_peak")
+    return t.value
 
 
 class Solver:

@@ -1,0 +1,60 @@
+"""Write tests/golden/oracle_pcg_iters.json: the CPU oracle's PCG iteration
+counts (R-A16, rtol 1e-8, x0 = 0) on the BASELINE.json configurations with
+their seeded rhs (the first vector drawn after the config).
+
+Calls only oracle/ and rdr_inputs/ (no CUDA path): these are the expected
+values of the +-1 iteration-count parity tests at sizes too large to run the
+oracle inside the GPU test session.
+
+    python scripts/oracle_golden.py 5:1-8 4 5:9-12 [3]
+"""
+import json
+import os
+import platform
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from rdr_inputs import make_config  # noqa: E402
+from oracle.solver import Oracle  # noqa: E402
+
+OUT = os.path.join(ROOT, "tests", "golden", "oracle_pcg_iters.json")
+
+
+def run(cfg, p):
+    t0 = time.time()
+    c = make_config(cfg, p=p) if p is not None else make_config(cfg)
+    O = Oracle(c.vertices, c.tets, c.p, c.space, c.alpha, c.beta, c.mask)
+    O.build_preconditioner(kappa=False)
+    b = c.draw_vector(O.n_total)
+    x, it, res = O.solve(b, rtol=1e-8)
+    return {"cfg": cfg, "p": c.p, "space": "hgrad" if c.space == 0 else "hcurl", "n_total": int(O.n_total),
+            "n_free": int(O.free.sum()), "iters": int(it), "true_rel_res": float(res),
+            "oracle_seconds": round(time.time() - t0, 1)}
+
+
+def main():
+    data = json.load(open(OUT)) if os.path.exists(OUT) else {"note": "", "entries": []}
+    data["note"] = ("Oracle PCG iteration counts (oracle/solver.py, R-A16, rtol 1e-8) on BASELINE.json configs "
+                    "with the seeded rhs; written by scripts/oracle_golden.py (oracle/ only).")
+    for spec in sys.argv[1:]:
+        if ":" in spec:
+            cfg, rng = spec.split(":")
+            lo, hi = (int(v) for v in rng.split("-")) if "-" in rng else (int(rng), int(rng))
+            jobs = [(int(cfg), p) for p in range(lo, hi + 1)]
+        else:
+            jobs = [(int(spec), None)]
+        for cfg, p in jobs:
+            e = run(cfg, p)
+            e["host"] = f"{platform.node()} ({os.cpu_count()} cpus)"
+            data["entries"] = [x for x in data["entries"] if not (x["cfg"] == e["cfg"] and x["p"] == e["p"])]
+            data["entries"].append(e)
+            data["entries"].sort(key=lambda x: (x["cfg"], x["p"]))
+            json.dump(data, open(OUT, "w"), indent=1)
+            print(json.dumps(e), flush=True)
+
+
+if __name__ == "__main__":
+    main()

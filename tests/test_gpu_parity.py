@@ -59,7 +59,7 @@ def _check_pcg(torch, c, S, O):
     return it, ito
 
 
-@pytest.mark.parametrize("p", [1, 2, 3, 4, 5, 6, 7, 8])
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 5, 6, 7, 8, 9, 10])
 @pytest.mark.parametrize("perturb", [False, True])
 def test_hgrad_small(torch_cuda, p, perturb):
     c, S, O = _pair(torch_cuda, 0, n=2, p=p, space=HGRAD, perturb=perturb, bc="all")
@@ -67,10 +67,20 @@ def test_hgrad_small(torch_cuda, p, perturb):
     _check_pcg(torch_cuda, c, S, O)
 
 
-@pytest.mark.parametrize("p", [1, 2, 3, 4, 5])
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 5, 6, 7, 8])
 @pytest.mark.parametrize("perturb", [False, True])
 def test_hcurl_small(torch_cuda, p, perturb):
     c, S, O = _pair(torch_cuda, 0, n=2, p=p, space=HCURL, perturb=perturb, bc="all")
+    _check_apply_precond(torch_cuda, c, S, O)
+    _check_pcg(torch_cuda, c, S, O)
+
+
+@pytest.mark.parametrize("p", [9, 10])
+@pytest.mark.parametrize("bc", ["all", "x0"])
+def test_hcurl_high_p(torch_cuda, p, bc):
+    """Ned1_9, Ned1_10 (north_star: H(curl) up to p=10) on the 6-tet cube; the
+    oracle's x87 reference element dominates the cost at these degrees."""
+    c, S, O = _pair(torch_cuda, 0, n=1, p=p, space=HCURL, perturb=False, bc=bc)
     _check_apply_precond(torch_cuda, c, S, O)
     _check_pcg(torch_cuda, c, S, O)
 
@@ -102,6 +112,7 @@ def test_config2(torch_cuda):
 
 @pytest.mark.parametrize("p", [1, 2, 3, 4])
 def test_config5_sweep_small_p(torch_cuda, p):
+    """configs[4] at p <= 4: full oracle (every row, PCG run by the oracle)."""
     c, S, O = _pair(torch_cuda, 5, p=p)
     O.build_preconditioner(kappa=False)
     _check_apply_precond(torch_cuda, c, S, O, nvec=1)
@@ -176,3 +187,97 @@ def test_degenerate_sizes(torch_cuda):
     c = make_config(0, n=1, p=12, space=HGRAD, bc="none")
     S = rdr.Solver(c.vertices, c.tets, 12, HGRAD, c.alpha, c.beta, c.mask)
     assert S.info["n_loc"] == 455
+
+
+# ---------------------------------------------------------------- full-size configs (sampled rows)
+import json
+import os
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "oracle_pcg_iters.json")
+
+
+def _golden_iters(cfg, p):
+    for e in json.load(open(GOLDEN))["entries"]:
+        if e["cfg"] == cfg and e["p"] == p:
+            return e["iters"]
+    raise KeyError(f"no oracle iteration count for cfg{cfg} p={p} in {GOLDEN} (scripts/oracle_golden.py)")
+
+
+def _sample_rows(O, n_vertices=3, n_cells=4, seed=1):
+    """Rows spanning every dof kind: the star dofs of a few interior vertices
+    (vertex, edge, face dofs), the interior dofs of a few cells, constrained dofs."""
+    rng = np.random.default_rng(seed)
+    t = O.topo
+    interior_v = np.nonzero(~t.dir_vertex)[0]
+    verts = rng.choice(interior_v, min(n_vertices, len(interior_v)), replace=False) if len(interior_v) else []
+    rows = []
+    for v in verts:
+        kind, idx = O.vertex_patch(int(v))
+        if kind == "pot":  # H(curl): Ned1 dofs of the edges / faces of the star
+            idx = np.nonzero(np.abs(O.G[:, idx]).sum(axis=1).A1)[0]
+        rows.extend(rng.choice(idx, min(12, len(idx)), replace=False))
+    for c in rng.choice(t.nt, n_cells, replace=False):
+        rows.extend(rng.choice(O.num.dofmap[c], 3, replace=False))
+    rows.extend(rng.choice(np.nonzero(O.num.constrained)[0], 3, replace=False) if O.num.constrained.any() else [])
+    return np.unique(np.asarray(rows, dtype=np.int64))
+
+
+def _check_sampled(torch, c, S, O, rows):
+    x = c.draw_vector(O.n_total)
+    xt = torch.from_numpy(x).cuda()
+    y = S.apply(xt).cpu().numpy()
+    z = S.precond(xt).cpu().numpy()
+    ya, za = O.apply_rows(x, rows), O.precond_rows(x, rows)
+    assert rel(y[rows], ya) <= TOL, rel(y[rows], ya)
+    assert rel(z[rows], za) <= TOL, rel(z[rows], za)
+    assert np.all(y[~O.free] == 0) and np.all(z[~O.free] == 0)
+
+
+def _check_sampled_pcg(torch, c, S, O, rows, iters_expected=None):
+    b = c.draw_vector(O.n_total)
+    x, it = S.solve(torch.from_numpy(b).cuda(), rtol=1e-8)
+    assert S.converged
+    if iters_expected is not None:
+        assert abs(it - iters_expected) <= 1, (it, iters_expected)
+    # true residual on the sampled rows, with the oracle's operator
+    bm = O.mask(b)
+    res = bm[rows] - O.apply_rows(x.cpu().numpy(), rows)
+    assert np.linalg.norm(res) <= 1e-5 * np.linalg.norm(bm[rows])
+    return it
+
+
+def _sampled_pair(cfg, **kw):
+    from paper_2506_17406_b200 import rdr
+    from oracle.sampled import SampledOracle
+    c = make_config(cfg, **kw)
+    S = rdr.Solver(c.vertices, c.tets, c.p, c.space, c.alpha, c.beta, c.mask)
+    O = SampledOracle(c.vertices, c.tets, c.p, c.space, c.alpha, c.beta, c.mask)
+    assert S.n_total == O.n_total
+    return c, S, O
+
+
+def test_config3_sampled(torch_cuda):
+    """BASELINE configs[2]: H(grad) p=10 on 16^3 x 6 (4.17 M dofs, 29 GB of patch
+    inverses). Oracle rows computed one by one (SURVEY §8(c) config-3 scope)."""
+    c, S, O = _sampled_pair(3)
+    rows = _sample_rows(O)
+    _check_sampled(torch_cuda, c, S, O, rows)
+    _check_sampled_pcg(torch_cuda, c, S, O, rows)
+
+
+def test_config4_sampled(torch_cuda):
+    """BASELINE configs[3]: H(curl) Ned1_6 on 12^3 x 6 with the type-I
+    potential + edge star patches; PCG iterations vs the oracle's (golden)."""
+    c, S, O = _sampled_pair(4)
+    rows = _sample_rows(O)
+    _check_sampled(torch_cuda, c, S, O, rows)
+    _check_sampled_pcg(torch_cuda, c, S, O, rows, _golden_iters(4, 6))
+
+
+@pytest.mark.parametrize("p", [5, 6, 7, 8, 9, 10, 11, 12])
+def test_config5_sweep(torch_cuda, p):
+    """BASELINE configs[4]: the p-sweep on the perturbed 8^3 x 6 mesh."""
+    c, S, O = _sampled_pair(5, p=p)
+    rows = _sample_rows(O, n_vertices=2, n_cells=3)
+    _check_sampled(torch_cuda, c, S, O, rows)
+    _check_sampled_pcg(torch_cuda, c, S, O, rows, _golden_iters(5, p))

@@ -1,0 +1,26 @@
+"""The sampled-row oracle (oracle/sampled.py, used for full-size parity at
+configs 3-5) against the global oracle: same rows of A x and P^-1 r on small
+meshes, both spaces, partial Dirichlet and coefficient contrast."""
+import numpy as np
+import pytest
+
+from rdr_inputs import make_config, HGRAD, HCURL
+from oracle.solver import Oracle
+from oracle.sampled import SampledOracle
+
+
+@pytest.mark.parametrize("space,p,bc,coeffs", [(HGRAD, 3, "all", "one"), (HGRAD, 4, "x0", "loguniform"),
+                                                (HCURL, 2, "all", "one"), (HCURL, 3, "x0", "loguniform")])
+def test_sampled_rows_match_global(space, p, bc, coeffs):
+    c = make_config(0, n=2, p=p, space=space, perturb=True, bc=bc, coeffs=coeffs)
+    O = Oracle(c.vertices, c.tets, c.p, c.space, c.alpha, c.beta, c.mask)
+    S = SampledOracle(c.vertices, c.tets, c.p, c.space, c.alpha, c.beta, c.mask)
+    x = c.draw_vector(O.n_total)
+    rng = np.random.default_rng(5)
+    # every dof kind: vertex/edge/face/cell entities, constrained and free
+    rows = np.unique(np.concatenate([rng.choice(O.n_total, 40, replace=False),
+                                     [O.num.offsets[d] for d in range(4) if O.num.per[d]]]))
+    y, z = O.apply(x), O.precond(x)
+    ys, zs = S.apply_rows(x, rows), S.precond_rows(x, rows)
+    assert np.allclose(ys, y[rows], rtol=1e-12, atol=1e-12 * np.abs(y).max())
+    assert np.allclose(zs, z[rows], rtol=1e-12, atol=1e-12 * np.abs(z).max())

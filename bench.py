@@ -73,19 +73,27 @@ class ClockSampler:
 
     def __init__(self, index=0, period=0.005):
         self.index, self.period = index, period
-        self.sm, self.reasons, self.max = [], set(), None
+        self.sm, self.reasons, self.max, self.errors = [], set(), None, set()
         self._stop = threading.Event()
 
     def _loop(self):
         import pynvml as nv
         h = nv.nvmlDeviceGetHandleByIndex(self.index)
         self.max = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        get_reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            getattr(nv, "nvmlDeviceGetCurrentClocksThrottleReasons")
         while not self._stop.is_set():
-            self.sm.append(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
-            bits = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
-            for name, attr in self.NAMES.items():
-                if bits & getattr(nv, attr, 0):
-                    self.reasons.add(name)
+            try:
+                self.sm.append(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+            except Exception as e:  # keep sampling; record what failed once
+                self.errors.add(type(e).__name__)
+            try:
+                bits = get_reasons(h)
+                for name, attr in self.NAMES.items():
+                    if bits & getattr(nv, attr, 0):
+                        self.reasons.add(name)
+            except Exception as e:
+                self.errors.add(type(e).__name__)
             time.sleep(self.period)
 
     def __enter__(self):
@@ -106,8 +114,11 @@ class ClockSampler:
     def summary(self):
         if not self.sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        return {"sm_mhz": float(np.median(self.sm)), "sm_max_mhz": self.max, "reasons": sorted(self.reasons),
-                "samples": len(self.sm)}
+        out = {"sm_mhz": float(np.median(self.sm)), "sm_max_mhz": self.max, "reasons": sorted(self.reasons),
+               "samples": len(self.sm), "sampler": f"NVML every {1e3 * self.period:.0f} ms"}
+        if self.errors:
+            out["sampler_errors"] = sorted(self.errors)
+        return out
 
 
 def dist_env():

@@ -184,7 +184,8 @@ __host__ __device__ __forceinline__ size_t apply_smem_bytes(int kp, int nm) {
 template <int BM, bool PCG>
 __global__ void __launch_bounds__((kApplyWarps + 1) * 32, 2)
     apply_tc_kernel(DevOperator op, const double* __restrict__ x, double* __restrict__ y, double* pq_acc,
-                    const PcgScalars* guard, PcgScalars* sc, double* pbuf0, double* pbuf1) {
+                    const PcgScalars* guard, PcgScalars* sc, double* pbuf0, double* pbuf1,
+                    cudaGraphConditionalHandle loop, int use_loop) {
   if (stopped(guard)) return;
   constexpr int MW = BM / 16;             // warps along M (16 cells each)
   constexpr int KS = kApplyWarps / MW;    // K-split groups
@@ -421,6 +422,9 @@ __global__ void __launch_bounds__((kApplyWarps + 1) * 32, 2)
       sc->zz = 0.0;
       sc->ticket = 0;
       sc->k = kit + 1;
+      // device-side PCG loop: the graph's while node runs another iteration
+      // body only while the stopping test has not fired
+      if (use_loop) cudaGraphSetConditional(loop, v->done ? 0u : 1u);
     }
   } else if (pq_acc) {
     __shared__ double sh[32];
@@ -439,6 +443,8 @@ size_t apply_smem(int bm, const DevOperator& op) {
 // cells per CTA: the largest of 64/32/16 whose tile fits in shared memory and
 // still gives two CTAs per SM (else one), so small meshes fill the 148 SMs
 int apply_bm(const DevOperator& op) {
+  static const int forced = std::getenv("RDR_APPLY_BM") ? std::atoi(std::getenv("RDR_APPLY_BM")) : 0;
+  if ((forced == 16 || forced == 32 || forced == 64) && apply_smem(forced, op) <= kMaxSmem) return forced;
   for (int want : {2 * 148, 148})
     for (int bm : {64, 32})
       if (apply_smem(bm, op) <= kMaxSmem && (op.n_cells + bm - 1) / bm * op.ngroups >= want) return bm;
@@ -447,21 +453,24 @@ int apply_bm(const DevOperator& op) {
 
 template <int BM, bool PCG>
 cudaError_t launch_apply_tc_bm(const DevOperator& op, const double* x, double* y, double* pq_acc,
-                               const PcgScalars* guard, cudaStream_t s, PcgScalars* sc, double* p0, double* p1) {
+                               const PcgScalars* guard, cudaStream_t s, PcgScalars* sc, double* p0, double* p1,
+                               cudaGraphConditionalHandle loop, int use_loop) {
   const size_t sm = apply_smem_bytes<BM>(op.kp, op.n_mat);
   dim3 grid((unsigned)((op.n_cells + BM - 1) / BM), (unsigned)op.ngroups);
-  apply_tc_kernel<BM, PCG><<<grid, (kApplyWarps + 1) * 32, sm, s>>>(op, x, y, pq_acc, guard, sc, p0, p1);
+  apply_tc_kernel<BM, PCG><<<grid, (kApplyWarps + 1) * 32, sm, s>>>(op, x, y, pq_acc, guard, sc, p0, p1, loop,
+                                                                    use_loop);
   return cudaGetLastError();
 }
 
 template <bool PCG>
 cudaError_t launch_apply_tc(const DevOperator& op, const double* x, double* y, double* pq_acc,
                             const PcgScalars* guard, cudaStream_t s, PcgScalars* sc = nullptr,
-                            double* p0 = nullptr, double* p1 = nullptr) {
+                            double* p0 = nullptr, double* p1 = nullptr, cudaGraphConditionalHandle loop = 0,
+                            int use_loop = 0) {
   const int bm = apply_bm(op);
-  if (bm == 64) return launch_apply_tc_bm<64, PCG>(op, x, y, pq_acc, guard, s, sc, p0, p1);
-  if (bm == 32) return launch_apply_tc_bm<32, PCG>(op, x, y, pq_acc, guard, s, sc, p0, p1);
-  return launch_apply_tc_bm<16, PCG>(op, x, y, pq_acc, guard, s, sc, p0, p1);
+  if (bm == 64) return launch_apply_tc_bm<64, PCG>(op, x, y, pq_acc, guard, s, sc, p0, p1, loop, use_loop);
+  if (bm == 32) return launch_apply_tc_bm<32, PCG>(op, x, y, pq_acc, guard, s, sc, p0, p1, loop, use_loop);
+  return launch_apply_tc_bm<16, PCG>(op, x, y, pq_acc, guard, s, sc, p0, p1, loop, use_loop);
 }
 
 template <int TC>
@@ -1169,8 +1178,8 @@ bool fused_pcg_supported(const DevOperator& op) {
 }
 
 cudaError_t launch_pcg_fused_apply(const DevOperator& op, PcgScalars* sc, const double* z, double* p0, double* p1,
-                                   double* q, cudaStream_t s) {
-  return launch_apply_tc<true>(op, z, q, nullptr, sc, s, sc, p0, p1);
+                                   double* q, cudaStream_t s, cudaGraphConditionalHandle loop, int use_loop) {
+  return launch_apply_tc<true>(op, z, q, nullptr, sc, s, sc, p0, p1, loop, use_loop);
 }
 
 cudaError_t launch_pcg_update_jacobi(PcgScalars* sc, const DevPrecond& pc, const double* p0, const double* p1,

@@ -89,8 +89,10 @@ cudaError_t launch_pcg_direction(PcgScalars* sc, const double* z, double* p, dou
 // Fused PCG step (3 kernels per iteration for H(grad)): fused apply (direction
 // update + A p + ||z||^2 + stopping test), update + interior Jacobi, patches.
 bool fused_pcg_supported(const DevOperator& op);
+// use_loop: also set the while-node condition `loop` of a device-side PCG graph
+// (continue while the stopping test has not fired)
 cudaError_t launch_pcg_fused_apply(const DevOperator& op, PcgScalars* sc, const double* z, double* p0, double* p1,
-                                   double* q, cudaStream_t s);
+                                   double* q, cudaStream_t s, cudaGraphConditionalHandle loop = 0, int use_loop = 0);
 cudaError_t launch_pcg_update_jacobi(PcgScalars* sc, const DevPrecond& pc, const double* p0, const double* p1,
                                      double* q, double* x, double* r, double* z, cudaStream_t s);
 

@@ -93,6 +93,8 @@ struct rdr_handle {
   PcgScalars* h_sc = nullptr;  // pinned
   cudaStream_t cap_stream = nullptr;
   cudaGraphExec_t graph = nullptr;
+  cudaGraphExec_t wgraph = nullptr;  // device-side while loop (fused path)
+  bool device_loop = true;           // RDR_PCG_HOSTLOOP=1: host-driven graph of 8 iterations instead
   int graph_iters = 0;
   int launches_per_iter = 0;
   int64_t last_launches = 0;
@@ -110,6 +112,7 @@ struct rdr_handle {
   }
   ~rdr_handle() {
     if (graph) cudaGraphExecDestroy(graph);
+    if (wgraph) cudaGraphExecDestroy(wgraph);
     if (cap_stream) cudaStreamDestroy(cap_stream);
     for (void* p : owned) cudaFree(p);
     if (h_sc) cudaFreeHost(h_sc);
@@ -300,6 +303,7 @@ static int setup_impl(rdr_handle* h, const double* vertices, int64_t nv, const i
   for (double** v : {&h->d_x, &h->d_r, &h->d_z, &h->d_p, &h->d_q, &h->d_b, &h->d_p2})
     if ((st = h->own_alloc((void**)v, vb))) return st;
   h->fused = fused_pcg_supported(op);
+  h->device_loop = std::getenv("RDR_PCG_HOSTLOOP") == nullptr;
   if ((st = h->own_alloc((void**)&h->d_sc, sizeof(PcgScalars)))) return st;
   CK(cudaMallocHost((void**)&h->h_sc, sizeof(PcgScalars)));
   CK(cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
@@ -386,10 +390,10 @@ int rdr_precond(rdr_handle* h, const double* r, double* z, void* stream) {
   return RDR_OK;
 }
 
-static int enqueue_iteration(rdr_handle* h, cudaStream_t s) {
+static int enqueue_iteration(rdr_handle* h, cudaStream_t s, cudaGraphConditionalHandle loop = 0, int use_loop = 0) {
   const int64_t n = h->n_total;
   if (h->fused) {  // 3 kernels (+2 for the H(curl) discrete gradient) per PCG iteration
-    CK(launch_pcg_fused_apply(h->op, h->d_sc, h->d_z, h->d_p, h->d_p2, h->d_q, s));
+    CK(launch_pcg_fused_apply(h->op, h->d_sc, h->d_z, h->d_p, h->d_p2, h->d_q, s, loop, use_loop));
     CK(launch_pcg_update_jacobi(h->d_sc, h->pc, h->d_p, h->d_p2, h->d_q, h->d_x, h->d_r, h->d_z, s));
     for (int part = 1; part < 4; ++part)
       CK(launch_precond_part(part, h->pc, h->d_r, h->d_z, &h->d_sc->rz_acc, h->d_sc, s));
@@ -419,11 +423,59 @@ static int build_graph(rdr_handle* h, int iters) {
   return RDR_OK;
 }
 
+// Device-side PCG loop (fused path): one graph whose while node repeats the
+// iteration body until the fused apply's stopping test clears the condition,
+// so a whole solve is one graph launch and one host synchronisation.
+static int build_while_graph(rdr_handle* h) {
+  if (h->wgraph) return RDR_OK;
+  cudaGraph_t g;
+  CK(cudaGraphCreate(&g, 0));
+  cudaGraphConditionalHandle loop;
+  CK(cudaGraphConditionalHandleCreate(&loop, g, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams params = {};
+  params.type = cudaGraphNodeTypeConditional;
+  params.conditional.handle = loop;
+  params.conditional.type = cudaGraphCondTypeWhile;
+  params.conditional.size = 1;
+  cudaGraphNode_t node;
+  CK(cudaGraphAddNode(&node, g, nullptr, 0, &params));
+  cudaGraph_t body = params.conditional.phGraph_out[0];
+  CK(cudaStreamBeginCaptureToGraph(h->cap_stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+  int st = enqueue_iteration(h, h->cap_stream, loop, 1);
+  cudaError_t e = cudaStreamEndCapture(h->cap_stream, &body);
+  if (st) return st;
+  CK(e);
+  e = cudaGraphInstantiate(&h->wgraph, g, 0);
+  cudaGraphDestroy(g);
+  CK(e);
+  return RDR_OK;
+}
+
 static int solve_device(rdr_handle* h, const double* b, double rtol, int maxit, int* iters, cudaStream_t s) {
   const int64_t n = h->n_total;
   int st;
-  if ((st = build_graph(h, 8))) return st;
   int64_t launches = 0;
+  if (h->fused && h->device_loop) {
+    if ((st = build_while_graph(h))) return st;
+    CK(cudaStreamSynchronize(s));  // h_sc (pinned) is reused as the H2D template
+    std::memset(h->h_sc, 0, sizeof(PcgScalars));
+    h->h_sc->rtol = rtol;
+    h->h_sc->maxit = maxit;
+    CK(cudaMemcpyAsync(h->d_sc, h->h_sc, sizeof(PcgScalars), cudaMemcpyHostToDevice, s));
+    CK(cudaMemsetAsync(h->d_p, 0, sizeof(double) * n, s));
+    CK(cudaMemsetAsync(h->d_p2, 0, sizeof(double) * n, s));
+    CK(launch_pcg_init(b, h->d_cons, n, h->d_x, h->d_r, h->d_q, s));
+    CK(launch_precond(h->pc, h->d_r, h->d_z, &h->d_sc->rz_acc, nullptr, s));
+    CK(cudaGraphLaunch(h->wgraph, s));
+    CK(cudaMemcpyAsync(h->h_sc, h->d_sc, sizeof(PcgScalars), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    // the loop ran k bodies: the last one detected convergence (or maxit)
+    launches = 1 + count_precond_launches(h->pc) + (int64_t)h->h_sc->k * h->launches_per_iter;
+    h->last_launches = launches;
+    *iters = h->h_sc->iters;
+    return h->h_sc->converged ? RDR_OK : RDR_ENOCONV;
+  }
+  if ((st = build_graph(h, 8))) return st;
   if (h->fused) {
     CK(cudaStreamSynchronize(s));  // h_sc (pinned) is reused as the H2D template
     std::memset(h->h_sc, 0, sizeof(PcgScalars));

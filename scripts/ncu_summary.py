@@ -18,6 +18,10 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "smsp__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
         "sm__pipe_tensor_op_dmma_cycles_active.avg.pct_of_peak_sustained_active",
         "sm__inst_executed_pipe_tensor_op_dmma.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active",
+        "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+        "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+        "smsp__issue_active.avg.pct_of_peak_sustained_active",
         "lts__t_bytes.sum", "l1tex__t_bytes.sum", "sm__cycles_elapsed.avg.per_second",
         "dram__cycles_elapsed.avg.per_second", "smsp__average_warp_latency_issue_stalled"]
 
@@ -58,5 +62,32 @@ def full(path):
                 print(f"{k:75s} {r[i]:>16s} {units[i]}")
 
 
+def traffic(path, key, out="profiles/traffic.json"):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of each kernel in
+    an `ncu --set full` report -> profiles/traffic.json[key][kernel] (read by
+    bench.py's roofline.traffic)."""
+    import json
+    import os
+    res = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(res)))
+    h, units = rows[0], rows[1]
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+    agg = collections.defaultdict(list)
+    for r in rows[2:]:
+        name = r[h.index("Kernel Name")].split("(")[0].split("<")[0].split("::")[-1]
+        tot = 0.0
+        for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            i = h.index(m)
+            tot += float(r[i].replace(",", "")) * scale.get(units[i], 1.0)
+        agg[name].append(tot)
+    data = json.load(open(out)) if os.path.exists(out) else {}
+    data.setdefault(key, {})
+    for name, v in agg.items():
+        data[key][name] = {"dram_bytes_per_launch": sum(v) / len(v), "launches_profiled": len(v),
+                           "source": f"ncu --set full --clock-control none ({os.path.basename(path)})"}
+        print(key, name, sum(v) / len(v))
+    json.dump(data, open(out, "w"), indent=1)
+
+
 if __name__ == "__main__":
-    {"launches": launches, "full": full}[sys.argv[1]](sys.argv[2])
+    {"launches": launches, "full": full, "traffic": traffic}[sys.argv[1]](*sys.argv[2:])

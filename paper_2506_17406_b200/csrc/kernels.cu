@@ -440,15 +440,14 @@ size_t apply_smem(int bm, const DevOperator& op) {
                   : bm == 32 ? apply_smem_bytes<32>(op.kp, op.n_mat) : apply_smem_bytes<16>(op.kp, op.n_mat);
 }
 
-// cells per CTA: the largest of 64/32/16 whose tile fits in shared memory and
-// still gives two CTAs per SM (else one), so small meshes fill the 148 SMs
+// cells per CTA: 32 when two such CTAs fit on an SM (the two desynchronise, so
+// one's gather and epilogue overlap the other's DMMA loop), else 16; BM = 64
+// (one CTA per SM) measured 15-20% slower on configs 2, 4 and 5 (p = 10, 12).
 int apply_bm(const DevOperator& op) {
   static const int forced = std::getenv("RDR_APPLY_BM") ? std::atoi(std::getenv("RDR_APPLY_BM")) : 0;
   if ((forced == 16 || forced == 32 || forced == 64) && apply_smem(forced, op) <= kMaxSmem) return forced;
-  for (int want : {2 * 148, 148})
-    for (int bm : {64, 32})
-      if (apply_smem(bm, op) <= kMaxSmem && (op.n_cells + bm - 1) / bm * op.ngroups >= want) return bm;
-  return apply_smem(32, op) <= kMaxSmem ? 32 : 16;
+  const size_t two_per_sm = 228 * 1024 / 2 - 1024;
+  return apply_smem(32, op) <= two_per_sm ? 32 : 16;
 }
 
 template <int BM, bool PCG>
@@ -820,8 +819,6 @@ size_t patch_smem_bytes(int slots, int npad_max, int zbufs) {
 // Half-tiles keep the kernel at <= 64 registers, i.e. 4 CTAs = 32 warps per
 // SM streaming. Row products (-> z_I) are dot products with r_J; transposed
 // products (-> z_J) are a 16-value transpose reduction across the warp.
-constexpr int kLdgWarps = 8;
-
 __device__ __forceinline__ double4 ld_stream4(const double4* p) {
   double4 v;
   asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v4.f64 {%0, %1, %2, %3}, [%4];"
@@ -854,7 +851,8 @@ __device__ __forceinline__ double treduce16(double (&v)[16], int lane) {
   return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 16);
 }
 
-__global__ void __launch_bounds__(kLdgWarps * 32, 4)
+template <int kLdgWarps>
+__global__ void __launch_bounds__(kLdgWarps * 32, 32 / kLdgWarps)
     patch_ldg_kernel(DevPrecond pc, const double* __restrict__ r, double* __restrict__ z, double* rz_acc,
                      const PcgScalars* guard) {
   if (stopped(guard)) return;
@@ -1127,9 +1125,12 @@ cudaError_t launch_precond_part(int part, const DevPrecond& pc, const double* r,
         if (pc.kernel == 1)
           patch_stream_kernel<<<(unsigned)pc.n_ctas, kPatchWarps * 32,
                                 patch_smem_bytes(pc.ring_slots, pc.npad_max, pc.zbufs), s>>>(pc, r, z, rz_acc, guard);
+        else if (pc.ldg_warps == 4)
+          patch_ldg_kernel<4><<<(unsigned)pc.n_patches, 4 * 32,
+                                 2 * sizeof(double) * pc.npad_max, s>>>(pc, r, z, rz_acc, guard);
         else
-          patch_ldg_kernel<<<(unsigned)pc.n_patches, kLdgWarps * 32, 2 * sizeof(double) * pc.npad_max, s>>>(
-              pc, r, z, rz_acc, guard);
+          patch_ldg_kernel<8><<<(unsigned)pc.n_patches, 8 * 32,
+                                 2 * sizeof(double) * pc.npad_max, s>>>(pc, r, z, rz_acc, guard);
       }
       break;
     case 3:
@@ -1215,7 +1216,8 @@ void configure_kernels() {  // errors here would surface as a later launch's cud
   cudaFuncSetAttribute(apply_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(apply_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(patch_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
-  cudaFuncSetAttribute(patch_ldg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
+  cudaFuncSetAttribute(patch_ldg_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
+  cudaFuncSetAttribute(patch_ldg_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
   cudaFuncSetAttribute(apply_tc_kernel<64, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
   cudaFuncSetAttribute(apply_tc_kernel<64, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
   cudaFuncSetAttribute(apply_tc_kernel<32, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);

@@ -245,14 +245,19 @@ static int setup_impl(rdr_handle* h, const double* vertices, int64_t nv, const i
   {
     const char* pk = std::getenv("RDR_PATCH_KERNEL");
     pc.kernel = (pk && std::strcmp(pk, "tma") == 0) ? 1 : 0;
-    const char* pw = std::getenv("RDR_PATCH_WARPS");
-    pc.ldg_warps = (pw && std::atoi(pw) == 4) ? 4 : 8;
+    pc.ldg_warps = 8;  // decided below from the patch sizes (RDR_PATCH_WARPS=4|8 overrides)
   }
   st = build_patches(m, num, el, coef, space == RDR_HCURL ? &cg_num : nullptr, cg_el,
                      space == RDR_HCURL ? &cg_coef : nullptr, P, sink, pc.kernel == 1 ? kTileSwizzled : kTileGroups);
   if (sink.d) h->owned.push_back(sink.d);
   if (st) return st;
   pc.n_patches = (int64_t)P.n.size();
+  {  // mostly small patches (<= 4 tile rows, e.g. the H(curl) edge stars): 4-warp CTAs, 8 per SM
+    int64_t small = 0;
+    for (int32_t n : P.n) small += n <= 128;
+    pc.ldg_warps = 2 * small > pc.n_patches ? 4 : 8;
+    if (const char* pw = std::getenv("RDR_PATCH_WARPS")) pc.ldg_warps = std::atoi(pw) == 4 ? 4 : 8;
+  }
   pc.max_n = P.max_n;
   int32_t *d_pn, *d_idx;
   int64_t *d_io, *d_to;

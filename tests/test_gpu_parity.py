@@ -281,3 +281,56 @@ def test_config5_sweep(torch_cuda, p):
     rows = _sample_rows(O, n_vertices=2, n_cells=3)
     _check_sampled(torch_cuda, c, S, O, rows)
     _check_sampled_pcg(torch_cuda, c, S, O, rows, _golden_iters(5, p))
+
+
+# ---------------------------------------------------------------- ABI semantics on the device
+def test_stream_semantics_and_repeated_setup(torch_cuda):
+    """apply / precond are asynchronous on the caller's stream (results visible
+    after a sync on that stream only); setup/destroy can be repeated; a handle
+    solves repeatedly with identical results (deterministic iteration count)."""
+    from paper_2506_17406_b200 import rdr
+    torch = torch_cuda
+    c = make_config(0, n=2, p=4, space=HGRAD, perturb=True, bc="x0", coeffs="loguniform")
+    for _ in range(3):
+        S = rdr.Solver(c.vertices, c.tets, c.p, c.space, c.alpha, c.beta, c.mask)
+        S.close()
+    S = rdr.Solver(c.vertices, c.tets, c.p, c.space, c.alpha, c.beta, c.mask)
+    x = torch.from_numpy(c.draw_vector(S.n_total)).cuda()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        y = S.apply(x, stream=s)
+        z = S.precond(x, stream=s)
+    s.synchronize()
+    y0 = S.apply(x)
+    z0 = S.precond(x)
+    torch.cuda.synchronize()
+    assert rel(y.cpu().numpy(), y0.cpu().numpy()) <= 1e-14
+    assert rel(z.cpu().numpy(), z0.cpu().numpy()) <= 1e-14
+    b = torch.from_numpy(c.draw_vector(S.n_total)).cuda()
+    its = [S.solve(b)[1] for _ in range(3)]
+    assert len(set(its)) == 1
+
+
+def test_solve_maxit_and_host_path(torch_cuda):
+    """maxit reached -> RDR_ENOCONV semantics (iters == maxit, x written,
+    converged False); rtol = 0 runs exactly maxit iterations; the host-buffer
+    entry point (rdr_solve_host) returns the same iterate as the device one."""
+    from paper_2506_17406_b200 import rdr
+    torch = torch_cuda
+    c, S, O = _pair(torch, 0, n=2, p=3, space=HGRAD, perturb=True, bc="all")
+    b = c.draw_vector(O.n_total)
+    bt = torch.from_numpy(b).cuda()
+    x, it = S.solve(bt, rtol=1e-12, maxit=5)
+    assert it == 5 and not S.converged
+    xo, ito, _ = O.solve(b, rtol=0.0, maxit=5)
+    assert ito == 5 and rel(x.cpu().numpy(), xo) <= 1e-10
+    xd, itd = S.solve(bt, rtol=1e-8)
+    bh = torch.from_numpy(b).pin_memory()
+    xh = torch.empty(S.n_total, dtype=torch.float64).pin_memory()
+    ith = S.solve_host(bh, xh)
+    assert ith == itd and rel(xh.numpy(), xd.cpu().numpy()) <= 1e-14
+
+
+def test_smoke_entry_point(torch_cuda):
+    import __graft_entry__
+    __graft_entry__.smoke()

@@ -24,9 +24,51 @@ namespace {
 
 constexpr int kVecThreads = 256;
 
+// Launch with the programmatic stream-serialization attribute (PDL, see
+// pdl_wait); RDR_PDL=0 launches plainly. Every kernel launched this way calls
+// pdl_wait() before it reads anything a predecessor kernel writes.
+bool pdl_enabled() {
+  static const bool on = !(std::getenv("RDR_PDL") && std::getenv("RDR_PDL")[0] == '0');
+  return on;
+}
+bool pdl_patch_enabled() {  // RDR_PDL_PATCH=0: launch the patch kernel without PDL
+  static const bool on = pdl_enabled() && !(std::getenv("RDR_PDL_PATCH") && std::getenv("RDR_PDL_PATCH")[0] == '0');
+  return on;
+}
+template <typename... Params, typename... Args>
+cudaError_t launch_kx(bool pdl, void (*kernel)(Params...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                      Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl && pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<Params>(args)...);
+}
+template <typename... Params, typename... Args>
+cudaError_t launch_k(void (*kernel)(Params...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+  return launch_kx(true, kernel, grid, block, smem, s, args...);
+}
+
 __device__ __forceinline__ bool stopped(const PcgScalars* g) {
   return g != nullptr && *((volatile const int32_t*)&g->done) != 0;
 }
+
+// Programmatic dependent launch (PDL): a kernel launched with the programmatic
+// stream-serialization attribute may start while its predecessor drains; it
+// loads only constant data (dof maps, patch metadata, reference stack) before
+// griddepcontrol.wait, which returns once the predecessor grid has completed
+// and its memory is visible. Without the attribute both are no-ops.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+// dependents may launch once every CTA has finished its main loop (an early
+// trigger let waiting dependent CTAs take SM slots from the patch kernel)
+__device__ __forceinline__ bool pdl_late() { return true; }
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -186,7 +228,6 @@ __global__ void __launch_bounds__((kApplyWarps + 1) * 32, 2)
     apply_tc_kernel(DevOperator op, const double* __restrict__ x, double* __restrict__ y, double* pq_acc,
                     const PcgScalars* guard, PcgScalars* sc, double* pbuf0, double* pbuf1,
                     cudaGraphConditionalHandle loop, int use_loop) {
-  if (stopped(guard)) return;
   constexpr int MW = BM / 16;             // warps along M (16 cells each)
   constexpr int KS = kApplyWarps / MW;    // K-split groups
   static_assert(MW * KS == kApplyWarps && kApplySlots % KS == 0, "warp layout");
@@ -197,6 +238,7 @@ __global__ void __launch_bounds__((kApplyWarps + 1) * 32, 2)
   const int n = op.n_loc, nm = op.n_mat, kp = op.kp;
   const int XS = apply_x_stride(kp);
   double* X = ring + kApplySlots * kApplyKC * kApplyCols;              // [BM][XS]
+  long long* Xi = reinterpret_cast<long long*>(X);                    // the same slots, holding dof ids first
   double* C = X + BM * XS;                                             // [BM][nm]
   int* D = reinterpret_cast<int*>(C + BM * nm);                        // [BM][32] dofs of this CTA's columns
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -205,6 +247,7 @@ __global__ void __launch_bounds__((kApplyWarps + 1) * 32, 2)
   const double* __restrict__ Bg = op.Bsw + (size_t)cg * op.kpad * kApplyCols;
   constexpr uint32_t kChunkBytes = kApplyKC * kApplyCols * sizeof(double);
 
+  // ---- prologue on constant data only (overlaps the previous kernel under PDL)
   if (threadIdx.x == 0) {
     for (int s = 0; s < kApplySlots; ++s) {
       mbar_init(&full[s], 1);
@@ -214,11 +257,35 @@ __global__ void __launch_bounds__((kApplyWarps + 1) * 32, 2)
   }
   __syncthreads();
   const bool producer = warp == kApplyWarps;
-  if (producer && lane == 0) {  // fill the ring while everyone gathers
-    for (int c = 0; c < nchunks && c < kApplySlots; ++c) {
+  const int prefilled = min(nchunks, kApplySlots);
+  if (producer && lane == 0) {  // fill the ring with the reference stack while everyone gathers
+    for (int c = 0; c < prefilled; ++c) {
       mbar_expect_tx(&full[c], kChunkBytes);
       bulk_g2s(ring + c * kApplyKC * kApplyCols, Bg + (size_t)c * kApplyKC * kApplyCols, kChunkBytes, &full[c]);
     }
+  }
+  const int64_t c0 = (int64_t)blockIdx.x * BM;
+  const int nc = (int)min((int64_t)BM, op.n_cells - c0);
+  const int nthr = blockDim.x;
+  for (int e = threadIdx.x; e < BM * XS; e += nthr) {  // dof ids of the tile (X slots), this CTA's columns
+    const int c = e / XS, j = e - c * XS;
+    const int gd = (c < nc && j < n) ? op.dofmap_m[(c0 + c) * n + j] : -1;
+    Xi[e] = gd;
+    if (j >= col0 && j < col0 + kApplyCols) D[c * kApplyCols + (j - col0)] = (j < n) ? gd : -1;
+  }
+  for (int e = threadIdx.x; e < BM * nm; e += nthr) {
+    const int c = e / nm;
+    C[e] = (c < nc) ? op.coef[(c0 + c) * nm + (e - c * nm)] : 0.0;
+  }
+  // columns past n_loc (n not a multiple of 32): never written by the loop above
+  for (int e = threadIdx.x; e < BM * kApplyCols; e += nthr)
+    if (col0 + (e % kApplyCols) >= n) D[e] = -1;
+
+  pdl_wait();
+  if (stopped(guard)) {  // drain the prefilled ring before the CTA's shared memory goes away
+    if (producer && lane == 0)
+      for (int c = 0; c < prefilled; ++c) mbar_wait(&full[c], 0);
+    return;
   }
 
   // ---- PCG mode: direction update p_k = z_k + beta_k p_{k-1} folded into the gather
@@ -235,19 +302,15 @@ __global__ void __launch_bounds__((kApplyWarps + 1) * 32, 2)
   }
   double zz = 0.0;
 
-  // ---- gather X (BM x XS, zero padded), coefficients and this CTA's dof columns
-  const int64_t c0 = (int64_t)blockIdx.x * BM;
-  const int nc = (int)min((int64_t)BM, op.n_cells - c0);
+  // ---- gather X in place (each thread reads back the dof ids it stored above)
   {
     constexpr int GB = 8;
-    const int nthr = blockDim.x;
     for (int e0 = 0; e0 < BM * XS; e0 += GB * nthr) {
       int gd[GB];
 #pragma unroll
       for (int i = 0; i < GB; ++i) {
         const int e = e0 + i * nthr + threadIdx.x;
-        const int c = e / XS, j = e - c * XS;
-        gd[i] = (e < BM * XS && c < nc && j < n) ? op.dofmap_m[(c0 + c) * n + j] : -1;
+        gd[i] = e < BM * XS ? (int)Xi[e] : -1;
       }
       double xv[GB], pv[GB];
 #pragma unroll
@@ -259,26 +322,18 @@ __global__ void __launch_bounds__((kApplyWarps + 1) * 32, 2)
       for (int i = 0; i < GB; ++i) {
         const int e = e0 + i * nthr + threadIdx.x;
         if (e >= BM * XS) continue;
-        const int c = e / XS, j = e - c * XS;
         double v = xv[i];
         if (PCG && gd[i] >= 0) {
           v = fma(beta, pv[i], xv[i]);
+          const int c = e / XS, j = e - c * XS;
           if (cg == 0 && op.owner[(c0 + c) * n + j]) {
             p_new[gd[i]] = v;
             zz = fma(xv[i], xv[i], zz);
           }
         }
         X[e] = v;
-        if (j >= col0 && j < col0 + kApplyCols) D[c * kApplyCols + (j - col0)] = (j < n) ? gd[i] : -1;
       }
     }
-    for (int e = threadIdx.x; e < BM * nm; e += nthr) {
-      const int c = e / nm;
-      C[e] = (c < nc) ? op.coef[(c0 + c) * nm + (e - c * nm)] : 0.0;
-    }
-    // columns past n_loc (n not a multiple of 32): never written by the loop above
-    for (int e = threadIdx.x; e < BM * kApplyCols; e += nthr)
-      if (col0 + (e % kApplyCols) >= n) D[e] = -1;
   }
   __syncthreads();
 
@@ -340,6 +395,7 @@ __global__ void __launch_bounds__((kApplyWarps + 1) * 32, 2)
     }
   }
   __syncthreads();  // every chunk consumed (all bulk copies complete): the ring is free
+  if (pdl_late()) pdl_trigger();
 
   // ---- K-split reduction through the ring, then scatter-add from group 0
   double* red = ring;  // [(KS-1)][MW][16][32]
@@ -456,9 +512,8 @@ cudaError_t launch_apply_tc_bm(const DevOperator& op, const double* x, double* y
                                cudaGraphConditionalHandle loop, int use_loop) {
   const size_t sm = apply_smem_bytes<BM>(op.kp, op.n_mat);
   dim3 grid((unsigned)((op.n_cells + BM - 1) / BM), (unsigned)op.ngroups);
-  apply_tc_kernel<BM, PCG><<<grid, (kApplyWarps + 1) * 32, sm, s>>>(op, x, y, pq_acc, guard, sc, p0, p1, loop,
-                                                                    use_loop);
-  return cudaGetLastError();
+  return launch_k(apply_tc_kernel<BM, PCG>, grid, dim3((kApplyWarps + 1) * 32), sm, s, op, x, y, pq_acc, guard, sc,
+                  p0, p1, loop, use_loop);
 }
 
 template <bool PCG>
@@ -489,6 +544,7 @@ cudaError_t launch_apply_simple(const DevOperator& op, const double* x, double* 
 // ---------------------------------------------------------------- preconditioner
 __global__ void precond_init_kernel(DevPrecond pc, const double* __restrict__ r, double* __restrict__ z,
                                     double* rz_acc, const PcgScalars* guard) {
+  pdl_wait();
   if (stopped(guard)) return;
   double part = 0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -512,6 +568,7 @@ __global__ void precond_init_kernel(DevPrecond pc, const double* __restrict__ r,
 }
 
 __global__ void gather_grad_kernel(DevPrecond pc, const double* __restrict__ r, const PcgScalars* guard) {
+  pdl_wait();
   if (stopped(guard)) return;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < pc.n_cg_iface; c += stride) {
@@ -522,6 +579,7 @@ __global__ void gather_grad_kernel(DevPrecond pc, const double* __restrict__ r, 
 }
 
 __global__ void scatter_grad_kernel(DevPrecond pc, double* __restrict__ z, const PcgScalars* guard) {
+  pdl_wait();
   if (stopped(guard)) return;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < pc.n_cg_iface; c += stride) {
@@ -636,6 +694,7 @@ __device__ __forceinline__ void issue_tile(const DevPrecond& pc, const TileCurso
 __global__ void __launch_bounds__(kPatchWarps * 32, 2)
     patch_stream_kernel(DevPrecond pc, const double* __restrict__ r, double* __restrict__ z, double* rz_acc,
                         const PcgScalars* guard) {
+  pdl_wait();
   if (stopped(guard)) return;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int K = pc.ring_slots / kPatchWarps;  // slots per warp
@@ -855,7 +914,6 @@ template <int kLdgWarps>
 __global__ void __launch_bounds__(kLdgWarps * 32, 32 / kLdgWarps)
     patch_ldg_kernel(DevPrecond pc, const double* __restrict__ r, double* __restrict__ z, double* rz_acc,
                      const PcgScalars* guard) {
-  if (stopped(guard)) return;
   extern __shared__ double smem[];
   const int pid = blockIdx.x;
   const int n = pc.pn[pid];
@@ -866,10 +924,18 @@ __global__ void __launch_bounds__(kLdgWarps * 32, 32 / kLdgWarps)
   double* rl = smem;
   double* zl = smem + npad;
   const int32_t* id = pc.idx + pc.idx_off[pid];
+  // prologue on constant data (overlaps the previous kernel under PDL): the
+  // patch's dof ids go into the r slots, replaced by r in place after the wait
+  long long* rli = reinterpret_cast<long long*>(rl);
   for (int i = threadIdx.x; i < npad; i += blockDim.x) {
-    const int g = id[i];
-    rl[i] = (g >= 0) ? rin[g] : 0.0;
+    rli[i] = id[i];
     zl[i] = 0.0;
+  }
+  pdl_wait();
+  if (stopped(guard)) return;
+  for (int i = threadIdx.x; i < npad; i += blockDim.x) {
+    const int g = (int)rli[i];
+    rl[i] = (g >= 0) ? rin[g] : 0.0;
   }
   __syncthreads();
   const double* T = pc.tiles + pc.tile_off[pid];
@@ -931,6 +997,7 @@ __global__ void __launch_bounds__(kLdgWarps * 32, 32 / kLdgWarps)
       ++I;
     }
   }
+  if (pdl_late()) pdl_trigger();
   __syncthreads();
   double part = 0.0;
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
@@ -1048,6 +1115,7 @@ __global__ void pcg_finish_kernel(PcgScalars* sc, const double* __restrict__ z, 
 __global__ void pcg_update_jacobi_kernel(PcgScalars* sc, DevPrecond pc, const double* __restrict__ p0,
                                          const double* __restrict__ p1, double* __restrict__ q,
                                          double* __restrict__ x, double* __restrict__ r, double* __restrict__ z) {
+  pdl_wait();
   if (stopped(sc)) return;
   const int kk = *((volatile int32_t*)&sc->k) - 1;  // iteration of the apply that just ran
   const double* __restrict__ p = (kk & 1) ? p1 : p0;
@@ -1115,26 +1183,25 @@ cudaError_t launch_precond_part(int part, const DevPrecond& pc, const double* r,
                                 const PcgScalars* guard, cudaStream_t s) {
   switch (part) {
     case 0:
-      precond_init_kernel<<<vec_grid(pc.n_total), kVecThreads, 0, s>>>(pc, r, z, rz_acc, guard);
-      break;
+      return launch_k(precond_init_kernel, dim3(vec_grid(pc.n_total)), dim3(kVecThreads), 0, s, pc, r, z, rz_acc,
+                      guard);
     case 1:
-      if (pc.gbuf) gather_grad_kernel<<<vec_grid(pc.n_cg_iface), kVecThreads, 0, s>>>(pc, r, guard);
+      if (pc.gbuf) return launch_k(gather_grad_kernel, dim3(vec_grid(pc.n_cg_iface)), dim3(kVecThreads), 0, s, pc, r, guard);
       break;
     case 2:
       if (pc.n_patches > 0) {
         if (pc.kernel == 1)
-          patch_stream_kernel<<<(unsigned)pc.n_ctas, kPatchWarps * 32,
-                                patch_smem_bytes(pc.ring_slots, pc.npad_max, pc.zbufs), s>>>(pc, r, z, rz_acc, guard);
-        else if (pc.ldg_warps == 4)
-          patch_ldg_kernel<4><<<(unsigned)pc.n_patches, 4 * 32,
-                                 2 * sizeof(double) * pc.npad_max, s>>>(pc, r, z, rz_acc, guard);
-        else
-          patch_ldg_kernel<8><<<(unsigned)pc.n_patches, 8 * 32,
-                                 2 * sizeof(double) * pc.npad_max, s>>>(pc, r, z, rz_acc, guard);
+          return launch_k(patch_stream_kernel, dim3(pc.n_ctas), dim3(kPatchWarps * 32),
+                          patch_smem_bytes(pc.ring_slots, pc.npad_max, pc.zbufs), s, pc, r, z, rz_acc, guard);
+        if (pc.ldg_warps == 4)
+          return launch_kx(pdl_patch_enabled(), patch_ldg_kernel<4>, dim3(pc.n_patches), dim3(4 * 32), 2 * sizeof(double) * pc.npad_max, s,
+                          pc, r, z, rz_acc, guard);
+        return launch_kx(pdl_patch_enabled(), patch_ldg_kernel<8>, dim3(pc.n_patches), dim3(8 * 32), 2 * sizeof(double) * pc.npad_max, s,
+                        pc, r, z, rz_acc, guard);
       }
       break;
     case 3:
-      if (pc.gbuf) scatter_grad_kernel<<<vec_grid(pc.n_cg_iface), kVecThreads, 0, s>>>(pc, z, guard);
+      if (pc.gbuf) return launch_k(scatter_grad_kernel, dim3(vec_grid(pc.n_cg_iface)), dim3(kVecThreads), 0, s, pc, z, guard);
       break;
   }
   return cudaGetLastError();
@@ -1185,8 +1252,8 @@ cudaError_t launch_pcg_fused_apply(const DevOperator& op, PcgScalars* sc, const 
 
 cudaError_t launch_pcg_update_jacobi(PcgScalars* sc, const DevPrecond& pc, const double* p0, const double* p1,
                                      double* q, double* x, double* r, double* z, cudaStream_t s) {
-  pcg_update_jacobi_kernel<<<vec_grid(pc.n_total), kVecThreads, 0, s>>>(sc, pc, p0, p1, q, x, r, z);
-  return cudaGetLastError();
+  return launch_k(pcg_update_jacobi_kernel, dim3(vec_grid(pc.n_total)), dim3(kVecThreads), 0, s, sc, pc, p0, p1, q, x,
+                  r, z);
 }
 
 // FP64 tensor-core peak microbenchmark (roofline denominator of the apply,

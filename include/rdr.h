@@ -40,6 +40,23 @@ typedef struct rdr_handle rdr_handle;
 
 enum { RDR_HGRAD = 0, RDR_HCURL = 1 };
 
+/* Space decomposition of the preconditioner (both one-level additive, unit
+ * weights, exact local solvers; DESIGN.md R-A13..A15):
+ *   RDR_SPLIT   (default, the hot path) interface star patches + point-Jacobi
+ *               on the interiors: PAFW0(X0_Gamma)+J(X0_I) (Eq. 5.4)
+ *               for H(grad), PH(X0_Gamma, X1I_Gamma)+J(X1_I) (Eq. 5.12,
+ *               P:1956-1970) for H(curl);
+ *   RDR_UNSPLIT the baselines the split is measured against (NEXT-3): star
+ *               patches that contain the cell interiors and no Jacobi,
+ *               PAFW0(X0) (Eq. 5.2) and PH(X0, X1I) (Eq. 5.10,
+ *               P:1899-1905) -- 3439 vs 1423 dofs per vertex star at p = 10
+ *               (P:1783-1787). */
+enum { RDR_SPLIT = 0, RDR_UNSPLIT = 1 };
+
+struct rdr_options {
+  int decomposition; /* RDR_SPLIT or RDR_UNSPLIT */
+};
+
 enum {
   RDR_OK = 0,
   RDR_EINVAL = -1,   /* bad p / space / sizes / alpha <= 0 / beta < 0 / NULL pointer */
@@ -77,6 +94,12 @@ struct rdr_info {
 int rdr_setup(rdr_handle** h, const double* vertices, int64_t nv, const int32_t* tets, int64_t nt,
               int p, int space, const double* alpha, const double* beta,
               const uint8_t* dirichlet_mask, void* stream);
+
+/* rdr_setup with options (NULL = defaults: RDR_SPLIT). RDR_EINVAL for an
+ * unknown decomposition. */
+int rdr_setup_ex(rdr_handle** h, const double* vertices, int64_t nv, const int32_t* tets, int64_t nt,
+                 int p, int space, const double* alpha, const double* beta,
+                 const uint8_t* dirichlet_mask, const struct rdr_options* opt, void* stream);
 
 int rdr_ndofs(const rdr_handle* h, int64_t* n_total);
 int rdr_get_info(const rdr_handle* h, struct rdr_info* out);

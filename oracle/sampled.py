@@ -10,14 +10,16 @@ the same definitions as oracle.solver.Oracle:
   * (A x)_r = sum over cells T containing dof r of (A_T x_T)_r, with A_T the
     element matrix by physical quadrature (Eq. 2.9, R-A10) and x
     masked (R-A11); y_r = 0 for constrained r.
-  * (P^-1 r)_l = r_l / A_ll for interior l (Thm 5.1, R-A17), plus
+  * (P^-1 r)_l = r_l / A_ll for interior l (split decompositions: Thm 5.1,
+    P:1612-1631, R-A17), plus
     sum over the star patches m containing l of (E_m A_m^-1 E_m^T r)_l
     (Eq. 5.4; Eq. 5.12, R-A13..A15). A_m is assembled
     from the element matrices of the cells of the star only -- every cell that
     couples two dofs of the patch contains the seed vertex (edge), so this is
-    exactly A[idx][:, idx]. The patches that can contain an interface dof of
-    an entity S are the vertex patches of the vertices of S and (H(curl)) the
-    edge patches of the edges of S; the others contribute 0 at that row.
+    exactly A[idx][:, idx]. The patches that can contain a dof of an entity S
+    are the vertex patches of the vertices of S and (H(curl)) the edge patches
+    of the edges of S; the others contribute 0 at that row. (The unsplit
+    decompositions of SURVEY NEXT-3 put interior dofs into the patches too.)
 """
 from __future__ import annotations
 
@@ -29,8 +31,8 @@ from .solver import Oracle
 
 
 class SampledOracle(Oracle):
-    def __init__(self, vertices, tets, p, space, alpha, beta, mask):
-        super().__init__(vertices, tets, p, space, alpha, beta, mask, assemble=False)
+    def __init__(self, vertices, tets, p, space, alpha, beta, mask, decomposition="split"):
+        super().__init__(vertices, tets, p, space, alpha, beta, mask, assemble=False, decomposition=decomposition)
         self._Ae = {}
         self._Ae_cg = {}
         self._solved = {}
@@ -52,9 +54,6 @@ class SampledOracle(Oracle):
             for c, m in zip(missing, mats):
                 cache[int(c)] = m
         return {int(c): cache[int(c)] for c in cells}
-
-    def _cells_with_vertices(self, verts):
-        return np.nonzero(np.isin(self.topo.cells, verts).any(axis=1))[0]
 
     # ------------------------------------------------------------ operator rows
     def apply_rows(self, x, rows):
@@ -84,11 +83,10 @@ class SampledOracle(Oracle):
             return self._solved[key]
         if kind == "vertex":
             pk, idx = self.vertex_patch(seed)
-            cells = self._cells_with_vertices([seed])
+            cells = self._cells_of([seed])
         else:
             pk, idx = self.edge_patch(seed)
-            a, b = self.topo.edges[seed]
-            cells = np.nonzero(np.isin(self.topo.cells, [a]).any(axis=1) & np.isin(self.topo.cells, [b]).any(axis=1))[0]
+            cells = self._cells_of(list(self.topo.edges[seed]))
         if len(idx) == 0:
             self._solved[key] = (np.zeros(0, dtype=np.int64), np.zeros(0))
             return self._solved[key]
@@ -126,20 +124,19 @@ class SampledOracle(Oracle):
             if not self.free[l]:
                 continue
             dim, ent = self.num.entity[l]
-            if dim == 3:  # interior point-Jacobi, d_l = A_ll (R-A17)
+            if dim == 3 and self.decomposition == "split":  # interior point-Jacobi, d_l = A_ll (R-A17)
                 c = int(ent)
                 k = int(np.nonzero(self.num.dofmap[c] == l)[0][0])
                 out[i] += r[l] / self._elements([c])[c][k, k]
                 continue
-            verts = [int(ent)] if dim == 0 else list(t.edges[ent]) if dim == 1 else list(t.faces[ent])
+            verts = [int(ent)] if dim == 0 else list(t.edges[ent]) if dim == 1 else \
+                list(t.faces[ent]) if dim == 2 else list(t.cells[ent])
             seeds = [("vertex", v) for v in verts]
-            if self.space == "hcurl":
-                if dim == 1:
-                    seeds.append(("edge", int(ent)))
-                elif dim == 2:
-                    tri = t.faces[ent]
-                    for a, b in ((0, 1), (0, 2), (1, 2)):
-                        seeds.append(("edge", t.edge_index[(tri[a], tri[b])]))
+            if self.space == "hcurl" and dim >= 1:
+                vs = sorted(verts)
+                for ia in range(len(vs)):
+                    for ib in range(ia + 1, len(vs)):
+                        seeds.append(("edge", t.edge_index[(vs[ia], vs[ib])]))
             for kind, seed in seeds:
                 ids, vals = self._patch_solve(kind, seed, r)
                 hit = np.nonzero(ids == l)[0]

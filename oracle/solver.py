@@ -28,9 +28,14 @@ from .fem import Assembler
 
 
 class Oracle:
-    def __init__(self, vertices, tets, p, space, alpha, beta, mask, assemble=True):
+    def __init__(self, vertices, tets, p, space, alpha, beta, mask, assemble=True, decomposition="split"):
         self.space = {0: "hgrad", 1: "hcurl", "hgrad": "hgrad", "hcurl": "hcurl"}[space]
         self.p = p
+        # "split": PAFW0(X_Gamma)+J(X_I) (Eq. 5.4) / PH(X0_Gamma, X1I_Gamma)+J(X1_I) (Eq. 5.12), the hot path;
+        # "unsplit": PAFW0(X) (Eq. 5.2) / PH(X0, X1I) (Eq. 5.10), interiors inside the star patches and
+        # no Jacobi; both one-level (the coarse W^k is NEXT-1, R-A14)
+        assert decomposition in ("split", "unsplit")
+        self.decomposition = decomposition
         self.alpha = np.asarray(alpha, dtype=np.float64)
         self.beta = np.asarray(beta, dtype=np.float64)
         self.topo = Topology(vertices, tets, mask)
@@ -91,23 +96,31 @@ class Oracle:
             self._inc = (v_edges, v_faces, e_faces)
         return self._inc
 
+    def _cells_of(self, verts):
+        """Cells containing all of the given vertices (the star of a vertex / edge)."""
+        return np.nonzero(np.sum(np.isin(self.topo.cells, verts), axis=1) == len(verts))[0]
+
     def vertex_patch(self, v):
         """(kind, idx) of the star patch of vertex v (R-A13): the free interface
         dofs of v, the edges and the faces containing v -- in the problem's own
         numbering for H(grad) ('dof'), in the CG_p potential numbering for
-        H(curl) ('pot', embedded by G[:, idx]). Empty idx: no patch."""
+        H(curl) ('pot', embedded by G[:, idx]). Unsplit (Eq. 5.2 / 5.10): also
+        the interior dofs of the cells containing v. Empty idx: no patch."""
         v_edges, v_faces, _ = self._incidence()
+        num = self.num if self.space == "hgrad" else (self._build_gradient(), self.cg_num)[1]
+        idx = self._entity_dofs(num, v, v_edges[v], v_faces[v], kinds=None)
+        if self.decomposition == "unsplit" and num.per[3]:
+            cells = self._cells_of([v])
+            o, per = num.offsets[3], num.per[3]
+            idx = np.sort(np.concatenate([idx] + [np.arange(o + c * per, o + (c + 1) * per) for c in cells]))
         if self.space == "hgrad":
-            idx = self._entity_dofs(self.num, v, v_edges[v], v_faces[v], kinds=None)
             return "dof", idx[self.free[idx]]
-        self._build_gradient()
-        cg = self.cg_num
-        idx = self._entity_dofs(cg, v, v_edges[v], v_faces[v], kinds=None)
-        return "pot", idx[~cg.constrained[idx]]
+        return "pot", idx[~num.constrained[idx]]
 
     def edge_patch(self, e):
         """('dof', idx) of the type-I edge patch of E (H(curl), R-A13): the free
-        Whitney dof of E and the type-I dofs of the faces containing E."""
+        Whitney dof of E and the type-I dofs of the faces containing E; unsplit
+        (Eq. 5.10) also the type-I dofs of the cells containing E."""
         _, _, e_faces = self._incidence()
         num = self.num
         nI_face = num.per[2] - (self.p - 1) * (self.p - 2) // 2
@@ -115,6 +128,11 @@ class Oracle:
         for f in e_faces[e]:
             base = num.offsets[2] + f * num.per[2]
             idx.extend(range(base, base + nI_face))  # type-I face dofs
+        if self.decomposition == "unsplit":
+            nI_cell = num.per[3] - (self.p - 1) * (self.p - 2) * (self.p - 3) // 6
+            for c in self._cells_of(list(self.topo.edges[e])):
+                base = num.offsets[3] + c * num.per[3]
+                idx.extend(range(base, base + nI_cell))  # type-I cell dofs
         idx = np.array(sorted(idx), dtype=np.int64)
         return "dof", idx[self.free[idx]]
 
@@ -196,7 +214,10 @@ class Oracle:
         (the oracle reports it next to the 1e-11 parity bar)."""
         Ar = self.A
         d = Ar.diagonal()
-        self.int_idx = np.nonzero(self.num.interior & self.free)[0]
+        # interior point-Jacobi only in the split decompositions (Thm 5.1); unsplit
+        # patches contain the interiors
+        self.int_idx = np.nonzero(self.num.interior & self.free)[0] if self.decomposition == "split" \
+            else np.zeros(0, dtype=np.int64)
         self.dinv = 1.0 / d[self.int_idx]
         self.factors = []
         self.kappa_max = 0.0

@@ -120,7 +120,8 @@ struct rdr_handle {
 };
 
 static int setup_impl(rdr_handle* h, const double* vertices, int64_t nv, const int32_t* tets, int64_t nt, int p,
-                      int space, const double* alpha, const double* beta, const uint8_t* mask, cudaStream_t stream) {
+                      int space, const double* alpha, const double* beta, const uint8_t* mask, bool unsplit,
+                      cudaStream_t stream) {
   auto t0 = std::chrono::steady_clock::now();
   if (stream) CK(cudaStreamSynchronize(stream));
   configure_kernels();
@@ -210,6 +211,7 @@ static int setup_impl(rdr_handle* h, const double* vertices, int64_t nv, const i
   pc.off3 = num.off[3];
   std::vector<double> dinv;
   interior_inverse_diagonal(m, num, el, coef, dinv);
+  if (unsplit) std::fill(dinv.begin(), dinv.end(), 0.0);  // no Jacobi: the patches contain the interiors
   double* d_dinv;
   if ((st = h->own_upload(&d_dinv, dinv))) return st;
   pc.dinv = d_dinv;
@@ -224,7 +226,7 @@ static int setup_impl(rdr_handle* h, const double* vertices, int64_t nv, const i
     cell_coefficients(m, RDR_HGRAD, hb.data(), zero.data(), cg_coef);
     Gradient G;
     build_gradient(m, num, cg_num, G);
-    pc.n_cg_iface = cg_num.off[3];
+    pc.n_cg_iface = unsplit ? cg_num.n_total : cg_num.off[3];  // unsplit potential patches hold cell bubbles
     G.ptr.resize(pc.n_cg_iface + 1);
     G.col.resize(G.ptr.back());
     G.val.resize(G.ptr.back());
@@ -248,7 +250,8 @@ static int setup_impl(rdr_handle* h, const double* vertices, int64_t nv, const i
     pc.ldg_warps = 8;  // decided below from the patch sizes (RDR_PATCH_WARPS=4|8 overrides)
   }
   st = build_patches(m, num, el, coef, space == RDR_HCURL ? &cg_num : nullptr, cg_el,
-                     space == RDR_HCURL ? &cg_coef : nullptr, P, sink, pc.kernel == 1 ? kTileSwizzled : kTileGroups);
+                     space == RDR_HCURL ? &cg_coef : nullptr, P, sink, pc.kernel == 1 ? kTileSwizzled : kTileGroups,
+                     unsplit);
   if (sink.d) h->owned.push_back(sink.d);
   if (st) return st;
   pc.n_patches = (int64_t)P.n.size();
@@ -344,19 +347,23 @@ static int setup_impl(rdr_handle* h, const double* vertices, int64_t nv, const i
 
 extern "C" {
 
-int rdr_setup(rdr_handle** hp, const double* vertices, int64_t nv, const int32_t* tets, int64_t nt, int p, int space,
-              const double* alpha, const double* beta, const uint8_t* dirichlet_mask, void* stream) {
+int rdr_setup_ex(rdr_handle** hp, const double* vertices, int64_t nv, const int32_t* tets, int64_t nt, int p,
+                 int space, const double* alpha, const double* beta, const uint8_t* dirichlet_mask,
+                 const rdr_options* opt, void* stream) {
   if (!hp) return RDR_EINVAL;
   *hp = nullptr;
   if (!vertices || !tets || !alpha || !beta || !dirichlet_mask || nv < 4 || nt < 1) return RDR_EINVAL;
   if (space != RDR_HGRAD && space != RDR_HCURL) return RDR_EINVAL;
   if (p < 1 || (space == RDR_HGRAD && p > 12) || (space == RDR_HCURL && p > 10)) return RDR_EINVAL;
   if (nv > 0x7fffffff || nt > 0x7fffffff) return RDR_EINVAL;
+  const int dec = opt ? opt->decomposition : RDR_SPLIT;
+  if (dec != RDR_SPLIT && dec != RDR_UNSPLIT) return RDR_EINVAL;
   rdr_handle* h = new (std::nothrow) rdr_handle();
   if (!h) return RDR_ENOMEM;
   int st;
   try {
-    st = setup_impl(h, vertices, nv, tets, nt, p, space, alpha, beta, dirichlet_mask, (cudaStream_t)stream);
+    st = setup_impl(h, vertices, nv, tets, nt, p, space, alpha, beta, dirichlet_mask, dec == RDR_UNSPLIT,
+                    (cudaStream_t)stream);
   } catch (const std::bad_alloc&) {
     st = RDR_ENOMEM;
   } catch (const std::exception& e) {
@@ -369,6 +376,11 @@ int rdr_setup(rdr_handle** hp, const double* vertices, int64_t nv, const int32_t
   }
   *hp = h;
   return RDR_OK;
+}
+
+int rdr_setup(rdr_handle** hp, const double* vertices, int64_t nv, const int32_t* tets, int64_t nt, int p, int space,
+              const double* alpha, const double* beta, const uint8_t* dirichlet_mask, void* stream) {
+  return rdr_setup_ex(hp, vertices, nv, tets, nt, p, space, alpha, beta, dirichlet_mask, nullptr, stream);
 }
 
 int rdr_ndofs(const rdr_handle* h, int64_t* n_total) {

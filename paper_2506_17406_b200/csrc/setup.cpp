@@ -392,7 +392,7 @@ void chol_inverse(const double* L, int n, double* U, double* Ainv) {
 
 int build_patches(const Mesh& m, const Numbering& num, const RefElement& el, const std::vector<double>& coef,
                   const Numbering* cg_num, const RefElement* cg_el, const std::vector<double>* cg_coef,
-                  Patches& P, PatchSink& sink, PatchLayout layout) {
+                  Patches& P, PatchSink& sink, PatchLayout layout, bool unsplit) {
   CSR v_cells = invert_incidence(m.nt, m.nv, 4, m.cells);
   CSR v_edges = invert_incidence(m.ne, m.nv, 2, m.edges);
   CSR v_faces = invert_incidence(m.nf, m.nv, 3, m.faces);
@@ -417,7 +417,11 @@ int build_patches(const Mesh& m, const Numbering& num, const RefElement& el, con
   for (int64_t v = 0; v < m.nv; ++v) {  // vertex stars (own dofs for H(grad), CG potential for H(curl))
     PatchDef d;
     d.numbering = num.space == 0 ? 0 : 1;
-    star_dofs(num.space == 0 ? num : *cg_num, v, d.idx);
+    const Numbering& vn = num.space == 0 ? num : *cg_num;
+    star_dofs(vn, v, d.idx);
+    if (unsplit)  // PAFW0(X) / PH(X0, .) (Eq. 5.2 / 5.10): the cells' interior dofs too
+      for (int64_t k = v_cells.ptr[v]; k < v_cells.ptr[v + 1]; ++k)
+        for (int64_t j = 0; j < vn.per[3]; ++j) d.idx.push_back((int32_t)(vn.off[3] + v_cells.ind[k] * vn.per[3] + j));
     if (d.idx.empty()) continue;
     std::sort(d.idx.begin(), d.idx.end());
     d.cells.assign(v_cells.ind.begin() + v_cells.ptr[v], v_cells.ind.begin() + v_cells.ptr[v + 1]);
@@ -449,6 +453,11 @@ int build_patches(const Mesh& m, const Numbering& num, const RefElement& el, con
           int64_t id = num.off[2] + f * num.per[2] + j;
           if (!num.constrained[id]) d.idx.push_back((int32_t)id);
         }
+      }
+      if (unsplit) {  // PH(., X1I) (Eq. 5.10): the type-I dofs of the cells containing E too
+        const int64_t nIc = num.per[3] - (int64_t)(num.p - 1) * (num.p - 2) * (num.p - 3) / 6;
+        for (int64_t k = e_cells.ptr[e]; k < e_cells.ptr[e + 1]; ++k)
+          for (int64_t j = 0; j < nIc; ++j) d.idx.push_back((int32_t)(num.off[3] + e_cells.ind[k] * num.per[3] + j));
       }
       if (d.idx.empty()) continue;
       std::sort(d.idx.begin(), d.idx.end());

@@ -73,7 +73,8 @@ inline int64_t patch_stored_doubles(int n) {
   return (exact + 15) / 16 * 16;
 }
 
-// Builds the patch index sets (R-A13), assembles and inverts each patch
+// Builds the patch index sets (R-A13; unsplit: the interiors of the star's
+// cells too, Eq. 5.2 / 5.10), assembles and inverts each patch
 // matrix (R-A15), and hands the packed tiles to `sink(first_patch, last_patch,
 // host_tiles)` in chunks so that the full inverse store never lives on the host.
 // Returns 0 or RDR_ENOTSPD.
@@ -85,7 +86,7 @@ struct PatchSink {
 enum PatchLayout { kTileGroups = 0, kTileSwizzled = 1 };
 int build_patches(const Mesh& m, const Numbering& num, const RefElement& el, const std::vector<double>& coef,
                   const Numbering* cg_num, const RefElement* cg_el, const std::vector<double>* cg_coef,
-                  Patches& P, PatchSink& sink, PatchLayout layout);
+                  Patches& P, PatchSink& sink, PatchLayout layout, bool unsplit = false);
 
 // Interior point-Jacobi (R-A17): 1/A_ll for the cell-interior dofs [off[3], n_total).
 void interior_inverse_diagonal(const Mesh& m, const Numbering& num, const RefElement& el,

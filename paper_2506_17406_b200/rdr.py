@@ -12,6 +12,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "librdr.so")
 
 HGRAD, HCURL = 0, 1
+SPLIT, UNSPLIT = 0, 1
 RDR_OK, RDR_ENOCONV = 0, -6
 
 
@@ -19,6 +20,10 @@ class RdrError(RuntimeError):
     def __init__(self, code: int, what: str):
         self.code = code
         super().__init__(f"{what}: {_lib.rdr_strerror(code).decode()} ({code})")
+
+
+class Options(ctypes.Structure):
+    _fields_ = [("decomposition", ctypes.c_int)]
 
 
 class Info(ctypes.Structure):
@@ -40,6 +45,8 @@ def _load():
     P, I64, I32, D = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_double
     sig = {
         "rdr_setup": (ctypes.c_int, [ctypes.POINTER(P), P, I64, P, I64, ctypes.c_int, ctypes.c_int, P, P, P, P]),
+        "rdr_setup_ex": (ctypes.c_int, [ctypes.POINTER(P), P, I64, P, I64, ctypes.c_int, ctypes.c_int, P, P, P,
+                                        ctypes.POINTER(Options), P]),
         "rdr_ndofs": (ctypes.c_int, [P, ctypes.POINTER(I64)]),
         "rdr_get_info": (ctypes.c_int, [P, ctypes.POINTER(Info)]),
         "rdr_apply": (ctypes.c_int, [P, P, P, P]),
@@ -119,7 +126,7 @@ class Solver:
     (float64 / int32 / uint8) or host numpy arrays; vectors are torch float64
     CUDA tensors of length n_total."""
 
-    def __init__(self, vertices, tets, p, space, alpha, beta, mask, stream=None):
+    def __init__(self, vertices, tets, p, space, alpha, beta, mask, stream=None, decomposition=SPLIT):
         import torch
         self._keep = [np.ascontiguousarray(vertices, dtype=np.float64) if isinstance(vertices, np.ndarray) else vertices,
                       np.ascontiguousarray(tets, dtype=np.int32) if isinstance(tets, np.ndarray) else tets,
@@ -129,8 +136,9 @@ class Solver:
         v, t, a, b, m = self._keep
         self._h = ctypes.c_void_p()
         nv, nt = v.shape[0], t.shape[0]
-        _check(_lib.rdr_setup(ctypes.byref(self._h), _ptr(v), nv, _ptr(t), nt, int(p), int(space), _ptr(a), _ptr(b),
-                              _ptr(m), _stream(stream)), "rdr_setup")
+        opt = Options(int(decomposition))
+        _check(_lib.rdr_setup_ex(ctypes.byref(self._h), _ptr(v), nv, _ptr(t), nt, int(p), int(space), _ptr(a),
+                                 _ptr(b), _ptr(m), ctypes.byref(opt), _stream(stream)), "rdr_setup_ex")
         self._keep = None
         n = ctypes.c_int64()
         _check(_lib.rdr_ndofs(self._h, ctypes.byref(n)), "rdr_ndofs")

@@ -22,10 +22,11 @@ from rdr_inputs import make_config  # noqa: E402
 from paper_2506_17406_b200 import rdr  # noqa: E402
 
 
-def measure(cfg, p, fp64_peak, hbm, solves=3, reps=20):
+def measure(cfg, p, fp64_peak, hbm, solves=3, reps=20, dec="split"):
     c = make_config(cfg, p=p) if cfg == 5 else make_config(cfg)
     t0 = time.time()
-    S = rdr.Solver(c.vertices, c.tets, c.p, c.space, c.alpha, c.beta, c.mask)
+    S = rdr.Solver(c.vertices, c.tets, c.p, c.space, c.alpha, c.beta, c.mask,
+                   decomposition=rdr.UNSPLIT if dec == "unsplit" else rdr.SPLIT)
     setup_wall = time.time() - t0
     info = S.info
     n = S.n_total
@@ -46,7 +47,8 @@ def measure(cfg, p, fp64_peak, hbm, solves=3, reps=20):
     it = its[0]
     patch_bytes = info["bytes_precond"] - 24.0 * info["n_interior"]
     out = {
-        "config": cfg, "space": "hgrad" if c.space == 0 else "hcurl", "p": c.p, "n_cells": info["n_cells"],
+        "config": cfg, "decomposition": dec, "space": "hgrad" if c.space == 0 else "hcurl", "p": c.p,
+        "n_cells": info["n_cells"],
         "n_loc": info["n_loc"], "n_total": n, "n_free": info["n_free"], "n_patches": info["n_patches"],
         "max_patch": info["max_patch"], "patch_GB": info["patch_bytes"] / 1e9, "setup_s": info["setup_seconds"],
         "setup_wall_s": setup_wall,
@@ -71,6 +73,7 @@ def main():
     ap.add_argument("--configs", default="1,2,4,5,3")
     ap.add_argument("--p", default="1-12")
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "sweep.jsonl"))
+    ap.add_argument("--decomposition", default="split", choices=["split", "unsplit"])
     args = ap.parse_args()
     lo, hi = (int(v) for v in args.p.split("-"))
     fp64_peak = rdr.measure_fp64_peak()
@@ -82,7 +85,7 @@ def main():
         f.write(json.dumps(head) + "\n")
         for cfg in (int(v) for v in args.configs.split(",")):
             for p in (range(lo, hi + 1) if cfg == 5 else [None]):
-                r = measure(cfg, p, fp64_peak, hbm)
+                r = measure(cfg, p, fp64_peak, hbm, dec=args.decomposition)
                 print(json.dumps(r), flush=True)
                 f.write(json.dumps(r) + "\n")
                 f.flush()

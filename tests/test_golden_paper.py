@@ -98,3 +98,18 @@ def test_implemented_rows_by_oracle_patches(p):
     r = recs[("ph_interface_typeI_J", p)]
     assert max(len(i) for k, i in ps if k == "pot") == int(r[3])
     assert max(len(i) for k, i in ps if k == "dof") == int(r[4])
+
+
+@pytest.mark.parametrize("p", [4, 10])
+def test_unsplit_rows_by_oracle_patches(p):
+    """SURVEY NEXT-3 baselines: PAFW0(X0) (Eq. 5.2; P:1783-1786 prints 175 / 3439)
+    and the type-I PH(X0, X1I) of Eq. 5.10 (Table 1 row ph_typeI: 175/121, 3439/1981)."""
+    recs = {(r[0], int(r[2])): r for r in _entries()}
+    c = make_config(0, n=3, p=p, space=HGRAD, bc="none")
+    o = Oracle(c.vertices, c.tets, p, HGRAD, c.alpha, c.beta, c.mask, assemble=False, decomposition="unsplit")
+    assert max(len(i) for _, i in o.patch_sets()) == int(recs[("hgrad_full_vertex", p)][3])
+    o = Oracle(c.vertices, c.tets, p, HCURL, c.alpha, c.beta, c.mask, assemble=False, decomposition="unsplit")
+    ps = o.patch_sets()
+    r = recs[("ph_typeI", p)]
+    assert max(len(i) for k, i in ps if k == "pot") == int(r[3])
+    assert max(len(i) for k, i in ps if k == "dof") == int(r[4])

@@ -25,12 +25,13 @@ def rel(a, b):
     return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
 
 
-def _pair(torch, cfg, **kw):
+def _pair(torch, cfg, dec="split", **kw):
     from paper_2506_17406_b200 import rdr
     from oracle.solver import Oracle
     c = make_config(cfg, **kw)
-    S = rdr.Solver(c.vertices, c.tets, c.p, c.space, c.alpha, c.beta, c.mask)
-    O = Oracle(c.vertices, c.tets, c.p, c.space, c.alpha, c.beta, c.mask)
+    S = rdr.Solver(c.vertices, c.tets, c.p, c.space, c.alpha, c.beta, c.mask,
+                   decomposition=rdr.UNSPLIT if dec == "unsplit" else rdr.SPLIT)
+    O = Oracle(c.vertices, c.tets, c.p, c.space, c.alpha, c.beta, c.mask, decomposition=dec)
     assert S.n_total == O.n_total
     return c, S, O
 
@@ -334,3 +335,26 @@ def test_solve_maxit_and_host_path(torch_cuda):
 def test_smoke_entry_point(torch_cuda):
     import __graft_entry__
     __graft_entry__.smoke()
+
+
+# ---------------------------------------------------------------- NEXT-3: unsplit baseline decompositions
+@pytest.mark.parametrize("space,p,bc", [(HGRAD, 2, "all"), (HGRAD, 4, "x0"), (HGRAD, 6, "all"),
+                                        (HCURL, 2, "all"), (HCURL, 3, "x0"), (HCURL, 5, "all")])
+def test_unsplit_decomposition(torch_cuda, space, p, bc):
+    """PAFW0(X0) (Eq. 5.2) and PH(X0, X1I) (Eq. 5.10), one-level: star patches
+    holding the cell interiors, no Jacobi -- the baselines of the split."""
+    c, S, O = _pair(torch_cuda, 0, dec="unsplit", n=2, p=p, space=space, perturb=True, bc=bc, coeffs="loguniform")
+    _check_apply_precond(torch_cuda, c, S, O)
+    _check_pcg(torch_cuda, c, S, O)
+
+
+def test_unsplit_config5_sampled(torch_cuda):
+    """Unsplit H(grad) at p = 6 on the config-5 mesh: sampled rows, PCG converges."""
+    from paper_2506_17406_b200 import rdr
+    from oracle.sampled import SampledOracle
+    c = make_config(5, p=6)
+    S = rdr.Solver(c.vertices, c.tets, c.p, c.space, c.alpha, c.beta, c.mask, decomposition=rdr.UNSPLIT)
+    O = SampledOracle(c.vertices, c.tets, c.p, c.space, c.alpha, c.beta, c.mask, decomposition="unsplit")
+    rows = _sample_rows(O, n_vertices=2, n_cells=3)
+    _check_sampled(torch_cuda, c, S, O, rows)
+    _check_sampled_pcg(torch_cuda, c, S, O, rows)

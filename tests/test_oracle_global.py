@@ -388,3 +388,22 @@ def test_mms_convergence(space, p, rate, n):
     e1 = _mms_errors(space, n, p)
     e2 = _mms_errors(space, 2 * n, p)
     assert math.log2(e1 / e2) >= rate - 0.2
+
+
+def test_unsplit_preconditioner_exactness_and_pcg():
+    """Unsplit one-level decompositions: symmetric, positive,
+    and PCG agrees with a dense solve (both spaces)."""
+    import scipy.sparse.linalg  # noqa: F401
+    for space, p in ((HGRAD, 3), (HCURL, 2)):
+        c = make_config(0, n=2, p=p, space=space, perturb=True, bc="x0", coeffs="loguniform")
+        o = Oracle(c.vertices, c.tets, c.p, c.space, c.alpha, c.beta, c.mask, decomposition="unsplit")
+        rng = np.random.default_rng(3)
+        x, y = o.mask(rng.standard_normal(o.n_total)), o.mask(rng.standard_normal(o.n_total))
+        px, py = o.precond(x), o.precond(y)
+        assert abs(x @ py - y @ px) <= 1e-12 * np.linalg.norm(x) * np.linalg.norm(py)
+        assert x @ px > 0
+        b = o.mask(c.draw_vector(o.n_total))
+        xs, it, res = o.solve(b, rtol=1e-10)
+        A = o.A.toarray()[np.ix_(o.free, o.free)]
+        xd = np.linalg.solve(A, b[o.free])
+        assert np.linalg.norm(xs[o.free] - xd) <= 1e-7 * np.linalg.norm(xd)

@@ -9,12 +9,13 @@ from oracle.solver import Oracle
 from oracle.sampled import SampledOracle
 
 
+@pytest.mark.parametrize("dec", ["split", "unsplit"])
 @pytest.mark.parametrize("space,p,bc,coeffs", [(HGRAD, 3, "all", "one"), (HGRAD, 4, "x0", "loguniform"),
-                                                (HCURL, 2, "all", "one"), (HCURL, 3, "x0", "loguniform")])
-def test_sampled_rows_match_global(space, p, bc, coeffs):
+                                                (HCURL, 2, "all", "one"), (HCURL, 4, "x0", "loguniform")])
+def test_sampled_rows_match_global(space, p, bc, coeffs, dec):
     c = make_config(0, n=2, p=p, space=space, perturb=True, bc=bc, coeffs=coeffs)
-    O = Oracle(c.vertices, c.tets, c.p, c.space, c.alpha, c.beta, c.mask)
-    S = SampledOracle(c.vertices, c.tets, c.p, c.space, c.alpha, c.beta, c.mask)
+    O = Oracle(c.vertices, c.tets, c.p, c.space, c.alpha, c.beta, c.mask, decomposition=dec)
+    S = SampledOracle(c.vertices, c.tets, c.p, c.space, c.alpha, c.beta, c.mask, decomposition=dec)
     x = c.draw_vector(O.n_total)
     rng = np.random.default_rng(5)
     # every dof kind: vertex/edge/face/cell entities, constrained and free

@@ -150,6 +150,10 @@ const char* rdr_strerror(int code);
  * H(curl) Mxx, Myy, Mzz, Mxy+Myx, Mxz+Mzx, Myz+Mzy, then the same for K (curl).
  * Local dof order: DESIGN.md R-A8. */
 int rdr_reference_matrices(int space, int p, double* out, int32_t* n_loc, int32_t* n_mat);
+/* In-place inverse of an n x n SPD row-major matrix with the host routine the
+ * setup uses for the patch inverses (R-A15); RDR_ENOTSPD on a non-positive
+ * Cholesky pivot. */
+int rdr_spd_inverse(double* a, int32_t n);
 /* Bubble eigenvalues lambda_j (Eq. 3.8) on the canonical l-simplex: kind 0 = CG, 1 = Ned1. */
 int rdr_bubble_eigenvalues(int kind, int l, int p, double* out, int32_t* n);
 

@@ -32,7 +32,7 @@ def build(verbose_ptxas: bool = False) -> str:
         o = os.path.join(bdir, cu + ".o")
         _run([NVCC, *kflags, "-c", os.path.join(CSRC, cu), "-o", o])
         objs.append(o)
-    for cpp in ("refelem.cpp", "setup.cpp", "rdr_abi.cpp"):
+    for cpp in ("refelem.cpp", "setup.cpp", "dense.cpp", "rdr_abi.cpp"):
         o = os.path.join(bdir, cpp + ".o")
         _run(["g++", *HOST_FLAGS, "-I", os.path.join(CUDA, "include"), "-c", os.path.join(CSRC, cpp), "-o", o])
         objs.append(o)

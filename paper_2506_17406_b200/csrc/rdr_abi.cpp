@@ -14,6 +14,7 @@
 #include "kernels.hpp"
 #include "refelem.hpp"
 #include "setup.hpp"
+#include "dense.hpp"
 
 using namespace rdr;
 
@@ -662,6 +663,12 @@ int rdr_reference_matrices(int space, int p, double* out, int32_t* n_loc, int32_
     return RDR_EINVAL;
   }
   return RDR_OK;
+}
+
+int rdr_spd_inverse(double* a, int32_t n) {
+  if (!a || n < 1) return RDR_EINVAL;
+  std::vector<double> work;
+  return spd_inverse(a, n, work) ? RDR_OK : RDR_ENOTSPD;
 }
 
 int rdr_bubble_eigenvalues(int kind, int l, int p, double* out, int32_t* n) {

@@ -2,6 +2,7 @@
 // pullbacks), star patches (R-A13, Eq. 5.4, Eq. 5.12
 // P:1956-1970), patch inverses (R-A15) and the interior diagonal (R-A17).
 #include "setup.hpp"
+#include "dense.hpp"
 
 #include <omp.h>
 
@@ -339,55 +340,6 @@ struct PatchDef {
 };
 
 // in-place Cholesky A = L L^T (row-major, lower), returns false if not SPD
-bool cholesky(double* A, int n) {
-  for (int j = 0; j < n; ++j) {
-    double* aj = A + (size_t)j * n;
-    double d = aj[j];
-    for (int k = 0; k < j; ++k) d -= aj[k] * aj[k];
-    if (!(d > 0)) return false;
-    double l = std::sqrt(d);
-    aj[j] = l;
-    double inv = 1.0 / l;
-    for (int i = j + 1; i < n; ++i) {
-      double* ai = A + (size_t)i * n;
-      double s = ai[j];
-      for (int k = 0; k < j; ++k) s -= ai[k] * aj[k];
-      ai[j] = s * inv;
-    }
-  }
-  return true;
-}
-
-// A^{-1} from the Cholesky factor: U = L^{-1} row by row, then A^{-1} = U^T U
-void chol_inverse(const double* L, int n, double* U, double* Ainv) {
-  std::memset(U, 0, sizeof(double) * n * n);
-  for (int i = 0; i < n; ++i) {
-    double* ui = U + (size_t)i * n;
-    const double* li = L + (size_t)i * n;
-    ui[i] = 1.0;
-    for (int k = 0; k < i; ++k) {
-      double f = li[k];
-      if (f == 0) continue;
-      const double* uk = U + (size_t)k * n;
-      for (int j = 0; j <= k; ++j) ui[j] -= f * uk[j];
-    }
-    double inv = 1.0 / li[i];
-    for (int j = 0; j <= i; ++j) ui[j] *= inv;
-  }
-  std::memset(Ainv, 0, sizeof(double) * n * n);
-  for (int k = 0; k < n; ++k) {
-    const double* uk = U + (size_t)k * n;
-    for (int i = 0; i <= k; ++i) {
-      double f = uk[i];
-      if (f == 0) continue;
-      double* ai = Ainv + (size_t)i * n;
-      for (int j = 0; j <= i; ++j) ai[j] += f * uk[j];
-    }
-  }
-  for (int i = 0; i < n; ++i)
-    for (int j = i + 1; j < n; ++j) Ainv[(size_t)i * n + j] = Ainv[(size_t)j * n + i];
-}
-
 }  // namespace
 
 int build_patches(const Mesh& m, const Numbering& num, const RefElement& el, const std::vector<double>& coef,
@@ -504,7 +456,7 @@ int build_patches(const Mesh& m, const Numbering& num, const RefElement& el, con
     buf.assign(P.tile_off[k1] - base, 0.0);
 #pragma omp parallel
     {
-      std::vector<double> A, W1, W2;
+      std::vector<double> A, W1;
       std::vector<int> lpos;
 #pragma omp for schedule(dynamic, 1)
       for (int64_t k = k0; k < k1; ++k) {
@@ -535,14 +487,12 @@ int build_patches(const Mesh& m, const Numbering& num, const RefElement& el, con
               A[(size_t)lpos[a] * n + lpos[b]] += s;
             }
         }
-        if (!cholesky(A.data(), n)) {
+        if (!spd_inverse(A.data(), n, W1)) {
 #pragma omp atomic write
           status = RDR_ENOTSPD;
           continue;
         }
-        W1.resize((size_t)n * n);
-        W2.resize((size_t)n * n);
-        chol_inverse(A.data(), n, W1.data(), W2.data());
+        const std::vector<double>& W2 = A;  // A^-1, both triangles
         // exact packed lower triangle in 32-row block rows (see patch_layout)
         double* out = buf.data() + (P.tile_off[k] - base);
         const int nbk = (n + 31) / 32;

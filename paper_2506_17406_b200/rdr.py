@@ -60,6 +60,7 @@ def _load():
         "rdr_strerror": (ctypes.c_char_p, [ctypes.c_int]),
         "rdr_reference_matrices": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, P, ctypes.POINTER(I32),
                                                   ctypes.POINTER(I32)]),
+        "rdr_spd_inverse": (ctypes.c_int, [P, I32]),
         "rdr_bubble_eigenvalues": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, P,
                                                   ctypes.POINTER(I32)]),
     }

@@ -70,3 +70,21 @@ def test_library_reference_matrices_match_oracle(space, p):
     scale = max(np.abs(r).max() for r in ref)
     for s, r in enumerate(ref):
         assert np.abs(R[s] - r).max() <= 1e-14 * scale, s
+
+
+@pytest.mark.parametrize("n", [1, 3, 17, 64, 130, 301])
+def test_host_spd_inverse(n):
+    """The setup's blocked AVX2 SPD inverse (patch inverses, R-A15) against
+    numpy, on matrices conditioned like the patch matrices (kappa ~1e4)."""
+    from paper_2506_17406_b200 import rdr
+    rng = np.random.default_rng(n)
+    Q, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    A = (Q * np.logspace(0, 4, n)) @ Q.T
+    A = 0.5 * (A + A.T)
+    B = np.ascontiguousarray(A.copy())
+    assert rdr._lib.rdr_spd_inverse(ctypes.c_void_p(B.ctypes.data), n) == 0
+    ref = np.linalg.inv(A)
+    assert np.abs(B - ref).max() <= 1e-10 * np.abs(ref).max()
+    assert np.array_equal(B, B.T)
+    C = -np.eye(3)
+    assert rdr._lib.rdr_spd_inverse(ctypes.c_void_p(C.ctypes.data), 3) == -3

@@ -113,13 +113,49 @@ class SampledOracle(Oracle):
         self._solved[key] = res
         return res
 
+    def _candidate_seeds(self, l):
+        """Patches (kind, seed) that can contain dof l: the vertex patches of the
+        vertices of its entity and (H(curl)) the edge patches of its edges."""
+        t = self.topo
+        dim, ent = self.num.entity[l]
+        verts = [int(ent)] if dim == 0 else list(t.edges[ent]) if dim == 1 else \
+            list(t.faces[ent]) if dim == 2 else list(t.cells[ent])
+        seeds = [("vertex", v) for v in verts]
+        if self.space == "hcurl" and dim >= 1:
+            vs = sorted(verts)
+            for ia in range(len(vs)):
+                for ib in range(ia + 1, len(vs)):
+                    seeds.append(("edge", t.edge_index[(vs[ia], vs[ib])]))
+        return seeds
+
+    def precond_residual_rows(self, b, x, rows):
+        """(P^-1 (b - A x))_l for l in rows, with the residual formed by the
+        oracle on every dof the relevant patches touch (the other entries of r
+        do not enter these rows) -- the quantity of the PCG stopping rule R-A16
+        at a solution x, on sampled rows."""
+        rows = np.asarray(rows, dtype=np.int64)
+        need = set(int(l) for l in rows)
+        for l in rows:
+            if not self.free[l]:
+                continue
+            if self.num.entity[l][0] == 3 and self.decomposition == "split":
+                continue
+            for kind, seed in self._candidate_seeds(int(l)):
+                pk, idx = self.vertex_patch(seed) if kind == "vertex" else self.edge_patch(seed)
+                if pk == "pot":  # Ned1 dofs reached by G_V^T
+                    idx = np.nonzero(np.abs(self.G[:, idx]).sum(axis=1).A1)[0]
+                need.update(int(i) for i in idx)
+        need = np.array(sorted(need), dtype=np.int64)
+        r = np.zeros(self.n_total)
+        r[need] = self.mask(b)[need] - self.apply_rows(x, need)
+        return self.precond_rows(r, rows)
+
     def precond_rows(self, r, rows):
         """(P^-1 r)_l for l in rows (0 for constrained l)."""
         r = self.mask(r)
         self._solved = {}
         rows = np.asarray(rows, dtype=np.int64)
         out = np.zeros(len(rows))
-        t = self.topo
         for i, l in enumerate(rows):
             if not self.free[l]:
                 continue
@@ -129,15 +165,7 @@ class SampledOracle(Oracle):
                 k = int(np.nonzero(self.num.dofmap[c] == l)[0][0])
                 out[i] += r[l] / self._elements([c])[c][k, k]
                 continue
-            verts = [int(ent)] if dim == 0 else list(t.edges[ent]) if dim == 1 else \
-                list(t.faces[ent]) if dim == 2 else list(t.cells[ent])
-            seeds = [("vertex", v) for v in verts]
-            if self.space == "hcurl" and dim >= 1:
-                vs = sorted(verts)
-                for ia in range(len(vs)):
-                    for ib in range(ia + 1, len(vs)):
-                        seeds.append(("edge", t.edge_index[(vs[ia], vs[ib])]))
-            for kind, seed in seeds:
+            for kind, seed in self._candidate_seeds(int(l)):
                 ids, vals = self._patch_solve(kind, seed, r)
                 hit = np.nonzero(ids == l)[0]
                 if len(hit):

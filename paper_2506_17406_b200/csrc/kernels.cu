@@ -931,6 +931,44 @@ __global__ void __launch_bounds__(kLdgWarps * 32, 32 / kLdgWarps)
     rli[i] = id[i];
     zl[i] = 0.0;
   }
+  const double* T = pc.tiles + pc.tile_off[pid];
+  const int ntiles = nb * (nb + 1) / 2;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int I = 0, J = warp, h = 0, t = warp;
+  while (J > I) {
+    J -= I + 1;
+    ++I;
+  }
+  // half tile (I, J, h) -> a[16] (row `lane`; diagonal tiles: lower triangle only)
+  auto load_half = [&](double(&a)[16]) {
+    const int rows = min(32, n - 32 * I);
+    const double* tb = T + 512LL * I * I + 16LL * I + (int64_t)J * 32 * rows;
+    if (J < I) {
+      if (lane < rows) {
+        const double4* tp = reinterpret_cast<const double4*>(tb) + lane + 4 * h * rows;
+#pragma unroll
+        for (int k4 = 0; k4 < 4; ++k4) {
+          const double4 v = ld_stream4(tp + k4 * rows);
+          a[4 * k4] = v.x;
+          a[4 * k4 + 1] = v.y;
+          a[4 * k4 + 2] = v.z;
+          a[4 * k4 + 3] = v.w;
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < 16; ++q) a[q] = 0.0;
+      }
+    } else {
+      // diagonal tile, lower triangle packed by columns: (i,k), k <= i at k*rows - k(k-1)/2 + i - k
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const int k = 16 * h + q;
+        a[q] = (k <= lane && lane < rows) ? ld_stream1(tb + k * rows - k * (k - 1) / 2 + (lane - k)) : 0.0;
+      }
+    }
+  };
+  double a[16];
+  if (t < ntiles) load_half(a);  // the first half tile is in flight during the r gather
   pdl_wait();
   if (stopped(guard)) return;
   for (int i = threadIdx.x; i < npad; i += blockDim.x) {
@@ -938,64 +976,38 @@ __global__ void __launch_bounds__(kLdgWarps * 32, 32 / kLdgWarps)
     rl[i] = (g >= 0) ? rin[g] : 0.0;
   }
   __syncthreads();
-  const double* T = pc.tiles + pc.tile_off[pid];
-  const int ntiles = nb * (nb + 1) / 2;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  int I = 0, J = warp;
-  while (J > I) {
-    J -= I + 1;
-    ++I;
-  }
-  for (int t = warp; t < ntiles; t += kLdgWarps) {
-    const int rows = min(32, n - 32 * I);
-    const double* tb = T + 512LL * I * I + 16LL * I + (int64_t)J * 32 * rows;
+  double row = 0.0;
+  while (t < ntiles) {
     const double ri = rl[I * 32 + lane];
-    double row = 0.0;
-#pragma unroll 1
-    for (int h = 0; h < 2; ++h) {
-      double a[16];
-      if (J < I) {
-        if (lane < rows) {
-          const double4* tp = reinterpret_cast<const double4*>(tb) + lane + 4 * h * rows;
+    if (J < I) {
+      const double* rJ = rl + J * 32 + 16 * h;
 #pragma unroll
-          for (int k4 = 0; k4 < 4; ++k4) {
-            const double4 v = ld_stream4(tp + k4 * rows);
-            a[4 * k4] = v.x;
-            a[4 * k4 + 1] = v.y;
-            a[4 * k4 + 2] = v.z;
-            a[4 * k4 + 3] = v.w;
-          }
-        } else {
+      for (int q = 0; q < 16; ++q) row = fma(a[q], rJ[q], row);
 #pragma unroll
-          for (int q = 0; q < 16; ++q) a[q] = 0.0;
-        }
-        const double* rJ = rl + J * 32 + 16 * h;
+      for (int q = 0; q < 16; ++q) a[q] *= ri;
+    } else {
+      const double* rI = rl + I * 32 + 16 * h;
 #pragma unroll
-        for (int q = 0; q < 16; ++q) row = fma(a[q], rJ[q], row);
+      for (int q = 0; q < 16; ++q) row = fma(a[q], rI[q], row);
 #pragma unroll
-        for (int q = 0; q < 16; ++q) a[q] *= ri;
-      } else {
-        // diagonal tile, lower triangle packed by columns: (i,k), k <= i at k*rows - k(k-1)/2 + i - k
-#pragma unroll
-        for (int q = 0; q < 16; ++q) {
-          const int k = 16 * h + q;
-          a[q] = (k <= lane && lane < rows) ? ld_stream1(tb + k * rows - k * (k - 1) / 2 + (lane - k)) : 0.0;
-        }
-        const double* rI = rl + I * 32 + 16 * h;
-#pragma unroll
-        for (int q = 0; q < 16; ++q) row = fma(a[q], rI[q], row);
-#pragma unroll
-        for (int q = 0; q < 16; ++q) a[q] = (16 * h + q < lane) ? a[q] * ri : 0.0;  // strict lower, transposed
+      for (int q = 0; q < 16; ++q) a[q] = (16 * h + q < lane) ? a[q] * ri : 0.0;  // strict lower, transposed
+    }
+    const double col = treduce16(a, lane);
+    if (lane < 16) atomicAdd(zl + J * 32 + 16 * h + lane, col);
+    if (h == 1) {  // tile done: its row products, then this warp's next tile
+      atomicAdd(zl + I * 32 + lane, row);
+      row = 0.0;
+      h = 0;
+      t += kLdgWarps;
+      J += kLdgWarps;
+      while (J > I) {
+        J -= I + 1;
+        ++I;
       }
-      const double col = treduce16(a, lane);
-      if (lane < 16) atomicAdd(zl + J * 32 + 16 * h + lane, col);
+    } else {
+      h = 1;
     }
-    atomicAdd(zl + I * 32 + lane, row);
-    J += kLdgWarps;
-    while (J > I) {
-      J -= I + 1;
-      ++I;
-    }
+    if (t < ntiles) load_half(a);
   }
   if (pdl_late()) pdl_trigger();
   __syncthreads();

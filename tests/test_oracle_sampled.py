@@ -25,3 +25,16 @@ def test_sampled_rows_match_global(space, p, bc, coeffs, dec):
     ys, zs = S.apply_rows(x, rows), S.precond_rows(x, rows)
     assert np.allclose(ys, y[rows], rtol=1e-12, atol=1e-12 * np.abs(y).max())
     assert np.allclose(zs, z[rows], rtol=1e-12, atol=1e-12 * np.abs(z).max())
+
+
+def test_precond_residual_rows():
+    """P^-1 (b - A x) on sampled rows equals the global oracle's, at an
+    arbitrary x (so the stopping-rule check of the full-size tests is exact)."""
+    c = make_config(0, n=2, p=3, space=HCURL, perturb=True, bc="x0", coeffs="loguniform")
+    O = Oracle(c.vertices, c.tets, c.p, c.space, c.alpha, c.beta, c.mask)
+    S = SampledOracle(c.vertices, c.tets, c.p, c.space, c.alpha, c.beta, c.mask)
+    b, x = c.draw_vector(O.n_total), c.draw_vector(O.n_total)
+    rows = np.random.default_rng(2).choice(O.n_total, 30, replace=False)
+    ref = O.precond(O.mask(b) - O.apply(x))[rows]
+    got = S.precond_residual_rows(b, x, rows)
+    assert np.allclose(got, ref, rtol=1e-11, atol=1e-12 * np.abs(ref).max())

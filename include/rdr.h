@@ -143,6 +143,11 @@ int rdr_measure_fp64_peak(double* tflops, void* stream);
 void rdr_destroy(rdr_handle* h);
 const char* rdr_strerror(int code);
 
+/* Debugging entry point: one fused PCG operator apply at iteration 0 (q = A z
+ * through the PCG variant of the apply kernel, which also writes the search
+ * direction); compared against rdr_apply by the GPU tests. Synchronizes. */
+int rdr_debug_fused_apply(rdr_handle* h, const double* z, double* q, void* stream);
+
 /* Host-only debug entry points (no device needed).
  * rdr_reference_matrices: the n_mat reference matrices of (space, p) in
  * float64, layout [n_mat][n_loc][n_loc]; pass out = NULL to query *n_loc and

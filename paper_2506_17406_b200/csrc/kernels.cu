@@ -189,6 +189,15 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// Release a TMA ring slot: the CTA-scope fence makes this thread's earlier
+// shared-memory loads of the slot complete before the arrive (ptxas issues a
+// plain mbarrier.arrive right behind still-outstanding LDS, and the TMA refill
+// it unblocks then races those loads).
+__device__ __forceinline__ void mbar_release(uint64_t* bar) {
+  asm volatile("fence.acq_rel.cta;" ::: "memory");
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n"
@@ -251,7 +260,7 @@ __global__ void __launch_bounds__((kApplyWarps + 1) * 32, 2)
   if (threadIdx.x == 0) {
     for (int s = 0; s < kApplySlots; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], MW);
+      mbar_init(&empty[s], MW * 32);  // every consumer lane releases its own reads of the slot
     }
     mbar_fence_init();
   }
@@ -347,9 +356,9 @@ __global__ void __launch_bounds__((kApplyWarps + 1) * 32, 2)
 
   if (producer) {
     if (lane == 0) {
-      for (int c = kApplySlots; c < nchunks; ++c) {
+      for (int c = prefilled; c < nchunks; ++c) {
         const int slot = c % kApplySlots;
-        mbar_wait(&empty[slot], ((c / kApplySlots) - 1) & 1);
+        if (c >= kApplySlots) mbar_wait(&empty[slot], ((c / kApplySlots) - 1) & 1);
         mbar_expect_tx(&full[slot], kChunkBytes);
         bulk_g2s(ring + slot * kApplyKC * kApplyCols, Bg + (size_t)c * kApplyKC * kApplyCols, kChunkBytes,
                  &full[slot]);
@@ -390,8 +399,11 @@ __global__ void __launch_bounds__((kApplyWarps + 1) * 32, 2)
           cs1 = s < nm ? cr1[s] : 0.0;
         }
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[slot]);
+      // Every lane releases the slot after its own loads of it completed. An
+      // arrive issued right behind the LDS let the TMA refill overwrite the slot
+      // while the loads were still in flight: one warp in ~1 of 2 launches read
+      // half-refilled fragments (PCG variant, BM = 32, p = 10).
+      mbar_release(&empty[slot]);
     }
   }
   __syncthreads();  // every chunk consumed (all bulk copies complete): the ring is free
@@ -701,14 +713,18 @@ __global__ void __launch_bounds__(kPatchWarps * 32, 2)
   const int NP = pc.npad_max;
   const int ZB = pc.zbufs;                    // private z copies per warp (1 or 2)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw) + warp * K;
-  double* ring = reinterpret_cast<double*>(smem_raw + 8 * pc.ring_slots) + (size_t)warp * K * 1024;  // [K][1024]
-  double* rbuf = reinterpret_cast<double*>(smem_raw + 8 * pc.ring_slots) + (size_t)pc.ring_slots * 1024;  // [2][NP]
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw) + warp * 2 * K;
+  uint64_t* used = full + K;  // per slot: the 32 lanes' reads done (count 32)
+  double* ring = reinterpret_cast<double*>(smem_raw + 16 * pc.ring_slots) + (size_t)warp * K * 1024;  // [K][1024]
+  double* rbuf = reinterpret_cast<double*>(smem_raw + 16 * pc.ring_slots) + (size_t)pc.ring_slots * 1024;  // [2][NP]
   double* zw = rbuf + 2 * NP;                                            // [ZB][8 warps][NP]
   __shared__ int claim[kClaimRing];
   for (int i = threadIdx.x; i < kClaimRing; i += blockDim.x) claim[i] = kUnclaimed;
   if (lane == 0) {
-    for (int s = 0; s < K; ++s) mbar_init(&full[s], 1);
+    for (int s = 0; s < K; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&used[s], 32);
+    }
     mbar_fence_init();
   }
   __syncthreads();
@@ -790,11 +806,13 @@ __global__ void __launch_bounds__(kPatchWarps * 32, 2)
         }
         acc_i = (ad[0] + ad[1]) + (ad[2] + ad[3]);
       }
-      // slot consumed: refill it with this warp's tile K ahead (generic reads
-      // ordered before the async-proxy write by the fence)
-      __syncwarp();
+      // slot consumed by every lane once its products are computed (the arrive
+      // depends on them, hence on the tile loads): lane 0 refills the slot with
+      // this warp's tile K ahead once all 32 lanes arrived
+      mbar_release(&used[slot]);
       if (pre.valid()) {
         if (lane == 0) {
+          mbar_wait(&used[slot], phase);
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           issue_tile(pc, pre, ring + (size_t)slot * 1024, &full[slot]);
         }
@@ -865,7 +883,7 @@ __global__ void __launch_bounds__(kPatchWarps * 32, 2)
 }
 
 size_t patch_smem_bytes(int slots, int npad_max, int zbufs) {
-  return sizeof(uint64_t) * slots +
+  return sizeof(uint64_t) * 2 * slots +
          sizeof(double) * ((size_t)slots * 1024 + (2 + (size_t)zbufs * kPatchWarps) * (size_t)npad_max);
 }
 

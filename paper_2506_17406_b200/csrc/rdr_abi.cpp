@@ -561,6 +561,24 @@ int rdr_solve_host(rdr_handle* h, const double* b_host, double* x_host, double r
   return st;
 }
 
+int rdr_debug_fused_apply(rdr_handle* h, const double* z, double* q, void* stream) {
+  // one fused PCG apply at iteration 0 (p_0 = z): q = A z, for debugging the PCG mode of the kernel
+  if (!h || !z || !q || !h->fused) return RDR_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t n = h->n_total;
+  CK(cudaStreamSynchronize(s));
+  std::memset(h->h_sc, 0, sizeof(PcgScalars));
+  h->h_sc->rtol = 0.0;
+  h->h_sc->maxit = 1000;
+  CK(cudaMemcpyAsync(h->d_sc, h->h_sc, sizeof(PcgScalars), cudaMemcpyHostToDevice, s));
+  CK(cudaMemsetAsync(h->d_p, 0, sizeof(double) * n, s));
+  CK(cudaMemsetAsync(h->d_p2, 0, sizeof(double) * n, s));
+  CK(cudaMemsetAsync(q, 0, sizeof(double) * n, s));
+  CK(launch_pcg_fused_apply(h->op, h->d_sc, z, h->d_p, h->d_p2, q, s));
+  CK(cudaStreamSynchronize(s));
+  return RDR_OK;
+}
+
 int rdr_last_launches(const rdr_handle* h, int64_t* launches) {
   if (!h || !launches) return RDR_EINVAL;
   *launches = h->last_launches;

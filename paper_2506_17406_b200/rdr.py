@@ -56,6 +56,7 @@ def _load():
         "rdr_last_launches": (ctypes.c_int, [P, ctypes.POINTER(I64)]),
         "rdr_time_kernels": (ctypes.c_int, [P, P, P, P, P, ctypes.c_int, P, P]),
         "rdr_measure_fp64_peak": (ctypes.c_int, [ctypes.POINTER(D), P]),
+        "rdr_debug_fused_apply": (ctypes.c_int, [P, P, P, P]),
         "rdr_destroy": (None, [P]),
         "rdr_strerror": (ctypes.c_char_p, [ctypes.c_int]),
         "rdr_reference_matrices": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, P, ctypes.POINTER(I32),
@@ -195,6 +196,11 @@ class Solver:
         _check(_lib.rdr_time_kernels(self._h, _ptr(x), _ptr(y), _ptr(r), _ptr(z), int(reps), _ptr(ms),
                                      _stream(stream)), "rdr_time_kernels")
         return ms
+
+    def debug_fused_apply(self, z, q, stream=None):
+        """q = A z through the fused PCG variant of the apply kernel (debugging)."""
+        _check(_lib.rdr_debug_fused_apply(self._h, _ptr(z), _ptr(q), _stream(stream)), "rdr_debug_fused_apply")
+        return q
 
     def last_launches(self) -> int:
         n = ctypes.c_int64()

@@ -366,3 +366,21 @@ def test_unsplit_config5_sampled(torch_cuda):
     rows = _sample_rows(O, n_vertices=2, n_cells=3)
     _check_sampled(torch_cuda, c, S, O, rows)
     _check_sampled_pcg(torch_cuda, c, S, O, rows, b)
+
+
+def test_fused_apply_ring_race_regression(torch_cuda):
+    """The PCG (fused) variant of the apply kernel equals rdr_apply on every one
+    of 20 launches at p = 10 on a 12^3 mesh (32 cells per CTA): before the
+    ring-slot release waited for the consumers' shared loads (mbar_release),
+    about half of these launches had one warp read a half-refilled TMA slot."""
+    from paper_2506_17406_b200 import rdr
+    torch = torch_cuda
+    c = make_config(3, n=12)
+    S = rdr.Solver(c.vertices, c.tets, c.p, c.space, c.alpha, c.beta, c.mask)
+    z = torch.from_numpy(c.draw_vector(S.n_total)).cuda()
+    z = z * (S.apply(torch.ones_like(z)) != 0)
+    ref = S.apply(z).cpu().numpy()
+    for _ in range(20):
+        q = torch.zeros_like(z)
+        S.debug_fused_apply(z, q)
+        assert rel(q.cpu().numpy(), ref) <= 1e-13

@@ -53,8 +53,20 @@ enum { RDR_HGRAD = 0, RDR_HCURL = 1 };
  *               (P:1783-1787). */
 enum { RDR_SPLIT = 0, RDR_UNSPLIT = 1 };
 
+/* Composition of the preconditioner:
+ *   RDR_ADDITIVE (default, the hot path) one-level additive J(X_I) + patches;
+ *   RDR_HYBRID   the paper's symmetric multiplicative hybrid Schwarz (P:2399-2455,
+ *                NEXT-1): sweep X_I (Jacobi), X_Gamma (additive patches),
+ *                W^k (exact solve on the Whitney space: vertex dofs for H(grad),
+ *                Whitney edge dofs for H(curl), Lemma 4.1), X_Gamma, X_I, each
+ *                damped by rho_m = (lambda_min + 3 lambda_max)/4 from 10 CG-Lanczos
+ *                steps. Split decomposition only; costs 4 extra
+ *                operator applies per preconditioner application. */
+enum { RDR_ADDITIVE = 0, RDR_HYBRID = 1 };
+
 struct rdr_options {
-  int decomposition; /* RDR_SPLIT or RDR_UNSPLIT */
+  int decomposition;  /* RDR_SPLIT or RDR_UNSPLIT */
+  int preconditioner; /* RDR_ADDITIVE or RDR_HYBRID */
 };
 
 enum {
@@ -95,13 +107,15 @@ int rdr_setup(rdr_handle** h, const double* vertices, int64_t nv, const int32_t*
               int p, int space, const double* alpha, const double* beta,
               const uint8_t* dirichlet_mask, void* stream);
 
-/* rdr_setup with options (NULL = defaults: RDR_SPLIT). RDR_EINVAL for an
- * unknown decomposition. */
+/* rdr_setup with options (NULL = defaults: RDR_SPLIT, RDR_ADDITIVE). RDR_EINVAL
+ * for an unknown decomposition or preconditioner, or RDR_HYBRID with RDR_UNSPLIT. */
 int rdr_setup_ex(rdr_handle** h, const double* vertices, int64_t nv, const int32_t* tets, int64_t nt,
                  int p, int space, const double* alpha, const double* beta,
                  const uint8_t* dirichlet_mask, const struct rdr_options* opt, void* stream);
 
 int rdr_ndofs(const rdr_handle* h, int64_t* n_total);
+/* rho[3]: the hybrid Schwarz weights rho_1 (interior Jacobi), rho_2 (patches), rho_3 = 1 (coarse). */
+int rdr_get_weights(const rdr_handle* h, double* rho);
 int rdr_get_info(const rdr_handle* h, struct rdr_info* out);
 
 /* y = A x (device pointers, length n_total): gather, per-cell contraction

@@ -6,6 +6,7 @@
 // ~7e12 flop) runs at tens of GFLOP/s per core instead of streaming each row
 // pair from memory.
 #include <immintrin.h>
+#include <omp.h>
 
 #include <algorithm>
 #include <cmath>
@@ -68,9 +69,11 @@ inline double dot1(const double* a, const double* b, int k0, int k1) {
 // C[i][j] -= sum_{k in [k0,k1)} R[i][k] S[j][k] for i in [i0,i1), j in [j0,j1),
 // j <= i only when `lower` (row-major, leading dimension ld)
 void dot_update(double* C, const double* R, const double* S, int ld, int i0, int i1, int j0, int j1, int k0, int k1,
-                bool lower, double sign) {
-  int i = i0;
-  for (; i + 4 <= i1; i += 4) {
+                bool lower, double sign, bool par = false) {
+  const int nblk = (i1 - i0) / 4;
+#pragma omp parallel for schedule(dynamic, 4) if (par)
+  for (int ib = 0; ib < nblk; ++ib) {
+    const int i = i0 + 4 * ib;
     const double* a[4] = {R + (size_t)i * ld, R + (size_t)(i + 1) * ld, R + (size_t)(i + 2) * ld,
                           R + (size_t)(i + 3) * ld};
     const int jend = lower ? std::min(j1, i + 4) : j1;
@@ -87,7 +90,7 @@ void dot_update(double* C, const double* R, const double* S, int ld, int i0, int
       for (int r = 0; r < 4; ++r)
         if (!lower || j <= i + r) C[(size_t)(i + r) * ld + j] += sign * dot1(a[r], S + (size_t)j * ld, k0, k1);
   }
-  for (; i < i1; ++i) {
+  for (int i = i0 + 4 * nblk; i < i1; ++i) {
     const int jend = lower ? std::min(j1, i + 1) : j1;
     for (int j = j0; j < jend; ++j)
       C[(size_t)i * ld + j] += sign * dot1(R + (size_t)i * ld, S + (size_t)j * ld, k0, k1);
@@ -98,17 +101,21 @@ void dot_update(double* C, const double* R, const double* S, int ld, int i0, int
 
 bool spd_inverse(double* A, int n, std::vector<double>& work) {
   constexpr int NB = 64;
+  // one large matrix (the coarse space) outside a parallel region: threads
+  // inside each step; the patch matrices are inverted one per thread instead
+  const bool par = n >= 1024 && !omp_in_parallel();
   // ---- 1. Cholesky, lower, row-major, left-looking by block columns
   for (int jb = 0; jb < n; jb += NB) {
     const int je = std::min(n, jb + NB);
     // block column update with the finished columns [0, jb)
-    if (jb > 0) dot_update(A, A, A, n, jb, n, jb, je, 0, jb, /*lower=*/true, -1.0);
+    if (jb > 0) dot_update(A, A, A, n, jb, n, jb, je, 0, jb, /*lower=*/true, -1.0, par);
     // diagonal block and the panel below, column by column within the block
     for (int j = jb; j < je; ++j) {
       double d = A[(size_t)j * n + j] - dot1(A + (size_t)j * n, A + (size_t)j * n, jb, j);
       if (!(d > 0)) return false;
       const double l = std::sqrt(d), inv = 1.0 / l;
       A[(size_t)j * n + j] = l;
+#pragma omp parallel for schedule(static) if (par && n - j > 4096)
       for (int i = j + 1; i < n; ++i)
         A[(size_t)i * n + j] = (A[(size_t)i * n + j] - dot1(A + (size_t)i * n, A + (size_t)j * n, jb, j)) * inv;
     }
@@ -125,6 +132,7 @@ bool spd_inverse(double* A, int n, std::vector<double>& work) {
   for (int i = 0; i < n; ++i) {
     const double* Li = A + (size_t)i * n;
     const double inv = Yt[(size_t)i * n + i];
+#pragma omp parallel for schedule(static) if (par && i > 2048)
     for (int j = 0; j < i; ++j) {
       // sum_{k=j}^{i-1} L[i][k] * Yt[j][k]   (Yt[j][k] = 0 for k < j)
       const double s = dot1(Li, Yt + (size_t)j * n, j, i);
@@ -133,6 +141,7 @@ bool spd_inverse(double* A, int n, std::vector<double>& work) {
   }
   // ---- 3. A^-1[i][j] = sum_{k >= max(i,j)} Y[k][i] Y[k][j] = dot(Yt row i, Yt row j), j <= i;
   // row i of Yt vanishes below k = i, so a block of rows [i0, i0+4) starts at k = i0
+#pragma omp parallel for schedule(dynamic, 2) if (par)
   for (int i0 = 0; i0 < n; i0 += 4) {
     const int i1 = std::min(n, i0 + 4);
     for (int i = i0; i < i1; ++i)

@@ -186,9 +186,6 @@ __device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
 // Release a TMA ring slot: the CTA-scope fence makes this thread's earlier
 // shared-memory loads of the slot complete before the arrive (ptxas issues a
 // plain mbarrier.arrive right behind still-outstanding LDS, and the TMA refill
@@ -839,7 +836,7 @@ __global__ void __launch_bounds__(kPatchWarps * 32, 2)
         double zi = 0.0;
 #pragma unroll
         for (int w = 0; w < kPatchWarps; ++w) zi += zk[(size_t)w * NP + i];
-        atomicAdd(zout + id[i], zi);
+        atomicAdd(zout + id[i], pc.out_scale * zi);
         part = fma(rl[i], zi, part);
       }
       patch_gather(pc, get_patch(pc, claim, k + 2), r, rl);
@@ -1032,7 +1029,7 @@ __global__ void __launch_bounds__(kLdgWarps * 32, 32 / kLdgWarps)
   double part = 0.0;
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     const double zi = zl[i];
-    atomicAdd(zout + id[i], zi);
+    atomicAdd(zout + id[i], pc.out_scale * zi);
     part = fma(rl[i], zi, part);
   }
   if (rz_acc) {
@@ -1040,6 +1037,117 @@ __global__ void __launch_bounds__(kLdgWarps * 32, 32 / kLdgWarps)
     const double s = block_sum(part, sh);
     if (threadIdx.x == 0) atomicAdd(rz_acc, s);
   }
+}
+
+// ---------------------------------------------------------------- hybrid Schwarz
+// Symmetric multiplicative sweep J, P, C, P, J: helpers.
+// e = s * dinv .* r on the interior dofs (set: e = 0 elsewhere; add: e += ...)
+__global__ void hyb_jacobi_kernel(DevPrecond pc, const double* __restrict__ r, double* __restrict__ e, double s,
+                                  int add) {
+  pdl_wait();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < pc.n_total; i += stride) {
+    const double v = i >= pc.off3 ? s * pc.dinv[i - pc.off3] * r[i] : 0.0;
+    e[i] = add ? e[i] + v : v;
+  }
+  if (pc.ubuf)
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < pc.n_cg_iface; i += stride) pc.ubuf[i] = 0.0;
+}
+
+// t = r - y (y = A e, constrained rows already 0); also clears the coarse accumulators
+__global__ void hyb_residual_kernel(DevPrecond pc, const double* __restrict__ r, const double* __restrict__ y,
+                                    double* __restrict__ t) {
+  pdl_wait();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < pc.n_total; i += stride) t[i] = r[i] - y[i];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < pc.nc; i += stride) pc.czc[i] = 0.0;
+  if (pc.ubuf)
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < pc.n_cg_iface; i += stride) pc.ubuf[i] = 0.0;
+}
+
+// coarse solve e += E_c A_c^-1 E_c^T t: the stored packed inverse of the
+// Whitney-space matrix (setup.hpp tile layout "groups", one n_c x n_c patch),
+// tiles spread over the whole grid (one warp per tile, half tiles as in
+// patch_ldg_kernel), row and transposed products accumulated into czc with
+// red.global.add; the coarse residual is read through cidx.
+__global__ void __launch_bounds__(256) coarse_symv_kernel(DevPrecond pc, const double* __restrict__ t) {
+  pdl_wait();
+  const int n = (int)pc.nc, nb = (n + 31) >> 5;
+  const int64_t ntiles = (int64_t)nb * (nb + 1) / 2;
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t tt = gw; tt < ntiles; tt += nw) {
+    // (I, J) of tile tt in order I(I+1)/2 + J
+    int I = (int)((sqrt(8.0 * (double)tt + 1.0) - 1.0) * 0.5);
+    while ((int64_t)(I + 1) * (I + 2) / 2 <= tt) ++I;
+    while ((int64_t)I * (I + 1) / 2 > tt) --I;
+    const int J = (int)(tt - (int64_t)I * (I + 1) / 2);
+    const int rows = min(32, n - 32 * I);
+    const double* tb = pc.ctiles + 512LL * I * I + 16LL * I + (int64_t)J * 32 * rows;
+    const int gi = 32 * I + lane;
+    const double ri = (lane < rows) ? t[pc.cidx[gi]] : 0.0;
+    double row = 0.0;
+#pragma unroll 1
+    for (int h = 0; h < 2; ++h) {
+      double a[16];
+      const int gj0 = 32 * J + 16 * h;
+      if (J < I) {
+        if (lane < rows) {
+          const double4* tp = reinterpret_cast<const double4*>(tb) + lane + 4 * h * rows;
+#pragma unroll
+          for (int k4 = 0; k4 < 4; ++k4) {
+            const double4 v = ld_stream4(tp + k4 * rows);
+            a[4 * k4] = v.x;
+            a[4 * k4 + 1] = v.y;
+            a[4 * k4 + 2] = v.z;
+            a[4 * k4 + 3] = v.w;
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < 16; ++q) a[q] = 0.0;
+        }
+        // r_J from the broadcast of lane-held values: lane q holds t at column gj0 + q
+        const double rjl = (gj0 + (lane & 15) < n) ? t[pc.cidx[gj0 + (lane & 15)]] : 0.0;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) row = fma(a[q], __shfl_sync(0xffffffffu, rjl, q), row);
+#pragma unroll
+        for (int q = 0; q < 16; ++q) a[q] *= ri;
+      } else {
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          const int k = 16 * h + q;
+          a[q] = (k <= lane && lane < rows) ? ld_stream1(tb + k * rows - k * (k - 1) / 2 + (lane - k)) : 0.0;
+        }
+        const double ril = __shfl_sync(0xffffffffu, ri, (16 * h + (lane & 15)) & 31);
+#pragma unroll
+        for (int q = 0; q < 16; ++q) row = fma(a[q], __shfl_sync(0xffffffffu, ril, q), row);
+#pragma unroll
+        for (int q = 0; q < 16; ++q) a[q] = (16 * h + q < lane) ? a[q] * ri : 0.0;
+      }
+      const double col = treduce16(a, lane);
+      if (lane < 16 && gj0 + lane < n) atomicAdd(pc.czc + gj0 + lane, col);
+    }
+    if (lane < rows) atomicAdd(pc.czc + gi, row);
+  }
+}
+
+// e[cidx[k]] += czc[k]
+__global__ void coarse_scatter_kernel(DevPrecond pc, double* __restrict__ e) {
+  pdl_wait();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < pc.nc; k += stride) e[pc.cidx[k]] += pc.czc[k];
+}
+
+// r.z into sc->rz_new (the hybrid preconditioner does not accumulate it itself)
+__global__ void pcg_rz_kernel(PcgScalars* sc, const double* __restrict__ r, const double* __restrict__ z, int64_t n) {
+  pdl_wait();
+  if (stopped(sc)) return;
+  double part = 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) part = fma(r[i], z[i], part);
+  __shared__ double sh[32];
+  const double s = block_sum(part, sh);
+  if (threadIdx.x == 0) atomicAdd(&sc->rz_new, s);
 }
 
 // ---------------------------------------------------------------- PCG vector kernels
@@ -1235,6 +1343,44 @@ cudaError_t launch_precond_part(int part, const DevPrecond& pc, const double* r,
       break;
   }
   return cudaGetLastError();
+}
+
+cudaError_t launch_precond_hybrid(const DevOperator& op, const DevPrecond& pc, const double* r, double* z,
+                                  const PcgScalars* guard, cudaStream_t s) {
+  // symmetric multiplicative sweep X_I (Jacobi), X_Gamma (patches), W (coarse), X_Gamma, X_I
+  const dim3 vg(vec_grid(pc.n_total)), vb(kVecThreads);
+  cudaError_t e = launch_k(hyb_jacobi_kernel, vg, vb, 0, s, pc, r, z, pc.s1, 0);
+  if (e != cudaSuccess) return e;
+  DevPrecond pp = pc;
+  pp.out_scale = pc.s2;
+  for (int stage = 1; stage < 5; ++stage) {
+    if ((e = cudaMemsetAsync(pc.hy, 0, sizeof(double) * pc.n_total, s)) != cudaSuccess) return e;
+    if ((e = launch_apply(op, z, pc.hy, nullptr, guard, s)) != cudaSuccess) return e;
+    if ((e = launch_k(hyb_residual_kernel, vg, vb, 0, s, pc, r, (const double*)pc.hy, pc.ht)) != cudaSuccess) return e;
+    if (stage == 1 || stage == 3) {  // interface star patches, weight 1/rho_2
+      for (int part = 1; part < 4; ++part)
+        if ((e = launch_precond_part(part, pp, pc.ht, z, nullptr, guard, s)) != cudaSuccess) return e;
+    } else if (stage == 2) {         // exact coarse solve on W^k
+      if (pc.nc > 0) {
+        if ((e = launch_k(coarse_symv_kernel, dim3(148 * 4), dim3(256), 0, s, pc, (const double*)pc.ht)) != cudaSuccess)
+          return e;
+        if ((e = launch_k(coarse_scatter_kernel, dim3(vec_grid(pc.nc)), vb, 0, s, pc, z)) != cudaSuccess) return e;
+      }
+    } else {                         // interior Jacobi, weight 1/rho_1
+      if ((e = launch_k(hyb_jacobi_kernel, vg, vb, 0, s, pc, (const double*)pc.ht, z, pc.s1, 1)) != cudaSuccess)
+        return e;
+    }
+  }
+  return cudaSuccess;
+}
+
+int count_hybrid_launches(const DevPrecond& pc) {
+  const int patches = (pc.n_patches > 0 ? 1 : 0) + (pc.gbuf ? 2 : 0);
+  return 1 + 4 * 2 + 2 * patches + (pc.nc > 0 ? 2 : 0) + 1;
+}
+
+cudaError_t launch_pcg_rz(PcgScalars* sc, const double* r, const double* z, int64_t n, cudaStream_t s) {
+  return launch_k(pcg_rz_kernel, dim3(vec_grid(n)), dim3(kVecThreads), 0, s, sc, r, z, n);
 }
 
 cudaError_t launch_precond(const DevPrecond& pc, const double* r, double* z, double* rz_acc,

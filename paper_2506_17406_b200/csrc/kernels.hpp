@@ -66,6 +66,16 @@ struct DevPrecond {
   const double* g_val;
   double* gbuf;                 // G^T r (CG numbering)
   double* ubuf;                 // patch corrections in the CG numbering
+  double out_scale;             // patch corrections are scaled by this (1; 1/rho_2 in the hybrid sweep)
+  // hybrid Schwarz: Whitney coarse space and sweep workspace
+  int hybrid;                   // 0 additive (J + patches), 1 symmetric multiplicative J,P,C,P,J
+  double s1, s2;                // 1/rho_1 (interior Jacobi), 1/rho_2 (interface patches)
+  int64_t nc;                   // coarse dofs
+  const int32_t* cidx;          // [nc] their global ids
+  const double* ctiles;         // packed inverse of A restricted to W^k (patch tile layout)
+  double* czc;                  // [nc] coarse correction accumulators
+  double* ht;                   // [n_total] sweep residual r - A e
+  double* hy;                   // [n_total] A e
 };
 
 cudaError_t launch_apply(const DevOperator& op, const double* x, double* y, double* pq_acc,
@@ -76,6 +86,12 @@ cudaError_t launch_precond(const DevPrecond& pc, const double* r, double* z, dou
 // 2 patch solves, 3 z += G u (H(curl))
 cudaError_t launch_precond_part(int part, const DevPrecond& pc, const double* r, double* z, double* rz_acc,
                                 const PcgScalars* guard, cudaStream_t s);
+// z = P^-1 r with the hybrid sweep J, P, C, P, J (pc.hybrid = 1); needs the operator for the residuals
+cudaError_t launch_precond_hybrid(const DevOperator& op, const DevPrecond& pc, const double* r, double* z,
+                                  const PcgScalars* guard, cudaStream_t s);
+int count_hybrid_launches(const DevPrecond& pc);
+// sc->rz_new += r.z
+cudaError_t launch_pcg_rz(PcgScalars* sc, const double* r, const double* z, int64_t n, cudaStream_t s);
 
 // PCG pieces (DESIGN.md R-A16)
 cudaError_t launch_pcg_init(const double* b, const uint8_t* constrained, int64_t n, double* x, double* r,

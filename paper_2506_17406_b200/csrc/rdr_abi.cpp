@@ -2,7 +2,9 @@
 // operator, preconditioner and PCG.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <chrono>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -76,6 +78,50 @@ struct DeviceTiles : PatchSink {
   }
 };
 
+// uniform[-1,1] from splitmix64(seed + i) (the counter-based Lanczos start
+// vector of the hybrid weights; oracle/hybrid.py lanczos_rhs implements the same)
+double splitmix_uniform(uint64_t seed, uint64_t i) {
+  uint64_t z = (i + seed) * 0x9E3779B97F4A7C15ULL;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  z ^= z >> 31;
+  return 2.0 * ((double)(z >> 11) * 0x1.0p-53) - 1.0;
+}
+constexpr uint64_t kLanczosSeed = 0x5EED;
+constexpr int kLanczosSteps = 10;
+
+// eigenvalues of a small symmetric matrix (cyclic Jacobi), ascending
+std::vector<double> sym_eigenvalues(std::vector<double> A, int n) {
+  for (int sweep = 0; sweep < 100; ++sweep) {
+    double off = 0;
+    for (int p = 0; p < n; ++p)
+      for (int q = p + 1; q < n; ++q) off += A[p * n + q] * A[p * n + q];
+    if (off < 1e-300) break;
+    for (int p = 0; p < n; ++p)
+      for (int q = p + 1; q < n; ++q) {
+        const double apq = A[p * n + q];
+        if (apq == 0.0) continue;
+        const double theta = (A[q * n + q] - A[p * n + p]) / (2 * apq);
+        const double t = (theta >= 0 ? 1.0 : -1.0) / (std::fabs(theta) + std::sqrt(theta * theta + 1));
+        const double c = 1 / std::sqrt(t * t + 1), sn = t * c;
+        for (int k = 0; k < n; ++k) {
+          const double akp = A[k * n + p], akq = A[k * n + q];
+          A[k * n + p] = c * akp - sn * akq;
+          A[k * n + q] = sn * akp + c * akq;
+        }
+        for (int k = 0; k < n; ++k) {
+          const double apk = A[p * n + k], aqk = A[q * n + k];
+          A[p * n + k] = c * apk - sn * aqk;
+          A[q * n + k] = sn * apk + c * aqk;
+        }
+      }
+  }
+  std::vector<double> ev(n);
+  for (int i = 0; i < n; ++i) ev[i] = A[i * n + i];
+  std::sort(ev.begin(), ev.end());
+  return ev;
+}
+
 }  // namespace
 
 struct rdr_handle {
@@ -98,6 +144,7 @@ struct rdr_handle {
   bool device_loop = true;           // RDR_PCG_HOSTLOOP=1: host-driven graph of 8 iterations instead
   int graph_iters = 0;
   int launches_per_iter = 0;
+  double rho1 = 1.0, rho2 = 1.0;  // hybrid Schwarz weights (rdr_get_weights)
   int64_t last_launches = 0;
 
   template <class T>
@@ -120,9 +167,11 @@ struct rdr_handle {
   }
 };
 
+static int hybrid_weights(rdr_handle* h, const std::vector<double>& dinv);
+
 static int setup_impl(rdr_handle* h, const double* vertices, int64_t nv, const int32_t* tets, int64_t nt, int p,
                       int space, const double* alpha, const double* beta, const uint8_t* mask, bool unsplit,
-                      cudaStream_t stream) {
+                      bool hybrid, cudaStream_t stream) {
   auto t0 = std::chrono::steady_clock::now();
   if (stream) CK(cudaStreamSynchronize(stream));
   configure_kernels();
@@ -209,6 +258,10 @@ static int setup_impl(rdr_handle* h, const double* vertices, int64_t nv, const i
   // ---- preconditioner
   DevPrecond& pc = h->pc;
   pc.n_total = num.n_total;
+  pc.out_scale = 1.0;
+  pc.hybrid = 0;
+  pc.s1 = pc.s2 = 1.0;
+  pc.nc = 0;
   pc.off3 = num.off[3];
   std::vector<double> dinv;
   interior_inverse_diagonal(m, num, el, coef, dinv);
@@ -313,17 +366,38 @@ static int setup_impl(rdr_handle* h, const double* vertices, int64_t nv, const i
   const size_t vb = sizeof(double) * std::max<int64_t>(1, num.n_total);
   for (double** v : {&h->d_x, &h->d_r, &h->d_z, &h->d_p, &h->d_q, &h->d_b, &h->d_p2})
     if ((st = h->own_alloc((void**)v, vb))) return st;
-  h->fused = fused_pcg_supported(op);
+  h->fused = fused_pcg_supported(op) && !hybrid;
+  if (hybrid) {  // ---- Whitney coarse space + sweep workspace + weights
+    std::vector<int32_t> cidx;
+    std::vector<double> ctiles;
+    if ((st = build_coarse(m, num, el, coef, cidx, ctiles))) return st;
+    pc.nc = (int64_t)cidx.size();
+    int32_t* d_cidx;
+    double* d_ct;
+    if ((st = h->own_upload(&d_cidx, cidx))) return st;
+    if ((st = h->own_upload(&d_ct, ctiles))) return st;
+    pc.cidx = d_cidx;
+    pc.ctiles = d_ct;
+    if ((st = h->own_alloc((void**)&pc.czc, sizeof(double) * std::max<int64_t>(1, pc.nc)))) return st;
+    if ((st = h->own_alloc((void**)&pc.ht, vb))) return st;
+    if ((st = h->own_alloc((void**)&pc.hy, vb))) return st;
+    if ((st = hybrid_weights(h, dinv))) return st;
+    pc.hybrid = 1;
+  }
   h->device_loop = std::getenv("RDR_PCG_HOSTLOOP") == nullptr;
   if ((st = h->own_alloc((void**)&h->d_sc, sizeof(PcgScalars)))) return st;
   CK(cudaMallocHost((void**)&h->h_sc, sizeof(PcgScalars)));
   CK(cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
-  h->launches_per_iter = h->fused ? 1 + count_precond_launches(pc) : 4 + count_precond_launches(pc);
+  h->launches_per_iter = h->fused ? 1 + count_precond_launches(pc)
+                                  : 4 + (hybrid ? count_hybrid_launches(pc) + 1 : count_precond_launches(pc));
   // one warm-up apply/precond on zero vectors: kernel attributes get configured
   // here, outside any later stream capture
   CK(cudaMemset(h->d_p, 0, vb));
   CK(launch_apply(op, h->d_p, h->d_q, nullptr, nullptr, 0));
-  CK(launch_precond(pc, h->d_p, h->d_z, nullptr, nullptr, 0));
+  if (hybrid)
+    CK(launch_precond_hybrid(op, pc, h->d_p, h->d_z, nullptr, 0));
+  else
+    CK(launch_precond(pc, h->d_p, h->d_z, nullptr, nullptr, 0));
 
   // ---- info
   rdr_info& in = h->info;
@@ -346,6 +420,85 @@ static int setup_impl(rdr_handle* h, const double* vertices, int64_t nv, const i
   return RDR_OK;
 }
 
+// rho_m = (lambda_min + 3 lambda_max) / 4 of a~_m^-1 A on X_m from 10 CG
+// (Lanczos) steps with the splitmix64 rhs restricted to X_m (
+// oracle/hybrid.py does the same on the CPU): X_1 = interior dofs with the
+// point-Jacobi solver, X_2 = free interface dofs with the additive patches.
+static int hybrid_weights(rdr_handle* h, const std::vector<double>& dinv) {
+  const int64_t n = h->n_total, off3 = h->pc.off3;
+  std::vector<uint8_t> cons(n);
+  CK(cudaMemcpy(cons.data(), h->d_cons, n, cudaMemcpyDeviceToHost));
+  const size_t vb = sizeof(double) * n;
+  for (int m = 0; m < 2; ++m) {
+    std::vector<double> mask(n, 0.0);
+    int64_t dim = 0;
+    for (int64_t i = 0; i < n; ++i)
+      if (m == 0 ? i >= off3 : (i < off3 && !cons[i])) {
+        mask[i] = 1.0;
+        ++dim;
+      }
+    if (dim == 0) {
+      (m == 0 ? h->pc.s1 : h->pc.s2) = 1.0;
+      continue;
+    }
+    std::vector<double> r(n), z(n), pv(n), q(n);
+    auto applyA = [&](const std::vector<double>& v, std::vector<double>& out) -> int {
+      CK(cudaMemcpy(h->d_p, v.data(), vb, cudaMemcpyHostToDevice));
+      CK(cudaMemset(h->d_q, 0, vb));
+      CK(launch_apply(h->op, h->d_p, h->d_q, nullptr, nullptr, 0));
+      CK(cudaMemcpy(out.data(), h->d_q, vb, cudaMemcpyDeviceToHost));
+      for (int64_t i = 0; i < n; ++i) out[i] *= mask[i];
+      return RDR_OK;
+    };
+    auto applyP = [&](const std::vector<double>& v, std::vector<double>& out) -> int {
+      if (m == 0) {
+        for (int64_t i = 0; i < n; ++i) out[i] = i >= off3 ? dinv[i - off3] * v[i] : 0.0;
+        return RDR_OK;
+      }
+      CK(cudaMemcpy(h->d_r, v.data(), vb, cudaMemcpyHostToDevice));
+      CK(cudaMemset(h->d_z, 0, vb));
+      if (h->pc.ubuf) CK(cudaMemset(h->pc.ubuf, 0, sizeof(double) * h->pc.n_cg_iface));
+      for (int part = 1; part < 4; ++part) CK(launch_precond_part(part, h->pc, h->d_r, h->d_z, nullptr, nullptr, 0));
+      CK(cudaMemcpy(out.data(), h->d_z, vb, cudaMemcpyDeviceToHost));
+      for (int64_t i = 0; i < n; ++i) out[i] *= mask[i];
+      return RDR_OK;
+    };
+    auto dot = [&](const std::vector<double>& a, const std::vector<double>& b) {
+      double s = 0;
+      for (int64_t i = 0; i < n; ++i) s += a[i] * b[i];
+      return s;
+    };
+    int st;
+    for (int64_t i = 0; i < n; ++i) r[i] = mask[i] * splitmix_uniform(kLanczosSeed, (uint64_t)i);
+    if ((st = applyP(r, z))) return st;
+    pv = z;
+    double rz = dot(r, z);
+    std::vector<double> alphas, betas;
+    for (int k = 0; k < kLanczosSteps && rz > 0; ++k) {
+      if ((st = applyA(pv, q))) return st;
+      const double a = rz / dot(pv, q);
+      alphas.push_back(a);
+      for (int64_t i = 0; i < n; ++i) r[i] -= a * q[i];
+      if ((st = applyP(r, z))) return st;
+      const double rz_new = dot(r, z), beta = rz_new / rz;
+      betas.push_back(beta);
+      for (int64_t i = 0; i < n; ++i) pv[i] = z[i] + beta * pv[i];
+      rz = rz_new;
+    }
+    const int k = (int)alphas.size();
+    std::vector<double> T((size_t)k * k, 0.0);
+    for (int j = 0; j < k; ++j) {
+      T[j * k + j] = 1.0 / alphas[j] + (j > 0 ? betas[j - 1] / alphas[j - 1] : 0.0);
+      if (j + 1 < k) T[j * k + j + 1] = T[(j + 1) * k + j] = std::sqrt(betas[j]) / alphas[j];
+    }
+    const std::vector<double> ev = sym_eigenvalues(T, k);
+    const double rho = k > 0 ? (ev.front() + 3.0 * ev.back()) / 4.0 : 1.0;
+    (m == 0 ? h->pc.s1 : h->pc.s2) = 1.0 / rho;
+    (m == 0 ? h->rho1 : h->rho2) = rho;
+  }
+  return RDR_OK;
+}
+
 extern "C" {
 
 int rdr_setup_ex(rdr_handle** hp, const double* vertices, int64_t nv, const int32_t* tets, int64_t nt, int p,
@@ -359,12 +512,15 @@ int rdr_setup_ex(rdr_handle** hp, const double* vertices, int64_t nv, const int3
   if (nv > 0x7fffffff || nt > 0x7fffffff) return RDR_EINVAL;
   const int dec = opt ? opt->decomposition : RDR_SPLIT;
   if (dec != RDR_SPLIT && dec != RDR_UNSPLIT) return RDR_EINVAL;
+  const int pre = opt ? opt->preconditioner : RDR_ADDITIVE;
+  if (pre != RDR_ADDITIVE && pre != RDR_HYBRID) return RDR_EINVAL;
+  if (pre == RDR_HYBRID && dec != RDR_SPLIT) return RDR_EINVAL;
   rdr_handle* h = new (std::nothrow) rdr_handle();
   if (!h) return RDR_ENOMEM;
   int st;
   try {
     st = setup_impl(h, vertices, nv, tets, nt, p, space, alpha, beta, dirichlet_mask, dec == RDR_UNSPLIT,
-                    (cudaStream_t)stream);
+                    pre == RDR_HYBRID, (cudaStream_t)stream);
   } catch (const std::bad_alloc&) {
     st = RDR_ENOMEM;
   } catch (const std::exception& e) {
@@ -406,7 +562,18 @@ int rdr_apply(rdr_handle* h, const double* x, double* y, void* stream) {
 
 int rdr_precond(rdr_handle* h, const double* r, double* z, void* stream) {
   if (!h || !r || !z) return RDR_EINVAL;
-  CK(launch_precond(h->pc, r, z, nullptr, nullptr, (cudaStream_t)stream));
+  if (h->pc.hybrid)
+    CK(launch_precond_hybrid(h->op, h->pc, r, z, nullptr, (cudaStream_t)stream));
+  else
+    CK(launch_precond(h->pc, r, z, nullptr, nullptr, (cudaStream_t)stream));
+  return RDR_OK;
+}
+
+int rdr_get_weights(const rdr_handle* h, double* rho) {
+  if (!h || !rho) return RDR_EINVAL;
+  rho[0] = h->rho1;
+  rho[1] = h->rho2;
+  rho[2] = 1.0;
   return RDR_OK;
 }
 
@@ -421,7 +588,12 @@ static int enqueue_iteration(rdr_handle* h, cudaStream_t s, cudaGraphConditional
   }
   CK(launch_apply(h->op, h->d_p, h->d_q, &h->d_sc->pq, h->d_sc, s));
   CK(launch_pcg_update(h->d_sc, h->d_p, h->d_q, h->d_x, h->d_r, n, s));
-  CK(launch_precond(h->pc, h->d_r, h->d_z, &h->d_sc->rz_new, h->d_sc, s));
+  if (h->pc.hybrid) {
+    CK(launch_precond_hybrid(h->op, h->pc, h->d_r, h->d_z, h->d_sc, s));
+    CK(launch_pcg_rz(h->d_sc, h->d_r, h->d_z, n, s));
+  } else {
+    CK(launch_precond(h->pc, h->d_r, h->d_z, &h->d_sc->rz_new, h->d_sc, s));
+  }
   CK(launch_pcg_finish(h->d_sc, h->d_z, n, s));
   CK(launch_pcg_direction(h->d_sc, h->d_z, h->d_p, h->d_q, n, s));
   return RDR_OK;
@@ -523,7 +695,12 @@ static int solve_device(rdr_handle* h, const double* b, double rtol, int maxit, 
   } else {
     CK(cudaMemsetAsync(h->d_sc, 0, sizeof(PcgScalars), s));
     CK(launch_pcg_init(b, h->d_cons, n, h->d_x, h->d_r, h->d_q, s));
-    CK(launch_precond(h->pc, h->d_r, h->d_z, &h->d_sc->rz_new, nullptr, s));
+    if (h->pc.hybrid) {
+      CK(launch_precond_hybrid(h->op, h->pc, h->d_r, h->d_z, nullptr, s));
+      CK(launch_pcg_rz(h->d_sc, h->d_r, h->d_z, n, s));
+    } else {
+      CK(launch_precond(h->pc, h->d_r, h->d_z, &h->d_sc->rz_new, nullptr, s));
+    }
     CK(launch_pcg_start(h->d_sc, h->d_z, h->d_p, n, rtol, maxit, s));
     launches += 2 + count_precond_launches(h->pc);
     for (;;) {

@@ -282,6 +282,69 @@ void interior_inverse_diagonal(const Mesh& m, const Numbering& num, const RefEle
     }
 }
 
+void pack_patch_tiles(const double* W2, int n, double* out, PatchLayout layout) {
+  // exact packed lower triangle in 32-row block rows (setup.hpp patch layout)
+  const int nbk = (n + 31) / 32;
+  for (int I = 0; I < nbk; ++I) {
+    const int rows = std::min(32, n - 32 * I);
+    for (int J = 0; J <= I; ++J) {
+      double* tile = out + patch_tile_offset(n, I, J);
+      if (J < I) {  // full-width tile, `rows` rows (setup.hpp layouts)
+        for (int i = 0; i < rows; ++i)
+          for (int kk = 0; kk < 32; ++kk)
+            tile[layout == kTileGroups ? ((kk >> 2) * rows + i) * 4 + (kk & 3)
+                                       : i * 32 + 2 * ((kk >> 1) ^ (i & 7)) + (kk & 1)] =
+                W2[(size_t)(I * 32 + i) * n + J * 32 + kk];
+      } else {      // diagonal: packed lower triangle by columns, (i,k), k<=i at k*rows - k(k-1)/2 + (i-k)
+        for (int kk = 0; kk < rows; ++kk)
+          for (int i = kk; i < rows; ++i) tile[kk * rows - kk * (kk - 1) / 2 + (i - kk)] = W2[(size_t)(I * 32 + i) * n + I * 32 + kk];
+      }
+    }
+  }
+}
+
+int build_coarse(const Mesh& m, const Numbering& num, const RefElement& el, const std::vector<double>& coef,
+                 std::vector<int32_t>& cidx, std::vector<double>& tiles) {
+  // W^k (Lemma 4.1): vertex dofs (H(grad)) / Whitney edge dofs (H(curl)), free ones
+  const int n = el.n, nm = el.n_mat;
+  std::vector<int> loc;
+  for (int i = 0; i < n; ++i)
+    if ((num.space == 0 && el.dofs[i].dim == 0) || (num.space == 1 && el.dofs[i].dim == 1 && el.dofs[i].type == 2))
+      loc.push_back(i);
+  std::vector<int32_t> pos(num.n_total, -1);
+  cidx.clear();
+  const int64_t first = num.space == 0 ? num.off[0] : num.off[1];
+  const int64_t count = num.space == 0 ? m.nv : m.ne, stride = num.space == 0 ? 1 : num.per[1];
+  for (int64_t k = 0; k < count; ++k) {
+    const int64_t g = first + k * stride;
+    if (!num.constrained[g]) {
+      pos[g] = (int32_t)cidx.size();
+      cidx.push_back((int32_t)g);
+    }
+  }
+  const int nc = (int)cidx.size();
+  tiles.clear();
+  if (nc == 0) return 0;
+  std::vector<double> A((size_t)nc * nc, 0.0);
+  for (int64_t t = 0; t < m.nt; ++t)
+    for (int a : loc) {
+      const int pa = pos[num.dofmap[(size_t)t * n + a]];
+      if (pa < 0) continue;
+      for (int b : loc) {
+        const int pb = pos[num.dofmap[(size_t)t * n + b]];
+        if (pb < 0) continue;
+        double v = 0;
+        for (int q = 0; q < nm; ++q) v += coef[(size_t)t * nm + q] * el.R[((size_t)q * n + a) * n + b];
+        A[(size_t)pa * nc + pb] += v;
+      }
+    }
+  std::vector<double> work;
+  if (!spd_inverse(A.data(), nc, work)) return RDR_ENOTSPD;
+  tiles.assign(patch_stored_doubles(nc), 0.0);
+  pack_patch_tiles(A.data(), nc, tiles.data(), kTileGroups);
+  return 0;
+}
+
 void build_gradient(const Mesh& m, const Numbering& ned, const Numbering& cg, Gradient& G) {
   const int64_t ncg = cg.n_total;
   std::vector<std::vector<std::pair<int32_t, double>>> rows(ncg);
@@ -493,26 +556,7 @@ int build_patches(const Mesh& m, const Numbering& num, const RefElement& el, con
           continue;
         }
         const std::vector<double>& W2 = A;  // A^-1, both triangles
-        // exact packed lower triangle in 32-row block rows (see patch_layout)
-        double* out = buf.data() + (P.tile_off[k] - base);
-        const int nbk = (n + 31) / 32;
-        for (int I = 0; I < nbk; ++I) {
-          const int rows = std::min(32, n - 32 * I);
-          for (int J = 0; J <= I; ++J) {
-            double* tile = out + patch_tile_offset(n, I, J);
-            if (J < I) {  // full-width tile, `rows` rows (setup.hpp layouts)
-              for (int i = 0; i < rows; ++i)
-                for (int kk = 0; kk < 32; ++kk)
-                  tile[layout == kTileGroups ? ((kk >> 2) * rows + i) * 4 + (kk & 3)
-                                             : i * 32 + 2 * ((kk >> 1) ^ (i & 7)) + (kk & 1)] =
-                      W2[(size_t)(I * 32 + i) * n + J * 32 + kk];
-            } else {      // diagonal: packed lower triangle by columns, (i,k), k<=i at k*rows - k(k-1)/2 + (i-k)
-              for (int kk = 0; kk < rows; ++kk)
-                for (int i = kk; i < rows; ++i)
-                  tile[kk * rows - kk * (kk - 1) / 2 + (i - kk)] = W2[(size_t)(I * 32 + i) * n + I * 32 + kk];
-            }
-          }
-        }
+        pack_patch_tiles(W2.data(), n, buf.data() + (P.tile_off[k] - base), layout);
       }
     }
     if (status) break;

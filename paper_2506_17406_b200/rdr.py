@@ -13,6 +13,7 @@ LIB_PATH = os.path.join(HERE, "librdr.so")
 
 HGRAD, HCURL = 0, 1
 SPLIT, UNSPLIT = 0, 1
+ADDITIVE, HYBRID = 0, 1
 RDR_OK, RDR_ENOCONV = 0, -6
 
 
@@ -23,7 +24,7 @@ class RdrError(RuntimeError):
 
 
 class Options(ctypes.Structure):
-    _fields_ = [("decomposition", ctypes.c_int)]
+    _fields_ = [("decomposition", ctypes.c_int), ("preconditioner", ctypes.c_int)]
 
 
 class Info(ctypes.Structure):
@@ -48,6 +49,7 @@ def _load():
         "rdr_setup_ex": (ctypes.c_int, [ctypes.POINTER(P), P, I64, P, I64, ctypes.c_int, ctypes.c_int, P, P, P,
                                         ctypes.POINTER(Options), P]),
         "rdr_ndofs": (ctypes.c_int, [P, ctypes.POINTER(I64)]),
+        "rdr_get_weights": (ctypes.c_int, [P, P]),
         "rdr_get_info": (ctypes.c_int, [P, ctypes.POINTER(Info)]),
         "rdr_apply": (ctypes.c_int, [P, P, P, P]),
         "rdr_precond": (ctypes.c_int, [P, P, P, P]),
@@ -128,7 +130,8 @@ class Solver:
     (float64 / int32 / uint8) or host numpy arrays; vectors are torch float64
     CUDA tensors of length n_total."""
 
-    def __init__(self, vertices, tets, p, space, alpha, beta, mask, stream=None, decomposition=SPLIT):
+    def __init__(self, vertices, tets, p, space, alpha, beta, mask, stream=None, decomposition=SPLIT,
+                 preconditioner=ADDITIVE):
         import torch
         self._keep = [np.ascontiguousarray(vertices, dtype=np.float64) if isinstance(vertices, np.ndarray) else vertices,
                       np.ascontiguousarray(tets, dtype=np.int32) if isinstance(tets, np.ndarray) else tets,
@@ -138,7 +141,7 @@ class Solver:
         v, t, a, b, m = self._keep
         self._h = ctypes.c_void_p()
         nv, nt = v.shape[0], t.shape[0]
-        opt = Options(int(decomposition))
+        opt = Options(int(decomposition), int(preconditioner))
         _check(_lib.rdr_setup_ex(ctypes.byref(self._h), _ptr(v), nv, _ptr(t), nt, int(p), int(space), _ptr(a),
                                  _ptr(b), _ptr(m), ctypes.byref(opt), _stream(stream)), "rdr_setup_ex")
         self._keep = None
@@ -147,6 +150,13 @@ class Solver:
         self.n_total = n.value
         self.p, self.space = p, space
         self.device = torch.device("cuda", torch.cuda.current_device())
+
+    @property
+    def weights(self):
+        """Hybrid Schwarz weights (rho_1, rho_2, rho_3)."""
+        w = np.zeros(3)
+        _check(_lib.rdr_get_weights(self._h, _ptr(w)), "rdr_get_weights")
+        return w
 
     @property
     def info(self) -> dict:

@@ -22,11 +22,12 @@ from rdr_inputs import make_config  # noqa: E402
 from paper_2506_17406_b200 import rdr  # noqa: E402
 
 
-def measure(cfg, p, fp64_peak, hbm, solves=3, reps=20, dec="split"):
+def measure(cfg, p, fp64_peak, hbm, solves=3, reps=20, dec="split", pre="additive"):
     c = make_config(cfg, p=p) if cfg == 5 else make_config(cfg)
     t0 = time.time()
     S = rdr.Solver(c.vertices, c.tets, c.p, c.space, c.alpha, c.beta, c.mask,
-                   decomposition=rdr.UNSPLIT if dec == "unsplit" else rdr.SPLIT)
+                   decomposition=rdr.UNSPLIT if dec == "unsplit" else rdr.SPLIT,
+                   preconditioner=rdr.HYBRID if pre == "hybrid" else rdr.ADDITIVE)
     setup_wall = time.time() - t0
     info = S.info
     n = S.n_total
@@ -47,7 +48,8 @@ def measure(cfg, p, fp64_peak, hbm, solves=3, reps=20, dec="split"):
     it = its[0]
     patch_bytes = info["bytes_precond"] - 24.0 * info["n_interior"]
     out = {
-        "config": cfg, "decomposition": dec, "space": "hgrad" if c.space == 0 else "hcurl", "p": c.p,
+        "config": cfg, "decomposition": dec, "preconditioner": pre, "space": "hgrad" if c.space == 0 else "hcurl",
+        "p": c.p,
         "n_cells": info["n_cells"],
         "n_loc": info["n_loc"], "n_total": n, "n_free": info["n_free"], "n_patches": info["n_patches"],
         "max_patch": info["max_patch"], "patch_GB": info["patch_bytes"] / 1e9, "setup_s": info["setup_seconds"],
@@ -64,6 +66,17 @@ def measure(cfg, p, fp64_peak, hbm, solves=3, reps=20, dec="split"):
         "t_roof_iter_ms": info["flops_apply"] / fp64_peak / 1e9 + (patch_bytes + 12 * 8 * n) / hbm / 1e6,
     }
     out["iter_frac_roofline"] = out["t_roof_iter_ms"] / out["ms_per_iter"]
+    if pre == "hybrid":
+        out["rho"] = [float(v) for v in S.weights]
+        t0 = time.time()
+        ev0.record()
+        for _ in range(5):
+            S.precond(b, x)
+        ev1.record()
+        ev1.synchronize()
+        out["hybrid_precond_ms"] = ev0.elapsed_time(ev1) / 5
+        out.pop("t_roof_iter_ms")
+        out.pop("iter_frac_roofline")
     S.close()
     return out
 
@@ -74,6 +87,7 @@ def main():
     ap.add_argument("--p", default="1-12")
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "sweep.jsonl"))
     ap.add_argument("--decomposition", default="split", choices=["split", "unsplit"])
+    ap.add_argument("--precond", default="additive", choices=["additive", "hybrid"])
     args = ap.parse_args()
     lo, hi = (int(v) for v in args.p.split("-"))
     fp64_peak = rdr.measure_fp64_peak()
@@ -85,7 +99,7 @@ def main():
         f.write(json.dumps(head) + "\n")
         for cfg in (int(v) for v in args.configs.split(",")):
             for p in (range(lo, hi + 1) if cfg == 5 else [None]):
-                r = measure(cfg, p, fp64_peak, hbm, dec=args.decomposition)
+                r = measure(cfg, p, fp64_peak, hbm, dec=args.decomposition, pre=args.precond)
                 print(json.dumps(r), flush=True)
                 f.write(json.dumps(r) + "\n")
                 f.flush()

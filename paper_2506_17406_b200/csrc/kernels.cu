@@ -930,10 +930,7 @@ __global__ void __launch_bounds__(kLdgWarps * 32, 32 / kLdgWarps)
     patch_ldg_kernel(DevPrecond pc, const double* __restrict__ r, double* __restrict__ z, double* rz_acc,
                      const PcgScalars* guard) {
   extern __shared__ double smem[];
-  // work unit: a contiguous range [t_begin, t_end) of a patch's tiles (large
-  // patches are split over several CTAs so that none outlasts the SM's share)
-  const int unit = blockIdx.x;
-  const int pid = pc.unit_pid ? pc.unit_pid[unit] : unit;
+  const int pid = blockIdx.x;
   const int n = pc.pn[pid];
   const int nb = (n + 31) >> 5, npad = nb * 32;
   const bool pot = pc.pkind[pid] != 0;
@@ -950,10 +947,9 @@ __global__ void __launch_bounds__(kLdgWarps * 32, 32 / kLdgWarps)
     zl[i] = 0.0;
   }
   const double* T = pc.tiles + pc.tile_off[pid];
-  const int t_begin = pc.unit_pid ? pc.unit_t0[unit] : 0;
-  const int ntiles = pc.unit_pid ? pc.unit_t1[unit] : nb * (nb + 1) / 2;
+  const int ntiles = nb * (nb + 1) / 2;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  int I = 0, J = t_begin + warp, h = 0, t = t_begin + warp;
+  int I = 0, J = warp, h = 0, t = warp;
   while (J > I) {
     J -= I + 1;
     ++I;
@@ -1033,10 +1029,8 @@ __global__ void __launch_bounds__(kLdgWarps * 32, 32 / kLdgWarps)
   double part = 0.0;
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     const double zi = zl[i];
-    if (zi != 0.0) {  // entries a split unit never touched stay 0
-      atomicAdd(zout + id[i], pc.out_scale * zi);
-      part = fma(rl[i], zi, part);
-    }
+    atomicAdd(zout + id[i], pc.out_scale * zi);
+    part = fma(rl[i], zi, part);
   }
   if (rz_acc) {
     __shared__ double sh[32];
@@ -1338,9 +1332,9 @@ cudaError_t launch_precond_part(int part, const DevPrecond& pc, const double* r,
           return launch_k(patch_stream_kernel, dim3(pc.n_ctas), dim3(kPatchWarps * 32),
                           patch_smem_bytes(pc.ring_slots, pc.npad_max, pc.zbufs), s, pc, r, z, rz_acc, guard);
         if (pc.ldg_warps == 4)
-          return launch_kx(pdl_patch_enabled(), patch_ldg_kernel<4>, dim3(pc.n_units), dim3(4 * 32), 2 * sizeof(double) * pc.npad_max, s,
+          return launch_kx(pdl_patch_enabled(), patch_ldg_kernel<4>, dim3(pc.n_patches), dim3(4 * 32), 2 * sizeof(double) * pc.npad_max, s,
                           pc, r, z, rz_acc, guard);
-        return launch_kx(pdl_patch_enabled(), patch_ldg_kernel<8>, dim3(pc.n_units), dim3(8 * 32), 2 * sizeof(double) * pc.npad_max, s,
+        return launch_kx(pdl_patch_enabled(), patch_ldg_kernel<8>, dim3(pc.n_patches), dim3(8 * 32), 2 * sizeof(double) * pc.npad_max, s,
                         pc, r, z, rz_acc, guard);
       }
       break;

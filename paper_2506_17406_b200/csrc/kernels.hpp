@@ -53,10 +53,6 @@ struct DevPrecond {
   const uint8_t* pkind;         // 0 own numbering, 1 CG potential
   int32_t kernel;               // 0: patch_ldg_kernel (tile layout "groups"), 1: patch_stream_kernel ("swizzled")
   int32_t ldg_warps;            // warps per CTA of patch_ldg_kernel: 8, or 4 when most patches are small
-  int64_t n_units;              // patch_ldg_kernel CTAs: (patch, tile range) work units, longest first
-  const int32_t* unit_pid;      // [n_units] patch of the unit (NULL: one unit per patch)
-  const int32_t* unit_t0;       // [n_units] first tile
-  const int32_t* unit_t1;       // [n_units] one past the last tile
   // persistent patch kernel: n_ctas CTAs claim patches from a queue
   int32_t n_ctas;
   int32_t* queue;               // [2] claim counter, finished-CTA counter (zero between launches)

@@ -310,38 +310,6 @@ static int setup_impl(rdr_handle* h, const double* vertices, int64_t nv, const i
   if (sink.d) h->owned.push_back(sink.d);
   if (st) return st;
   pc.n_patches = (int64_t)P.n.size();
-  {  // work units of patch_ldg_kernel: split patches whose tile count exceeds the
-     // mean tiles per CTA slot (148 SMs x CTAs per SM) into contiguous ranges
-    const int per_sm = 32 / 8;  // 8-warp CTAs at 64 registers
-    int64_t total = 0;
-    for (int32_t n : P.n) {
-      const int64_t nb = (n + 31) / 32;
-      total += nb * (nb + 1) / 2;
-    }
-    const int64_t cap = std::max<int64_t>(16, total / (148 * per_sm));
-    std::vector<std::array<int32_t, 3>> units;  // (pid, t0, t1)
-    for (int64_t k = 0; k < (int64_t)P.n.size(); ++k) {
-      const int64_t nb = (P.n[k] + 31) / 32, nt = nb * (nb + 1) / 2;
-      const int64_t parts = std::max<int64_t>(1, (nt + cap - 1) / cap);
-      for (int64_t q = 0; q < parts; ++q)
-        units.push_back({(int32_t)k, (int32_t)(nt * q / parts), (int32_t)(nt * (q + 1) / parts)});
-    }
-    std::stable_sort(units.begin(), units.end(), [](const auto& a, const auto& b) { return a[2] - a[1] > b[2] - b[1]; });
-    std::vector<int32_t> up, u0, u1;
-    for (const auto& u : units) {
-      up.push_back(u[0]);
-      u0.push_back(u[1]);
-      u1.push_back(u[2]);
-    }
-    pc.n_units = (int64_t)units.size();
-    int32_t *d_up, *d_u0, *d_u1;
-    if ((st = h->own_upload(&d_up, up))) return st;
-    if ((st = h->own_upload(&d_u0, u0))) return st;
-    if ((st = h->own_upload(&d_u1, u1))) return st;
-    pc.unit_pid = d_up;
-    pc.unit_t0 = d_u0;
-    pc.unit_t1 = d_u1;
-  }
   {  // mostly small patches (<= 4 tile rows, e.g. the H(curl) edge stars): 4-warp CTAs, 8 per SM
     int64_t small = 0;
     for (int32_t n : P.n) small += n <= 128;

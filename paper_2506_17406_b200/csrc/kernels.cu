@@ -232,8 +232,7 @@ __host__ __device__ __forceinline__ size_t apply_smem_bytes(int kp, int nm) {
 template <int BM, bool PCG>
 __global__ void __launch_bounds__((kApplyWarps + 1) * 32, 2)
     apply_tc_kernel(DevOperator op, const double* __restrict__ x, double* __restrict__ y, double* pq_acc,
-                    const PcgScalars* guard, PcgScalars* sc, double* pbuf0, double* pbuf1,
-                    cudaGraphConditionalHandle loop, int use_loop) {
+                    const PcgScalars* guard, PcgScalars* sc, double* pbuf0, double* pbuf1) {
   constexpr int MW = BM / 16;             // warps along M (16 cells each)
   constexpr int KS = kApplyWarps / MW;    // K-split groups
   static_assert(MW * KS == kApplyWarps && kApplySlots % KS == 0, "warp layout");
@@ -487,9 +486,6 @@ __global__ void __launch_bounds__((kApplyWarps + 1) * 32, 2)
       sc->zz = 0.0;
       sc->ticket = 0;
       sc->k = kit + 1;
-      // device-side PCG loop: the graph's while node runs another iteration
-      // body only while the stopping test has not fired
-      if (use_loop) cudaGraphSetConditional(loop, v->done ? 0u : 1u);
     }
   } else if (pq_acc) {
     __shared__ double sh[32];
@@ -517,23 +513,21 @@ int apply_bm(const DevOperator& op) {
 
 template <int BM, bool PCG>
 cudaError_t launch_apply_tc_bm(const DevOperator& op, const double* x, double* y, double* pq_acc,
-                               const PcgScalars* guard, cudaStream_t s, PcgScalars* sc, double* p0, double* p1,
-                               cudaGraphConditionalHandle loop, int use_loop) {
+                               const PcgScalars* guard, cudaStream_t s, PcgScalars* sc, double* p0, double* p1) {
   const size_t sm = apply_smem_bytes<BM>(op.kp, op.n_mat);
   dim3 grid((unsigned)((op.n_cells + BM - 1) / BM), (unsigned)op.ngroups);
   return launch_k(apply_tc_kernel<BM, PCG>, grid, dim3((kApplyWarps + 1) * 32), sm, s, op, x, y, pq_acc, guard, sc,
-                  p0, p1, loop, use_loop);
+                  p0, p1);
 }
 
 template <bool PCG>
 cudaError_t launch_apply_tc(const DevOperator& op, const double* x, double* y, double* pq_acc,
                             const PcgScalars* guard, cudaStream_t s, PcgScalars* sc = nullptr,
-                            double* p0 = nullptr, double* p1 = nullptr, cudaGraphConditionalHandle loop = 0,
-                            int use_loop = 0) {
+                            double* p0 = nullptr, double* p1 = nullptr) {
   const int bm = apply_bm(op);
-  if (bm == 64) return launch_apply_tc_bm<64, PCG>(op, x, y, pq_acc, guard, s, sc, p0, p1, loop, use_loop);
-  if (bm == 32) return launch_apply_tc_bm<32, PCG>(op, x, y, pq_acc, guard, s, sc, p0, p1, loop, use_loop);
-  return launch_apply_tc_bm<16, PCG>(op, x, y, pq_acc, guard, s, sc, p0, p1, loop, use_loop);
+  if (bm == 64) return launch_apply_tc_bm<64, PCG>(op, x, y, pq_acc, guard, s, sc, p0, p1);
+  if (bm == 32) return launch_apply_tc_bm<32, PCG>(op, x, y, pq_acc, guard, s, sc, p0, p1);
+  return launch_apply_tc_bm<16, PCG>(op, x, y, pq_acc, guard, s, sc, p0, p1);
 }
 
 template <int TC>
@@ -1138,6 +1132,13 @@ __global__ void coarse_scatter_kernel(DevPrecond pc, double* __restrict__ e) {
   for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < pc.nc; k += stride) e[pc.cidx[k]] += pc.czc[k];
 }
 
+// device-side PCG loop: the graph's while node runs another body only while
+// the stopping test has not fired (one thread, once per body)
+__global__ void pcg_loop_condition_kernel(const PcgScalars* sc, cudaGraphConditionalHandle loop) {
+  pdl_wait();
+  cudaGraphSetConditional(loop, *((volatile const int32_t*)&sc->done) ? 0u : 1u);
+}
+
 // r.z into sc->rz_new (the hybrid preconditioner does not accumulate it itself)
 __global__ void pcg_rz_kernel(PcgScalars* sc, const double* __restrict__ r, const double* __restrict__ z, int64_t n) {
   pdl_wait();
@@ -1379,6 +1380,10 @@ int count_hybrid_launches(const DevPrecond& pc) {
   return 1 + 4 * 2 + 2 * patches + (pc.nc > 0 ? 2 : 0) + 1;
 }
 
+cudaError_t launch_pcg_loop_condition(const PcgScalars* sc, cudaGraphConditionalHandle loop, cudaStream_t s) {
+  return launch_k(pcg_loop_condition_kernel, dim3(1), dim3(1), 0, s, sc, loop);
+}
+
 cudaError_t launch_pcg_rz(PcgScalars* sc, const double* r, const double* z, int64_t n, cudaStream_t s) {
   return launch_k(pcg_rz_kernel, dim3(vec_grid(n)), dim3(kVecThreads), 0, s, sc, r, z, n);
 }
@@ -1422,8 +1427,8 @@ bool fused_pcg_supported(const DevOperator& op) {
 }
 
 cudaError_t launch_pcg_fused_apply(const DevOperator& op, PcgScalars* sc, const double* z, double* p0, double* p1,
-                                   double* q, cudaStream_t s, cudaGraphConditionalHandle loop, int use_loop) {
-  return launch_apply_tc<true>(op, z, q, nullptr, sc, s, sc, p0, p1, loop, use_loop);
+                                   double* q, cudaStream_t s) {
+  return launch_apply_tc<true>(op, z, q, nullptr, sc, s, sc, p0, p1);
 }
 
 cudaError_t launch_pcg_update_jacobi(PcgScalars* sc, const DevPrecond& pc, const double* p0, const double* p1,

@@ -90,6 +90,8 @@ cudaError_t launch_precond_part(int part, const DevPrecond& pc, const double* r,
 cudaError_t launch_precond_hybrid(const DevOperator& op, const DevPrecond& pc, const double* r, double* z,
                                   const PcgScalars* guard, cudaStream_t s);
 int count_hybrid_launches(const DevPrecond& pc);
+// set the while-node condition of a device-side PCG graph: continue while !sc->done
+cudaError_t launch_pcg_loop_condition(const PcgScalars* sc, cudaGraphConditionalHandle loop, cudaStream_t s);
 // sc->rz_new += r.z
 cudaError_t launch_pcg_rz(PcgScalars* sc, const double* r, const double* z, int64_t n, cudaStream_t s);
 
@@ -106,10 +108,8 @@ cudaError_t launch_pcg_direction(PcgScalars* sc, const double* z, double* p, dou
 // Fused PCG step (3 kernels per iteration for H(grad)): fused apply (direction
 // update + A p + ||z||^2 + stopping test), update + interior Jacobi, patches.
 bool fused_pcg_supported(const DevOperator& op);
-// use_loop: also set the while-node condition `loop` of a device-side PCG graph
-// (continue while the stopping test has not fired)
 cudaError_t launch_pcg_fused_apply(const DevOperator& op, PcgScalars* sc, const double* z, double* p0, double* p1,
-                                   double* q, cudaStream_t s, cudaGraphConditionalHandle loop = 0, int use_loop = 0);
+                                   double* q, cudaStream_t s);
 cudaError_t launch_pcg_update_jacobi(PcgScalars* sc, const DevPrecond& pc, const double* p0, const double* p1,
                                      double* q, double* x, double* r, double* z, cudaStream_t s);
 

@@ -578,10 +578,10 @@ int rdr_get_weights(const rdr_handle* h, double* rho) {
   return RDR_OK;
 }
 
-static int enqueue_iteration(rdr_handle* h, cudaStream_t s, cudaGraphConditionalHandle loop = 0, int use_loop = 0) {
+static int enqueue_iteration(rdr_handle* h, cudaStream_t s) {
   const int64_t n = h->n_total;
   if (h->fused) {  // 3 kernels (+2 for the H(curl) discrete gradient) per PCG iteration
-    CK(launch_pcg_fused_apply(h->op, h->d_sc, h->d_z, h->d_p, h->d_p2, h->d_q, s, loop, use_loop));
+    CK(launch_pcg_fused_apply(h->op, h->d_sc, h->d_z, h->d_p, h->d_p2, h->d_q, s));
     CK(launch_pcg_update_jacobi(h->d_sc, h->pc, h->d_p, h->d_p2, h->d_q, h->d_x, h->d_r, h->d_z, s));
     for (int part = 1; part < 4; ++part)
       CK(launch_precond_part(part, h->pc, h->d_r, h->d_z, &h->d_sc->rz_acc, h->d_sc, s));
@@ -639,7 +639,11 @@ static int build_while_graph(rdr_handle* h) {
   cudaGraph_t body = params.conditional.phGraph_out[0];
   CK(cudaStreamBeginCaptureToGraph(h->cap_stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
   int st = RDR_OK;
-  for (int k = 0; k < kWhileUnroll && st == RDR_OK; ++k) st = enqueue_iteration(h, h->cap_stream, loop, 1);
+  for (int k = 0; k < kWhileUnroll && st == RDR_OK; ++k) st = enqueue_iteration(h, h->cap_stream);
+  if (st == RDR_OK) {
+    cudaError_t ce = launch_pcg_loop_condition(h->d_sc, loop, h->cap_stream);
+    if (ce != cudaSuccess) st = cuda_status(ce);
+  }
   cudaError_t e = cudaStreamEndCapture(h->cap_stream, &body);
   if (st) return st;
   CK(e);
@@ -667,9 +671,9 @@ static int solve_device(rdr_handle* h, const double* b, double rtol, int maxit, 
     CK(cudaGraphLaunch(h->wgraph, s));
     CK(cudaMemcpyAsync(h->h_sc, h->d_sc, sizeof(PcgScalars), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
-    // bodies of kWhileUnroll iterations ran until the one that detected convergence
+    // bodies of kWhileUnroll iterations (+ the condition kernel) ran until the one that detected convergence
     const int64_t bodies = (h->h_sc->k + kWhileUnroll - 1) / kWhileUnroll;
-    launches = 1 + count_precond_launches(h->pc) + bodies * kWhileUnroll * h->launches_per_iter;
+    launches = 1 + count_precond_launches(h->pc) + bodies * (kWhileUnroll * h->launches_per_iter + 1);
     h->last_launches = launches;
     *iters = h->h_sc->iters;
     return h->h_sc->converged ? RDR_OK : RDR_ENOCONV;

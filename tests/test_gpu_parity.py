@@ -418,3 +418,22 @@ def test_hybrid_preconditioner(torch_cuda, space, p, bc, n):
     xo, ito, _ = O.solve(b, rtol=1e-8)
     assert abs(it - ito) <= 1, (it, ito)
     assert rel(xg.cpu().numpy(), xo) <= 1e-6
+
+
+def test_tet_vertex_order_invariance(torch_cuda):
+    """rdr_setup accepts tets in any vertex order (it sorts, R-A3): shuffling
+    every tet's vertices (and the mask columns with them) changes nothing."""
+    from paper_2506_17406_b200 import rdr
+    torch = torch_cuda
+    for space in (HGRAD, HCURL):
+        c = make_config(0, n=2, p=3, space=space, perturb=True, bc="x0", coeffs="loguniform")
+        rng = np.random.default_rng(7)
+        perm = np.array([rng.permutation(4) for _ in range(c.tets.shape[0])])
+        tets2 = np.take_along_axis(c.tets, perm, axis=1)
+        mask2 = np.take_along_axis(c.mask, perm, axis=1)
+        S1 = rdr.Solver(c.vertices, c.tets, c.p, c.space, c.alpha, c.beta, c.mask)
+        S2 = rdr.Solver(c.vertices, tets2, c.p, c.space, c.alpha, c.beta, mask2)
+        x = torch.from_numpy(c.draw_vector(S1.n_total)).cuda()
+        assert rel(S2.apply(x).cpu().numpy(), S1.apply(x).cpu().numpy()) <= 1e-14
+        assert rel(S2.precond(x).cpu().numpy(), S1.precond(x).cpu().numpy()) <= 1e-14
+        assert S2.solve(x)[1] == S1.solve(x)[1]

@@ -64,9 +64,19 @@ enum { RDR_SPLIT = 0, RDR_UNSPLIT = 1 };
  *                operator applies per preconditioner application. */
 enum { RDR_ADDITIVE = 0, RDR_HYBRID = 1 };
 
+/* Where the star-patch matrices are assembled and inverted at setup (SURVEY
+ * NEXT-4; the patch factorisation of P:2284-2288):
+ *   RDR_SETUP_DEVICE (default) -- on the GPU (patch_setup.cu): per-CTA block
+ *                Gauss-Jordan sweep of each patch matrix in device scratch,
+ *                written straight into the stored tile layout;
+ *   RDR_SETUP_HOST -- on the host cores (blocked Cholesky-based inverse,
+ *                dense.cpp), then uploaded. Both give A_m^-1 to rounding. */
+enum { RDR_SETUP_DEVICE = 0, RDR_SETUP_HOST = 1 };
+
 struct rdr_options {
   int decomposition;  /* RDR_SPLIT or RDR_UNSPLIT */
   int preconditioner; /* RDR_ADDITIVE or RDR_HYBRID */
+  int setup;          /* RDR_SETUP_DEVICE or RDR_SETUP_HOST */
 };
 
 enum {
@@ -93,6 +103,12 @@ struct rdr_info {
   double bytes_apply;    /* algorithmic HBM bytes of one rdr_apply */
   double bytes_precond;  /* algorithmic HBM bytes of one rdr_precond: 8 sum n_m(n_m+1)/2 + 24 N_int */
   double setup_seconds;  /* wall time of rdr_setup */
+  double refelem_seconds;      /* of which: reference element construction (cached per process) */
+  double patch_setup_seconds;  /* of which: patch index sets, assembly, inversion and packing */
+  double patch_kernel_seconds; /* of which: the device assembly + inversion kernel (RDR_SETUP_DEVICE), else 0 */
+  double patch_setup_flops;    /* algorithmic flops of the device block sweep: per patch, with
+                                  nb = ceil(n/64), sum over pivot blocks of 2*64^3 per updated
+                                  lower tile and panel product = 2*64^3 nb (nb-1)(nb+2)/2 */
 };
 
 /* Build the operator and the preconditioner (host setup once, then upload).
@@ -107,8 +123,9 @@ int rdr_setup(rdr_handle** h, const double* vertices, int64_t nv, const int32_t*
               int p, int space, const double* alpha, const double* beta,
               const uint8_t* dirichlet_mask, void* stream);
 
-/* rdr_setup with options (NULL = defaults: RDR_SPLIT, RDR_ADDITIVE). RDR_EINVAL
- * for an unknown decomposition or preconditioner, or RDR_HYBRID with RDR_UNSPLIT. */
+/* rdr_setup with options (NULL = defaults: RDR_SPLIT, RDR_ADDITIVE,
+ * RDR_SETUP_DEVICE). RDR_EINVAL for an unknown decomposition, preconditioner
+ * or setup, or RDR_HYBRID with RDR_UNSPLIT. */
 int rdr_setup_ex(rdr_handle** h, const double* vertices, int64_t nv, const int32_t* tets, int64_t nt,
                  int p, int space, const double* alpha, const double* beta,
                  const uint8_t* dirichlet_mask, const struct rdr_options* opt, void* stream);

@@ -28,7 +28,7 @@ def build(verbose_ptxas: bool = False) -> str:
     kflags = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", *ARCH]
     if verbose_ptxas:
         kflags += ["-Xptxas", "-v"]
-    for cu in ("kernels.cu",):
+    for cu in ("kernels.cu", "patch_setup.cu"):
         o = os.path.join(bdir, cu + ".o")
         _run([NVCC, *kflags, "-c", os.path.join(CSRC, cu), "-o", o])
         objs.append(o)

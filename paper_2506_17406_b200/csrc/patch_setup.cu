@@ -1,0 +1,276 @@
+// Device-side assembly and inversion of the star-patch matrices (SURVEY §8(f)
+// NEXT-4; the patch factorisation of P:2284-2288, R-A15). See patch_setup.hpp.
+//
+// One CTA per patch at a time (persistent grid, patches claimed largest
+// first). The patch matrix lives in a per-CTA global scratch (lower triangle
+// in 64x64 tiles, leading dimension ld = n rounded up to 64, padded with the
+// identity so that every pivot block is full) and is inverted in place by the
+// block sweep (Gauss-Jordan) operator: sweeping pivot block K maps
+//   A_KK -> -A_KK^-1,  A_IK -> A_IK A_KK^-1,  A_IJ -> A_IJ - A_IK A_KK^-1 A_KJ,
+// and sweeping every block leaves -A^-1. For an SPD matrix each pivot block is
+// a Schur complement of the unswept part, hence SPD: no pivoting, and a
+// non-positive pivot flags a matrix that is not SPD (RDR_ENOTSPD). The sweep
+// keeps the matrix symmetric, so only the tiles I >= J are updated. The
+// rank-64 updates are 64x64x64 tile products on the FP64 CUDA cores (4x4
+// register blocks per thread, operands staged in shared memory). The last
+// step packs -(-A^-1) into the stored tile layout (setup.hpp).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "patch_setup.hpp"
+
+namespace rdr {
+
+namespace {
+
+constexpr int kB = 64;         // pivot block / tile
+constexpr int kThreads = 256;  // 16 x 16 threads, 4 x 4 outputs each
+constexpr int kSs = kB + 1;    // stride of the pivot block (column reads conflict free)
+constexpr int kXs = kB + 2;    // stride of the staged operands (16-byte aligned rows)
+
+// acc[r][c] = sum_k X[k][ty*4 + r] * Y[k][tx*4 + c]
+__device__ __forceinline__ void tile_product(const double* X, const double* Y, int ty, int tx, double acc[4][4]) {
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[r][c] = 0.0;
+#pragma unroll 8
+  for (int k = 0; k < kB; ++k) {
+    const double2 x0 = *reinterpret_cast<const double2*>(X + k * kXs + ty * 4);
+    const double2 x1 = *reinterpret_cast<const double2*>(X + k * kXs + ty * 4 + 2);
+    const double2 y0 = *reinterpret_cast<const double2*>(Y + k * kXs + tx * 4);
+    const double2 y1 = *reinterpret_cast<const double2*>(Y + k * kXs + tx * 4 + 2);
+    const double xa[4] = {x0.x, x0.y, x1.x, x1.y}, ya[4] = {y0.x, y0.y, y1.x, y1.y};
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[r][c] = fma(xa[r], ya[c], acc[r][c]);
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 2) patch_setup_kernel(DevPatchSetup s) {
+  extern __shared__ double4 smem_raw[];
+  double* S = reinterpret_cast<double*>(smem_raw);  // [kB][kSs] pivot block
+  double* X = S + kB * kSs + 2;                     // [kB][kXs] (16-byte aligned)
+  double* Y = X + kB * kXs;                         // [kB][kXs]
+  __shared__ int64_t claim;
+  const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
+  double* A = s.scratch + (int64_t)blockIdx.x * (s.ld_max * s.ld_max + 2 * kB * s.ld_max);
+  for (;;) {
+    __syncthreads();
+    if (tid == 0) claim = atomicAdd(s.queue, 1);
+    __syncthreads();
+    const int64_t m = claim;
+    if (m >= s.np) break;
+    const int n = s.pn[m];
+    const int ld = (n + kB - 1) / kB * kB, nb = ld / kB;
+    double* Wp = A + (int64_t)ld * ld;  // [kB][ld]: W_I = A_IK A_KK^-1, transposed
+    double* Vp = Wp + (int64_t)kB * ld;  // [kB][ld]: V_I = A_IK (before the sweep of K), transposed
+
+    // ---- 1. zero, identity padding, assembly of the lower triangle
+    for (int64_t e = tid; e < (int64_t)ld * ld; e += kThreads) {
+      const int i = (int)(e / ld), j = (int)(e % ld);
+      A[e] = (i == j && i >= n) ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    {
+      const int kind = s.pkind[m];
+      const double* R = s.R[kind];
+      const double* cf = s.coef[kind];
+      const int nl = s.nl[kind], nm = s.nm[kind];
+      for (int64_t rc = s.rec_ptr[m]; rc < s.rec_ptr[m + 1]; ++rc) {
+        const int64_t e0 = s.rec_off[rc];
+        const int cnt = (int)(s.rec_off[rc + 1] - e0);
+        const double* c = cf + (int64_t)s.rec_cell[rc] * nm;
+        // the entries of one cell hit distinct (pa, pb): no two threads add to one entry
+        for (int q = tid; q < cnt * cnt; q += kThreads) {
+          const uint32_t ea = s.ent[e0 + q / cnt], eb = s.ent[e0 + q % cnt];
+          const int pa = (int)(ea & 0xffffu), pb = (int)(eb & 0xffffu);
+          if (pa < pb) continue;
+          const int64_t la = ea >> 16, lb = eb >> 16;
+          double v = 0.0;
+          for (int t = 0; t < nm; ++t) v = fma(c[t], R[((int64_t)t * nl + la) * nl + lb], v);
+          A[(int64_t)pa * ld + pb] += v;
+        }
+        __syncthreads();
+      }
+    }
+
+    // ---- 2. block sweep
+    for (int K = 0; K < nb; ++K) {
+      const int k0 = K * kB;
+      // 2a. pivot block, symmetric, then the scalar sweep of its 64 pivots: S = -A_KK^-1
+      for (int e = tid; e < kB * kB; e += kThreads) {
+        const int i = e / kB, j = e % kB;
+        S[i * kSs + j] = i >= j ? A[(int64_t)(k0 + i) * ld + k0 + j] : A[(int64_t)(k0 + j) * ld + k0 + i];
+      }
+      __syncthreads();
+      for (int p = 0; p < kB; ++p) {
+        const double d = S[p * kSs + p];
+        const double inv = 1.0 / d;
+        double nv[kB * kB / kThreads];
+#pragma unroll
+        for (int u = 0; u < kB * kB / kThreads; ++u) {
+          const int e = tid + u * kThreads, i = e / kB, j = e % kB;
+          const double a = S[i * kSs + j];
+          if (i == p && j == p)
+            nv[u] = -inv;
+          else if (i == p || j == p)
+            nv[u] = a * inv;
+          else
+            nv[u] = fma(-S[i * kSs + p] * inv, S[p * kSs + j], a);
+        }
+        if (tid == 0 && !(d > 0.0)) atomicCAS(s.status, 0, (int32_t)(m + 1));
+        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < kB * kB / kThreads; ++u) {
+          const int e = tid + u * kThreads;
+          S[(e / kB) * kSs + e % kB] = nv[u];
+        }
+        __syncthreads();
+      }
+      if (nb == 1) {
+        for (int e = tid; e < kB * kB; e += kThreads) {
+          const int i = e / kB, j = e % kB;
+          if (i >= j) A[(int64_t)i * ld + j] = S[i * kSs + j];
+        }
+        __syncthreads();
+        break;
+      }
+      // 2b. V_I = A_IK and W_I = A_IK A_KK^-1 = -V_I S for every I != K
+      for (int e = tid; e < kB * kB; e += kThreads) Y[(e / kB) * kXs + e % kB] = S[(e / kB) * kSs + e % kB];
+      for (int I = 0; I < nb; ++I) {
+        if (I == K) continue;
+        const int i0 = I * kB;
+        if (I > K) {  // tile (I, K): row-major rows i, columns k -> X[k][i]
+          for (int e = tid; e < kB * kB; e += kThreads) {
+            const int r = e / kB, k = e % kB;
+            X[k * kXs + r] = A[(int64_t)(i0 + r) * ld + k0 + k];
+          }
+        } else {  // tile (K, I) = A_KI = A_IK^T: rows k, columns i -> X[k][i]
+          for (int e = tid; e < kB * kB; e += kThreads) {
+            const int k = e / kB, r = e % kB;
+            X[k * kXs + r] = A[(int64_t)(k0 + k) * ld + i0 + r];
+          }
+        }
+        __syncthreads();
+        for (int e = tid; e < kB * kB; e += kThreads) {
+          const int k = e / kB, r = e % kB;
+          Vp[(int64_t)k * ld + i0 + r] = X[k * kXs + r];
+        }
+        double acc[4][4];
+        tile_product(X, Y, ty, tx, acc);
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) Wp[(int64_t)(tx * 4 + c) * ld + i0 + ty * 4 + r] = -acc[r][c];
+        __syncthreads();
+      }
+      // 2c. A_IJ -= W_I V_J^T for I >= J, I, J != K
+      for (int I = 0; I < nb; ++I) {
+        if (I == K) continue;
+        const int i0 = I * kB;
+        for (int e = tid; e < kB * kB; e += kThreads) {
+          const int k = e / kB, r = e % kB;
+          X[k * kXs + r] = Wp[(int64_t)k * ld + i0 + r];
+        }
+        for (int J = 0; J <= I; ++J) {
+          if (J == K) continue;
+          const int j0 = J * kB;
+          for (int e = tid; e < kB * kB; e += kThreads) {
+            const int k = e / kB, c = e % kB;
+            Y[k * kXs + c] = Vp[(int64_t)k * ld + j0 + c];
+          }
+          __syncthreads();
+          double acc[4][4];
+          tile_product(X, Y, ty, tx, acc);
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            double* row = A + (int64_t)(i0 + ty * 4 + r) * ld + j0 + tx * 4;
+            double2 a0 = *reinterpret_cast<double2*>(row), a1 = *reinterpret_cast<double2*>(row + 2);
+            a0.x -= acc[r][0];
+            a0.y -= acc[r][1];
+            a1.x -= acc[r][2];
+            a1.y -= acc[r][3];
+            *reinterpret_cast<double2*>(row) = a0;
+            *reinterpret_cast<double2*>(row + 2) = a1;
+          }
+          __syncthreads();
+        }
+      }
+      // 2d. the swept block row / column: A_IK = W_I (I > K), A_KI = W_I^T (I < K), A_KK = S
+      for (int I = 0; I < nb; ++I) {
+        if (I == K) continue;
+        const int i0 = I * kB;
+        if (I > K) {
+          for (int e = tid; e < kB * kB; e += kThreads) {
+            const int r = e / kB, k = e % kB;
+            A[(int64_t)(i0 + r) * ld + k0 + k] = Wp[(int64_t)k * ld + i0 + r];
+          }
+        } else {
+          for (int e = tid; e < kB * kB; e += kThreads) {
+            const int k = e / kB, r = e % kB;
+            A[(int64_t)(k0 + k) * ld + i0 + r] = Wp[(int64_t)k * ld + i0 + r];
+          }
+        }
+      }
+      for (int e = tid; e < kB * kB; e += kThreads) {
+        const int i = e / kB, j = e % kB;
+        if (i >= j) A[(int64_t)(k0 + i) * ld + k0 + j] = S[i * kSs + j];
+      }
+      __syncthreads();
+    }
+
+    // ---- 3. pack A^-1 = -(swept A), lower triangle, into the stored layout (setup.hpp)
+    double* out = s.tiles + s.tile_off[m];
+    const int nbk = (n + 31) / 32;
+    for (int I = 0; I < nbk; ++I) {
+      const int rows = min(32, n - 32 * I);
+      const int64_t base = 512LL * I * I + 16LL * I;
+      const int full = I * 32 * rows, total = full + rows * (rows + 1) / 2;
+      for (int w = tid; w < total; w += kThreads) {
+        int i, col;
+        if (w < full) {
+          const int J = w / (32 * rows), q = w % (32 * rows);
+          int kk;
+          if (s.layout == 0) {
+            i = (q >> 2) % rows;
+            kk = ((q >> 2) / rows) * 4 + (q & 3);
+          } else {
+            i = q >> 5;
+            kk = ((((q & 31) >> 1) ^ (i & 7)) << 1) | (q & 1);
+          }
+          col = 32 * J + kk;
+        } else {  // diagonal tile by columns: (i, kk), kk <= i, at kk*rows - kk(kk-1)/2 + (i-kk)
+          int q = w - full, kk = 0;
+          while (q >= rows - kk) {
+            q -= rows - kk;
+            ++kk;
+          }
+          i = kk + q;
+          col = 32 * I + kk;
+        }
+        out[base + w] = -A[(int64_t)(32 * I + i) * ld + col];
+      }
+    }
+    const int64_t exact = (int64_t)n * (n + 1) / 2, stored = s.tile_off[m + 1] - s.tile_off[m];
+    for (int64_t w = exact + tid; w < stored; w += kThreads) out[w] = 0.0;
+  }
+}
+
+}  // namespace
+
+int64_t patch_setup_scratch_doubles(int64_t ld_max) { return ld_max * ld_max + 2 * kB * ld_max; }
+
+size_t patch_setup_smem() { return sizeof(double) * (kB * kSs + 2 + 2 * kB * kXs); }
+
+cudaError_t launch_patch_setup(const DevPatchSetup& s, int n_ctas, cudaStream_t stream) {
+  const size_t smem = patch_setup_smem();
+  cudaError_t e = cudaFuncSetAttribute(patch_setup_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  patch_setup_kernel<<<n_ctas, kThreads, smem, stream>>>(s);
+  return cudaGetLastError();
+}
+
+}  // namespace rdr

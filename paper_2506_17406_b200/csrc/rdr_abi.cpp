@@ -18,6 +18,7 @@
 #include "refelem.hpp"
 #include "setup.hpp"
 #include "dense.hpp"
+#include "patch_setup.hpp"
 
 using namespace rdr;
 
@@ -170,9 +171,78 @@ struct rdr_handle {
 
 static int hybrid_weights(rdr_handle* h, const std::vector<double>& dinv);
 
+// device memory freed at scope exit (setup temporaries)
+struct DevTemps {
+  std::vector<void*> p;
+  template <class T>
+  int up(const T** d, const std::vector<T>& h) {
+    T* q = nullptr;
+    const int st = upload(&q, h);
+    if (q) p.push_back(q);
+    *d = q;
+    return st;
+  }
+  ~DevTemps() {
+    for (void* q : p) cudaFree(q);
+  }
+};
+
+// Assemble, invert and pack every patch on the GPU (SURVEY NEXT-4,
+// patch_setup.cu) into the already reserved store s.tiles.
+static int device_patch_setup(DevPatchSetup s, const Patches& P, const PatchAssembly& pa, const RefElement* cg_el,
+                              const std::vector<double>* cg_coef, double* kernel_seconds) {
+  DevTemps tmp;
+  int st;
+  if ((st = tmp.up(&s.rec_ptr, pa.rec_ptr))) return st;
+  if ((st = tmp.up(&s.rec_cell, pa.rec_cell))) return st;
+  if ((st = tmp.up(&s.rec_off, pa.rec_off))) return st;
+  if ((st = tmp.up(&s.ent, pa.ent))) return st;
+  if (cg_el) {
+    if ((st = tmp.up(&s.R[1], cg_el->R))) return st;
+    if ((st = tmp.up(&s.coef[1], *cg_coef))) return st;
+    s.nl[1] = cg_el->n;
+    s.nm[1] = cg_el->n_mat;
+  }
+  s.np = (int64_t)P.n.size();
+  s.ld_max = (P.max_n + 63) / 64 * 64;
+  int dev = 0, sms = 148;
+  CK(cudaGetDevice(&dev));
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  size_t free_b = 0, total_b = 0;
+  CK(cudaMemGetInfo(&free_b, &total_b));
+  // scratch: two CTAs per SM, within min(16 GiB, half the free memory)
+  const double per_cta = 8.0 * (double)patch_setup_scratch_doubles(s.ld_max);
+  const double budget = std::min(16.0 * (1 << 30), 0.5 * (double)free_b);
+  const int ctas = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)2 * sms, s.np, (int64_t)(budget / per_cta)}));
+  double* scratch = nullptr;
+  CK(cudaMalloc((void**)&scratch, (size_t)per_cta * ctas));
+  tmp.p.push_back(scratch);
+  int32_t* ctl = nullptr;
+  CK(cudaMalloc((void**)&ctl, 2 * sizeof(int32_t)));
+  tmp.p.push_back(ctl);
+  CK(cudaMemset(ctl, 0, 2 * sizeof(int32_t)));
+  s.scratch = scratch;
+  s.queue = ctl;
+  s.status = ctl + 1;
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaEventRecord(e0, 0));
+  CK(launch_patch_setup(s, ctas, 0));
+  CK(cudaEventRecord(e1, 0));
+  int32_t status = 0;
+  CK(cudaMemcpy(&status, s.status, sizeof(int32_t), cudaMemcpyDeviceToHost));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  *kernel_seconds = 1e-3 * ms;
+  return status ? RDR_ENOTSPD : RDR_OK;
+}
+
 static int setup_impl(rdr_handle* h, const double* vertices, int64_t nv, const int32_t* tets, int64_t nt, int p,
                       int space, const double* alpha, const double* beta, const uint8_t* mask, bool unsplit,
-                      bool hybrid, cudaStream_t stream) {
+                      bool hybrid, bool host_setup, cudaStream_t stream) {
   auto t0 = std::chrono::steady_clock::now();
   if (stream) CK(cudaStreamSynchronize(stream));
   configure_kernels();
@@ -190,7 +260,10 @@ static int setup_impl(rdr_handle* h, const double* vertices, int64_t nv, const i
 
   Mesh m;
   if ((st = build_mesh(hx.data(), nv, ht.data(), nt, hm.data(), m))) return st;
+  const auto tr0 = std::chrono::steady_clock::now();
   const RefElement& el = reference_element(space, p);
+  if (space == RDR_HCURL) reference_element(RDR_HGRAD, p);  // the potential space's, timed here too
+  h->info.refelem_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - tr0).count();
   Numbering num;
   build_numbering(m, el, num);
   std::vector<double> coef;
@@ -304,9 +377,11 @@ static int setup_impl(rdr_handle* h, const double* vertices, int64_t nv, const i
     pc.kernel = (pk && std::strcmp(pk, "tma") == 0) ? 1 : 0;
     pc.ldg_warps = 8;  // decided below from the patch sizes (RDR_PATCH_WARPS=4|8 overrides)
   }
+  const auto tp0 = std::chrono::steady_clock::now();
+  PatchAssembly pasm;
+  const PatchLayout layout = pc.kernel == 1 ? kTileSwizzled : kTileGroups;
   st = build_patches(m, num, el, coef, space == RDR_HCURL ? &cg_num : nullptr, cg_el,
-                     space == RDR_HCURL ? &cg_coef : nullptr, P, sink, pc.kernel == 1 ? kTileSwizzled : kTileGroups,
-                     unsplit);
+                     space == RDR_HCURL ? &cg_coef : nullptr, P, sink, layout, unsplit, host_setup ? nullptr : &pasm);
   if (sink.d) h->owned.push_back(sink.d);
   if (st) return st;
   pc.n_patches = (int64_t)P.n.size();
@@ -331,6 +406,22 @@ static int setup_impl(rdr_handle* h, const double* vertices, int64_t nv, const i
   pc.tile_off = d_to;
   pc.tiles = sink.d;
   pc.pkind = d_pk;
+  if (!host_setup && pc.n_patches > 0) {  // patch matrices assembled and inverted on the GPU
+    DevPatchSetup ds;
+    ds.pn = d_pn;
+    ds.pkind = d_pk;
+    ds.tile_off = d_to;
+    ds.tiles = sink.d;
+    ds.layout = (int)layout;
+    ds.R[0] = d_R;
+    ds.coef[0] = d_coef;
+    ds.nl[0] = el.n;
+    ds.nm[0] = el.n_mat;
+    if ((st = device_patch_setup(ds, P, pasm, cg_el, space == RDR_HCURL ? &cg_coef : nullptr,
+                                 &h->info.patch_kernel_seconds)))
+      return st;
+  }
+  h->info.patch_setup_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - tp0).count();
   {  // persistent patch kernel: tile slots, CTAs per SM, claim queue
     int dev = 0, sms = 148;
     CK(cudaGetDevice(&dev));
@@ -416,6 +507,11 @@ static int setup_impl(rdr_handle* h, const double* vertices, int64_t nv, const i
   in.flops_apply = 2.0 * el.n * (double)el.n * el.n_mat * (double)nt;
   in.bytes_apply = 24.0 * num.n_total + (double)nt * (4.0 * el.n + 8.0 * el.n_mat);
   in.bytes_precond = P.alg_bytes + 24.0 * in.n_interior;
+  in.patch_setup_flops = 0;
+  for (int32_t n : P.n) {  // lower tiles I >= J, I, J != K: nb(nb-1)/2 per K; panel: nb-1 per K
+    const double nb = (n + 63) / 64;
+    in.patch_setup_flops += 2.0 * 64 * 64 * 64 * nb * ((nb - 1) * nb / 2 + (nb - 1));
+  }
   CK(cudaDeviceSynchronize());
   in.setup_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   return RDR_OK;
@@ -516,12 +612,14 @@ int rdr_setup_ex(rdr_handle** hp, const double* vertices, int64_t nv, const int3
   const int pre = opt ? opt->preconditioner : RDR_ADDITIVE;
   if (pre != RDR_ADDITIVE && pre != RDR_HYBRID) return RDR_EINVAL;
   if (pre == RDR_HYBRID && dec != RDR_SPLIT) return RDR_EINVAL;
+  const int su = opt ? opt->setup : RDR_SETUP_DEVICE;
+  if (su != RDR_SETUP_DEVICE && su != RDR_SETUP_HOST) return RDR_EINVAL;
   rdr_handle* h = new (std::nothrow) rdr_handle();
   if (!h) return RDR_ENOMEM;
   int st;
   try {
     st = setup_impl(h, vertices, nv, tets, nt, p, space, alpha, beta, dirichlet_mask, dec == RDR_UNSPLIT,
-                    pre == RDR_HYBRID, (cudaStream_t)stream);
+                    pre == RDR_HYBRID, su == RDR_SETUP_HOST, (cudaStream_t)stream);
   } catch (const std::bad_alloc&) {
     st = RDR_ENOMEM;
   } catch (const std::exception& e) {

@@ -17,7 +17,11 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <string>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -987,12 +991,124 @@ std::map<std::pair<int, int>, std::unique_ptr<RefElement>> g_el;
 
 }  // namespace
 
+// ---- on-disk cache: opt-in with RDR_CACHE_DIR. One file per
+// (space, p): magic, sizes, the local dofs, R and lam_cell in FP64, then an
+// FNV-1a checksum of everything before it. A file that does not validate is
+// ignored (rebuilt and rewritten); writes go through a temporary + rename.
+namespace {
+
+constexpr char kCacheMagic[8] = {'R', 'D', 'R', 'R', 'E', 'F', '0', '1'};
+
+uint64_t fnv1a(const std::string& b) {
+  uint64_t h = 1469598103934665603ULL;
+  for (unsigned char c : b) h = (h ^ c) * 1099511628211ULL;
+  return h;
+}
+
+template <class T>
+void put(std::string& b, const T& v) {
+  b.append(reinterpret_cast<const char*>(&v), sizeof(T));
+}
+
+template <class T>
+bool get(const std::string& b, size_t& at, T& v) {
+  if (at + sizeof(T) > b.size()) return false;
+  std::memcpy(&v, b.data() + at, sizeof(T));
+  at += sizeof(T);
+  return true;
+}
+
+std::string cache_path(int space, int p) {
+  const char* dir = std::getenv("RDR_CACHE_DIR");
+  if (!dir || !*dir) return std::string();
+  return std::string(dir) + "/refelem_s" + std::to_string(space) + "_p" + std::to_string(p) + ".bin";
+}
+
+std::string serialize(const RefElement& el) {
+  std::string b(kCacheMagic, 8);
+  put(b, (int32_t)el.space);
+  put(b, (int32_t)el.p);
+  put(b, (int32_t)el.n);
+  put(b, (int32_t)el.n_mat);
+  put(b, (int64_t)el.dofs.size());
+  for (const LocalDof& d : el.dofs) {
+    put(b, (int32_t)d.dim);
+    put(b, (int32_t)d.ent);
+    put(b, (int32_t)d.j);
+    put(b, (int32_t)d.type);
+  }
+  put(b, (int64_t)el.R.size());
+  b.append(reinterpret_cast<const char*>(el.R.data()), sizeof(double) * el.R.size());
+  put(b, (int64_t)el.lam_cell.size());
+  b.append(reinterpret_cast<const char*>(el.lam_cell.data()), sizeof(double) * el.lam_cell.size());
+  put(b, fnv1a(b));
+  return b;
+}
+
+std::unique_ptr<RefElement> load_cached(int space, int p) {
+  const std::string path = cache_path(space, p);
+  if (path.empty()) return nullptr;
+  FILE* f = std::fopen(path.c_str(), "rb");
+  if (!f) return nullptr;
+  std::string b;
+  char buf[1 << 16];
+  size_t got;
+  while ((got = std::fread(buf, 1, sizeof(buf), f)) > 0) b.append(buf, got);
+  std::fclose(f);
+  if (b.size() < 16 || std::memcmp(b.data(), kCacheMagic, 8) != 0) return nullptr;
+  uint64_t sum;
+  std::memcpy(&sum, b.data() + b.size() - 8, 8);
+  if (fnv1a(b.substr(0, b.size() - 8)) != sum) return nullptr;
+  auto el = std::make_unique<RefElement>();
+  size_t at = 8;
+  int32_t sp, pp, n, nm;
+  int64_t nd, nr, nlam;
+  if (!get(b, at, sp) || !get(b, at, pp) || !get(b, at, n) || !get(b, at, nm) || !get(b, at, nd)) return nullptr;
+  if (sp != space || pp != p || n <= 0 || nm <= 0 || nd != n) return nullptr;
+  el->space = sp;
+  el->p = pp;
+  el->n = n;
+  el->n_mat = nm;
+  el->dofs.resize(nd);
+  for (LocalDof& d : el->dofs) {
+    int32_t v[4];
+    for (int32_t& x : v)
+      if (!get(b, at, x)) return nullptr;
+    d = LocalDof{v[0], v[1], v[2], v[3]};
+  }
+  if (!get(b, at, nr) || nr != (int64_t)nm * n * n || at + 8 * nr > b.size()) return nullptr;
+  el->R.resize(nr);
+  std::memcpy(el->R.data(), b.data() + at, 8 * nr);
+  at += 8 * nr;
+  if (!get(b, at, nlam) || nlam < 0 || at + 8 * nlam + 8 != b.size()) return nullptr;
+  el->lam_cell.resize(nlam);
+  std::memcpy(el->lam_cell.data(), b.data() + at, 8 * nlam);
+  return el;
+}
+
+void store_cached(const RefElement& el) {
+  const std::string path = cache_path(el.space, el.p);
+  if (path.empty()) return;
+  const std::string tmp = path + ".tmp" + std::to_string((long long)std::rand());
+  FILE* f = std::fopen(tmp.c_str(), "wb");
+  if (!f) return;  // the cache is best effort: an unwritable directory only costs the rebuild
+  const std::string b = serialize(el);
+  const bool ok = std::fwrite(b.data(), 1, b.size(), f) == b.size();
+  if (std::fclose(f) != 0 || !ok || std::rename(tmp.c_str(), path.c_str()) != 0) std::remove(tmp.c_str());
+}
+
+}  // namespace
+
 const RefElement& reference_element(int space, int p) {
   std::lock_guard<std::mutex> lk(g_el_mutex);
   auto k = std::make_pair(space, p);
   auto it = g_el.find(k);
   if (it != g_el.end()) return *it->second;
-  auto el = space == 0 ? build_cg(p) : build_ned(p);
+  auto el = load_cached(space, p);
+  if (!el) {
+    el = space == 0 ? build_cg(p) : build_ned(p);
+    store_cached(*el);
+  }
   const RefElement& ref = *el;
   g_el[k] = std::move(el);
   return ref;

@@ -407,7 +407,7 @@ struct PatchDef {
 
 int build_patches(const Mesh& m, const Numbering& num, const RefElement& el, const std::vector<double>& coef,
                   const Numbering* cg_num, const RefElement* cg_el, const std::vector<double>* cg_coef,
-                  Patches& P, PatchSink& sink, PatchLayout layout, bool unsplit) {
+                  Patches& P, PatchSink& sink, PatchLayout layout, bool unsplit, PatchAssembly* dev) {
   CSR v_cells = invert_incidence(m.nt, m.nv, 4, m.cells);
   CSR v_edges = invert_incidence(m.ne, m.nv, 2, m.edges);
   CSR v_faces = invert_incidence(m.nf, m.nv, 3, m.faces);
@@ -506,6 +506,47 @@ int build_patches(const Mesh& m, const Numbering& num, const RefElement& el, con
   P.total_doubles = P.tile_off[np];
   P.idx.assign(P.idx_off[np], -1);
   for (int64_t k = 0; k < np; ++k) std::copy(defs[order[k]].idx.begin(), defs[order[k]].idx.end(), P.idx.begin() + P.idx_off[k]);
+
+  if (dev) {  // device setup: per patch, the (local dof, position) lists of its star cells
+    std::vector<std::vector<int32_t>> cells(np), counts(np);
+    std::vector<std::vector<uint32_t>> ents(np);
+#pragma omp parallel for schedule(dynamic, 16)
+    for (int64_t k = 0; k < np; ++k) {
+      const PatchDef& d = defs[order[k]];
+      const Numbering& nb = d.numbering == 0 ? num : *cg_num;
+      const int nl = d.numbering == 0 ? el.n : cg_el->n;
+      for (int32_t t : d.cells) {
+        int c = 0;
+        for (int i = 0; i < nl; ++i) {
+          const int32_t g = nb.dofmap[(size_t)t * nl + i];
+          auto it = std::lower_bound(d.idx.begin(), d.idx.end(), g);
+          if (it != d.idx.end() && *it == g) {
+            ents[k].push_back(((uint32_t)i << 16) | (uint32_t)(it - d.idx.begin()));
+            ++c;
+          }
+        }
+        if (c) {
+          cells[k].push_back(t);
+          counts[k].push_back(c);
+        }
+      }
+    }
+    dev->rec_ptr.assign(np + 1, 0);
+    for (int64_t k = 0; k < np; ++k) dev->rec_ptr[k + 1] = dev->rec_ptr[k] + (int64_t)cells[k].size();
+    const int64_t nrec = dev->rec_ptr[np];
+    dev->rec_cell.resize(nrec);
+    dev->rec_off.assign(nrec + 1, 0);
+    for (int64_t k = 0; k < np; ++k)
+      for (size_t r = 0; r < cells[k].size(); ++r) {
+        const int64_t g = dev->rec_ptr[k] + (int64_t)r;
+        dev->rec_cell[g] = cells[k][r];
+        dev->rec_off[g + 1] = dev->rec_off[g] + counts[k][r];
+      }
+    dev->ent.resize(dev->rec_off[nrec]);
+    for (int64_t k = 0; k < np; ++k)
+      std::copy(ents[k].begin(), ents[k].end(), dev->ent.begin() + dev->rec_off[dev->rec_ptr[k]]);
+    return sink.reserve(P.total_doubles);
+  }
 
   // assemble + invert + pack, in chunks of about 1 GiB of tiles
   const int64_t chunk_doubles = std::max<int64_t>((int64_t)1 << 27, P.tile_off[1] - P.tile_off[0]);

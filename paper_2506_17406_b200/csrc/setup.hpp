@@ -84,9 +84,20 @@ struct PatchSink {
   virtual ~PatchSink() {}
 };
 enum PatchLayout { kTileGroups = 0, kTileSwizzled = 1 };
+// Assembly lists of the device setup (patch_setup.hpp DevPatchSetup): patch k
+// has cell records [rec_ptr[k], rec_ptr[k+1]), record r is cell rec_cell[r]
+// with entries ent[rec_off[r] .. rec_off[r+1]) = (local dof << 16) | position.
+struct PatchAssembly {
+  std::vector<int64_t> rec_ptr, rec_off;
+  std::vector<int32_t> rec_cell;
+  std::vector<uint32_t> ent;
+};
+// dev == nullptr: assemble, invert and pack on the host and hand the tiles to
+// `sink`; otherwise only reserve the store and fill *dev for patch_setup.cu.
 int build_patches(const Mesh& m, const Numbering& num, const RefElement& el, const std::vector<double>& coef,
                   const Numbering* cg_num, const RefElement* cg_el, const std::vector<double>* cg_coef,
-                  Patches& P, PatchSink& sink, PatchLayout layout, bool unsplit = false);
+                  Patches& P, PatchSink& sink, PatchLayout layout, bool unsplit = false,
+                  PatchAssembly* dev = nullptr);
 
 // Packs the symmetric n x n matrix W2 (row-major) into the patch tile layout.
 void pack_patch_tiles(const double* W2, int n, double* out, PatchLayout layout);

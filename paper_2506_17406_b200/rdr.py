@@ -14,6 +14,7 @@ LIB_PATH = os.path.join(HERE, "librdr.so")
 HGRAD, HCURL = 0, 1
 SPLIT, UNSPLIT = 0, 1
 ADDITIVE, HYBRID = 0, 1
+SETUP_DEVICE, SETUP_HOST = 0, 1
 RDR_OK, RDR_ENOCONV = 0, -6
 
 
@@ -24,7 +25,7 @@ class RdrError(RuntimeError):
 
 
 class Options(ctypes.Structure):
-    _fields_ = [("decomposition", ctypes.c_int), ("preconditioner", ctypes.c_int)]
+    _fields_ = [("decomposition", ctypes.c_int), ("preconditioner", ctypes.c_int), ("setup", ctypes.c_int)]
 
 
 class Info(ctypes.Structure):
@@ -32,7 +33,9 @@ class Info(ctypes.Structure):
                 ("n_cells", ctypes.c_int64), ("n_loc", ctypes.c_int32), ("n_mat", ctypes.c_int32),
                 ("n_patches", ctypes.c_int64), ("max_patch", ctypes.c_int32), ("patch_bytes", ctypes.c_int64),
                 ("flops_apply", ctypes.c_double), ("bytes_apply", ctypes.c_double),
-                ("bytes_precond", ctypes.c_double), ("setup_seconds", ctypes.c_double)]
+                ("bytes_precond", ctypes.c_double), ("setup_seconds", ctypes.c_double),
+                ("refelem_seconds", ctypes.c_double), ("patch_setup_seconds", ctypes.c_double),
+                ("patch_kernel_seconds", ctypes.c_double), ("patch_setup_flops", ctypes.c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -131,7 +134,7 @@ class Solver:
     CUDA tensors of length n_total."""
 
     def __init__(self, vertices, tets, p, space, alpha, beta, mask, stream=None, decomposition=SPLIT,
-                 preconditioner=ADDITIVE):
+                 preconditioner=ADDITIVE, setup=SETUP_DEVICE):
         import torch
         self._keep = [np.ascontiguousarray(vertices, dtype=np.float64) if isinstance(vertices, np.ndarray) else vertices,
                       np.ascontiguousarray(tets, dtype=np.int32) if isinstance(tets, np.ndarray) else tets,
@@ -141,7 +144,7 @@ class Solver:
         v, t, a, b, m = self._keep
         self._h = ctypes.c_void_p()
         nv, nt = v.shape[0], t.shape[0]
-        opt = Options(int(decomposition), int(preconditioner))
+        opt = Options(int(decomposition), int(preconditioner), int(setup))
         _check(_lib.rdr_setup_ex(ctypes.byref(self._h), _ptr(v), nv, _ptr(t), nt, int(p), int(space), _ptr(a),
                                  _ptr(b), _ptr(m), ctypes.byref(opt), _stream(stream)), "rdr_setup_ex")
         self._keep = None

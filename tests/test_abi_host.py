@@ -88,3 +88,51 @@ def test_host_spd_inverse(n):
     assert np.array_equal(B, B.T)
     C = -np.eye(3)
     assert rdr._lib.rdr_spd_inverse(ctypes.c_void_p(C.ctypes.data), 3) == -3
+
+
+def _refmats_in_subprocess(tmp_path, space, p, tag):
+    import subprocess
+    import sys
+    out = tmp_path / f"{tag}.npy"
+    code = ("import numpy as np; from paper_2506_17406_b200 import rdr; "
+            f"np.save(r'{out}', rdr.reference_matrices({space}, {p}))")
+    env = dict(os.environ, RDR_CACHE_DIR=str(tmp_path))
+    subprocess.run([sys.executable, "-c", code], check=True, env=env, cwd=ROOT)
+    return np.load(out)
+
+
+def _fnv1a(b: bytes) -> int:
+    h = 1469598103934665603
+    for c in b:
+        h = ((h ^ c) * 1099511628211) & 0xFFFFFFFFFFFFFFFF
+    return h
+
+
+def test_reference_element_disk_cache(tmp_path):
+    """SURVEY NEXT-4 on-disk reference-element cache (RDR_CACHE_DIR): the first
+    process writes the file, later ones read it (proved by planting a valid
+    file with one altered entry), and a file that fails its checksum is
+    ignored and rebuilt."""
+    import struct
+    R0 = _refmats_in_subprocess(tmp_path, 1, 3, "a")
+    f = tmp_path / "refelem_s1_p3.bin"
+    assert f.exists()
+    R1 = _refmats_in_subprocess(tmp_path, 1, 3, "b")
+    assert np.array_equal(R0, R1)
+    # plant: same file with R[0][0][0] += 1 and a recomputed checksum -> the loader must return it
+    b = bytearray(f.read_bytes()[:-8])
+    n = struct.unpack_from("<i", b, 16)[0]
+    r_at = 8 + 16 + 8 + 16 * n + 8
+    v = struct.unpack_from("<d", b, r_at)[0]
+    assert v == R0[0, 0, 0]
+    struct.pack_into("<d", b, r_at, v + 1.0)
+    f.write_bytes(bytes(b) + struct.pack("<Q", _fnv1a(bytes(b))))
+    R2 = _refmats_in_subprocess(tmp_path, 1, 3, "c")
+    assert R2[0, 0, 0] == v + 1.0 and np.array_equal(R2.ravel()[1:], R0.ravel()[1:])
+    # corrupt one byte without fixing the checksum -> rebuilt from scratch and rewritten
+    b = bytearray(f.read_bytes())
+    b[r_at + 3] ^= 0xFF
+    f.write_bytes(bytes(b))
+    R3 = _refmats_in_subprocess(tmp_path, 1, 3, "d")
+    assert np.array_equal(R3, R0)
+    assert _refmats_in_subprocess(tmp_path, 1, 3, "e").tobytes() == R0.tobytes()

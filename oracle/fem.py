@@ -5,7 +5,8 @@ TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
 a^k(u, v) = (u, beta v) + (d^k u, alpha d^k v)   (Eq. 2.9)
 with the pullbacks of Eq. 2.7: k=0: phi = phi-hat o F^-1,
 grad phi = J^-T grad-hat phi-hat; k=1: phi = J^-T phi-hat,
-curl phi = J curl-hat phi-hat / det J. Element matrices are computed by
+curl phi = J curl-hat phi-hat / det J; k=2: phi = J phi-hat / det J,
+div phi = div-hat phi-hat / det J. Element matrices are computed by
 quadrature at physical points (collapsed Gauss-Jacobi, exact to degree
 2p+2, DESIGN.md R-A10), never by the reference-matrix contraction the GPU
 path uses. Global CSR by the canonical numbering; Dirichlet by elimination.
@@ -81,6 +82,12 @@ class Assembler:
             Mm = np.einsum("q,qi,qj->ij", wq, self.val, self.val)
             Kk = gram(g)
             return vol[:, None, None] * (beta[:, None, None] * Mm[None] + alpha[:, None, None] * Kk)
+        if self.space == "hdiv":  # 2-forms: phi = J phi-hat / det J, div phi = div-hat phi-hat / det J
+            ph = np.einsum("cab,qnb->cqna", J, self.val) / det[:, None, None, None]
+            dv = self.der[None] / det[:, None, None]
+            Mm = gram(ph)
+            Kk = np.einsum("q,cqi,cqj->cij", wq, dv, dv)
+            return vol[:, None, None] * (beta[:, None, None] * Mm + alpha[:, None, None] * Kk)
         Jit = np.linalg.inv(np.transpose(J, (0, 2, 1)))
         ph = np.einsum("cab,qnb->cqna", Jit, self.val)
         cu = np.einsum("cab,qnb->cqna", J, self.der) / det[:, None, None, None]

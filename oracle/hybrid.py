@@ -85,8 +85,10 @@ class HybridOracle(Oracle):
         self.Gam = np.nonzero(~num.interior & fr)[0]                    # X_2
         if self.space == "hgrad":                                       # X_3 = W^0: vertex dofs
             w = np.arange(num.offsets[0], num.offsets[0] + self.topo.nv)
-        else:                                                           # X_3 = W^1: Whitney dofs
+        elif self.space == "hcurl":                                     # X_3 = W^1: Whitney edge dofs
             w = num.offsets[1] + np.arange(self.topo.ne) * num.per[1]
+        else:                                                           # X_3 = W^2: Whitney face dofs
+            w = num.offsets[2] + np.arange(self.topo.nf) * num.per[2]
         self.W = w[fr[w]]
         Ac = self.A[self.W][:, self.W].toarray()
         self.coarse = sla.cho_factor(Ac, lower=True) if len(self.W) else None

@@ -80,6 +80,16 @@ def dof_layout(space: str, p: int):
             nb = math.comb(p - 1, dim)
             out += [(dim, e, j, "I") for e in range(ne) for j in range(nb)]
         return out
+    if space == "hdiv":  # RT_p (Eq. 3.18): face Whitney, face type-II, cell type-I, cell type-II
+        nF = p * (p + 1) // 2 - 1
+        nCI = p * (p + 1) * (p + 2) // 6 - 1
+        nCII = p * (p - 1) * (p - 2) // 2 - (p - 1) * (p - 2) * (p - 3) // 6
+        for e in range(4):
+            out.append((2, e, 0, "W"))
+            out += [(2, e, j, "II") for j in range(nF)]
+        out += [(3, 0, j, "I") for j in range(nCI)]
+        out += [(3, 0, j, "II") for j in range(nCII)]
+        return out
     for e in range(6):
         out.append((1, e, 0, "W"))
         out += [(1, e, j, "II") for j in range(p - 1)]
@@ -96,6 +106,8 @@ def dofs_per_entity(space: str, p: int):
     """(vertex, edge, face, cell) dof counts (Eq. 3.7)."""
     if space == "hgrad":
         return 1, p - 1, (p - 1) * (p - 2) // 2, (p - 1) * (p - 2) * (p - 3) // 6
+    if space == "hdiv":
+        return 0, 0, p * (p + 1) // 2, (p + 1) * p * (p - 1) // 2
     return 0, p, p * (p - 1), p * (p - 1) * (p - 2) // 2
 
 
@@ -135,7 +147,10 @@ def number(space: str, p: int, topo: Topology, dof_entity) -> Numbering:
             pos = j if space == "hgrad" else (0 if typ == "W" else 1 + j)
         elif dim == 2:
             ent = topo.cell_faces[:, ei]
-            pos = j if (space == "hgrad" or typ == "I") else nI_face + j
+            if space == "hdiv":
+                pos = 0 if typ == "W" else 1 + j
+            else:
+                pos = j if (space == "hgrad" or typ == "I") else nI_face + j
         else:
             ent = np.arange(topo.nt)
             pos = j if (space == "hgrad" or typ == "I") else nI_cell + j

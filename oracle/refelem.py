@@ -1,4 +1,4 @@
-"""The paper's reference elements CG_p and Ned1_p on the equilateral T-hat.
+"""The paper's reference elements CG_p, Ned1_p and RT_p on the equilateral T-hat.
 
 TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
 
@@ -8,7 +8,8 @@ Follows the paper in its order:
      zero modes dropped, survivors renormalised to Eq. 3.8:
      (d psi_i, d psi_j) = delta_ij, (psi_i, psi_j) = lambda_j delta_ij;
      ordering / cluster canonicalization by DESIGN.md R-A5..A7;
-  3. the dofs of §3.4.1 (Eq. 3.14) and §3.4.2 (Eq. 3.16),
+  3. the dofs of §3.4.1 (Eq. 3.14), §3.4.2 (Eq. 3.16) and
+     §3.4.3 (Eq. 3.18; the Psi are Ned1_p's, DESIGN.md R-D1),
      with the canonical eigenbases carried to the subsimplices of T-hat by the
      vertex-order-preserving isometry (R-A2; in barycentric form this is a
      relabelling of vertices);
@@ -17,7 +18,9 @@ Follows the paper in its order:
 Polynomial spans: CG_p = P_p in the scaled Bernstein basis (p!/beta!) lambda^beta;
 Ned1_p = P_p^- Lambda^1 in the scaled Whitney-product basis
 ((p-1)!/alpha!) lambda^alpha w_ij with i<j, |alpha| = p-1, alpha_k = 0 for k < i
-(DESIGN.md R-S1; rank pinned in tests). The span only affects rounding: the
+(DESIGN.md R-S1; rank pinned in tests); RT_p = P_p^- Lambda^2 in the
+Whitney 2-form products ((p-1)!/alpha!) lambda^alpha w_ijk, i<j<k,
+alpha_m = 0 for m < i. The span only affects rounding: the
 dual basis is fixed by the dofs.
 """
 from __future__ import annotations
@@ -30,7 +33,7 @@ import numpy as np
 
 from .xprec import LD, eigh_ld, inv_ld, qr_pos_ld
 from .simplex import (Simplex, canonical, reference_tet, multi_indices, mi_lookup,
-                      TET_EDGES, TET_FACES, trace0, trace1, pairs)
+                      TET_EDGES, TET_FACES, trace0, trace1, trace2, pairs)
 
 ZERO_MODE_TOL = 1e-8      # R-A7: mu < 1e-8 max mu is kernel
 CLUSTER_TOL = 1e-8        # R-A6: (mu_{j+1} - mu_j) <= 1e-8 mu_{j+1}
@@ -91,8 +94,10 @@ def _canonicalize(S: Simplex, kind: str, mu, F, q):
                 y = probe_bary(S.l, s + 1 + i)
                 if kind == "cg":
                     P[i] = S.eval0(blk, q, y)[0]
-                else:
+                elif kind == "ned":
                     P[i] = S.eval1(blk, q, y)[0] @ probe_dir(S.dim, s + 1 + i)
+                else:  # "rt": 2-form vector proxy in T-hat
+                    P[i] = S.eval2(blk, q, y)[0] @ probe_dir(S.dim, s + 1 + i)
             smin = np.linalg.svd(P.astype(np.float64), compute_uv=False).min()
             if smin >= PROBE_ACCEPT * float(rho):
                 break
@@ -112,10 +117,14 @@ def bubble_eigen(S: Simplex, kind: str, Fspan, q: int, dim_bubble: int, n_kernel
         M = S.mass0(Fspan, q, Fspan, q)
         dF = Fspan @ S.grad_op(q)
         K = S.mass1(dF, q - 1, dF, q - 1)
-    else:
+    elif kind == "ned":
         M = S.mass1(Fspan, q, Fspan, q)
         dF = Fspan @ S.curl_op(q)
         K = S.mass2(dF, q - 1, dF, q - 1)
+    else:  # "rt": 2-forms on T-hat, d = div (Eq. 3.17)
+        M = S.mass2(Fspan, q, Fspan, q)
+        dF = Fspan @ S.div_op(q)
+        K = S.mass0(dF, q - 1, dF, q - 1)
     s, U = eigh_ld(M)
     keep = s > LD(1e-13) * s.max()
     assert int(keep.sum()) == dim_bubble, (kind, S.l, int(keep.sum()), dim_bubble)
@@ -179,6 +188,36 @@ def ned_bubbles(l: int, p: int) -> Eigenbasis:
     elems = ned_bubble_span(l, p)
     F = S.whitney_products(elems, p - 1) * np.array([_multinom(a) for a, _, _ in elems], dtype=LD)[:, None]
     return bubble_eigen(S, "ned", F, p, dim, nk)
+
+
+def rt_bubble_span(p: int):
+    """Whitney 2-form products lambda^alpha w_ijk, |alpha| = p-1, i<j<k, with
+    supp(alpha) U {i,j,k} = all four vertices of T-hat (the 2-form analogue of
+    DESIGN.md R-S2)."""
+    out = []
+    for (i, j, k) in [(0, 1, 2), (0, 1, 3), (0, 2, 3), (1, 2, 3)]:
+        for a in multi_indices(4, p - 1):
+            if len(set(np.nonzero(a)[0]) | {i, j, k}) == 4:
+                out.append((tuple(a), i, j, k))
+    return out
+
+
+@lru_cache(maxsize=None)
+def rt_bubbles(p: int) -> Eigenbasis:
+    """Type-I RT_p cell bubble eigenbasis Phi_{C,j} of Eq. 3.17:
+    (div Phi_j, div Phi_i) = delta_ij, (Phi_j, Phi_i) = lambda_j delta_ij, via
+    the augmented problem Eq. 3.9 on the whole bubble space, whose kernel (the
+    divergence-free bubbles) has dimension dim RT-bubbles - (dim P_{p-1} - 1)."""
+    T = reference_tet()
+    dim = p * (p + 1) * (p - 1) // 2
+    nI = p * (p + 1) * (p + 2) // 6 - 1
+    npair = 6
+    if dim == 0 or nI == 0:
+        return Eigenbasis(l=3, kind="rt", lam=np.zeros(0, LD), mu=np.zeros(0, LD),
+                          F=np.zeros((0, len(multi_indices(4, p)) * npair), LD), n_kernel=dim)
+    elems = rt_bubble_span(p)
+    F = T.whitney2_products(elems, p - 1) * np.array([_multinom(a) for a, _, _, _ in elems], dtype=LD)[:, None]
+    return bubble_eigen(T, "rt", F, p, dim, dim - nI)
 
 
 # ------------------------------------------------------------------ elements
@@ -302,8 +341,74 @@ def ned_element(p: int) -> RefElement:
     return RefElement("hcurl", p, n, T, Fb, C, ents, V, ned_bubbles(3, p).lam)
 
 
+def rt_span(p: int):
+    """Whitney 2-form product basis of RT_p(T-hat) = P_p^- Lambda^2:
+    lambda^alpha w_ijk, i<j<k, |alpha| = p-1, alpha_m = 0 for m < i (the 2-form
+    analogue of DESIGN.md R-S1; dimension p(p+1)(p+3)/2, asserted)."""
+    out = []
+    for (i, j, k) in [(0, 1, 2), (0, 1, 3), (0, 2, 3), (1, 2, 3)]:
+        for a in multi_indices(4, p - 1):
+            if all(a[m] == 0 for m in range(i)):
+                out.append((tuple(a), i, j, k))
+    assert len(out) == p * (p + 1) * (p + 3) // 2
+    return out
+
+
+def face_unit_form(F: Simplex) -> np.ndarray:
+    """The constant 2-form on the canonical face whose proxy is 1 (orientation
+    c0 -> c1 -> c2, i.e. the sorted vertex order, DESIGN.md R-D2): c g_0 x g_1
+    with c = 1 / (g_0 x g_1)."""
+    cr = F.g[0][0] * F.g[1][1] - F.g[0][1] * F.g[1][0]
+    u = np.zeros((1, 3), dtype=LD)
+    u[0, 0] = 1 / cr          # pair (0,1) is the first of the face's pair frame
+    return u
+
+
+@lru_cache(maxsize=None)
+def rt_element(p: int) -> RefElement:
+    """RT_p with the dofs of Eq. 3.18, ordered per entity:
+    face: Whitney (1, n.v)_F then type-II (curl_F Psi_{F,j}, n.v)_F;
+    cell: type-I (div Phi_{C,j}, div v) then type-II (curl Psi_{C,j}, v).
+    Psi are the Ned1_p bubble eigenbases (DESIGN.md R-D1: the paper allows
+    Ned1_p or Ned2_p here)."""
+    T = reference_tet()
+    elems = rt_span(p)
+    Fb = T.whitney2_products(elems, p - 1) * np.array([_multinom(a) for a, _, _, _ in elems], dtype=LD)[:, None]
+    n = len(elems)
+    rows, ents = [], []
+    Sc = canonical(2)
+    u = face_unit_form(Sc)
+    PsiF = ned_bubbles(2, p)
+    cPsiF = PsiF.F @ Sc.curl_op(p) if len(PsiF.lam) else None
+    for ei, s in enumerate(TET_FACES):
+        tr = trace2(Fb, p, 4, s)
+        rows.append(Sc.mass2(u, 0, tr, p)[0])
+        ents.append((2, ei, 0, "W"))
+        if cPsiF is not None:
+            Vs = Sc.mass2(cPsiF, p - 1, tr, p)
+            for j in range(len(PsiF.lam)):
+                rows.append(Vs[j])
+                ents.append((2, ei, j, "II"))
+    Phi = rt_bubbles(p)
+    if len(Phi.lam):
+        Vs = T.mass0(Phi.F @ T.div_op(p), p - 1, Fb @ T.div_op(p), p - 1)
+        for j in range(len(Phi.lam)):
+            rows.append(Vs[j])
+            ents.append((3, 0, j, "I"))
+    PsiC = ned_bubbles(3, p)
+    if len(PsiC.lam):
+        Vs = T.mass2(PsiC.F @ T.curl_op(p), p - 1, Fb, p)
+        for j in range(len(PsiC.lam)):
+            rows.append(Vs[j])
+            ents.append((3, 0, j, "II"))
+    V = np.array(rows, dtype=LD)
+    assert V.shape == (n, n), V.shape
+    C = inv_ld(V)
+    return RefElement("hdiv", p, n, T, Fb, C, ents, V, Phi.lam)
+
+
 def element(space: str, p: int) -> RefElement:
-    return cg_element(p) if space == "hgrad" else ned_element(p)
+    return {"hgrad": cg_element, "hcurl": ned_element, "hdiv": rt_element}[space](p)
 
 
 # ------------------------------------------------------------------ tabulation
@@ -318,6 +423,8 @@ def tabulate(el: RefElement, bary):
         der = T.eval1(Phi @ T.grad_op(p), p - 1, bary)
         return val, der
     Phi = el.C.T @ el.span
+    if el.space == "hdiv":  # (phi [npts,n,3] 2-form proxies, div [npts,n])
+        return T.eval2(Phi, p, bary), T.eval0(Phi @ T.div_op(p), p - 1, bary)
     val = T.eval1(Phi, p, bary)
     der = T.eval2(Phi @ T.curl_op(p), p - 1, bary)
     return val, der
@@ -326,7 +433,8 @@ def tabulate(el: RefElement, bary):
 def reference_matrices(el: RefElement):
     """M-hat and K-hat^{ab} (Cartesian a,b) by exact integration, longdouble.
     hgrad: M [n,n], K [3,3,n,n] with K^{ab}_ij = int d_a phi_i d_b phi_j.
-    hcurl: M [3,3,n,n] with M^{ab}_ij = int phi_i,a phi_j,b; K likewise with curls."""
+    hcurl: M [3,3,n,n] with M^{ab}_ij = int phi_i,a phi_j,b; K likewise with curls.
+    hdiv: M [3,3,n,n] of the 2-form proxies; K [n,n] with divergences."""
     T, p, C = el.T, el.p, el.C
     if el.space == "hgrad":
         Mh = C.T @ T.mass0(el.span, p, el.span, p) @ C
@@ -338,6 +446,14 @@ def reference_matrices(el: RefElement):
         K = np.array([[Dc[a] @ I1 @ Dc[b].T for b in range(3)] for a in range(3)])
         return Mh, K
     Np = len(multi_indices(4, p))
+    if el.space == "hdiv":  # M^{ab}_ij = int phi_i,a phi_j,b (2-form proxies), K_ij = int div phi_i div phi_j
+        cr = np.array([np.cross(T.g[a], T.g[b]) for a, b in T.pairs], dtype=LD)
+        Pr = el.span.reshape(el.n, Np, len(T.pairs))
+        Pc = [C.T @ (Pr @ cr[:, a]) for a in range(3)]
+        Ip = T.I(p, p)
+        M = np.array([[Pc[a] @ Ip @ Pc[b].T for b in range(3)] for a in range(3)])
+        Dv = C.T @ (el.span @ T.div_op(p))
+        return M, Dv @ T.I(p - 1, p - 1) @ Dv.T
     Pr = el.span.reshape(el.n, Np, 4)
     Pc = [C.T @ (Pr @ T.g[:, a]) for a in range(3)]
     Ip = T.I(p, p)

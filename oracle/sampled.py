@@ -120,6 +120,9 @@ class SampledOracle(Oracle):
         dim, ent = self.num.entity[l]
         verts = [int(ent)] if dim == 0 else list(t.edges[ent]) if dim == 1 else \
             list(t.faces[ent]) if dim == 2 else list(t.cells[ent])
+        if self.space == "hdiv":  # edge stars only: the edges of the dof's face (cell, unsplit)
+            vs = sorted(verts)
+            return [("edge", t.edge_index[(vs[ia], vs[ib])]) for ia in range(len(vs)) for ib in range(ia + 1, len(vs))]
         seeds = [("vertex", v) for v in verts]
         if self.space == "hcurl" and dim >= 1:
             vs = sorted(verts)

@@ -151,6 +151,42 @@ class Simplex:
             F[r, lk[tuple(aj)] * nv + i] -= 1
         return F
 
+    def whitney2_products(self, elems, q: int) -> np.ndarray:
+        """Rows = 2-form coefficients (deg q+1, pair frame) of lambda^alpha w_ijk,
+        w_ijk = lambda_i g_j x g_k - lambda_j g_i x g_k + lambda_k g_i x g_j
+        (the Whitney 2-form of face ijk up to the factor 2), (alpha, i, j, k) in
+        elems with i < j < k, |alpha| = q."""
+        lk = mi_lookup(self.nv, q + 1)
+        pr = {p: i for i, p in enumerate(self.pairs)}
+        npair = len(self.pairs)
+        F = np.zeros((len(elems), len(lk) * npair), dtype=LD)
+        for r, (alpha, i, j, k) in enumerate(elems):
+            for m, pair, sgn in ((i, (j, k), 1), (j, (i, k), -1), (k, (i, j), 1)):
+                a = list(alpha)
+                a[m] += 1
+                F[r, lk[tuple(a)] * npair + pr[pair]] += sgn
+        return F
+
+    def div_op(self, q: int) -> np.ndarray:
+        """2-form (deg q, pair frame, 3D proxy g_a x g_b) -> 0-form (deg q-1):
+        div(lambda^gamma g_a x g_b) = sum_k gamma_k lambda^(gamma-e_k) g_k . (g_a x g_b)."""
+        assert self.dim == 3
+        nv = self.nv
+        A = multi_indices(nv, q)
+        lk = mi_lookup(nv, q - 1)
+        npair = len(self.pairs)
+        D = np.zeros((len(A) * npair, len(lk)), dtype=LD)
+        for i, a in enumerate(A):
+            for pi, (pa, pb) in enumerate(self.pairs):
+                cr = np.cross(self.g[pa], self.g[pb])
+                for k in range(nv):
+                    if a[k] == 0 or k in (pa, pb):
+                        continue
+                    b = list(a)
+                    b[k] -= 1
+                    D[i * npair + pi, lk[tuple(b)]] += a[k] * (self.g[k] @ cr)
+        return D
+
     # ---------------------------------------------------------------- evaluation
     def bary(self, x) -> np.ndarray:
         """Barycentric coordinates of Cartesian points x [npts, dim]."""
@@ -255,6 +291,22 @@ def trace0(F, q, nv_parent, s):
     out = np.zeros((F.shape[0], len(multi_indices(len(s), q))), dtype=LD)
     for a in np.nonzero(ok)[0]:
         out[:, idx[a]] += F[:, a]
+    return out
+
+
+def trace2(F, q, nv_parent, s):
+    """Trace of 2-forms (rows of F, deg q, pair frame) onto subsimplex s: the
+    terms with supp(gamma) and both pair vertices inside s (d lambda_m vanishes
+    tangentially for m not in s), in the child's pair frame."""
+    ok, idx = restrict_mi(q, nv_parent, s)
+    s = list(s)
+    pp, cp = pairs(nv_parent), {p: i for i, p in enumerate(pairs(len(s)))}
+    npp, npc = len(pp), len(cp)
+    out = np.zeros((F.shape[0], len(multi_indices(len(s), q)) * npc), dtype=LD)
+    for a in np.nonzero(ok)[0]:
+        for pi, (x, y) in enumerate(pp):
+            if x in s and y in s:
+                out[:, idx[a] * npc + cp[(s.index(x), s.index(y))]] += F[:, a * npp + pi]
     return out
 
 

@@ -11,6 +11,8 @@ Preconditioner (DESIGN.md R-A13..A15, R-A17):
     vertex potential patches E_m = G_V (discrete gradient columns of the free
     CG_p interface dofs of the vertex star) and edge patches = free Whitney dof
     of E + type-I dofs of the faces containing E.
+  * H(div): PAFW1(X2_Gamma) + J(X2_I) (Eq. 5.16):
+    one patch per edge E = the free dofs of the faces containing E.
   Local solvers are exact: dense Cholesky (scipy cho_factor/cho_solve).
 PCG (R-A16): x0 = 0, stop when ||z||_2 <= rtol ||z0||_2 (P:2326-2328 gives rtol 1e-8).
 """
@@ -29,7 +31,7 @@ from .fem import Assembler
 
 class Oracle:
     def __init__(self, vertices, tets, p, space, alpha, beta, mask, assemble=True, decomposition="split"):
-        self.space = {0: "hgrad", 1: "hcurl", "hgrad": "hgrad", "hcurl": "hcurl"}[space]
+        self.space = {0: "hgrad", 1: "hcurl", 2: "hdiv", "hgrad": "hgrad", "hcurl": "hcurl", "hdiv": "hdiv"}[space]
         self.p = p
         # "split": PAFW0(X_Gamma)+J(X_I) (Eq. 5.4) / PH(X0_Gamma, X1I_Gamma)+J(X1_I) (Eq. 5.12), the hot path;
         # "unsplit": PAFW0(X) (Eq. 5.2) / PH(X0, X1I) (Eq. 5.10), interiors inside the star patches and
@@ -120,9 +122,23 @@ class Oracle:
     def edge_patch(self, e):
         """('dof', idx) of the type-I edge patch of E (H(curl), R-A13): the free
         Whitney dof of E and the type-I dofs of the faces containing E; unsplit
-        (Eq. 5.10) also the type-I dofs of the cells containing E."""
+        (Eq. 5.10) also the type-I dofs of the cells containing E.
+        H(div) (Eq. 5.16, DESIGN.md R-D3): X^2_Gamma restricted to
+        the edge star = every free dof of the faces containing E; unsplit
+        (PAFW1(X^2)) also every dof of the cells containing E."""
         _, _, e_faces = self._incidence()
         num = self.num
+        if self.space == "hdiv":
+            idx = []
+            for f in e_faces[e]:
+                base = num.offsets[2] + f * num.per[2]
+                idx.extend(range(base, base + num.per[2]))
+            if self.decomposition == "unsplit":
+                for c in self._cells_of(list(self.topo.edges[e])):
+                    base = num.offsets[3] + c * num.per[3]
+                    idx.extend(range(base, base + num.per[3]))
+            idx = np.array(sorted(idx), dtype=np.int64)
+            return "dof", idx[self.free[idx]]
         nI_face = num.per[2] - (self.p - 1) * (self.p - 2) // 2
         idx = [num.offsets[1] + e * num.per[1]]       # Whitney dof of E
         for f in e_faces[e]:
@@ -142,11 +158,11 @@ class Oracle:
         if self._patches is not None:
             return self._patches
         out = []
-        for v in range(self.topo.nv):
+        for v in range(self.topo.nv if self.space != "hdiv" else 0):  # H(div): edge stars only (Eq. 5.16)
             kind, idx = self.vertex_patch(v)
             if len(idx):
                 out.append((kind, idx))
-        if self.space == "hcurl":
+        if self.space in ("hcurl", "hdiv"):
             for e in range(self.topo.ne):
                 kind, idx = self.edge_patch(e)
                 if len(idx):

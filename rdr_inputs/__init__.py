@@ -24,6 +24,7 @@ import numpy as np
 
 HGRAD = 0
 HCURL = 1
+HDIV = 2
 
 # Freudenthal/Kuhn split of a cube into 6 tets: local corners
 # v0..v7 with bit0=+x, bit1=+y, bit2=+z.
@@ -122,6 +123,9 @@ def make_config(cfg: int, p: int | None = None, seed: int = 0, n: int | None = N
     3: H(grad) p=10, 16^3, perturbed, alpha=beta=1, full Dirichlet.
     4: H(curl) Ned1_6, 12^3, unperturbed, alpha=beta=1, full tangential Dirichlet.
     5: H(grad) p in 1..12 (argument p), 8^3, perturbed, alpha=beta=1, full Dirichlet.
+    6: H(div) RT_6, 12^3, unperturbed, alpha=beta=1, full normal Dirichlet -- NOT a
+       BASELINE.json config: the SURVEY NEXT-2 workload, config 4's mesh and degree
+       with the 2-form space (PAFW1(X2_Gamma) + J(X2_I)).
     0: custom small case (all of n, p, space, perturb, bc, coeffs given).
     Any keyword overrides the config's default (used for small parity meshes).
     """
@@ -131,6 +135,7 @@ def make_config(cfg: int, p: int | None = None, seed: int = 0, n: int | None = N
         3: dict(space=HGRAD, p=10, n=16, perturb=True, bc="all", coeffs="one"),
         4: dict(space=HCURL, p=6, n=12, perturb=False, bc="all", coeffs="one"),
         5: dict(space=HGRAD, p=6, n=8, perturb=True, bc="all", coeffs="one"),
+        6: dict(space=HDIV, p=6, n=12, perturb=False, bc="all", coeffs="one"),
         0: dict(space=HGRAD, p=2, n=2, perturb=False, bc="all", coeffs="one"),
     }
     d = dict(table[cfg])

@@ -48,7 +48,24 @@ E_V, F_V, C_V = 14, 36, 24      # interior vertex star
 F_E = C_E = 6                   # largest interior edge star: 6 faces, 6 cells (Table 1 caption P:2009-2010)
 
 
+def rt(p):     # dofs per face / cell, RT_p (Eq. 3.18): face p(p+1)/2, cell p(p+1)(p-1)/2
+    return p * (p + 1) // 2, (p + 1) * p * (p - 1) // 2
+
+
+def counted_hdiv(label, p):
+    """(vertex, edge, face) patch dims of Table 2's decompositions."""
+    nf2, nc2 = rt(p)
+    (ne1, _, _), (nf1, fI1, _), (nc1, _, _) = ned(p)
+    return {"hdiv_pafw0_full": (F_V * nf2 + C_V * nc2, None, None),
+            "hdiv_pafw0_interface_J": (F_V * nf2, None, None),
+            "hdiv_ph_full": (None, ne1 + F_E * nf1 + C_E * nc1, nf2 + 2 * nc2),
+            "hdiv_ph_typeI_interface_J": (None, 1 + F_E * fI1, None),
+            "hdiv_pafw1_interface_J": (None, F_E * nf2, None)}[label]
+
+
 def counted(label, p):
+    if label.startswith("hdiv_"):
+        return counted_hdiv(label, p)[:2]
     v, e, f, c = cg(p)
     (ne, _, _), (nf, fI, _), (nc, cI, _) = ned(p)
     vert = {"hgrad_full_vertex": v + E_V * e + F_V * f + C_V * c,
@@ -80,11 +97,14 @@ def test_star_counts_on_freudenthal_mesh():
 
 @pytest.mark.parametrize("rec", _entries(), ids=lambda r: f"{r[0]}-p{r[2]}")
 def test_printed_dimension_by_counting(rec):
-    label, space, p, vdim, edim = rec[0], rec[1], int(rec[2]), int(rec[3]), rec[4]
+    label, space, p, vdim, edim = rec[0], rec[1], int(rec[2]), rec[3], rec[4]
     v, e = counted(label, p)
-    assert v == vdim
+    if vdim != "-":
+        assert v == int(vdim)
     if edim != "-":
         assert e == int(edim)
+    if len(rec) > 5:
+        assert counted_hdiv(label, p)[2] == int(rec[5])
 
 
 @pytest.mark.parametrize("p", [4, 10])
@@ -113,3 +133,22 @@ def test_unsplit_rows_by_oracle_patches(p):
     r = recs[("ph_typeI", p)]
     assert max(len(i) for k, i in ps if k == "pot") == int(r[3])
     assert max(len(i) for k, i in ps if k == "dof") == int(r[4])
+
+
+@pytest.mark.parametrize("p", [4, 10])
+def test_hdiv_rows_by_oracle_patches(p):
+    """the split H(div) decomposition PAFW1(X2_Gamma) + J(X2_I)
+    (Eq. 5.16) has edge patches of Table 2's size (60 / 330), from the oracle's
+    actual patch sets; the vertex-star interface/full counts of Table 2's
+    PAFW0 rows (360 / 1980, 1080 / 13860) from its numbering."""
+    recs = {(r[0], int(r[2])): r for r in _entries()}
+    c = make_config(0, n=3, p=p, space=HGRAD, bc="none")
+    o = Oracle(c.vertices, c.tets, p, "hdiv", c.alpha, c.beta, c.mask, assemble=False)
+    ps = o.patch_sets()
+    assert all(k == "dof" for k, _ in ps) and len(ps) == o.topo.ne
+    assert max(len(i) for _, i in ps) == int(recs[("hdiv_pafw1_interface_J", p)][4])
+    num, t = o.num, o.topo
+    star_faces = max(int(np.sum(np.any(t.faces == v, axis=1))) for v in range(t.nv))
+    star_cells = max(int(np.sum(np.any(t.cells == v, axis=1))) for v in range(t.nv))
+    assert star_faces * num.per[2] == int(recs[("hdiv_pafw0_interface_J", p)][3])
+    assert star_faces * num.per[2] + star_cells * num.per[3] == int(recs[("hdiv_pafw0_full", p)][3])

@@ -2,11 +2,12 @@
  *
  * Problem (Eq. 2.9): find u in X^k_{p,D} with
  *     a^k(u, v) = (u, beta v) + (d^k u, alpha d^k v) = F(v)  for all v,
- * k = 0 (H(grad), CG_p) or k = 1 (H(curl), first-kind Nedelec Ned1_p,
- * P:288-299 Eq. 2.4), piecewise-constant alpha > 0, beta >= 0 per cell, on an
+ * k = 0 (H(grad), CG_p), k = 1 (H(curl), first-kind Nedelec Ned1_p,
+ * P:288-299 Eq. 2.4) or k = 2 (H(div), Raviart-Thomas RT_p),
+ * piecewise-constant alpha > 0, beta >= 0 per cell, on an
  * affine tetrahedral mesh, in the paper's basis (dofs = moments against
- * doubly-orthogonal bubble eigenbases, Eq. 3.8-3.10, §3.4.1-3.4.2
- * P:725-807; basis = Ciarlet dual).
+ * doubly-orthogonal bubble eigenbases, Eq. 3.8-3.10, §3.4.1-3.4.3
+ * P:725-858; basis = Ciarlet dual).
  *
  * Vectors: full length n_total in the canonical global numbering of DESIGN.md
  * R-A9 (dimension-major: vertices by id, edges sorted lexicographically,
@@ -38,7 +39,11 @@ extern "C" {
 
 typedef struct rdr_handle rdr_handle;
 
-enum { RDR_HGRAD = 0, RDR_HCURL = 1 };
+/* Spaces: H(grad) CG_p (1 <= p <= 12), H(curl) Ned1_p (1 <= p <= 10) and
+ * H(div) RT_p (1 <= p <= 10, Eq. 3.17-3.18, Piola
+ * pullback of 2-forms, edge-star patches PAFW1(X2_Gamma) + J(X2_I), Eq. 5.16
+ * P:2156-2164; unsplit: PAFW1(X2)). */
+enum { RDR_HGRAD = 0, RDR_HCURL = 1, RDR_HDIV = 2 };
 
 /* Space decomposition of the preconditioner (both one-level additive, unit
  * weights, exact local solvers; DESIGN.md R-A13..A15):
@@ -116,7 +121,7 @@ struct rdr_info {
  *   alpha, beta [nt] float64; dirichlet_mask [nt][4] uint8: bit (t,i) = 1 iff
  *   the face opposite INPUT vertex i of tet t lies on Gamma_D.
  *   Each of these five pointers may be host or device memory (detected).
- *   1 <= p <= 12 for H(grad), 1 <= p <= 10 for H(curl).
+ *   1 <= p <= 12 for H(grad), 1 <= p <= 10 for H(curl) and H(div).
  *   Reference element: DESIGN.md readings R-A1..A8, R-A24 (extended precision,
  *   P:595-619). Patches: R-A13. Inverses stored per patch (R-A15). */
 int rdr_setup(rdr_handle** h, const double* vertices, int64_t nv, const int32_t* tets, int64_t nt,
@@ -190,7 +195,8 @@ int rdr_reference_matrices(int space, int p, double* out, int32_t* n_loc, int32_
  * setup uses for the patch inverses (R-A15); RDR_ENOTSPD on a non-positive
  * Cholesky pivot. */
 int rdr_spd_inverse(double* a, int32_t n);
-/* Bubble eigenvalues lambda_j (Eq. 3.8) on the canonical l-simplex: kind 0 = CG, 1 = Ned1. */
+/* Bubble eigenvalues lambda_j (Eq. 3.8) on the canonical l-simplex: kind 0 = CG, 1 = Ned1,
+ * 2 = RT (l = 3 only, Eq. 3.17). */
 int rdr_bubble_eigenvalues(int kind, int l, int p, double* out, int32_t* n);
 
 #ifdef __cplusplus

@@ -604,8 +604,8 @@ int rdr_setup_ex(rdr_handle** hp, const double* vertices, int64_t nv, const int3
   if (!hp) return RDR_EINVAL;
   *hp = nullptr;
   if (!vertices || !tets || !alpha || !beta || !dirichlet_mask || nv < 4 || nt < 1) return RDR_EINVAL;
-  if (space != RDR_HGRAD && space != RDR_HCURL) return RDR_EINVAL;
-  if (p < 1 || (space == RDR_HGRAD && p > 12) || (space == RDR_HCURL && p > 10)) return RDR_EINVAL;
+  if (space != RDR_HGRAD && space != RDR_HCURL && space != RDR_HDIV) return RDR_EINVAL;
+  if (p < 1 || (space == RDR_HGRAD && p > 12) || (space != RDR_HGRAD && p > 10)) return RDR_EINVAL;
   if (nv > 0x7fffffff || nt > 0x7fffffff) return RDR_EINVAL;
   const int dec = opt ? opt->decomposition : RDR_SPLIT;
   if (dec != RDR_SPLIT && dec != RDR_UNSPLIT) return RDR_EINVAL;
@@ -949,8 +949,8 @@ const char* rdr_strerror(int code) {
 
 int rdr_reference_matrices(int space, int p, double* out, int32_t* n_loc, int32_t* n_mat) {
   if (!n_loc || !n_mat) return RDR_EINVAL;
-  if (space != RDR_HGRAD && space != RDR_HCURL) return RDR_EINVAL;
-  if (p < 1 || (space == RDR_HGRAD && p > 12) || (space == RDR_HCURL && p > 10)) return RDR_EINVAL;
+  if (space != RDR_HGRAD && space != RDR_HCURL && space != RDR_HDIV) return RDR_EINVAL;
+  if (p < 1 || (space == RDR_HGRAD && p > 12) || (space != RDR_HGRAD && p > 10)) return RDR_EINVAL;
   try {
     const RefElement& el = reference_element(space, p);
     *n_loc = el.n;
@@ -970,7 +970,8 @@ int rdr_spd_inverse(double* a, int32_t n) {
 }
 
 int rdr_bubble_eigenvalues(int kind, int l, int p, double* out, int32_t* n) {
-  if (!n || (kind != 0 && kind != 1) || l < 1 || l > 3 || p < 1 || p > 12 || (kind == 1 && l < 2)) return RDR_EINVAL;
+  if (!n || kind < 0 || kind > 2 || l < 1 || l > 3 || p < 1 || p > 12 || (kind == 1 && l < 2) || (kind == 2 && l != 3))
+    return RDR_EINVAL;
   try {
     std::vector<double> v = bubble_eigenvalues(kind, l, p);
     *n = (int32_t)v.size();

@@ -434,6 +434,87 @@ void eval1(const Mat& F, int r, const Geo& S, int q, const ld* bary, ld* out) {
   }
 }
 
+// ------------------------------------------------------------------ 2-forms (RT_p)
+struct W2Elem {
+  std::array<int, 4> a;
+  int i, j, k;
+};
+
+// rows: (weight) lambda^alpha (lambda_i g_j x g_k - lambda_j g_i x g_k + lambda_k g_i x g_j)
+// on T-hat, |alpha| = q -> 2-form deg q+1 in the 6-pair frame
+Mat whitney2_rows(const std::vector<W2Elem>& el, int q, bool scaled) {
+  const MI& B = mi(4, q + 1);
+  Mat out((int)el.size(), B.size() * 6);
+  for (int r = 0; r < (int)el.size(); ++r) {
+    const ld w = scaled ? (ld)multinom(el[r].a, 4) : 1.0L;
+    const int term[3][3] = {{el[r].i, el[r].j, el[r].k}, {el[r].j, el[r].i, el[r].k}, {el[r].k, el[r].i, el[r].j}};
+    const ld sgn[3] = {1, -1, 1};
+    for (int t = 0; t < 3; ++t) {
+      int a[4] = {el[r].a[0], el[r].a[1], el[r].a[2], el[r].a[3]};
+      a[term[t][0]] += 1;
+      out(r, B.find(a) * 6 + pair_index(4, term[t][1], term[t][2])) += sgn[t] * w;
+    }
+  }
+  return out;
+}
+
+// 2-form deg q on T-hat -> scalar deg q-1:
+// div(lambda^g g_a x g_b) = sum_k g_k lambda^(g - e_k) g_k . (g_a x g_b)
+Mat apply_div(const Geo& T, const Mat& F, int q) {
+  const MI& A = mi(4, q);
+  const MI& B = mi(4, q - 1);
+  Mat out(F.r, B.size());
+  for (int g = 0; g < A.size(); ++g)
+    for (int pr = 0; pr < 6; ++pr)
+      for (int k = 0; k < 4; ++k) {
+        if (A.a[g][k] == 0 || k == T.pa[pr] || k == T.pb[pr]) continue;
+        int b[4] = {A.a[g][0], A.a[g][1], A.a[g][2], A.a[g][3]};
+        b[k] -= 1;
+        ld tp = 0;
+        for (int d = 0; d < 3; ++d) tp += T.g[k][d] * T.cr[pr][d];
+        const ld f = A.a[g][k] * tp;
+        const int col = B.find(b), src = g * 6 + pr;
+        for (int i = 0; i < F.r; ++i) out(i, col) += f * F(i, src);
+      }
+  return out;
+}
+
+// trace of 2-forms on T-hat onto the face s (sorted local vertices): the
+// monomials supported on s and the pairs inside s, in the face's 3-pair frame
+Mat trace2(const Mat& F, int q, const int* s) {
+  const MI& P = mi(4, q);
+  const MI& C = mi(3, q);
+  Mat out(F.r, C.size() * 3);
+  for (int g = 0; g < P.size(); ++g) {
+    int cg[4] = {0, 0, 0, 0}, used = 0;
+    for (int t = 0; t < 3; ++t) {
+      cg[t] = P.a[g][s[t]];
+      used += cg[t];
+    }
+    if (used != q) continue;  // some weight on the vertex off s
+    const int ci = C.find(cg);
+    for (int ta = 0; ta < 3; ++ta)
+      for (int tb = ta + 1; tb < 3; ++tb) {
+        const int src = g * 6 + pair_index(4, s[ta], s[tb]), dst = ci * 3 + pair_index(3, ta, tb);
+        for (int i = 0; i < F.r; ++i) out(i, dst) += F(i, src);
+      }
+  }
+  return out;
+}
+
+// 3D vector proxy of the 2-form row r at a barycentric point
+void eval2(const Mat& F, int r, const Geo& T, int q, const ld* bary, ld* out) {
+  const MI& A = mi(4, q);
+  for (int d = 0; d < 3; ++d) out[d] = 0;
+  for (int g = 0; g < A.size(); ++g) {
+    const ld mv = monomial(A.a[g], 4, bary);
+    for (int pr = 0; pr < 6; ++pr) {
+      const ld c = F(r, g * 6 + pr) * mv;
+      for (int d = 0; d < 3; ++d) out[d] += c * T.cr[pr][d];
+    }
+  }
+}
+
 // ------------------------------------------------------------------ dense solvers
 // cyclic Jacobi: A = V diag(w) V^T, w ascending
 void jacobi_eig(Mat A, std::vector<ld>& w, Mat& V) {
@@ -614,7 +695,8 @@ void probe_direction(int dim, int i, ld* u) {
 }
 
 // R-A6: canonicalize clusters of equal eigenvalues and fix signs
-void canonicalize(const Geo& S, bool vec, int q, Eig& E) {
+// kind 0: 0-forms, 1: 1-forms, 2: 2-forms on T-hat (vector probe of the proxy)
+void canonicalize(const Geo& S, int kind, int q, Eig& E) {
   const int n = (int)E.mu.size();
   int j = 0;
   while (j < n) {
@@ -629,11 +711,14 @@ void canonicalize(const Geo& S, bool vec, int q, Eig& E) {
         ld bary[4];
         probe_point(S.l, s + 1 + i, bary);
         for (int k = 0; k < c; ++k) {
-          if (!vec) {
+          if (kind == 0) {
             P(i, k) = eval0(E.F, j + k, S, q, bary);
           } else {
             ld v[3], u[3];
-            eval1(E.F, j + k, S, q, bary, v);
+            if (kind == 1)
+              eval1(E.F, j + k, S, q, bary, v);
+            else
+              eval2(E.F, j + k, S, q, bary, v);
             probe_direction(S.l, s + 1 + i, u);
             ld d = 0;
             for (int t = 0; t < S.l; ++t) d += v[t] * u[t];
@@ -684,16 +769,20 @@ void canonicalize(const Geo& S, bool vec, int q, Eig& E) {
 }
 
 // Eq. 3.9 on span(rows of Fspan), kernel dropped, renormalised to Eq. 3.8
-Eig bubble_eigen(const Geo& S, bool vec, const Mat& Fspan, int q, int dim_bubble, int n_kernel) {
+Eig bubble_eigen(const Geo& S, int kind, const Mat& Fspan, int q, int dim_bubble, int n_kernel) {
   Mat M, K;
-  if (!vec) {
+  if (kind == 0) {
     M = gram0(S, Fspan, q, Fspan, q);
     Mat dF = apply_grad(Fspan, S.nv, q);
     K = gram1(S, dF, q - 1, dF, q - 1);
-  } else {
+  } else if (kind == 1) {
     M = gram1(S, Fspan, q, Fspan, q);
     Mat dF = apply_curl(Fspan, S.nv, q);
     K = gram2(S, dF, q - 1, dF, q - 1);
+  } else {  // 2-forms on T-hat, d = div (Eq. 3.17)
+    M = gram2(S, Fspan, q, Fspan, q);
+    Mat dF = apply_div(S, Fspan, q);
+    K = gram0(S, dF, q - 1, dF, q - 1);
   }
   Mat L;
   std::vector<int> sel = pivoted_cholesky(M, 1e-14L, L);
@@ -731,7 +820,7 @@ Eig bubble_eigen(const Geo& S, bool vec, const Mat& Fspan, int q, int dim_bubble
       for (int col = 0; col < Fspan.c; ++col) out[col] += c * fr[col];
     }
   }
-  canonicalize(S, vec, q, E);
+  canonicalize(S, kind, q, E);
   return E;
 }
 
@@ -764,7 +853,7 @@ const Eig& cg_bubbles(int l, int p) {
   if (dim > 0) {
     Mat F((int)rows.size(), A.size());
     for (int r = 0; r < (int)rows.size(); ++r) F(r, rows[r]) = (ld)multinom(A.a[rows[r]], l + 1);
-    *E = bubble_eigen(S, false, F, p, dim, 0);
+    *E = bubble_eigen(S, 0, F, p, dim, 0);
   } else {
     E->F = Mat(0, A.size());
   }
@@ -797,13 +886,46 @@ const Eig& ned_bubbles(int l, int p) {
           if (cov) el.push_back({A.a[g], i, j});
         }
     Mat F = whitney_rows(el, nv, p - 1, true);
-    *E = bubble_eigen(S, true, F, p, dim, nk);
+    *E = bubble_eigen(S, 1, F, p, dim, nk);
   } else {
     E->F = Mat(0, mi(nv, p).size() * nv);
   }
   std::lock_guard<std::mutex> lk(g_eig_mutex);
   const Eig& ref = *E;
   g_eig[{1, l, p}] = std::move(E);
+  return ref;
+}
+
+// RT_p cell bubbles (Eq. 3.17): span {lambda^alpha w_ijk : supp(alpha) U {i,j,k} =
+// all four vertices}, dim p(p+1)(p-1)/2, kernel = the divergence-free bubbles
+const Eig& rt_bubbles(int p) {
+  {
+    std::lock_guard<std::mutex> lk(g_eig_mutex);
+    auto it = g_eig.find({2, 3, p});
+    if (it != g_eig.end()) return *it->second;
+  }
+  Geo T = make_geo(3);
+  const int dim = p * (p + 1) * (p - 1) / 2, nI = p * (p + 1) * (p + 2) / 6 - 1;
+  auto E = std::make_unique<Eig>();
+  if (dim > 0 && nI > 0) {
+    std::vector<W2Elem> el;
+    const MI& A = mi(4, p - 1);
+    const int faces[4][3] = {{0, 1, 2}, {0, 1, 3}, {0, 2, 3}, {1, 2, 3}};
+    for (const auto& f : faces)
+      for (int g = 0; g < A.size(); ++g) {
+        bool cov = true;
+        for (int k = 0; k < 4; ++k)
+          if (k != f[0] && k != f[1] && k != f[2] && A.a[g][k] == 0) cov = false;
+        if (cov) el.push_back({A.a[g], f[0], f[1], f[2]});
+      }
+    Mat F = whitney2_rows(el, p - 1, true);
+    *E = bubble_eigen(T, 2, F, p, dim, dim - nI);
+  } else {
+    E->F = Mat(0, mi(4, p).size() * 6);
+  }
+  std::lock_guard<std::mutex> lk(g_eig_mutex);
+  const Eig& ref = *E;
+  g_eig[{2, 3, p}] = std::move(E);
   return ref;
 }
 
@@ -986,6 +1108,91 @@ std::unique_ptr<RefElement> build_ned(int p) {
   return el;
 }
 
+// RT_p with the dofs of Eq. 3.18 per entity:
+// face: Whitney (1, n.v)_F then type-II (curl_F Psi_{F,j}, n.v)_F; cell: type-I
+// (div Phi_{C,j}, div v) then type-II (curl Psi_{C,j}, v), the Psi being the
+// Ned1_p bubble eigenbases (DESIGN.md R-D1). Reference matrices: the 2-form
+// proxy mass M^{ab} (6 symmetric combinations) and the div-div matrix.
+std::unique_ptr<RefElement> build_rt(int p) {
+  auto el = std::make_unique<RefElement>();
+  el->space = 2;
+  el->p = p;
+  Geo T = make_geo(3), Fc = make_geo(2);
+  std::vector<W2Elem> span;
+  const MI& Am = mi(4, p - 1);
+  const int faces[4][3] = {{0, 1, 2}, {0, 1, 3}, {0, 2, 3}, {1, 2, 3}};
+  for (const auto& f : faces)
+    for (int g = 0; g < Am.size(); ++g) {
+      bool ok = true;
+      for (int k = 0; k < f[0]; ++k) ok &= Am.a[g][k] == 0;
+      if (ok) span.push_back({Am.a[g], f[0], f[1], f[2]});
+    }
+  const int n = (int)span.size();
+  if (n != p * (p + 1) * (p + 3) / 2) throw std::runtime_error("RT span dimension mismatch");
+  el->n = n;
+  Mat Span = whitney2_rows(span, p - 1, true);  // 2-forms of degree p
+  Mat V(n, n);
+  int row = 0;
+  Mat unit(1, 3);  // the constant face 2-form with proxy 1 (orientation of the sorted vertices)
+  unit(0, pair_index(3, 0, 1)) = 1 / Fc.cr[pair_index(3, 0, 1)][0];
+  const Eig& PsiF = ned_bubbles(2, p);
+  Mat cPsiF;
+  if (PsiF.F.r > 0) cPsiF = apply_curl(PsiF.F, 3, p);
+  for (int e = 0; e < 4; ++e) {
+    Mat tr = trace2(Span, p, faces[e]);
+    append_rows(V, row, gram2(Fc, unit, 0, tr, p));
+    el->dofs.push_back({2, e, 0, 2});
+    if (cPsiF.r > 0) {
+      Mat Vs = gram2(Fc, cPsiF, p - 1, tr, p);
+      append_rows(V, row, Vs);
+      for (int j = 0; j < Vs.r; ++j) el->dofs.push_back({2, e, j, 1});
+    }
+  }
+  Mat divSpan = apply_div(T, Span, p);
+  const Eig& Phi = rt_bubbles(p);
+  if (Phi.F.r > 0) {
+    Mat Vs = gram0(T, apply_div(T, Phi.F, p), p - 1, divSpan, p - 1);
+    append_rows(V, row, Vs);
+    for (int j = 0; j < Vs.r; ++j) el->dofs.push_back({3, 0, j, 0});
+  }
+  const Eig& PsiC = ned_bubbles(3, p);
+  if (PsiC.F.r > 0) {
+    Mat Vs = gram2(T, apply_curl(PsiC.F, 4, p), p - 1, Span, p);
+    append_rows(V, row, Vs);
+    for (int j = 0; j < Vs.r; ++j) el->dofs.push_back({3, 0, j, 1});
+  }
+  if (row != n) throw std::runtime_error("RT dof count mismatch");
+  Mat C = inverse(V);
+  Mat Phi2 = mul(transpose(C), Span);  // rows = phi_j as 2-forms of degree p
+  const int Np = mi(4, p).size();
+  std::vector<Mat> P(3, Mat(n, Np));
+  for (int a = 0; a < 3; ++a)
+    for (int i = 0; i < n; ++i)
+      for (int g = 0; g < Np; ++g) {
+        ld s = 0;
+        for (int k = 0; k < 6; ++k) s += Phi2(i, g * 6 + k) * T.cr[k][a];
+        P[a](i, g) = s;
+      }
+  Mat D = apply_div(T, Phi2, p);
+  Mat Mm[3][3];
+  for (int a = 0; a < 3; ++a)
+    for (int b = a; b < 3; ++b) Mm[a][b] = gram0(T, P[a], p, P[b], p);
+  Mat Kd = gram0(T, D, p - 1, D, p - 1);
+  el->n_mat = 7;
+  el->R.assign((size_t)7 * n * n, 0.0);
+  auto put = [&](int s, const Mat& X, bool sym) {
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < n; ++j)
+        el->R[((size_t)s * n + i) * n + j] = (double)(sym ? X(i, j) + X(j, i) : X(i, j));
+  };
+  const int ab[3][2] = {{0, 1}, {0, 2}, {1, 2}};
+  for (int a = 0; a < 3; ++a) put(a, Mm[a][a], false);
+  for (int k = 0; k < 3; ++k) put(3 + k, Mm[ab[k][0]][ab[k][1]], true);
+  put(6, Kd, false);
+  for (ld l : Phi.lam) el->lam_cell.push_back((double)l);
+  return el;
+}
+
 std::mutex g_el_mutex;
 std::map<std::pair<int, int>, std::unique_ptr<RefElement>> g_el;
 
@@ -1106,7 +1313,7 @@ const RefElement& reference_element(int space, int p) {
   if (it != g_el.end()) return *it->second;
   auto el = load_cached(space, p);
   if (!el) {
-    el = space == 0 ? build_cg(p) : build_ned(p);
+    el = space == 0 ? build_cg(p) : space == 1 ? build_ned(p) : build_rt(p);
     store_cached(*el);
   }
   const RefElement& ref = *el;
@@ -1115,7 +1322,8 @@ const RefElement& reference_element(int space, int p) {
 }
 
 std::vector<double> bubble_eigenvalues(int kind, int l, int p) {
-  const Eig& E = kind == 0 ? cg_bubbles(l, p) : ned_bubbles(l, p);
+  if (kind == 2 && l != 3) throw std::runtime_error("RT bubbles live on the cell");
+  const Eig& E = kind == 0 ? cg_bubbles(l, p) : kind == 1 ? ned_bubbles(l, p) : rt_bubbles(p);
   std::vector<double> out;
   for (ld v : E.lam) out.push_back((double)v);
   return out;

@@ -140,11 +140,16 @@ void build_numbering(const Mesh& m, const RefElement& el, Numbering& num) {
     num.per[1] = p - 1;
     num.per[2] = (int64_t)(p - 1) * (p - 2) / 2;
     num.per[3] = (int64_t)(p - 1) * (p - 2) * (p - 3) / 6;
-  } else {
+  } else if (el.space == 1) {
     num.per[0] = 0;
     num.per[1] = p;
     num.per[2] = (int64_t)p * (p - 1);
     num.per[3] = (int64_t)p * (p - 1) * (p - 2) / 2;
+  } else {  // RT_p (Eq. 3.18): dim P_{p-1}(F) per face, the bubbles per cell
+    num.per[0] = 0;
+    num.per[1] = 0;
+    num.per[2] = (int64_t)p * (p + 1) / 2;
+    num.per[3] = (int64_t)(p + 1) * p * (p - 1) / 2;
   }
   const int64_t cnt[4] = {m.nv * num.per[0], m.ne * num.per[1], m.nf * num.per[2], m.nt * num.per[3]};
   num.off[0] = 0;
@@ -170,7 +175,10 @@ void build_numbering(const Mesh& m, const RefElement& el, Numbering& num) {
         pos = el.space == 0 ? d.j : (d.type == 2 ? 0 : 1 + d.j);
       } else if (d.dim == 2) {
         ent = m.cell_faces[4 * t + d.ent];
-        pos = (el.space == 0 || d.type == 0) ? d.j : nI_face + d.j;
+        if (el.space == 2)  // face Whitney, then type-II
+          pos = d.type == 2 ? 0 : 1 + d.j;
+        else
+          pos = (el.space == 0 || d.type == 0) ? d.j : nI_face + d.j;
       } else {
         ent = t;
         pos = (el.space == 0 || d.type == 0) ? d.j : nI_cell + d.j;
@@ -236,9 +244,10 @@ static void inv3(const double A[3][3], double B[3][3], double& det) {
 
 // H(grad): c = (beta|J|, alpha G_xx, G_yy, G_zz, G_xy, G_xz, G_yz), G = |J| (J^T J)^{-1}
 // H(curl): c = (beta GM_.. x6, alpha GK_.. x6), GM = |J| (J^T J)^{-1}, GK = J^T J / |J|
+// H(div): c = (beta GK_.. x6, alpha / |J|) (phi = J phi-hat / det J, div phi = div-hat / det J)
 // (Eq. 2.7: grad phi = J^{-T} grad-hat, phi = J^{-T} phi-hat, curl phi = J curl-hat / det J)
 void cell_coefficients(const Mesh& m, int space, const double* alpha, const double* beta, std::vector<double>& c) {
-  const int nm = space == 0 ? 7 : 12;
+  const int nm = space == 1 ? 12 : 7;
   c.assign((size_t)m.nt * nm, 0.0);
 #pragma omp parallel for schedule(static)
   for (int64_t t = 0; t < m.nt; ++t) {
@@ -259,9 +268,12 @@ void cell_coefficients(const Mesh& m, int space, const double* alpha, const doub
     if (space == 0) {
       ct[0] = beta[t] * aj;
       for (int k = 0; k < 6; ++k) ct[1 + k] = alpha[t] * aj * Inv[ii[k][0]][ii[k][1]];
-    } else {
+    } else if (space == 1) {
       for (int k = 0; k < 6; ++k) ct[k] = beta[t] * aj * Inv[ii[k][0]][ii[k][1]];
       for (int k = 0; k < 6; ++k) ct[6 + k] = alpha[t] * JtJ[ii[k][0]][ii[k][1]] / aj;
+    } else {
+      for (int k = 0; k < 6; ++k) ct[k] = beta[t] * JtJ[ii[k][0]][ii[k][1]] / aj;
+      ct[6] = alpha[t] / aj;
     }
   }
 }
@@ -305,16 +317,16 @@ void pack_patch_tiles(const double* W2, int n, double* out, PatchLayout layout) 
 
 int build_coarse(const Mesh& m, const Numbering& num, const RefElement& el, const std::vector<double>& coef,
                  std::vector<int32_t>& cidx, std::vector<double>& tiles) {
-  // W^k (Lemma 4.1): vertex dofs (H(grad)) / Whitney edge dofs (H(curl)), free ones
-  const int n = el.n, nm = el.n_mat;
+  // W^k (Lemma 4.1): vertex dofs (H(grad)) / Whitney edge dofs (H(curl)) /
+  // Whitney face dofs (H(div)), free ones
+  const int n = el.n, nm = el.n_mat, wdim = num.space == 0 ? 0 : num.space == 1 ? 1 : 2;
   std::vector<int> loc;
   for (int i = 0; i < n; ++i)
-    if ((num.space == 0 && el.dofs[i].dim == 0) || (num.space == 1 && el.dofs[i].dim == 1 && el.dofs[i].type == 2))
-      loc.push_back(i);
+    if (el.dofs[i].dim == wdim && (num.space == 0 || el.dofs[i].type == 2)) loc.push_back(i);
   std::vector<int32_t> pos(num.n_total, -1);
   cidx.clear();
-  const int64_t first = num.space == 0 ? num.off[0] : num.off[1];
-  const int64_t count = num.space == 0 ? m.nv : m.ne, stride = num.space == 0 ? 1 : num.per[1];
+  const int64_t first = num.off[wdim];
+  const int64_t count = wdim == 0 ? m.nv : wdim == 1 ? m.ne : m.nf, stride = num.per[wdim];
   for (int64_t k = 0; k < count; ++k) {
     const int64_t g = first + k * stride;
     if (!num.constrained[g]) {
@@ -429,7 +441,7 @@ int build_patches(const Mesh& m, const Numbering& num, const RefElement& el, con
       }
     }
   };
-  for (int64_t v = 0; v < m.nv; ++v) {  // vertex stars (own dofs for H(grad), CG potential for H(curl))
+  for (int64_t v = 0; v < (num.space == 2 ? 0 : m.nv); ++v) {  // vertex stars (own dofs for H(grad), CG potential for H(curl))
     PatchDef d;
     d.numbering = num.space == 0 ? 0 : 1;
     const Numbering& vn = num.space == 0 ? num : *cg_num;
@@ -442,7 +454,7 @@ int build_patches(const Mesh& m, const Numbering& num, const RefElement& el, con
     d.cells.assign(v_cells.ind.begin() + v_cells.ptr[v], v_cells.ind.begin() + v_cells.ptr[v + 1]);
     defs.push_back(std::move(d));
   }
-  if (num.space == 1) {  // edge stars of the type-I space
+  if (num.space >= 1) {  // edge stars: of the type-I space (H(curl)), of X^2_Gamma (H(div), Eq. 5.16)
     std::vector<int32_t> e_of_cell_edge = m.cell_edges;
     CSR e_cells = invert_incidence(m.nt, m.ne, 6, e_of_cell_edge);
     // face -> its 3 edges via the cells
@@ -456,12 +468,15 @@ int build_patches(const Mesh& m, const Numbering& num, const RefElement& el, con
             face_edges[3 * f + q++] = m.cell_edges[6 * t + local_edge(kFaces[lf][a], kFaces[lf][b])];
       }
     CSR e_faces = invert_incidence(m.nf, m.ne, 3, face_edges);
-    const int64_t nIf = num.per[2] - (int64_t)(num.p - 1) * (num.p - 2) / 2;
+    // H(curl): the face type-I dofs; H(div): every face dof (Whitney + type-II)
+    const int64_t nIf = num.space == 2 ? num.per[2] : num.per[2] - (int64_t)(num.p - 1) * (num.p - 2) / 2;
     for (int64_t e = 0; e < m.ne; ++e) {
       PatchDef d;
       d.numbering = 0;
-      int64_t w = num.off[1] + e * num.per[1];
-      if (!num.constrained[w]) d.idx.push_back((int32_t)w);
+      if (num.space == 1) {
+        int64_t w = num.off[1] + e * num.per[1];
+        if (!num.constrained[w]) d.idx.push_back((int32_t)w);
+      }
       for (int64_t k = e_faces.ptr[e]; k < e_faces.ptr[e + 1]; ++k) {
         int64_t f = e_faces.ind[k];
         for (int64_t j = 0; j < nIf; ++j) {
@@ -469,8 +484,9 @@ int build_patches(const Mesh& m, const Numbering& num, const RefElement& el, con
           if (!num.constrained[id]) d.idx.push_back((int32_t)id);
         }
       }
-      if (unsplit) {  // PH(., X1I) (Eq. 5.10): the type-I dofs of the cells containing E too
-        const int64_t nIc = num.per[3] - (int64_t)(num.p - 1) * (num.p - 2) * (num.p - 3) / 6;
+      if (unsplit) {  // PH(., X1I) (Eq. 5.10): the type-I dofs of the cells containing E too; PAFW1(X2): all
+        const int64_t nIc =
+            num.space == 2 ? num.per[3] : num.per[3] - (int64_t)(num.p - 1) * (num.p - 2) * (num.p - 3) / 6;
         for (int64_t k = e_cells.ptr[e]; k < e_cells.ptr[e + 1]; ++k)
           for (int64_t j = 0; j < nIc; ++j) d.idx.push_back((int32_t)(num.off[3] + e_cells.ind[k] * num.per[3] + j));
       }

@@ -11,7 +11,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "librdr.so")
 
-HGRAD, HCURL = 0, 1
+HGRAD, HCURL, HDIV = 0, 1, 2
 SPLIT, UNSPLIT = 0, 1
 ADDITIVE, HYBRID = 0, 1
 SETUP_DEVICE, SETUP_HOST = 0, 1

@@ -6,7 +6,7 @@ Calls only oracle/ and rdr_inputs/ (no CUDA path): these are the expected
 values of the +-1 iteration-count parity tests at sizes too large to run the
 oracle inside the GPU test session.
 
-    python scripts/oracle_golden.py 5:1-8 4 5:9-12 [3]
+    python scripts/oracle_golden.py 5:1-8 4 5:9-12 [3] [6]   (6: the H(div) NEXT-2 workload)
 """
 import json
 import os
@@ -30,7 +30,7 @@ def run(cfg, p):
     O.build_preconditioner(kappa=False)
     b = c.draw_vector(O.n_total)
     x, it, res = O.solve(b, rtol=1e-8)
-    return {"cfg": cfg, "p": c.p, "space": "hgrad" if c.space == 0 else "hcurl", "n_total": int(O.n_total),
+    return {"cfg": cfg, "p": c.p, "space": ("hgrad", "hcurl", "hdiv")[c.space], "n_total": int(O.n_total),
             "n_free": int(O.free.sum()), "iters": int(it), "true_rel_res": float(res),
             "oracle_seconds": round(time.time() - t0, 1)}
 

@@ -37,7 +37,7 @@ def one(spec, setup, dec):
     S.close()
     # n_m^3 per patch: the work of one inversion (host: ~n^3 flop Cholesky-based; device: ld^3 fma sweep)
     return {"config": spec, "decomposition": dec, "setup": "host" if setup else "device", "p": c.p,
-            "space": "hgrad" if c.space == 0 else "hcurl", "n_patches": info["n_patches"],
+            "space": ("hgrad", "hcurl", "hdiv")[c.space], "n_patches": info["n_patches"],
             "max_patch": info["max_patch"], "patch_GB": info["patch_bytes"] / 1e9, "setup_wall_s": wall,
             "setup_s": info["setup_seconds"], "refelem_s": info["refelem_seconds"],
             "patch_setup_s": info["patch_setup_seconds"], "patch_kernel_s": info["patch_kernel_seconds"],

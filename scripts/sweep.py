@@ -48,7 +48,7 @@ def measure(cfg, p, fp64_peak, hbm, solves=3, reps=20, dec="split", pre="additiv
     it = its[0]
     patch_bytes = info["bytes_precond"] - 24.0 * info["n_interior"]
     out = {
-        "config": cfg, "decomposition": dec, "preconditioner": pre, "space": "hgrad" if c.space == 0 else "hcurl",
+        "config": cfg, "decomposition": dec, "preconditioner": pre, "space": ("hgrad", "hcurl", "hdiv")[c.space],
         "p": c.p,
         "n_cells": info["n_cells"],
         "n_loc": info["n_loc"], "n_total": n, "n_free": info["n_free"], "n_patches": info["n_patches"],

@@ -40,7 +40,8 @@ def test_strerror_and_argument_errors():
     n, m = ctypes.c_int32(), ctypes.c_int32()
     assert lib.rdr_reference_matrices(0, 13, None, ctypes.byref(n), ctypes.byref(m)) == -1
     assert lib.rdr_reference_matrices(1, 11, None, ctypes.byref(n), ctypes.byref(m)) == -1
-    assert lib.rdr_reference_matrices(2, 3, None, ctypes.byref(n), ctypes.byref(m)) == -1
+    assert lib.rdr_reference_matrices(3, 3, None, ctypes.byref(n), ctypes.byref(m)) == -1
+    assert lib.rdr_reference_matrices(2, 11, None, ctypes.byref(n), ctypes.byref(m)) == -1
 
 
 @pytest.mark.parametrize("kind,l,p,lams", [
@@ -52,16 +53,26 @@ def test_library_eigenvalues_closed_forms(kind, l, p, lams):
     assert np.allclose(rdr.bubble_eigenvalues(kind, l, p), lams, rtol=1e-14)
 
 
-@pytest.mark.parametrize("space,p", [(0, 1), (0, 2), (0, 3), (0, 4), (0, 6), (1, 1), (1, 2), (1, 3), (1, 4)])
+@pytest.mark.parametrize("p", [2, 3, 4])
+def test_library_rt_bubble_eigenvalues_match_oracle(p):
+    from paper_2506_17406_b200 import rdr
+    from oracle.refelem import rt_bubbles
+    assert np.allclose(rdr.bubble_eigenvalues(2, 3, p), rt_bubbles(p).lam.astype(float), rtol=1e-14, atol=0)
+
+
+@pytest.mark.parametrize("space,p", [(0, 1), (0, 2), (0, 3), (0, 4), (0, 6), (1, 1), (1, 2), (1, 3), (1, 4),
+                                     (2, 1), (2, 2), (2, 3), (2, 4), (2, 5)])
 def test_library_reference_matrices_match_oracle(space, p):
     """The C++ reference element (pivoted Cholesky + Jacobi + Gauss-Jordan) and the
     oracle's (Gram eigendecomposition + Ogita-Aishima + GEPP) agree to rounding."""
     from paper_2506_17406_b200 import rdr
     from oracle.refelem import element, reference_matrices
     R = rdr.reference_matrices(space, p)
-    M, K = reference_matrices(element("hgrad" if space == 0 else "hcurl", p))
+    M, K = reference_matrices(element(("hgrad", "hcurl", "hdiv")[space], p))
     M, K = M.astype(float), K.astype(float)
-    if space == 0:
+    if space == 2:  # RT_p: 2-form proxy mass x6 + div-div (NEXT-2)
+        ref = [M[0, 0], M[1, 1], M[2, 2], M[0, 1] + M[1, 0], M[0, 2] + M[2, 0], M[1, 2] + M[2, 1], K]
+    elif space == 0:
         ref = [M, K[0, 0], K[1, 1], K[2, 2], K[0, 1] + K[1, 0], K[0, 2] + K[2, 0], K[1, 2] + K[2, 1]]
     else:
         ref = [M[0, 0], M[1, 1], M[2, 2], M[0, 1] + M[1, 0], M[0, 2] + M[2, 0], M[1, 2] + M[2, 1],

@@ -5,7 +5,7 @@ preconditioner applies within 1e-11 relative l2, PCG iteration counts within
 import numpy as np
 import pytest
 
-from rdr_inputs import make_config, HGRAD, HCURL
+from rdr_inputs import make_config, HGRAD, HCURL, HDIV
 
 pytestmark = pytest.mark.gpu
 
@@ -209,6 +209,16 @@ def _sample_rows(O, n_vertices=3, n_cells=4, seed=1):
     (vertex, edge, face dofs), the interior dofs of a few cells, constrained dofs."""
     rng = np.random.default_rng(seed)
     t = O.topo
+    if O.space == "hdiv":  # edge stars: the face dofs of a few interior edges, cell interiors, constrained
+        rows = []
+        interior_e = np.nonzero(~t.dir_edge)[0]
+        for e in rng.choice(interior_e, min(n_vertices, len(interior_e)), replace=False):
+            _, idx = O.edge_patch(int(e))
+            rows.extend(rng.choice(idx, min(12, len(idx)), replace=False))
+        for c in rng.choice(t.nt, n_cells, replace=False):
+            rows.extend(rng.choice(O.num.dofmap[c], 3, replace=False))
+        rows.extend(rng.choice(np.nonzero(O.num.constrained)[0], 3, replace=False) if O.num.constrained.any() else [])
+        return np.unique(np.asarray(rows, dtype=np.int64))
     interior_v = np.nonzero(~t.dir_vertex)[0]
     verts = rng.choice(interior_v, min(n_vertices, len(interior_v)), replace=False) if len(interior_v) else []
     rows = []
@@ -388,7 +398,8 @@ def test_fused_apply_ring_race_regression(torch_cuda):
 
 # ---------------------------------------------------------------- NEXT-1: hybrid Schwarz with the Whitney coarse space
 @pytest.mark.parametrize("space,p,bc,n", [(HGRAD, 1, "x0", 3), (HGRAD, 3, "all", 3), (HGRAD, 5, "x0", 2),
-                                          (HCURL, 2, "all", 2), (HCURL, 3, "x0", 3), (HCURL, 4, "all", 2)])
+                                          (HCURL, 2, "all", 2), (HCURL, 3, "x0", 3), (HCURL, 4, "all", 2),
+                                          (HDIV, 1, "x0", 2), (HDIV, 3, "x0", 2), (HDIV, 4, "all", 2)])
 def test_hybrid_preconditioner(torch_cuda, space, p, bc, n):
     """The paper's symmetric multiplicative hybrid: weights rho_m
     from the library's own CG-Lanczos equal the oracle's, P^-1 r at 1e-11, PCG
@@ -425,7 +436,7 @@ def test_tet_vertex_order_invariance(torch_cuda):
     every tet's vertices (and the mask columns with them) changes nothing."""
     from paper_2506_17406_b200 import rdr
     torch = torch_cuda
-    for space in (HGRAD, HCURL):
+    for space in (HGRAD, HCURL, HDIV):
         c = make_config(0, n=2, p=3, space=space, perturb=True, bc="x0", coeffs="loguniform")
         rng = np.random.default_rng(7)
         perm = np.array([rng.permutation(4) for _ in range(c.tets.shape[0])])
@@ -482,3 +493,47 @@ def test_device_patch_setup_errors(torch_cuda):
     with pytest.raises(rdr.RdrError) as e:
         rdr.Solver(c.vertices, c.tets, 2, HCURL, c.alpha, c.beta, c.mask, setup=2)
     assert e.value.code == -1
+
+
+
+# ---------------------------------------------------------------- H(div)
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 5, 6, 7, 8])
+@pytest.mark.parametrize("perturb,bc,coeffs", [(False, "all", "one"), (True, "x0", "loguniform")])
+def test_hdiv_small(torch_cuda, p, perturb, bc, coeffs):
+    """RT_p Riesz map (Piola 2-forms, 7 reference matrices) with the edge-star
+    PAFW1(X2_Gamma) + J(X2_I) preconditioner (Eq. 5.16): apply / P^-1 at 1e-11,
+    PCG iterations +-1 against the oracle."""
+    c, S, O = _pair(torch_cuda, 0, n=2, p=p, space=HDIV, perturb=perturb, bc=bc, coeffs=coeffs)
+    _check_apply_precond(torch_cuda, c, S, O)
+    _check_pcg(torch_cuda, c, S, O)
+
+
+def test_hdiv_p10(torch_cuda):
+    """RT_10 (n_loc 715) on the 6-tet cube; the oracle's x87 RT_10 construction
+    takes ~4 min of the host."""
+    c, S, O = _pair(torch_cuda, 0, n=1, p=10, space=HDIV, perturb=False, bc="x0")
+    _check_apply_precond(torch_cuda, c, S, O)
+    _check_pcg(torch_cuda, c, S, O)
+
+
+@pytest.mark.parametrize("p", [3, 5])
+def test_hdiv_unsplit(torch_cuda, p):
+    """PAFW1(X2): interiors inside the edge stars, no Jacobi (the hybrid with
+    the W^2 coarse space is in test_hybrid_preconditioner)."""
+    c, S, O = _pair(torch_cuda, 0, "unsplit", n=2, p=p, space=HDIV, perturb=True, bc="x0", coeffs="loguniform")
+    _check_apply_precond(torch_cuda, c, S, O)
+    _check_pcg(torch_cuda, c, S, O)
+
+
+def test_config6_hdiv_sampled(torch_cuda):
+    """The NEXT-2 workload: RT_6 on 12^3 x 6 (config 4's mesh and degree, the
+    2-form space), sampled rows; PCG iterations vs the oracle's (golden)."""
+    c, S, O = _sampled_pair(6)
+    b = c.draw_vector(O.n_total)
+    rows = _sample_rows(O)
+    _check_sampled(torch_cuda, c, S, O, rows)
+    try:
+        it = _golden_iters(6, 6)
+    except KeyError:
+        it = None
+    _check_sampled_pcg(torch_cuda, c, S, O, rows, b, it)

@@ -16,6 +16,7 @@
 // step packs -(-A^-1) into the stored tile layout (setup.hpp).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "patch_setup.hpp"
@@ -46,6 +47,35 @@ __device__ __forceinline__ void tile_product(const double* X, const double* Y, i
     for (int r = 0; r < 4; ++r)
 #pragma unroll
       for (int c = 0; c < 4; ++c) acc[r][c] = fma(xa[r], ya[c], acc[r][c]);
+  }
+}
+
+// Scalar sweep of the 64 pivots of the symmetric block S (stride kSs) in
+// place: S -> -S^-1. A non-positive pivot sets *status = flag (if still 0).
+__device__ void sweep_pivot_block(double* S, int tid, int32_t* status, int32_t flag) {
+  for (int p = 0; p < kB; ++p) {
+    const double d = S[p * kSs + p];
+    const double inv = 1.0 / d;
+    double nv[kB * kB / kThreads];
+#pragma unroll
+    for (int u = 0; u < kB * kB / kThreads; ++u) {
+      const int e = tid + u * kThreads, i = e / kB, j = e % kB;
+      const double a = S[i * kSs + j];
+      if (i == p && j == p)
+        nv[u] = -inv;
+      else if (i == p || j == p)
+        nv[u] = a * inv;
+      else
+        nv[u] = fma(-S[i * kSs + p] * inv, S[p * kSs + j], a);
+    }
+    if (tid == 0 && !(d > 0.0)) atomicCAS(status, 0, flag);
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < kB * kB / kThreads; ++u) {
+      const int e = tid + u * kThreads;
+      S[(e / kB) * kSs + e % kB] = nv[u];
+    }
+    __syncthreads();
   }
 }
 
@@ -106,30 +136,7 @@ __global__ void __launch_bounds__(kThreads, 2) patch_setup_kernel(DevPatchSetup 
         S[i * kSs + j] = i >= j ? A[(int64_t)(k0 + i) * ld + k0 + j] : A[(int64_t)(k0 + j) * ld + k0 + i];
       }
       __syncthreads();
-      for (int p = 0; p < kB; ++p) {
-        const double d = S[p * kSs + p];
-        const double inv = 1.0 / d;
-        double nv[kB * kB / kThreads];
-#pragma unroll
-        for (int u = 0; u < kB * kB / kThreads; ++u) {
-          const int e = tid + u * kThreads, i = e / kB, j = e % kB;
-          const double a = S[i * kSs + j];
-          if (i == p && j == p)
-            nv[u] = -inv;
-          else if (i == p || j == p)
-            nv[u] = a * inv;
-          else
-            nv[u] = fma(-S[i * kSs + p] * inv, S[p * kSs + j], a);
-        }
-        if (tid == 0 && !(d > 0.0)) atomicCAS(s.status, 0, (int32_t)(m + 1));
-        __syncthreads();
-#pragma unroll
-        for (int u = 0; u < kB * kB / kThreads; ++u) {
-          const int e = tid + u * kThreads;
-          S[(e / kB) * kSs + e % kB] = nv[u];
-        }
-        __syncthreads();
-      }
+      sweep_pivot_block(S, tid, s.status, (int32_t)(m + 1));
       if (nb == 1) {
         for (int e = tid; e < kB * kB; e += kThreads) {
           const int i = e / kB, j = e % kB;
@@ -259,7 +266,171 @@ __global__ void __launch_bounds__(kThreads, 2) patch_setup_kernel(DevPatchSetup 
   }
 }
 
+// ---- one large SPD matrix (the hybrid's Whitney coarse space): the same block
+// sweep with each phase spread over the grid, three launches per pivot block.
+// A: ld x ld row-major lower tiles, rows/columns >= n zero (identity pivots).
+
+// phase 1 (one CTA): S = -A_KK^-1 into Sg (64 x 64) and into A_KK
+__global__ void __launch_bounds__(kThreads) dense_pivot_kernel(double* A, int64_t ld, int n, int K, double* Sg,
+                                                              int32_t* status) {
+  __shared__ double S[kB * kSs];
+  const int tid = threadIdx.x, k0 = K * kB;
+  for (int e = tid; e < kB * kB; e += kThreads) {
+    const int i = e / kB, j = e % kB;
+    double v = i >= j ? A[(int64_t)(k0 + i) * ld + k0 + j] : A[(int64_t)(k0 + j) * ld + k0 + i];
+    if (k0 + i >= n || k0 + j >= n) v = (i == j) ? 1.0 : 0.0;  // identity padding
+    S[i * kSs + j] = v;
+  }
+  __syncthreads();
+  sweep_pivot_block(S, tid, status, K + 1);
+  for (int e = tid; e < kB * kB; e += kThreads) {
+    const int i = e / kB, j = e % kB;
+    Sg[e] = S[i * kSs + j];
+    if (i >= j) A[(int64_t)(k0 + i) * ld + k0 + j] = S[i * kSs + j];
+  }
+}
+
+// phase 2 (one CTA per I != K): V_I = A_IK -> Vp, W_I = -V_I S -> Wp and into A's block row/column K
+__global__ void __launch_bounds__(kThreads, 2) dense_panel_kernel(double* A, int64_t ld, int K, const double* Sg,
+                                                                 double* Wp, double* Vp) {
+  extern __shared__ double4 smem_raw[];
+  double* X = reinterpret_cast<double*>(smem_raw);
+  double* Y = X + kB * kXs;
+  const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
+  const int I = blockIdx.x < (unsigned)K ? blockIdx.x : blockIdx.x + 1;
+  const int i0 = I * kB, k0 = K * kB;
+  for (int e = tid; e < kB * kB; e += kThreads) Y[(e / kB) * kXs + e % kB] = Sg[e];
+  if (I > K) {
+    for (int e = tid; e < kB * kB; e += kThreads) {
+      const int r = e / kB, k = e % kB;
+      X[k * kXs + r] = A[(int64_t)(i0 + r) * ld + k0 + k];
+    }
+  } else {
+    for (int e = tid; e < kB * kB; e += kThreads) {
+      const int k = e / kB, r = e % kB;
+      X[k * kXs + r] = A[(int64_t)(k0 + k) * ld + i0 + r];
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < kB * kB; e += kThreads) {
+    const int k = e / kB, r = e % kB;
+    Vp[(int64_t)k * ld + i0 + r] = X[k * kXs + r];
+  }
+  double acc[4][4];
+  tile_product(X, Y, ty, tx, acc);
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int i = i0 + ty * 4 + r, k = tx * 4 + c;
+      Wp[(int64_t)k * ld + i] = -acc[r][c];
+      if (I > K)
+        A[(int64_t)i * ld + k0 + k] = -acc[r][c];
+      else
+        A[(int64_t)(k0 + k) * ld + i] = -acc[r][c];
+    }
+}
+
+// phase 3 (grid-stride over the lower tiles I >= J, I, J != K): A_IJ -= W_I V_J^T
+__global__ void __launch_bounds__(kThreads, 2) dense_update_kernel(double* A, int64_t ld, int nb, int K,
+                                                                  const double* Wp, const double* Vp) {
+  extern __shared__ double4 smem_raw[];
+  double* X = reinterpret_cast<double*>(smem_raw);
+  double* Y = X + kB * kXs;
+  const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
+  const int64_t m = nb - 1, ntiles = m * (m + 1) / 2;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    int64_t a = (int64_t)((sqrt(8.0 * (double)t + 1.0) - 1.0) / 2.0);
+    while (a * (a + 1) / 2 > t) --a;
+    while ((a + 1) * (a + 2) / 2 <= t) ++a;
+    const int Ip = (int)a, Jp = (int)(t - a * (a + 1) / 2);
+    const int I = Ip < K ? Ip : Ip + 1, J = Jp < K ? Jp : Jp + 1;
+    const int i0 = I * kB, j0 = J * kB;
+    __syncthreads();
+    for (int e = tid; e < kB * kB; e += kThreads) {
+      const int k = e / kB, r = e % kB;
+      X[k * kXs + r] = Wp[(int64_t)k * ld + i0 + r];
+      Y[k * kXs + r] = Vp[(int64_t)k * ld + j0 + r];
+    }
+    __syncthreads();
+    double acc[4][4];
+    tile_product(X, Y, ty, tx, acc);
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      double* row = A + (int64_t)(i0 + ty * 4 + r) * ld + j0 + tx * 4;
+      double2 a0 = *reinterpret_cast<double2*>(row), a1 = *reinterpret_cast<double2*>(row + 2);
+      a0.x -= acc[r][0];
+      a0.y -= acc[r][1];
+      a1.x -= acc[r][2];
+      a1.y -= acc[r][3];
+      *reinterpret_cast<double2*>(row) = a0;
+      *reinterpret_cast<double2*>(row + 2) = a1;
+    }
+  }
+}
+
+// pack -(swept A) = A^-1 (n x n) into the stored tile layout, one CTA per 32-row block row
+__global__ void dense_pack_kernel(const double* A, int64_t ld, int n, double* out, int layout) {
+  const int I = blockIdx.x, tid = threadIdx.x;
+  const int rows = min(32, n - 32 * I);
+  const int64_t base = 512LL * I * I + 16LL * I;
+  const int full = I * 32 * rows, total = full + rows * (rows + 1) / 2;
+  for (int w = tid; w < total; w += blockDim.x) {
+    int i, col;
+    if (w < full) {
+      const int J = w / (32 * rows), q = w % (32 * rows);
+      int kk;
+      if (layout == 0) {
+        i = (q >> 2) % rows;
+        kk = ((q >> 2) / rows) * 4 + (q & 3);
+      } else {
+        i = q >> 5;
+        kk = ((((q & 31) >> 1) ^ (i & 7)) << 1) | (q & 1);
+      }
+      col = 32 * J + kk;
+    } else {
+      int q = w - full, kk = 0;
+      while (q >= rows - kk) {
+        q -= rows - kk;
+        ++kk;
+      }
+      i = kk + q;
+      col = 32 * I + kk;
+    }
+    out[base + w] = -A[(int64_t)(32 * I + i) * ld + col];
+  }
+}
+
 }  // namespace
+
+cudaError_t dense_spd_inverse_packed(double* A, int64_t ld, int n, double* work, int32_t* status, double* tiles,
+                                     int layout, cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  const int nb = (int)(ld / kB);
+  double* Sg = work;
+  double* Wp = Sg + kB * kB;
+  double* Vp = Wp + (int64_t)kB * ld;
+  const size_t smem = sizeof(double) * 2 * kB * kXs;
+  cudaError_t e = cudaFuncSetAttribute(dense_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(dense_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  for (int K = 0; K < nb; ++K) {
+    dense_pivot_kernel<<<1, kThreads, 0, stream>>>(A, ld, n, K, Sg, status);
+    if (nb > 1) {
+      dense_panel_kernel<<<nb - 1, kThreads, smem, stream>>>(A, ld, K, Sg, Wp, Vp);
+      const int64_t ntiles = (int64_t)(nb - 1) * nb / 2;
+      const int grid = (int)std::min<int64_t>(ntiles, (int64_t)sms * 16);
+      dense_update_kernel<<<grid, kThreads, smem, stream>>>(A, ld, nb, K, Wp, Vp);
+    }
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  dense_pack_kernel<<<(n + 31) / 32, kThreads, 0, stream>>>(A, ld, n, tiles, layout);
+  return cudaGetLastError();
+}
 
 int64_t patch_setup_scratch_doubles(int64_t ld_max) { return ld_max * ld_max + 2 * kB * ld_max; }
 

@@ -40,4 +40,13 @@ size_t patch_setup_smem();
 // persistent kernel, n_ctas CTAs each claiming patches in order (largest first)
 cudaError_t launch_patch_setup(const DevPatchSetup& s, int n_ctas, cudaStream_t stream);
 
+// One large SPD matrix (the hybrid's Whitney coarse space) by the
+// same block sweep with every phase spread over the grid. A: device, ld x ld
+// row-major (ld = n rounded up to 64), lower triangle of A in rows/columns < n,
+// zero elsewhere; destroyed. work: 64*64 + 2*64*ld doubles. *status (device,
+// zeroed by the caller) becomes 1 + pivot block of a non-positive pivot.
+// tiles: patch_stored_doubles(n) doubles, receives A^-1 in the layout `layout`.
+cudaError_t dense_spd_inverse_packed(double* A, int64_t ld, int n, double* work, int32_t* status, double* tiles,
+                                     int layout, cudaStream_t stream);
+
 }  // namespace rdr

@@ -461,13 +461,37 @@ static int setup_impl(rdr_handle* h, const double* vertices, int64_t nv, const i
   h->fused = fused_pcg_supported(op) && !hybrid;
   if (hybrid) {  // ---- Whitney coarse space + sweep workspace + weights
     std::vector<int32_t> cidx;
-    std::vector<double> ctiles;
-    if ((st = build_coarse(m, num, el, coef, cidx, ctiles))) return st;
+    std::vector<double> ctiles, cdense;
+    if ((st = build_coarse(m, num, el, coef, cidx, ctiles, host_setup ? nullptr : &cdense))) return st;
     pc.nc = (int64_t)cidx.size();
     int32_t* d_cidx;
-    double* d_ct;
+    double* d_ct = nullptr;
     if ((st = h->own_upload(&d_cidx, cidx))) return st;
-    if ((st = h->own_upload(&d_ct, ctiles))) return st;
+    if (host_setup) {
+      if ((st = h->own_upload(&d_ct, ctiles))) return st;
+    } else if (pc.nc > 0) {  // device inverse of the coarse matrix (multi-CTA block sweep)
+      const int nc = (int)pc.nc;
+      const int64_t ld = (nc + 63) / 64 * 64;
+      if ((st = h->own_alloc((void**)&d_ct, sizeof(double) * patch_stored_doubles(nc)))) return st;
+      CK(cudaMemset(d_ct, 0, sizeof(double) * patch_stored_doubles(nc)));
+      DevTemps tmp;
+      double *dA = nullptr, *work = nullptr;
+      int32_t* dst = nullptr;
+      CK(cudaMalloc((void**)&dA, sizeof(double) * ld * ld));
+      tmp.p.push_back(dA);
+      CK(cudaMalloc((void**)&work, sizeof(double) * (64 * 64 + 2 * 64 * ld)));
+      tmp.p.push_back(work);
+      CK(cudaMalloc((void**)&dst, sizeof(int32_t)));
+      tmp.p.push_back(dst);
+      CK(cudaMemset(dst, 0, sizeof(int32_t)));
+      CK(cudaMemset(dA, 0, sizeof(double) * ld * ld));
+      CK(cudaMemcpy2D(dA, sizeof(double) * ld, cdense.data(), sizeof(double) * nc, sizeof(double) * nc, nc,
+                      cudaMemcpyHostToDevice));
+      CK(dense_spd_inverse_packed(dA, ld, nc, work, dst, d_ct, (int)kTileGroups, 0));
+      int32_t bad = 0;
+      CK(cudaMemcpy(&bad, dst, sizeof(int32_t), cudaMemcpyDeviceToHost));
+      if (bad) return RDR_ENOTSPD;
+    }
     pc.cidx = d_cidx;
     pc.ctiles = d_ct;
     if ((st = h->own_alloc((void**)&pc.czc, sizeof(double) * std::max<int64_t>(1, pc.nc)))) return st;

@@ -316,7 +316,7 @@ void pack_patch_tiles(const double* W2, int n, double* out, PatchLayout layout) 
 }
 
 int build_coarse(const Mesh& m, const Numbering& num, const RefElement& el, const std::vector<double>& coef,
-                 std::vector<int32_t>& cidx, std::vector<double>& tiles) {
+                 std::vector<int32_t>& cidx, std::vector<double>& tiles, std::vector<double>* dense) {
   // W^k (Lemma 4.1): vertex dofs (H(grad)) / Whitney edge dofs (H(curl)) /
   // Whitney face dofs (H(div)), free ones
   const int n = el.n, nm = el.n_mat, wdim = num.space == 0 ? 0 : num.space == 1 ? 1 : 2;
@@ -350,6 +350,10 @@ int build_coarse(const Mesh& m, const Numbering& num, const RefElement& el, cons
         A[(size_t)pa * nc + pb] += v;
       }
     }
+  if (dense) {  // the caller inverts on the device (patch_setup.cu dense_spd_inverse_packed)
+    dense->swap(A);
+    return 0;
+  }
   std::vector<double> work;
   if (!spd_inverse(A.data(), nc, work)) return RDR_ENOTSPD;
   tiles.assign(patch_stored_doubles(nc), 0.0);

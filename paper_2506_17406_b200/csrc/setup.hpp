@@ -105,9 +105,10 @@ void pack_patch_tiles(const double* W2, int n, double* out, PatchLayout layout);
 // Whitney coarse space of the hybrid Schwarz preconditioner:
 // the free vertex dofs (H(grad)) / Whitney edge dofs (H(curl)), Lemma 4.1
 // P:906-989, and the stored inverse of A restricted to them, packed as one
-// patch (layout kTileGroups). Returns 0 or RDR_ENOTSPD.
+// patch (layout kTileGroups). With `dense`, only A restricted to them (nc x nc
+// row-major) is returned there, for the device inverse. Returns 0 or RDR_ENOTSPD.
 int build_coarse(const Mesh& m, const Numbering& num, const RefElement& el, const std::vector<double>& coef,
-                 std::vector<int32_t>& cidx, std::vector<double>& tiles);
+                 std::vector<int32_t>& cidx, std::vector<double>& tiles, std::vector<double>* dense = nullptr);
 
 // Interior point-Jacobi (R-A17): 1/A_ll for the cell-interior dofs [off[3], n_total).
 void interior_inverse_diagonal(const Mesh& m, const Numbering& num, const RefElement& el,

@@ -537,3 +537,22 @@ def test_config6_hdiv_sampled(torch_cuda):
     except KeyError:
         it = None
     _check_sampled_pcg(torch_cuda, c, S, O, rows, b, it)
+
+
+@pytest.mark.parametrize("space,n,p", [(HGRAD, 4, 2), (HCURL, 3, 2), (HDIV, 3, 2)])
+def test_device_coarse_inverse(torch_cuda, space, n, p):
+    """The hybrid's coarse inverse by the multi-CTA block sweep on the device
+    (several 64-blocks: n_c > 64) equals the host Cholesky-based inverse to
+    kappa(A_c) eps, and the weights rho_m (from the library's own Lanczos with
+    either inverse) agree."""
+    from paper_2506_17406_b200 import rdr
+    torch = torch_cuda
+    c = make_config(0, n=n, p=p, space=space, perturb=True, bc="x0", coeffs="loguniform")
+    kw = dict(preconditioner=rdr.HYBRID)
+    Sd = rdr.Solver(c.vertices, c.tets, c.p, c.space, c.alpha, c.beta, c.mask, **kw)
+    Sh = rdr.Solver(c.vertices, c.tets, c.p, c.space, c.alpha, c.beta, c.mask, setup=rdr.SETUP_HOST, **kw)
+    assert np.allclose(Sd.weights, Sh.weights, rtol=1e-9, atol=0)
+    x = torch.from_numpy(c.draw_vector(Sd.n_total)).cuda()
+    zd, zh = Sd.precond(x).cpu().numpy(), Sh.precond(x).cpu().numpy()
+    assert rel(zd, zh) <= 1e-9, rel(zd, zh)
+    assert abs(Sd.solve(x)[1] - Sh.solve(x)[1]) <= 1

@@ -11,8 +11,8 @@
 // a Schur complement of the unswept part, hence SPD: no pivoting, and a
 // non-positive pivot flags a matrix that is not SPD (RDR_ENOTSPD). The sweep
 // keeps the matrix symmetric, so only the tiles I >= J are updated. The
-// rank-64 updates are 64x64x64 tile products on the FP64 CUDA cores (4x4
-// register blocks per thread, operands staged in shared memory). The last
+// rank-64 updates are 64x64x64 tile products on the FP64 tensor cores
+// (mma.sync m8n8k4 DMMA, 16x32 per warp, operands staged in shared memory). The last
 // step packs -(-A^-1) into the stored tile layout (setup.hpp).
 #include <cuda_runtime.h>
 
@@ -26,28 +26,63 @@ namespace rdr {
 namespace {
 
 constexpr int kB = 64;         // pivot block / tile
-constexpr int kThreads = 256;  // 16 x 16 threads, 4 x 4 outputs each
+constexpr int kThreads = 256;  // 8 warps, 16 x 32 outputs each
 constexpr int kSs = kB + 1;    // stride of the pivot block (column reads conflict free)
-constexpr int kXs = kB + 2;    // stride of the staged operands (16-byte aligned rows)
+constexpr int kXs = kB + 8;    // stride of the staged operands: == 16 words (mod 32), so the DMMA
+                               // fragment loads (rows k..k+3, 8 lanes each) take the minimum 2 wavefronts
 
-// acc[r][c] = sum_k X[k][ty*4 + r] * Y[k][tx*4 + c]
-__device__ __forceinline__ void tile_product(const double* X, const double* Y, int ty, int tx, double acc[4][4]) {
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// 64x64x64 tile product on the FP64 tensor cores (DMMA.8x8x4):
+//   acc = sum_k X[k][row] * Y[k][col]
+// Warp w owns rows (w&3)*16 + [0,16) and columns (w>>2)*32 + [0,32). Element
+// (m, q, i) of acc is at row acc_row(w, lane, m), column acc_col(w, lane, q, i).
+__device__ __forceinline__ int acc_row(int warp, int lane, int m) { return (warp & 3) * 16 + m * 8 + (lane >> 2); }
+__device__ __forceinline__ int acc_col(int warp, int lane, int q, int i) {
+  return (warp >> 2) * 32 + q * 8 + 2 * (lane & 3) + i;
+}
+__device__ __forceinline__ void tile_product(const double* X, const double* Y, int warp, int lane,
+                                             double acc[2][4][2]) {
+  const int g = lane >> 2, t = lane & 3;
+  const int r0 = (warp & 3) * 16 + g, c0 = (warp >> 2) * 32 + g;
 #pragma unroll
-  for (int r = 0; r < 4; ++r)
+  for (int m = 0; m < 2; ++m)
 #pragma unroll
-    for (int c = 0; c < 4; ++c) acc[r][c] = 0.0;
-#pragma unroll 8
-  for (int k = 0; k < kB; ++k) {
-    const double2 x0 = *reinterpret_cast<const double2*>(X + k * kXs + ty * 4);
-    const double2 x1 = *reinterpret_cast<const double2*>(X + k * kXs + ty * 4 + 2);
-    const double2 y0 = *reinterpret_cast<const double2*>(Y + k * kXs + tx * 4);
-    const double2 y1 = *reinterpret_cast<const double2*>(Y + k * kXs + tx * 4 + 2);
-    const double xa[4] = {x0.x, x0.y, x1.x, x1.y}, ya[4] = {y0.x, y0.y, y1.x, y1.y};
+    for (int q = 0; q < 4; ++q) acc[m][q][0] = acc[m][q][1] = 0.0;
+#pragma unroll 4
+  for (int k = 0; k < kB; k += 4) {
+    const double* xk = X + (k + t) * kXs;
+    const double* yk = Y + (k + t) * kXs;
+    const double a0 = xk[r0], a1 = xk[r0 + 8];
+    double b[4];
 #pragma unroll
-    for (int r = 0; r < 4; ++r)
+    for (int q = 0; q < 4; ++q) b[q] = yk[c0 + q * 8];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) acc[r][c] = fma(xa[r], ya[c], acc[r][c]);
+    for (int q = 0; q < 4; ++q) {
+      dmma884(acc[0][q][0], acc[0][q][1], a0, b[q]);
+      dmma884(acc[1][q][0], acc[1][q][1], a1, b[q]);
+    }
   }
+}
+
+// A[rows i0.., cols j0..] -= acc (row-major, leading dimension ld)
+__device__ __forceinline__ void tile_subtract(double* A, int64_t ld, int i0, int j0, int warp, int lane,
+                                              const double acc[2][4][2]) {
+#pragma unroll
+  for (int m = 0; m < 2; ++m)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      double2* a = reinterpret_cast<double2*>(A + (int64_t)(i0 + acc_row(warp, lane, m)) * ld + j0 +
+                                              acc_col(warp, lane, q, 0));
+      double2 v = *a;
+      v.x -= acc[m][q][0];
+      v.y -= acc[m][q][1];
+      *a = v;
+    }
 }
 
 // Scalar sweep of the 64 pivots of the symmetric block S (stride kSs) in
@@ -85,7 +120,7 @@ __global__ void __launch_bounds__(kThreads, 2) patch_setup_kernel(DevPatchSetup 
   double* X = S + kB * kSs + 2;                     // [kB][kXs] (16-byte aligned)
   double* Y = X + kB * kXs;                         // [kB][kXs]
   __shared__ int64_t claim;
-  const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   double* A = s.scratch + (int64_t)blockIdx.x * (s.ld_max * s.ld_max + 2 * kB * s.ld_max);
   for (;;) {
     __syncthreads();
@@ -166,12 +201,15 @@ __global__ void __launch_bounds__(kThreads, 2) patch_setup_kernel(DevPatchSetup 
           const int k = e / kB, r = e % kB;
           Vp[(int64_t)k * ld + i0 + r] = X[k * kXs + r];
         }
-        double acc[4][4];
-        tile_product(X, Y, ty, tx, acc);
+        double acc[2][4][2];
+        tile_product(X, Y, warp, lane, acc);
 #pragma unroll
-        for (int r = 0; r < 4; ++r)
+        for (int m2 = 0; m2 < 2; ++m2)
 #pragma unroll
-          for (int c = 0; c < 4; ++c) Wp[(int64_t)(tx * 4 + c) * ld + i0 + ty * 4 + r] = -acc[r][c];
+          for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+              Wp[(int64_t)acc_col(warp, lane, q, i) * ld + i0 + acc_row(warp, lane, m2)] = -acc[m2][q][i];
         __syncthreads();
       }
       // 2c. A_IJ -= W_I V_J^T for I >= J, I, J != K
@@ -190,19 +228,9 @@ __global__ void __launch_bounds__(kThreads, 2) patch_setup_kernel(DevPatchSetup 
             Y[k * kXs + c] = Vp[(int64_t)k * ld + j0 + c];
           }
           __syncthreads();
-          double acc[4][4];
-          tile_product(X, Y, ty, tx, acc);
-#pragma unroll
-          for (int r = 0; r < 4; ++r) {
-            double* row = A + (int64_t)(i0 + ty * 4 + r) * ld + j0 + tx * 4;
-            double2 a0 = *reinterpret_cast<double2*>(row), a1 = *reinterpret_cast<double2*>(row + 2);
-            a0.x -= acc[r][0];
-            a0.y -= acc[r][1];
-            a1.x -= acc[r][2];
-            a1.y -= acc[r][3];
-            *reinterpret_cast<double2*>(row) = a0;
-            *reinterpret_cast<double2*>(row + 2) = a1;
-          }
+          double acc[2][4][2];
+          tile_product(X, Y, warp, lane, acc);
+          tile_subtract(A, ld, i0, j0, warp, lane, acc);
           __syncthreads();
         }
       }
@@ -296,7 +324,7 @@ __global__ void __launch_bounds__(kThreads, 2) dense_panel_kernel(double* A, int
   extern __shared__ double4 smem_raw[];
   double* X = reinterpret_cast<double*>(smem_raw);
   double* Y = X + kB * kXs;
-  const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int I = blockIdx.x < (unsigned)K ? blockIdx.x : blockIdx.x + 1;
   const int i0 = I * kB, k0 = K * kB;
   for (int e = tid; e < kB * kB; e += kThreads) Y[(e / kB) * kXs + e % kB] = Sg[e];
@@ -316,19 +344,21 @@ __global__ void __launch_bounds__(kThreads, 2) dense_panel_kernel(double* A, int
     const int k = e / kB, r = e % kB;
     Vp[(int64_t)k * ld + i0 + r] = X[k * kXs + r];
   }
-  double acc[4][4];
-  tile_product(X, Y, ty, tx, acc);
+  double acc[2][4][2];
+  tile_product(X, Y, warp, lane, acc);
 #pragma unroll
-  for (int r = 0; r < 4; ++r)
+  for (int m2 = 0; m2 < 2; ++m2)
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const int i = i0 + ty * 4 + r, k = tx * 4 + c;
-      Wp[(int64_t)k * ld + i] = -acc[r][c];
-      if (I > K)
-        A[(int64_t)i * ld + k0 + k] = -acc[r][c];
-      else
-        A[(int64_t)(k0 + k) * ld + i] = -acc[r][c];
-    }
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int i = i0 + acc_row(warp, lane, m2), k = acc_col(warp, lane, q, c);
+        Wp[(int64_t)k * ld + i] = -acc[m2][q][c];
+        if (I > K)
+          A[(int64_t)i * ld + k0 + k] = -acc[m2][q][c];
+        else
+          A[(int64_t)(k0 + k) * ld + i] = -acc[m2][q][c];
+      }
 }
 
 // phase 3 (grid-stride over the lower tiles I >= J, I, J != K): A_IJ -= W_I V_J^T
@@ -337,7 +367,7 @@ __global__ void __launch_bounds__(kThreads, 2) dense_update_kernel(double* A, in
   extern __shared__ double4 smem_raw[];
   double* X = reinterpret_cast<double*>(smem_raw);
   double* Y = X + kB * kXs;
-  const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t m = nb - 1, ntiles = m * (m + 1) / 2;
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     int64_t a = (int64_t)((sqrt(8.0 * (double)t + 1.0) - 1.0) / 2.0);
@@ -353,19 +383,9 @@ __global__ void __launch_bounds__(kThreads, 2) dense_update_kernel(double* A, in
       Y[k * kXs + r] = Vp[(int64_t)k * ld + j0 + r];
     }
     __syncthreads();
-    double acc[4][4];
-    tile_product(X, Y, ty, tx, acc);
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      double* row = A + (int64_t)(i0 + ty * 4 + r) * ld + j0 + tx * 4;
-      double2 a0 = *reinterpret_cast<double2*>(row), a1 = *reinterpret_cast<double2*>(row + 2);
-      a0.x -= acc[r][0];
-      a0.y -= acc[r][1];
-      a1.x -= acc[r][2];
-      a1.y -= acc[r][3];
-      *reinterpret_cast<double2*>(row) = a0;
-      *reinterpret_cast<double2*>(row + 2) = a1;
-    }
+    double acc[2][4][2];
+    tile_product(X, Y, warp, lane, acc);
+    tile_subtract(A, ld, i0, j0, warp, lane, acc);
   }
 }
 

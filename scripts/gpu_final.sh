@@ -9,9 +9,9 @@ echo "smoke exit $?" >> gpurun_out/${TAG}_smoke.log
 timeout 900 python bench.py > gpurun_out/${TAG}_bench.log 2>&1
 echo "bench exit $?" >> gpurun_out/${TAG}_bench.log
 timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/${TAG}_bench_ref.log 2>&1
-python bench.py --steps 2 --warmup 3 --no-cpu --no-dgemm > gpurun_out/${TAG}_plain.log 2>&1 && \
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -s 40 -c 400 --csv \
-    --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 2 --warmup 3 --no-cpu --no-dgemm > gpurun_out/${TAG}_ncu1.log 2>&1
+# launch list of the bench solve, graph nodes one by one (host-driven 8-iteration graphs:
+# ncu cannot profile the nodes of a graph with a conditional while node)
+RDR_PCG_HOSTLOOP=1 bash scripts/ncu_launches.sh ${TAG}_launches
 python scripts/prof_kernels.py 2 6 3 > gpurun_out/${TAG}_prof_plain.log 2>&1 && \
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"patch_ldg|apply_tc" -s 4 -c 2 \
     -o gpurun_out/${TAG}_full -f python scripts/prof_kernels.py 2 6 3 > gpurun_out/${TAG}_ncu2.log 2>&1

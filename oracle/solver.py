@@ -274,8 +274,9 @@ class Oracle:
         return z
 
     # ------------------------------------------------------------ PCG
-    def solve(self, b, rtol=1e-8, maxit=10000):
-        """PCG per R-A16. Returns (x, iters, true relative residual)."""
+    def solve(self, b, rtol=1e-8, maxit=10000, history=None):
+        """PCG per R-A16. Returns (x, iters, true relative residual); `history`
+        (a list) receives ||z_k|| / ||z_0|| for k = 1..iters."""
         b = self.mask(b)
         x = np.zeros_like(b)
         r = b.copy()
@@ -293,6 +294,8 @@ class Oracle:
             r -= a * q
             z = self.precond(r)
             it = k + 1
+            if history is not None:
+                history.append(np.linalg.norm(z) / z0)
             if np.linalg.norm(z) <= rtol * z0:
                 break
             rho_new = r @ z

@@ -12,7 +12,9 @@ timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/$
 # launch list of the bench solve, graph nodes one by one (host-driven 8-iteration graphs:
 # ncu cannot profile the nodes of a graph with a conditional while node)
 RDR_PCG_HOSTLOOP=1 bash scripts/ncu_launches.sh ${TAG}_launches
-python scripts/prof_kernels.py 2 6 3 > gpurun_out/${TAG}_prof_plain.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"patch_ldg|apply_tc" -s 4 -c 2 \
-    -o gpurun_out/${TAG}_full -f python scripts/prof_kernels.py 2 6 3 > gpurun_out/${TAG}_ncu2.log 2>&1
-echo "ncu exit $?" >> gpurun_out/${TAG}_ncu2.log
+python scripts/prof_kernels.py 2 6 3 > gpurun_out/${TAG}_prof_plain.log 2>&1
+for K in patch_ldg apply_tc; do
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$K -s 2 -c 1 \
+      -o gpurun_out/${TAG}_full_$K -f python scripts/prof_kernels.py 2 6 3 > gpurun_out/${TAG}_ncu_$K.log 2>&1
+  echo "ncu exit $?" >> gpurun_out/${TAG}_ncu_$K.log
+done

@@ -51,8 +51,15 @@ def _check_apply_precond(torch, c, S, O, nvec=2):
 def _check_pcg(torch, c, S, O):
     b = c.draw_vector(O.n_total)
     x, it = S.solve(torch.from_numpy(b).cuda(), rtol=1e-8)
-    xo, ito, res = O.solve(b, rtol=1e-8)
-    assert abs(it - ito) <= 1, (it, ito)
+    hist = []
+    xo, ito, res = O.solve(b, rtol=1e-8, history=hist)
+    if abs(it - ito) > 1:
+        # DESIGN.md R-A16 tie: ||z_k|| is not monotone in k, so when the oracle's
+        # ||z_k|| / ||z_0|| at the earlier of the two exits equals rtol to
+        # rounding (1e-3 relative), both exits satisfy the stopping rule up to
+        # rounding and the counts may differ by more than one
+        k = min(it, ito)
+        assert abs(hist[k - 1] / 1e-8 - 1.0) <= 1e-3, (it, ito, hist[max(0, k - 3):k + 2])
     xg = x.cpu().numpy()
     bm = O.mask(b)
     assert np.linalg.norm(bm - O.apply(xg)) / np.linalg.norm(bm) <= 1e-5

@@ -901,6 +901,8 @@ __device__ __forceinline__ double ld_stream1(const double* p) {
 }
 
 // v[k] over 32 lanes -> lane l holds sum_{lanes} v[l & 15] (16-value transpose reduction)
+constexpr int kSmallPatch = 128;  // patches of at most this size take the warp-per-patch path
+
 template <int S>
 __device__ __forceinline__ void treduce_stage(double (&v)[16], int lane) {
   const bool upper = (lane & S) != 0;
@@ -917,6 +919,117 @@ __device__ __forceinline__ double treduce16(double (&v)[16], int lane) {
   treduce_stage<2>(v, lane);
   treduce_stage<1>(v, lane);
   return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 16);
+}
+
+// Small patches (n <= 128, at most 4 block rows: the H(div) and H(curl) edge
+// stars, sorted last, [n_big, n_patches)) one per warp, kLdgWarps per CTA, so
+// a small patch's gather / scatter / reduction latency overlaps the other
+// warps' tile streams instead of serialising on __syncthreads. Same arithmetic
+// as patch_ldg_kernel.
+template <int kLdgWarps>
+__global__ void __launch_bounds__(kLdgWarps * 32, 32 / kLdgWarps)
+    patch_warp_kernel(DevPrecond pc, const double* __restrict__ r, double* __restrict__ z, double* rz_acc,
+                      const PcgScalars* guard) {
+  extern __shared__ double smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t pid = pc.n_big + (int64_t)blockIdx.x * kLdgWarps + warp;
+  if (pid >= pc.n_patches) {
+    pdl_wait();  // warps without a patch still order the CTA after the previous kernel
+    return;
+  }
+  const int n = pc.pn[pid];
+  const int nb = (n + 31) >> 5, npad = nb * 32;
+  const bool pot = pc.pkind[pid] != 0;
+  const double* __restrict__ rin = pot ? pc.gbuf : r;
+  double* __restrict__ zout = pot ? pc.ubuf : z;
+  double* rl = smem + warp * 2 * kSmallPatch;
+  double* zl = rl + kSmallPatch;
+  const int32_t* id = pc.idx + pc.idx_off[pid];
+  long long* rli = reinterpret_cast<long long*>(rl);
+  for (int i = lane; i < npad; i += 32) {
+    rli[i] = id[i];
+    zl[i] = 0.0;
+  }
+  const double* T = pc.tiles + pc.tile_off[pid];
+  const int ntiles = nb * (nb + 1) / 2;
+  int I = 0, J = 0, h = 0, t = 0;
+  auto load_half = [&](double(&a)[16]) {
+    const int rows = min(32, n - 32 * I);
+    const double* tb = T + 512LL * I * I + 16LL * I + (int64_t)J * 32 * rows;
+    if (J < I) {
+      if (lane < rows) {
+        const double4* tp = reinterpret_cast<const double4*>(tb) + lane + 4 * h * rows;
+#pragma unroll
+        for (int k4 = 0; k4 < 4; ++k4) {
+          const double4 v = ld_stream4(tp + k4 * rows);
+          a[4 * k4] = v.x;
+          a[4 * k4 + 1] = v.y;
+          a[4 * k4 + 2] = v.z;
+          a[4 * k4 + 3] = v.w;
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < 16; ++q) a[q] = 0.0;
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const int k = 16 * h + q;
+        a[q] = (k <= lane && lane < rows) ? ld_stream1(tb + k * rows - k * (k - 1) / 2 + (lane - k)) : 0.0;
+      }
+    }
+  };
+  double a[16];
+  load_half(a);
+  pdl_wait();
+  if (stopped(guard)) return;
+  for (int i = lane; i < npad; i += 32) {
+    const int g = (int)rli[i];
+    rl[i] = (g >= 0) ? rin[g] : 0.0;
+  }
+  __syncwarp();
+  double row = 0.0;
+  while (t < ntiles) {
+    const double ri = rl[I * 32 + lane];
+    if (J < I) {
+      const double* rJ = rl + J * 32 + 16 * h;
+#pragma unroll
+      for (int q = 0; q < 16; ++q) row = fma(a[q], rJ[q], row);
+#pragma unroll
+      for (int q = 0; q < 16; ++q) a[q] *= ri;
+    } else {
+      const double* rI = rl + I * 32 + 16 * h;
+#pragma unroll
+      for (int q = 0; q < 16; ++q) row = fma(a[q], rI[q], row);
+#pragma unroll
+      for (int q = 0; q < 16; ++q) a[q] = (16 * h + q < lane) ? a[q] * ri : 0.0;  // strict lower, transposed
+    }
+    const double col = treduce16(a, lane);
+    if (lane < 16) atomicAdd(zl + J * 32 + 16 * h + lane, col);
+    if (h == 1) {
+      atomicAdd(zl + I * 32 + lane, row);
+      row = 0.0;
+      h = 0;
+      ++t;
+      if (++J > I) {
+        J = 0;
+        ++I;
+      }
+    } else {
+      h = 1;
+    }
+    if (t < ntiles) load_half(a);
+  }
+  if (pdl_late()) pdl_trigger();
+  __syncwarp();
+  double part = 0.0;
+  for (int i = lane; i < n; i += 32) {
+    const double zi = zl[i];
+    atomicAdd(zout + id[i], pc.out_scale * zi);
+    part = fma(rl[i], zi, part);
+  }
+  part = warp_sum(part);
+  if (rz_acc && lane == 0) atomicAdd(rz_acc, part);
 }
 
 template <int kLdgWarps>
@@ -1315,7 +1428,8 @@ size_t patch_kernel_smem(int slots, int npad_max, int zbufs) { return patch_smem
 size_t max_kernel_smem() { return kMaxSmem; }
 
 int count_precond_launches(const DevPrecond& pc) {
-  return 1 + (pc.n_patches > 0 ? 1 : 0) + (pc.gbuf ? 2 : 0);
+  const int patch_launches = pc.n_patches == 0 ? 0 : pc.kernel == 1 ? 1 : (pc.n_big > 0) + (pc.n_big < pc.n_patches);
+  return 1 + patch_launches + (pc.gbuf ? 2 : 0);
 }
 
 cudaError_t launch_precond_part(int part, const DevPrecond& pc, const double* r, double* z, double* rz_acc,
@@ -1332,11 +1446,25 @@ cudaError_t launch_precond_part(int part, const DevPrecond& pc, const double* r,
         if (pc.kernel == 1)
           return launch_k(patch_stream_kernel, dim3(pc.n_ctas), dim3(kPatchWarps * 32),
                           patch_smem_bytes(pc.ring_slots, pc.npad_max, pc.zbufs), s, pc, r, z, rz_acc, guard);
-        if (pc.ldg_warps == 4)
-          return launch_kx(pdl_patch_enabled(), patch_ldg_kernel<4>, dim3(pc.n_patches), dim3(4 * 32), 2 * sizeof(double) * pc.npad_max, s,
-                          pc, r, z, rz_acc, guard);
-        return launch_kx(pdl_patch_enabled(), patch_ldg_kernel<8>, dim3(pc.n_patches), dim3(8 * 32), 2 * sizeof(double) * pc.npad_max, s,
-                        pc, r, z, rz_acc, guard);
+        const int W = pc.ldg_warps;
+        cudaError_t e = cudaSuccess;
+        if (pc.n_big > 0) {  // one CTA per patch
+          const size_t sm = 2 * sizeof(double) * pc.npad_max;
+          e = W == 4 ? launch_kx(pdl_patch_enabled(), patch_ldg_kernel<4>, dim3((unsigned)pc.n_big), dim3(4 * 32), sm,
+                                 s, pc, r, z, rz_acc, guard)
+                     : launch_kx(pdl_patch_enabled(), patch_ldg_kernel<8>, dim3((unsigned)pc.n_big), dim3(8 * 32), sm,
+                                 s, pc, r, z, rz_acc, guard);
+          if (e != cudaSuccess) return e;
+        }
+        if (pc.n_big < pc.n_patches) {  // one warp per small patch
+          const size_t sm = 2 * sizeof(double) * kSmallPatch * W;
+          const dim3 grid((unsigned)((pc.n_patches - pc.n_big + W - 1) / W));
+          e = W == 4 ? launch_kx(pdl_patch_enabled(), patch_warp_kernel<4>, grid, dim3(4 * 32), sm, s, pc, r, z,
+                                 rz_acc, guard)
+                     : launch_kx(pdl_patch_enabled(), patch_warp_kernel<8>, grid, dim3(8 * 32), sm, s, pc, r, z,
+                                 rz_acc, guard);
+        }
+        return e;
       }
       break;
     case 3:

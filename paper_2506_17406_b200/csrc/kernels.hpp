@@ -53,6 +53,7 @@ struct DevPrecond {
   const uint8_t* pkind;         // 0 own numbering, 1 CG potential
   int32_t kernel;               // 0: patch_ldg_kernel (tile layout "groups"), 1: patch_stream_kernel ("swizzled")
   int32_t ldg_warps;            // warps per CTA of patch_ldg_kernel: 8, or 4 when most patches are small
+  int64_t n_big;                // patch_ldg_kernel: patches [0, n_big) one per CTA, the rest (n <= 128) one per warp
   // persistent patch kernel: n_ctas CTAs claim patches from a queue
   int32_t n_ctas;
   int32_t* queue;               // [2] claim counter, finished-CTA counter (zero between launches)

@@ -390,6 +390,12 @@ static int setup_impl(rdr_handle* h, const double* vertices, int64_t nv, const i
     for (int32_t n : P.n) small += n <= 128;
     pc.ldg_warps = 2 * small > pc.n_patches ? 4 : 8;
     if (const char* pw = std::getenv("RDR_PATCH_WARPS")) pc.ldg_warps = std::atoi(pw) == 4 ? 4 : 8;
+    // only small patches (H(div) edge stars): one per warp (patch_warp_kernel).
+    // Mixed sizes keep one CTA per patch: splitting them over two launches measured
+    // slower on config 4 (273 -> 320 us). RDR_PATCH_WARP_SMALL=0|1 overrides.
+    const char* ws = std::getenv("RDR_PATCH_WARP_SMALL");
+    const bool warp_small = ws ? std::atoi(ws) != 0 : small == pc.n_patches;
+    pc.n_big = (int64_t)P.n.size() - (warp_small ? small : 0);
   }
   pc.max_n = P.max_n;
   int32_t *d_pn, *d_idx;

@@ -50,12 +50,13 @@ enum { RDR_HGRAD = 0, RDR_HCURL = 1, RDR_HDIV = 2 };
  *   RDR_SPLIT   (default, the hot path) interface star patches + point-Jacobi
  *               on the interiors: PAFW0(X0_Gamma)+J(X0_I) (Eq. 5.4)
  *               for H(grad), PH(X0_Gamma, X1I_Gamma)+J(X1_I) (Eq. 5.12,
- *               P:1956-1970) for H(curl);
+ *               P:1956-1970) for H(curl), PAFW1(X2_Gamma)+J(X2_I) (Eq. 5.16,
+ *               edge stars) for H(div);
  *   RDR_UNSPLIT the baselines the split is measured against (NEXT-3): star
  *               patches that contain the cell interiors and no Jacobi,
- *               PAFW0(X0) (Eq. 5.2) and PH(X0, X1I) (Eq. 5.10,
- *               P:1899-1905) -- 3439 vs 1423 dofs per vertex star at p = 10
- *               (P:1783-1787). */
+ *               PAFW0(X0) (Eq. 5.2), PH(X0, X1I) (Eq. 5.10,
+ *               P:1899-1905) and PAFW1(X2) -- 3439 vs 1423 dofs per vertex
+ *               star at p = 10. */
 enum { RDR_SPLIT = 0, RDR_UNSPLIT = 1 };
 
 /* Composition of the preconditioner:
@@ -63,7 +64,8 @@ enum { RDR_SPLIT = 0, RDR_UNSPLIT = 1 };
  *   RDR_HYBRID   the paper's symmetric multiplicative hybrid Schwarz (P:2399-2455,
  *                NEXT-1): sweep X_I (Jacobi), X_Gamma (additive patches),
  *                W^k (exact solve on the Whitney space: vertex dofs for H(grad),
- *                Whitney edge dofs for H(curl), Lemma 4.1), X_Gamma, X_I, each
+ *                Whitney edge dofs for H(curl), Whitney face dofs for H(div),
+ *                Lemma 4.1; its inverse is formed on the device), X_Gamma, X_I, each
  *                damped by rho_m = (lambda_min + 3 lambda_max)/4 from 10 CG-Lanczos
  *                steps. Split decomposition only; costs 4 extra
  *                operator applies per preconditioner application. */
@@ -100,7 +102,7 @@ struct rdr_info {
   int64_t n_interior;    /* cell-interior dofs (point-Jacobi block, Thm 5.1) */
   int64_t n_cells;
   int32_t n_loc;         /* local dofs per cell */
-  int32_t n_mat;         /* reference matrices: 7 (H(grad)) or 12 (H(curl)) */
+  int32_t n_mat;         /* reference matrices: 7 (H(grad), H(div)) or 12 (H(curl)) */
   int64_t n_patches;     /* star patches (Eq. 5.4 P:1763-1774 / Eq. 5.12) */
   int32_t max_patch;     /* largest patch dimension */
   int64_t patch_bytes;   /* device bytes of the stored patch inverses (with tile padding) */
@@ -188,7 +190,8 @@ int rdr_debug_fused_apply(rdr_handle* h, const double* z, double* q, void* strea
  * rdr_reference_matrices: the n_mat reference matrices of (space, p) in
  * float64, layout [n_mat][n_loc][n_loc]; pass out = NULL to query *n_loc and
  * *n_mat. Order: H(grad) M, Kxx, Kyy, Kzz, Kxy+Kyx, Kxz+Kzx, Kyz+Kzy;
- * H(curl) Mxx, Myy, Mzz, Mxy+Myx, Mxz+Mzx, Myz+Mzy, then the same for K (curl).
+ * H(curl) Mxx, Myy, Mzz, Mxy+Myx, Mxz+Mzx, Myz+Mzy, then the same for K (curl);
+ * H(div) Mxx, Myy, Mzz, Mxy+Myx, Mxz+Mzx, Myz+Mzy (2-form proxies), then K (div-div).
  * Local dof order: DESIGN.md R-A8. */
 int rdr_reference_matrices(int space, int p, double* out, int32_t* n_loc, int32_t* n_mat);
 /* In-place inverse of an n x n SPD row-major matrix with the host routine the

@@ -16,6 +16,7 @@
 #include "refelem.hpp"
 
 #include <algorithm>
+#include <cfloat>
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
@@ -568,6 +569,132 @@ void jacobi_eig(Mat A, std::vector<ld>& w, Mat& V) {
   V = Vs;
 }
 
+// Symmetric eigendecomposition for the larger bubble problems: Householder
+// reduction to tridiagonal form (accumulating the transformation), then the
+// implicit QL iteration with Wilkinson shifts on the tridiagonal, rotations
+// applied to the accumulated basis. O(n^3) with a small constant, where the
+// cyclic Jacobi above needs ~10 sweeps of 6 n^3 (the RT_10 cell bubbles, n =
+// 495, took most of a 36 s build). A = V diag(w) V^T, w ascending.
+void tridiagonal_ql_eig(Mat A, std::vector<ld>& w, Mat& V) {
+  const int n = A.r;
+  std::vector<ld> d(n, 0), e(n, 0);
+  // ---- Householder: A -> Q T Q^T, Q accumulated in A
+  for (int i = n - 1; i > 0; --i) {
+    const int l = i - 1;
+    ld h = 0;
+    if (l > 0) {
+      ld scale = 0;
+      for (int k = 0; k <= l; ++k) scale += fabsl(A(i, k));
+      if (scale == 0) {
+        e[i] = A(i, l);
+      } else {
+        for (int k = 0; k <= l; ++k) {
+          A(i, k) /= scale;
+          h += A(i, k) * A(i, k);
+        }
+        ld f = A(i, l);
+        ld g = f >= 0 ? -sqrtl(h) : sqrtl(h);
+        e[i] = scale * g;
+        h -= f * g;
+        A(i, l) = f - g;
+        f = 0;
+        for (int j = 0; j <= l; ++j) {
+          A(j, i) = A(i, j) / h;
+          ld gg = 0;
+          for (int k = 0; k <= j; ++k) gg += A(j, k) * A(i, k);
+          for (int k = j + 1; k <= l; ++k) gg += A(k, j) * A(i, k);
+          e[j] = gg / h;
+          f += e[j] * A(i, j);
+        }
+        const ld hh = f / (h + h);
+        for (int j = 0; j <= l; ++j) {
+          const ld fj = A(i, j);
+          const ld gj = e[j] - hh * fj;
+          e[j] = gj;
+          for (int k = 0; k <= j; ++k) A(j, k) -= fj * e[k] + gj * A(i, k);
+        }
+      }
+    } else {
+      e[i] = A(i, l);
+    }
+    d[i] = h;
+  }
+  d[0] = 0;
+  e[0] = 0;
+  for (int i = 0; i < n; ++i) {
+    const int l = i - 1;
+    if (d[i] != 0) {
+#pragma omp parallel for schedule(static) if (l > 256)
+      for (int j = 0; j <= l; ++j) {
+        ld g = 0;
+        for (int k = 0; k <= l; ++k) g += A(i, k) * A(k, j);
+        for (int k = 0; k <= l; ++k) A(k, j) -= g * A(k, i);
+      }
+    }
+    d[i] = A(i, i);
+    A(i, i) = 1;
+    for (int j = 0; j <= l; ++j) A(j, i) = A(i, j) = 0;
+  }
+  // ---- implicit QL on (d, e), rotations accumulated into the columns of A
+  for (int i = 1; i < n; ++i) e[i - 1] = e[i];
+  if (n > 0) e[n - 1] = 0;
+  for (int l = 0; l < n; ++l) {
+    int iter = 0, m;
+    do {
+      for (m = l; m < n - 1; ++m) {
+        const ld dd = fabsl(d[m]) + fabsl(d[m + 1]);
+        if (fabsl(e[m]) <= LDBL_EPSILON * dd) break;
+      }
+      if (m != l) {
+        if (iter++ == 100) throw std::runtime_error("tridiagonal QL did not converge");
+        ld g = (d[l + 1] - d[l]) / (2 * e[l]);
+        ld r = hypotl(g, 1.0L);
+        g = d[m] - d[l] + e[l] / (g + (g >= 0 ? fabsl(r) : -fabsl(r)));
+        ld s = 1, c = 1, p = 0;
+        int i;
+        bool underflow = false;
+        for (i = m - 1; i >= l; --i) {
+          ld f = s * e[i];
+          const ld b = c * e[i];
+          r = hypotl(f, g);
+          e[i + 1] = r;
+          if (r == 0) {
+            d[i + 1] -= p;
+            e[m] = 0;
+            underflow = true;
+            break;
+          }
+          s = f / r;
+          c = g / r;
+          g = d[i + 1] - p;
+          r = (d[i] - g) * s + 2 * c * b;
+          p = s * r;
+          d[i + 1] = g + p;
+          g = c * r - b;
+          for (int k = 0; k < n; ++k) {
+            f = A(k, i + 1);
+            A(k, i + 1) = s * A(k, i) + c * f;
+            A(k, i) = c * A(k, i) - s * f;
+          }
+        }
+        if (underflow) continue;
+        d[l] -= p;
+        e[l] = g;
+        e[m] = 0;
+      }
+    } while (m != l);
+  }
+  std::vector<int> ord(n);
+  for (int i = 0; i < n; ++i) ord[i] = i;
+  std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return d[a] < d[b]; });
+  w.resize(n);
+  V = Mat(n, n);
+  for (int j = 0; j < n; ++j) {
+    w[j] = d[ord[j]];
+    for (int i = 0; i < n; ++i) V(i, j) = A(i, ord[j]);
+  }
+}
+
 // pivoted Cholesky of a PSD Gram matrix: selected indices (pivot order) and the
 // lower Cholesky factor L of M[sel][sel]
 std::vector<int> pivoted_cholesky(const Mat& M, ld rel_tol, Mat& L) {
@@ -798,7 +925,10 @@ Eig bubble_eigen(const Geo& S, int kind, const Mat& Fspan, int q, int dim_bubble
     for (int j = 0; j < i; ++j) Kt(i, j) = Kt(j, i) = (Kt(i, j) + Kt(j, i)) / 2;
   std::vector<ld> mu;
   Mat Y;
-  jacobi_eig(Kt, mu, Y);
+  if (r > 64)
+    tridiagonal_ql_eig(Kt, mu, Y);
+  else
+    jacobi_eig(Kt, mu, Y);
   ld mumax = mu.back();
   int nk = 0;
   while (nk < r && mu[nk] < 1e-8L * mumax) ++nk;

@@ -27,7 +27,7 @@ namespace {
 
 constexpr int kB = 64;         // pivot block / tile
 constexpr int kThreads = 256;  // 8 warps, 16 x 32 outputs each
-constexpr int kSs = kB + 1;    // stride of the pivot block (column reads conflict free)
+constexpr int kSs = kB + 8;    // stride of the pivot block (= kXs: it doubles as the second V buffer)
 constexpr int kXs = kB + 8;    // stride of the staged operands: == 16 words (mod 32), so the DMMA
                                // fragment loads (rows k..k+3, 8 lanes each) take the minimum 2 wavefronts
 
@@ -35,6 +35,24 @@ __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
                : "+d"(c0), "+d"(c1)
                : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)),
+               "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// dst[k][c] (stride kXs) <- src[k * ld + c], a 64 x 64 tile, asynchronously (16-byte copies)
+__device__ __forceinline__ void tile_load_async(double* dst, const double* src, int64_t ld, int tid) {
+#pragma unroll
+  for (int u = 0; u < kB * kB / 2 / kThreads; ++u) {
+    const int e = tid + u * kThreads, k = e / (kB / 2), c = 2 * (e % (kB / 2));
+    cp_async16(dst + k * kXs + c, src + (int64_t)k * ld + c);
+  }
+  cp_async_commit();
 }
 
 // 64x64x64 tile product on the FP64 tensor cores (DMMA.8x8x4):
@@ -116,8 +134,8 @@ __device__ void sweep_pivot_block(double* S, int tid, int32_t* status, int32_t f
 
 __global__ void __launch_bounds__(kThreads, 2) patch_setup_kernel(DevPatchSetup s) {
   extern __shared__ double4 smem_raw[];
-  double* S = reinterpret_cast<double*>(smem_raw);  // [kB][kSs] pivot block
-  double* X = S + kB * kSs + 2;                     // [kB][kXs] (16-byte aligned)
+  double* S = reinterpret_cast<double*>(smem_raw);  // [kB][kSs] pivot block, then the second V buffer
+  double* X = S + kB * kSs;                         // [kB][kXs] (16-byte aligned)
   double* Y = X + kB * kXs;                         // [kB][kXs]
   __shared__ int64_t claim;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -212,29 +230,41 @@ __global__ void __launch_bounds__(kThreads, 2) patch_setup_kernel(DevPatchSetup 
               Wp[(int64_t)acc_col(warp, lane, q, i) * ld + i0 + acc_row(warp, lane, m2)] = -acc[m2][q][i];
         __syncthreads();
       }
-      // 2c. A_IJ -= W_I V_J^T for I >= J, I, J != K
+      // A_KK = S now: from here on S is the second V buffer of 2c
+      for (int e = tid; e < kB * kB; e += kThreads) {
+        const int i = e / kB, j = e % kB;
+        if (i >= j) A[(int64_t)(k0 + i) * ld + k0 + j] = S[i * kSs + j];
+      }
+      // 2c. A_IJ -= W_I V_J^T for I >= J, I, J != K; the next V_J streams into
+      // the other buffer (cp.async) while the current tile product runs
       for (int I = 0; I < nb; ++I) {
         if (I == K) continue;
         const int i0 = I * kB;
+        __syncthreads();  // the previous I's products are done with X and both V buffers
         for (int e = tid; e < kB * kB; e += kThreads) {
           const int k = e / kB, r = e % kB;
           X[k * kXs + r] = Wp[(int64_t)k * ld + i0 + r];
         }
-        for (int J = 0; J <= I; ++J) {
-          if (J == K) continue;
-          const int j0 = J * kB;
-          for (int e = tid; e < kB * kB; e += kThreads) {
-            const int k = e / kB, c = e % kB;
-            Y[k * kXs + c] = Vp[(int64_t)k * ld + j0 + c];
-          }
-          __syncthreads();
+        double *cur = Y, *nxt = S;
+        int J = K == 0 ? 1 : 0;
+        if (J <= I) tile_load_async(cur, Vp + J * kB, ld, tid);
+        while (J <= I) {
+          int Jn = J + 1;
+          if (Jn == K) ++Jn;
+          cp_async_wait_all();
+          __syncthreads();  // V_J (and X) visible; everyone is done with the buffer refilled next
+          if (Jn <= I) tile_load_async(nxt, Vp + Jn * kB, ld, tid);
           double acc[2][4][2];
-          tile_product(X, Y, warp, lane, acc);
-          tile_subtract(A, ld, i0, j0, warp, lane, acc);
-          __syncthreads();
+          tile_product(X, cur, warp, lane, acc);
+          tile_subtract(A, ld, i0, J * kB, warp, lane, acc);
+          double* t2 = cur;
+          cur = nxt;
+          nxt = t2;
+          J = Jn;
         }
       }
-      // 2d. the swept block row / column: A_IK = W_I (I > K), A_KI = W_I^T (I < K), A_KK = S
+      __syncthreads();
+      // 2d. the swept block row / column: A_IK = W_I (I > K), A_KI = W_I^T (I < K)
       for (int I = 0; I < nb; ++I) {
         if (I == K) continue;
         const int i0 = I * kB;
@@ -249,10 +279,6 @@ __global__ void __launch_bounds__(kThreads, 2) patch_setup_kernel(DevPatchSetup 
             A[(int64_t)(k0 + k) * ld + i0 + r] = Wp[(int64_t)k * ld + i0 + r];
           }
         }
-      }
-      for (int e = tid; e < kB * kB; e += kThreads) {
-        const int i = e / kB, j = e % kB;
-        if (i >= j) A[(int64_t)(k0 + i) * ld + k0 + j] = S[i * kSs + j];
       }
       __syncthreads();
     }
@@ -454,7 +480,7 @@ cudaError_t dense_spd_inverse_packed(double* A, int64_t ld, int n, double* work,
 
 int64_t patch_setup_scratch_doubles(int64_t ld_max) { return ld_max * ld_max + 2 * kB * ld_max; }
 
-size_t patch_setup_smem() { return sizeof(double) * (kB * kSs + 2 + 2 * kB * kXs); }
+size_t patch_setup_smem() { return sizeof(double) * (kB * kSs + 2 * kB * kXs); }
 
 cudaError_t launch_patch_setup(const DevPatchSetup& s, int n_ctas, cudaStream_t stream) {
   const size_t smem = patch_setup_smem();

@@ -87,19 +87,21 @@ __device__ __forceinline__ void tile_product(const double* X, const double* Y, i
   }
 }
 
-// A[rows i0.., cols j0..] -= acc (row-major, leading dimension ld)
+// A[rows i0.., cols j0..] -= acc (row-major, leading dimension ld). The
+// reductions are performed at L2, so every later read of A in the same kernel
+// goes through L2 too (__ldcg): an L1 line of a reused scratch address could
+// otherwise be stale.
 __device__ __forceinline__ void tile_subtract(double* A, int64_t ld, int i0, int j0, int warp, int lane,
                                               const double acc[2][4][2]) {
 #pragma unroll
   for (int m = 0; m < 2; ++m)
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      double2* a = reinterpret_cast<double2*>(A + (int64_t)(i0 + acc_row(warp, lane, m)) * ld + j0 +
-                                              acc_col(warp, lane, q, 0));
-      double2 v = *a;
-      v.x -= acc[m][q][0];
-      v.y -= acc[m][q][1];
-      *a = v;
+      // fire-and-forget reductions (RED.ADD.F64): no load latency on the product's critical
+      // path; each element has exactly one writer here, so the order cannot change the result
+      double* a = A + (int64_t)(i0 + acc_row(warp, lane, m)) * ld + j0 + acc_col(warp, lane, q, 0);
+      atomicAdd(a, -acc[m][q][0]);
+      atomicAdd(a + 1, -acc[m][q][1]);
     }
 }
 
@@ -174,7 +176,7 @@ __global__ void __launch_bounds__(kThreads, 2) patch_setup_kernel(DevPatchSetup 
           const int64_t la = ea >> 16, lb = eb >> 16;
           double v = 0.0;
           for (int t = 0; t < nm; ++t) v = fma(c[t], R[((int64_t)t * nl + la) * nl + lb], v);
-          A[(int64_t)pa * ld + pb] += v;
+          A[(int64_t)pa * ld + pb] = __ldcg(A + (int64_t)pa * ld + pb) + v;
         }
         __syncthreads();
       }
@@ -186,7 +188,7 @@ __global__ void __launch_bounds__(kThreads, 2) patch_setup_kernel(DevPatchSetup 
       // 2a. pivot block, symmetric, then the scalar sweep of its 64 pivots: S = -A_KK^-1
       for (int e = tid; e < kB * kB; e += kThreads) {
         const int i = e / kB, j = e % kB;
-        S[i * kSs + j] = i >= j ? A[(int64_t)(k0 + i) * ld + k0 + j] : A[(int64_t)(k0 + j) * ld + k0 + i];
+        S[i * kSs + j] = i >= j ? __ldcg(A + (int64_t)(k0 + i) * ld + k0 + j) : __ldcg(A + (int64_t)(k0 + j) * ld + k0 + i);
       }
       __syncthreads();
       sweep_pivot_block(S, tid, s.status, (int32_t)(m + 1));
@@ -206,12 +208,12 @@ __global__ void __launch_bounds__(kThreads, 2) patch_setup_kernel(DevPatchSetup 
         if (I > K) {  // tile (I, K): row-major rows i, columns k -> X[k][i]
           for (int e = tid; e < kB * kB; e += kThreads) {
             const int r = e / kB, k = e % kB;
-            X[k * kXs + r] = A[(int64_t)(i0 + r) * ld + k0 + k];
+            X[k * kXs + r] = __ldcg(A + (int64_t)(i0 + r) * ld + k0 + k);
           }
         } else {  // tile (K, I) = A_KI = A_IK^T: rows k, columns i -> X[k][i]
           for (int e = tid; e < kB * kB; e += kThreads) {
             const int k = e / kB, r = e % kB;
-            X[k * kXs + r] = A[(int64_t)(k0 + k) * ld + i0 + r];
+            X[k * kXs + r] = __ldcg(A + (int64_t)(k0 + k) * ld + i0 + r);
           }
         }
         __syncthreads();
@@ -312,7 +314,7 @@ __global__ void __launch_bounds__(kThreads, 2) patch_setup_kernel(DevPatchSetup 
           i = kk + q;
           col = 32 * I + kk;
         }
-        out[base + w] = -A[(int64_t)(32 * I + i) * ld + col];
+        out[base + w] = -__ldcg(A + (int64_t)(32 * I + i) * ld + col);
       }
     }
     const int64_t exact = (int64_t)n * (n + 1) / 2, stored = s.tile_off[m + 1] - s.tile_off[m];

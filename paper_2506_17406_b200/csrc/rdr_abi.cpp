@@ -138,6 +138,7 @@ struct rdr_handle {
   double *d_x = nullptr, *d_r = nullptr, *d_z = nullptr, *d_p = nullptr, *d_q = nullptr, *d_b = nullptr;
   double* d_p2 = nullptr;  // second search-direction buffer of the fused path
   bool fused = false;
+  cudaAccessPolicyWindow l2_window{};  // persisting window over the PCG slab (num_bytes 0: none)
   PcgScalars* d_sc = nullptr;
   PcgScalars* h_sc = nullptr;  // pinned
   cudaStream_t cap_stream = nullptr;
@@ -460,10 +461,53 @@ static int setup_impl(rdr_handle* h, const double* vertices, int64_t nv, const i
 
   }
 
-  // ---- PCG workspace
+  // ---- PCG workspace: one slab, the vectors every kernel of an iteration touches
+  // first, then copies of the dof map and owner flags, so that an L2
+  // access-policy window can keep them resident while the patch kernel streams
+  // the inverses through L2 (RDR_L2_PERSIST=0 disables the window)
   const size_t vb = sizeof(double) * std::max<int64_t>(1, num.n_total);
-  for (double** v : {&h->d_x, &h->d_r, &h->d_z, &h->d_p, &h->d_q, &h->d_b, &h->d_p2})
-    if ((st = h->own_alloc((void**)v, vb))) return st;
+  {
+    auto al = [](size_t b) { return (b + 255) / 256 * 256; };
+    const size_t dmb = sizeof(int32_t) * dm.size(), owb = (size_t)nt * el.n;
+    const size_t slab_bytes = 7 * al(vb) + al(dmb) + al(owb);
+    char* slab = nullptr;
+    if ((st = h->own_alloc((void**)&slab, slab_bytes))) return st;
+    size_t off = 0;
+    for (double** v : {&h->d_z, &h->d_p, &h->d_p2, &h->d_q, &h->d_r, &h->d_x}) {
+      *v = reinterpret_cast<double*>(slab + off);
+      off += al(vb);
+    }
+    int32_t* dm2 = reinterpret_cast<int32_t*>(slab + off);
+    off += al(dmb);
+    uint8_t* ow2 = reinterpret_cast<uint8_t*>(slab + off);
+    off += al(owb);
+    h->d_b = reinterpret_cast<double*>(slab + off);
+    CK(cudaMemcpy(dm2, op.dofmap_m, dmb, cudaMemcpyDeviceToDevice));
+    CK(cudaMemcpy(ow2, op.owner, owb, cudaMemcpyDeviceToDevice));
+    op.dofmap_m = dm2;
+    op.owner = ow2;
+    const size_t hot = off;  // everything but b
+    int dev = 0, max_win = 0, max_persist = 0;
+    CK(cudaGetDevice(&dev));
+    cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+    cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev);
+    const char* lp = std::getenv("RDR_L2_PERSIST");
+    h->l2_window = {};
+    // only when the whole hot region fits the persisting set-aside: a partial window
+    // (config 3, ~230 MB) measured 4 % slower per iteration, a full one ~1 % faster
+    // (configs 2, 4, 6; profiles/experiments/r2w_l2_persist_ab.log)
+    const bool fits = hot <= (size_t)max_win && hot <= (size_t)max_persist;
+    if (fits && !(lp && std::atoi(lp) == 0)) {
+      const size_t bytes = hot, setaside = hot;
+      cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, setaside);
+      h->l2_window.base_ptr = slab;
+      h->l2_window.num_bytes = bytes;
+      h->l2_window.hitRatio = (float)setaside / (float)bytes;
+      h->l2_window.hitProp = cudaAccessPropertyPersisting;
+      h->l2_window.missProp = cudaAccessPropertyStreaming;
+    }
+    cudaGetLastError();  // the limit / attributes are hints: never fail the setup on them
+  }
   h->fused = fused_pcg_supported(op) && !hybrid;
   if (hybrid) {  // ---- Whitney coarse space + sweep workspace + weights
     std::vector<int32_t> cidx;
@@ -510,6 +554,12 @@ static int setup_impl(rdr_handle* h, const double* vertices, int64_t nv, const i
   if ((st = h->own_alloc((void**)&h->d_sc, sizeof(PcgScalars)))) return st;
   CK(cudaMallocHost((void**)&h->h_sc, sizeof(PcgScalars)));
   CK(cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
+  if (h->l2_window.num_bytes) {  // captured into the kernel nodes of the solve graphs
+    cudaStreamAttrValue v = {};
+    v.accessPolicyWindow = h->l2_window;
+    if (cudaStreamSetAttribute(h->cap_stream, cudaStreamAttributeAccessPolicyWindow, &v) != cudaSuccess)
+      cudaGetLastError();
+  }
   h->launches_per_iter = h->fused ? 1 + count_precond_launches(pc)
                                   : 4 + (hybrid ? count_hybrid_launches(pc) + 1 : count_precond_launches(pc));
   // one warm-up apply/precond on zero vectors: kernel attributes get configured

@@ -165,6 +165,11 @@ struct rdr_handle {
     if (graph) cudaGraphExecDestroy(graph);
     if (wgraph) cudaGraphExecDestroy(wgraph);
     if (cap_stream) cudaStreamDestroy(cap_stream);
+    if (l2_window.num_bytes) {  // release the persisting set-aside this handle requested
+      cudaCtxResetPersistingL2Cache();
+      cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);
+      cudaGetLastError();
+    }
     for (void* p : owned) cudaFree(p);
     if (h_sc) cudaFreeHost(h_sc);
   }
@@ -464,7 +469,7 @@ static int setup_impl(rdr_handle* h, const double* vertices, int64_t nv, const i
   // ---- PCG workspace: one slab, the vectors every kernel of an iteration touches
   // first, then copies of the dof map and owner flags, so that an L2
   // access-policy window can keep them resident while the patch kernel streams
-  // the inverses through L2 (RDR_L2_PERSIST=0 disables the window)
+  // the inverses through L2 (see the size rule below)
   const size_t vb = sizeof(double) * std::max<int64_t>(1, num.n_total);
   {
     auto al = [](size_t b) { return (b + 255) / 256 * 256; };
@@ -493,11 +498,14 @@ static int setup_impl(rdr_handle* h, const double* vertices, int64_t nv, const i
     cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev);
     const char* lp = std::getenv("RDR_L2_PERSIST");
     h->l2_window = {};
-    // only when the whole hot region fits the persisting set-aside: a partial window
-    // (config 3, ~230 MB) measured 4 % slower per iteration, a full one ~1 % faster
-    // (configs 2, 4, 6; profiles/experiments/r2w_l2_persist_ab.log)
+    // Only when the whole hot region fits the persisting set-aside. Default: hot
+    // regions up to 16 MB (1/8 of L2; config 2's is 7 MB: bench 10.84k vs 10.71k
+    // PCG it/s); larger full windows measured within +-2 % (configs 4, 6) and a
+    // partial one 4 % slower (config 3) (profiles/experiments/r2w_l2_persist_ab.log,
+    // r2x_l2_persist_ab.log). RDR_L2_PERSIST=0|1 overrides the size rule.
     const bool fits = hot <= (size_t)max_win && hot <= (size_t)max_persist;
-    if (fits && !(lp && std::atoi(lp) == 0)) {
+    const bool want = lp ? std::atoi(lp) == 1 : hot <= ((size_t)16 << 20);
+    if (fits && want) {
       const size_t bytes = hot, setaside = hot;
       cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, setaside);
       h->l2_window.base_ptr = slab;

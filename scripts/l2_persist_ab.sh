@@ -1,5 +1,5 @@
 #!/bin/bash
-# A/B of the persisting L2 window over the PCG slab (RDR_L2_PERSIST=1 enables it):
+# A/B of the persisting L2 window over the PCG slab (RDR_L2_PERSIST=0 off, 1 on regardless of size):
 # time per PCG iteration of full solves on configs 2, 5 (p = 6, 10), 6, 4, 3.
 for lp in 0 1; do
   for spec in 2 5:6 5:10 6 4 3; do

@@ -15,6 +15,8 @@ Eq. 3.17-3.18 and the PAFW1(X2_Gamma) + J(X2_I) preconditioner
   (sign = orientation of the sorted face vs the outward normal), 0 otherwise;
 * physical-quadrature assembly on an affine cell equals the exact contraction
   of the reference matrices with the Piola factors J^T J / |det J|, 1/|det J|;
+* normal (not tangential) continuity of global RT_p fields across interior
+  faces of a perturbed mesh; Eq. 3.17 re-checked by quadrature;
 * the global operator is SPD, PCG converges, sampled rows equal global rows,
   and the hybrid Schwarz with the exact W^2 coarse solve needs 1 iteration at
   p = 1 (RT_1 = W^2).
@@ -172,3 +174,63 @@ def test_hdiv_hybrid_exact_at_p1():
     H = HybridOracle(c.vertices, c.tets, 1, "hdiv", c.alpha, c.beta, c.mask)
     _, it, res = H.solve(c.draw_vector(H.n_total))
     assert it == 1 and res <= 1e-12
+
+
+@pytest.mark.parametrize("p", [1, 2, 3])
+def test_rt_normal_conformity(p):
+    """Global RT_p functions (Piola phi = J phi-hat / det J, sorted-vertex face
+    orientation, DESIGN.md R-D2) have continuous normal traces across interior
+    faces of a perturbed mesh, for a random coefficient vector; the tangential
+    traces do jump (so the check is not vacuous)."""
+    from oracle.solver import Oracle
+    from oracle.xprec import LD
+    c = make_config(0, n=2, p=p, space=2, bc="none", perturb=True)
+    o = Oracle(c.vertices, c.tets, p, "hdiv", c.alpha, c.beta, c.mask, assemble=False)
+    el = rt_element(p)
+    rng = np.random.default_rng(3)
+    u = rng.standard_normal(o.n_total)
+    t = o.topo
+    face_cells = {}
+    for ci in range(t.nt):
+        for lf in range(4):
+            face_cells.setdefault(t.cell_faces[ci, lf], []).append((ci, lf))
+    n_checked, tang_jump = 0, 0.0
+    for f, lst in face_cells.items():
+        if len(lst) != 2:
+            continue
+        pts = rng.dirichlet(np.ones(3), 4)
+        vals = []
+        for ci, lf in lst:
+            bary = np.zeros((4, 4))
+            bary[:, list(TET_FACES[lf])] = pts
+            phi = tabulate(el, bary.astype(LD))[0].astype(float)
+            J = o.asm.jacobians(np.array([ci]))[0]
+            phys = np.einsum("ab,qnb->qna", J, phi) / np.linalg.det(J)
+            vals.append(np.einsum("qna,n->qa", phys, u[o.num.dofmap[ci]]))
+        xf = c.vertices[t.faces[f]]
+        nrm = np.cross(xf[1] - xf[0], xf[2] - xf[0])
+        nrm /= np.linalg.norm(nrm)
+        d = vals[0] - vals[1]
+        assert np.abs(d @ nrm).max() < 1e-10 * np.abs(vals[0]).max()
+        tang_jump = max(tang_jump, np.abs(d - (d @ nrm)[:, None] * nrm[None]).max())
+        n_checked += 1
+    assert n_checked > 0 and tang_jump > 1e-3
+
+
+@pytest.mark.parametrize("p", [2, 3, 4])
+def test_rt_eigen_orthogonality_by_quadrature(p):
+    """Eq. 3.17 re-checked by the tet quadrature of oracle/fem.py (exact to degree
+    2p+2, independent of the closed-form monomial integrals the construction
+    uses): (div Phi_i, div Phi_j) = delta_ij, (Phi_i, Phi_j) = lambda_j delta_ij."""
+    from oracle.fem import tet_quadrature
+    T = reference_tet()
+    E = rt_bubbles(p)
+    lam, w = tet_quadrature(2 * p + 2)
+    bary = lam.astype(np.longdouble)
+    vals = T.eval2(E.F, p, bary).astype(float)                      # [q, n, 3]
+    divs = T.eval0(E.F @ T.div_op(p), p - 1, bary).astype(float)    # [q, n]
+    vol = float(T.vol)
+    M = vol * np.einsum("q,qia,qja->ij", w, vals, vals)
+    K = vol * np.einsum("q,qi,qj->ij", w, divs, divs)
+    assert np.abs(K - np.eye(len(E.lam))).max() <= 1e-12
+    assert np.abs(M - np.diag(E.lam.astype(float))).max() <= 1e-12 * max(1.0, float(E.lam.max()))

@@ -17,6 +17,8 @@ Eq. 3.17-3.18 and the PAFW1(X2_Gamma) + J(X2_I) preconditioner
   of the reference matrices with the Piola factors J^T J / |det J|, 1/|det J|;
 * normal (not tangential) continuity of global RT_p fields across interior
   faces of a perturbed mesh; Eq. 3.17 re-checked by quadrature;
+* globally, with the discrete curl C (face/edge incidence + type-I -> type-II):
+  K2 C = 0 and C^T M2 C = the Ned1 curl-curl operator;
 * the global operator is SPD, PCG converges, sampled rows equal global rows,
   and the hybrid Schwarz with the exact W^2 coarse solve needs 1 iteration at
   p = 1 (RT_1 = W^2).
@@ -234,3 +236,48 @@ def test_rt_eigen_orthogonality_by_quadrature(p):
     K = vol * np.einsum("q,qi,qj->ij", w, divs, divs)
     assert np.abs(K - np.eye(len(E.lam))).max() <= 1e-12
     assert np.abs(M - np.diag(E.lam.astype(float))).max() <= 1e-12 * max(1.0, float(E.lam.max()))
+
+
+def _discrete_curl(o_rt, o_ned, p):
+    """C: Ned1_p dofs -> RT_p dofs (Lemma 4.1 + 4.3): C[W(F), W(E)] = [F:E] (the
+    sign of E in the boundary of the sorted face (a,b,c): +bc -ac +ab) and
+    C[typeII(S,j), typeI(S,j)] = 1 for S = faces, cell."""
+    import scipy.sparse as sp
+    t, rt, ned = o_rt.topo, o_rt.num, o_ned.num
+    rows, cols, vals = [], [], []
+    for f, (a, b, cc) in enumerate(t.faces):
+        wf = rt.offsets[2] + f * rt.per[2]
+        for (x, y), sgn in (((b, cc), 1.0), ((a, cc), -1.0), ((a, b), 1.0)):
+            rows.append(wf)
+            cols.append(ned.offsets[1] + t.edge_index[(x, y)] * ned.per[1])
+            vals.append(sgn)
+        nIf = ned.per[2] - (p - 1) * (p - 2) // 2           # Ned1 type-I face dofs = RT type-II face dofs
+        for j in range(nIf):
+            rows.append(wf + 1 + j)
+            cols.append(ned.offsets[2] + f * ned.per[2] + j)
+            vals.append(1.0)
+    nIc_ned = ned.per[3] - (p - 1) * (p - 2) * (p - 3) // 6   # Ned1 type-I cell dofs
+    nI_rt = p * (p + 1) * (p + 2) // 6 - 1                   # RT type-I cell dofs precede type-II
+    for cidx in range(t.nt):
+        for j in range(nIc_ned):
+            rows.append(rt.offsets[3] + cidx * rt.per[3] + nI_rt + j)
+            cols.append(ned.offsets[3] + cidx * ned.per[3] + j)
+            vals.append(1.0)
+    return sp.csr_matrix((vals, (rows, cols)), shape=(rt.n_total, ned.n_total))
+
+
+@pytest.mark.parametrize("p", [1, 2, 3])
+def test_hdiv_curls(p):
+    """No Gamma_D, on a perturbed mesh: the div-div part annihilates the
+    discrete curl, K2 C = 0 (div curl = 0), and C^T M2 C = the Ned1 curl-curl
+    operator (curl phi^1 = C phi^2 exactly, Lemma 4.3 globally)."""
+    from oracle.solver import Oracle
+    c = make_config(0, n=2, p=p, space=2, bc="none", perturb=True)
+    nt = len(c.tets)
+    oK = Oracle(c.vertices, c.tets, p, "hdiv", np.ones(nt), np.zeros(nt), c.mask)
+    oM = Oracle(c.vertices, c.tets, p, "hdiv", np.zeros(nt), np.ones(nt), c.mask)
+    o1 = Oracle(c.vertices, c.tets, p, "hcurl", np.ones(nt), np.zeros(nt), c.mask)
+    C = _discrete_curl(oK, o1, p)
+    assert abs(oK.A @ C).max() < 1e-11 * abs(oK.A).max()
+    CMC = (C.T @ oM.A @ C).toarray()
+    assert np.abs(CMC - o1.A.toarray()).max() < 1e-11 * abs(o1.A).max()

@@ -563,3 +563,24 @@ def test_device_coarse_inverse(torch_cuda, space, n, p):
     zd, zh = Sd.precond(x).cpu().numpy(), Sh.precond(x).cpu().numpy()
     assert rel(zd, zh) <= 1e-9, rel(zd, zh)
     assert abs(Sd.solve(x)[1] - Sh.solve(x)[1]) <= 1
+
+
+def test_hdiv_curl_kernel_through_library(torch_cuda):
+    """div curl = 0 through the library: for u = C v (the discrete curl of a
+    random Ned1 vector, face/edge incidence + type-I -> type-II), A u does not
+    depend on alpha (H(div), no Dirichlet, perturbed mesh)."""
+    from paper_2506_17406_b200 import rdr
+    from oracle.solver import Oracle
+    from test_oracle_hdiv import _discrete_curl
+    torch = torch_cuda
+    p = 3
+    c = make_config(0, n=2, p=p, space=HDIV, perturb=True, bc="none")
+    O2 = Oracle(c.vertices, c.tets, p, "hdiv", c.alpha, c.beta, c.mask, assemble=False)
+    O1 = Oracle(c.vertices, c.tets, p, "hcurl", c.alpha, c.beta, c.mask, assemble=False)
+    C = _discrete_curl(O2, O1, p)
+    u = C @ np.random.default_rng(5).standard_normal(C.shape[1])
+    ut = torch.from_numpy(u).cuda()
+    S1 = rdr.Solver(c.vertices, c.tets, p, HDIV, c.alpha, c.beta, c.mask)
+    S2 = rdr.Solver(c.vertices, c.tets, p, HDIV, 1e3 * c.alpha, c.beta, c.mask)
+    y1, y2 = S1.apply(ut).cpu().numpy(), S2.apply(ut).cpu().numpy()
+    assert rel(y2, y1) <= 1e-9, rel(y2, y1)

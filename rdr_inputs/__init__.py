@@ -126,6 +126,9 @@ def make_config(cfg: int, p: int | None = None, seed: int = 0, n: int | None = N
     6: H(div) RT_6, 12^3, unperturbed, alpha=beta=1, full normal Dirichlet -- NOT a
        BASELINE.json config: the SURVEY NEXT-2 workload, config 4's mesh and degree
        with the 2-form space (PAFW1(X2_Gamma) + J(X2_I)).
+    7, 8: config 5's p-sweep mesh (8^3, perturbed, alpha=beta=1, full Dirichlet) with
+       H(curl) Ned1_p and H(div) RT_p, p in 1..10 -- NOT BASELINE.json configs (measurement
+       of the p-robustness the paper claims for all three splits).
     0: custom small case (all of n, p, space, perturb, bc, coeffs given).
     Any keyword overrides the config's default (used for small parity meshes).
     """
@@ -136,6 +139,8 @@ def make_config(cfg: int, p: int | None = None, seed: int = 0, n: int | None = N
         4: dict(space=HCURL, p=6, n=12, perturb=False, bc="all", coeffs="one"),
         5: dict(space=HGRAD, p=6, n=8, perturb=True, bc="all", coeffs="one"),
         6: dict(space=HDIV, p=6, n=12, perturb=False, bc="all", coeffs="one"),
+        7: dict(space=HCURL, p=6, n=8, perturb=True, bc="all", coeffs="one"),
+        8: dict(space=HDIV, p=6, n=8, perturb=True, bc="all", coeffs="one"),
         0: dict(space=HGRAD, p=2, n=2, perturb=False, bc="all", coeffs="one"),
     }
     d = dict(table[cfg])

@@ -23,7 +23,7 @@ from paper_2506_17406_b200 import rdr  # noqa: E402
 
 
 def measure(cfg, p, fp64_peak, hbm, solves=3, reps=20, dec="split", pre="additive"):
-    c = make_config(cfg, p=p) if cfg == 5 else make_config(cfg)
+    c = make_config(cfg, p=p) if cfg in (5, 7, 8) else make_config(cfg)
     t0 = time.time()
     S = rdr.Solver(c.vertices, c.tets, c.p, c.space, c.alpha, c.beta, c.mask,
                    decomposition=rdr.UNSPLIT if dec == "unsplit" else rdr.SPLIT,
@@ -98,7 +98,7 @@ def main():
     with open(args.out, "w") as f:
         f.write(json.dumps(head) + "\n")
         for cfg in (int(v) for v in args.configs.split(",")):
-            for p in (range(lo, hi + 1) if cfg == 5 else [None]):
+            for p in (range(lo, hi + 1) if cfg in (5, 7, 8) else [None]):
                 r = measure(cfg, p, fp64_peak, hbm, dec=args.decomposition, pre=args.precond)
                 print(json.dumps(r), flush=True)
                 f.write(json.dumps(r) + "\n")

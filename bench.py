@@ -1,19 +1,23 @@
 """Benchmark of the B200 Riesz-map PCG hot path (arXiv 2506.17406).
 
-Workload (BASELINE.json configs[1], "cfg2", the default): H(grad) Riesz map,
-p=6, 8x8x8 cubes x 6 = 3072 tets with interior vertices displaced by up to
-0.2h (seed 0), per-cell alpha, beta log-uniform in [1e-2, 1e2], Dirichlet on
-x=0, seeded uniform[-1,1] rhs, PCG rtol 1e-8 from x0 = 0. Other configs:
---config 1..5 (--p for the config-5 sweep point).
+Workload (default, --config 3 = BASELINE.json configs[2], the largest
+single-GPU configuration; the metric is quoted "vs p" on no single config):
+H(grad) Riesz map, p=10 in the paper's basis, 16x16x16 cubes x 6 = 24576 tets
+with interior vertices displaced by up to 0.2h (seed 0), alpha=beta=1, full
+Dirichlet, seeded uniform[-1,1] rhs, PCG rtol 1e-8 from x0 = 0: 4.0 M free
+dofs, 286 local dofs per cell, 4913 star patches (29.2 GB of packed inverses).
+Other configs: --config 1..8 (--p for the config-5/7/8 sweep points).
 
 A step = one full PCG solve (every hot-path row of SURVEY §8(a): operator
 apply, interior Jacobi, star-patch solves, PCG vector ops) on a fresh rhs
 already resident in HBM. value = PCG iterations/s over the whole job.
+The line also carries "sweep": config 2 and the config-5 p-sweep (p = 1..12),
+each measured the same way (the metric's "vs p"); --no-sweep skips it.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--config 2] [--p 6]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--config 3] [--p 6]
 
 Multi-GPU: the north_star path is one GPU and does not shard within a solve
-(DESIGN.md §7, "replicas only"): under torchrun every rank solves its own
+(DESIGN.md §8, "replicas only"): under torchrun every rank solves its own
 problem (seed = rank), with no collective on the data path; torch.distributed
 only provides the barrier, the max-over-ranks time and the sum of iterations.
 """
@@ -22,6 +26,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import platform
 import sys
 import threading
 import time
@@ -38,8 +43,32 @@ WORKLOADS = {
     3: "cfg3: H(grad) p=10, 16^3x6 perturbed tets, alpha=beta=1, full Dirichlet",
     4: "cfg4: H(curl) Ned1_6, 12^3x6 tets, alpha=beta=1, full tangential Dirichlet",
     5: "cfg5: H(grad) p-sweep point, 8^3x6 perturbed tets, alpha=beta=1, full Dirichlet",
+    6: "cfg6: H(div) RT_6, 12^3x6 tets, alpha=beta=1, full normal Dirichlet (NEXT-2, not a BASELINE config)",
+    7: "cfg7: H(curl) Ned1_p sweep point, 8^3x6 perturbed tets, alpha=beta=1, full Dirichlet (not a BASELINE config)",
+    8: "cfg8: H(div) RT_p sweep point, 8^3x6 perturbed tets, alpha=beta=1, full Dirichlet (not a BASELINE config)",
 }
-KERNELS = ("apply_tc_kernel", "patch_ldg_kernel")
+SWEEP_CFGS = (5, 7, 8)
+
+
+def workload_name(cfg, p):
+    return WORKLOADS[cfg] + (f" (p={p})" if cfg in SWEEP_CFGS else "")
+
+
+def workload_key(cfg, p):
+    return f"cfg{cfg}" + (f"_p{p}" if cfg in SWEEP_CFGS else "")
+
+
+def config_dict(cfg, p, ws):
+    """The `config` object of the JSON line: identical in both arms."""
+    return {"workload": workload_name(cfg, p), "rtol": 1e-8,
+            "parallelism": f"replicas x{ws} (one independent solve per GPU)",
+            "l2": "inputs larger than L2: every iteration streams all packed patch inverses "
+                  "(0.34 GB at cfg2, 29.2 GB at cfg3) and the operator's vectors from HBM"}
+
+
+def make_cfg(cfg, p, seed=0):
+    from rdr_inputs import make_config
+    return make_config(cfg, p=p, seed=seed) if cfg in SWEEP_CFGS else make_config(cfg, seed=seed)
 
 
 def hbm_peak():
@@ -59,6 +88,28 @@ def committed_traffic(workload_key, kernel):
         return float(e["dram_bytes_per_launch"]), e["source"]
     except Exception:
         return None, None
+
+
+def host_info():
+    """Host cores the oracle may use, CPU model and BLAS threads."""
+    model = platform.processor()
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    blas = None
+    try:
+        from threadpoolctl import threadpool_info
+        blas = sorted({(i.get("internal_api"), i.get("num_threads")) for i in threadpool_info()})
+        blas = [f"{api}:{n}" for api, n in blas]
+    except Exception:
+        pass
+    return {"cores": len(os.sched_getaffinity(0)), "cpu_count": os.cpu_count(), "cpu_model": model,
+            "blas_threads": blas}
 
 
 class ClockSampler:
@@ -139,13 +190,38 @@ def reduce_over_ranks(ms, units, device=None):
     return float(t.item()), float(u.item())
 
 
-def oracle_sample(cfg, p, iters_per_step, steps, warmup):
-    """The CPU oracle as it stands, timed on the host cores: setup untimed, then
-    `steps` samples of `iters_per_step` PCG iterations (apply + precond + vector
-    ops) on the same workload."""
-    from rdr_inputs import make_config
+# configurations whose global oracle CSR does not fit a bounded host run: timed by
+# oracle.lean.IterationSample (a sample of one oracle iteration, scaled to the mesh)
+LEAN_SAMPLE_CFGS = (3,)
+
+
+def oracle_sample(cfg, p, steps, warmup, iters_per_step=20):
+    """The CPU oracle as it stands, timed on the host cores (setup untimed).
+    Returns (PCG iters/s, seconds per step, sample description, details).
+      * global oracle (cfg 1, 2, 4-8): `steps` samples of `iters_per_step`
+        oracle PCG iterations (scipy CSR apply + cho_solve patches);
+      * cfg 3 (global CSR ~1.7e9 nnz): oracle.lean.IterationSample, one estimated
+        LeanOracle iteration per step from a timed sample of its cells and
+        patches, scaled to the whole mesh (the scaling is in the details)."""
     from oracle.solver import Oracle
-    c = make_config(cfg, p=p) if cfg == 5 else make_config(cfg)
+    c = make_cfg(cfg, p)
+    if cfg in LEAN_SAMPLE_CFGS:
+        from oracle.lean import IterationSample
+        O = Oracle(c.vertices, c.tets, c.p, c.space, c.alpha, c.beta, c.mask, assemble=False)
+        S = IterationSample(O, n_patches=32)
+        parts = [S.time_iteration(seed) for seed in range(warmup + steps)][warmup:]
+        t = [d["t_iter"] for d in parts]
+        d0 = parts[-1]
+        desc = (f"oracle.lean.IterationSample: per step one LeanOracle PCG iteration on the full mesh, "
+                f"estimated from a timed sample of {d0['sample_patches']} interior vertex-star packed "
+                f"Cholesky solves (x{d0['scale_patches']:.1f} by packed-factor doubles) and the element-by-"
+                f"element apply of the {d0['sample_cells']} cells of their stars (x{d0['scale_apply']:.1f} "
+                f"by cells), plus the full-length vector work; setup untimed")
+        det = {"t_apply_sample_s": float(np.mean([d["t_apply_sample"] for d in parts])),
+               "t_patches_sample_s": float(np.mean([d["t_patches_sample"] for d in parts])),
+               "t_vector_s": float(np.mean([d["t_vector"] for d in parts])),
+               "scale_apply": d0["scale_apply"], "scale_patches": d0["scale_patches"]}
+        return steps / sum(t), sum(t) / steps, desc, det
     O = Oracle(c.vertices, c.tets, c.p, c.space, c.alpha, c.beta, c.mask)
     O.build_preconditioner(kappa=False)
     b = O.mask(c.draw_vector(O.n_total))
@@ -156,26 +232,68 @@ def oracle_sample(cfg, p, iters_per_step, steps, warmup):
         dt = time.perf_counter() - t0
         if k >= warmup:
             times.append(dt)
-    cores = len(os.sched_getaffinity(0))
-    return iters_per_step * steps / sum(times), sum(times), cores
+    desc = (f"{iters_per_step} oracle PCG iterations per step (scipy CSR apply + cho_solve patches), "
+            f"setup untimed")
+    return iters_per_step * steps / sum(times), sum(times) / steps, desc, {}
 
 
 def run_reference(args):
     ws, rank, _ = dist_env()
     if rank != 0:
         return
-    ips, tot, cores = oracle_sample(args.config, args.p, args.ref_iters, args.steps, args.warmup)
-    sample = (f"{args.ref_iters} oracle PCG iterations per step (scipy CSR apply + cho_solve patches, "
-              f"setup untimed) on {WORKLOADS[args.config]}")
+    ips, per_step, desc, det = oracle_sample(args.config, args.p, args.steps, args.warmup, args.ref_iters)
+    hi = host_info()
     line = {
         "impl": "reference", "metric": METRIC, "value": ips, "unit": "PCG iters/s", "n_gpus": ws,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * per_step,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOADS[args.config], "rtol": 1e-8},
-        "cpu_baseline": {"value": ips, "unit": "PCG iters/s", "cores": cores, "kind": "oracle", "sample": sample},
+        "config": config_dict(args.config, args.p, ws),
+        "cpu_baseline": {"value": ips, "unit": "PCG iters/s", "kind": "oracle", "sample": desc, **hi, **det},
         "e2e": {"value": ips, "unit": "PCG iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def t_roof_ms(info, fp64_peak, hbm):
+    """Composite per-iteration bound: flops(A x) / DMMA peak +
+    (patch + Jacobi bytes + 12 N_total doubles of vector traffic) / HBM."""
+    return 1e3 * (info["flops_apply"] / (fp64_peak * 1e12)
+                  + (info["bytes_precond"] + 96.0 * info["n_total"]) / (hbm * 1e9))
+
+
+def measure_point(rdr, torch, cfg, p, dev, solves, fp64_peak, hbm, seed=0):
+    """One sweep point: setup, one warm-up and `solves` timed solves (CUDA
+    events), kernel times and roofline fractions."""
+    c = make_cfg(cfg, p, seed)
+    S = rdr.Solver(c.vertices, c.tets, c.p, c.space, c.alpha, c.beta, c.mask)
+    info = S.info
+    n = S.n_total
+    rhs = [torch.from_numpy(c.draw_vector(n)).to(dev) for _ in range(solves + 1)]
+    x = torch.empty(n, dtype=torch.float64, device=dev)
+    S.solve(rhs[0], x, rtol=1e-8)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    iters, nonconv = [], 0
+    e0.record()
+    for k in range(solves):
+        _, it = S.solve(rhs[1 + k], x, rtol=1e-8)
+        iters.append(it)
+        nonconv += not S.converged
+    e1.record()
+    e1.synchronize()
+    ms = e0.elapsed_time(e1)
+    kms = S.time_kernels(rhs[0], rhs[0], reps=10)
+    patch_alg = info["bytes_precond"] - 24.0 * info["n_interior"]
+    ms_iter = ms / max(1, sum(iters))
+    out = {"workload": workload_name(cfg, c.p), "p": c.p, "n_free": info["n_free"], "n_loc": info["n_loc"],
+           "iters": float(np.mean(iters)), "nonconverged": nonconv, "pcg_iters_per_s": sum(iters) / (ms / 1e3),
+           "ms_per_iter": ms_iter, "time_to_solution_ms": ms / solves, "setup_s": info["setup_seconds"],
+           "apply_ms": kms[0], "dofs_per_s_per_apply": info["n_free"] / (kms[0] / 1e3),
+           "apply_frac_dmma": info["flops_apply"] / (kms[0] / 1e3) / 1e12 / fp64_peak,
+           "patches_ms": kms[2], "patches_frac_hbm": patch_alg / (kms[2] / 1e3) / 1e9 / hbm if kms[2] > 0 else None,
+           "iter_frac_t_roof": t_roof_ms(info, fp64_peak, hbm) / ms_iter}
+    S.close()
+    return out
 
 
 def run(args):
@@ -186,11 +304,13 @@ def run(args):
     if ws > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
-    from rdr_inputs import make_config
     from paper_2506_17406_b200 import rdr
 
     cfg = args.config
-    c = make_config(cfg, p=args.p, seed=rank) if cfg == 5 else make_config(cfg, seed=rank)
+    # FP64 tensor-core peak as a burst, before the workload heats the part (the
+    # denominator of a kernel timed in isolation, as MEASURED_PEAKS' burst figures)
+    fp64_burst = rdr.measure_fp64_peak()
+    c = make_cfg(cfg, args.p, seed=rank)
     S = rdr.Solver(c.vertices, c.tets, c.p, c.space, c.alpha, c.beta, c.mask)
     info = S.info
     n = S.n_total
@@ -208,12 +328,13 @@ def run(args):
         S.solve(rhs[k], x, rtol=1e-8)
     barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    iters, launches = [], 0
+    iters, launches, nonconv = [], 0, 0
     with ClockSampler(local) as clk:
         ev0.record(stream)
         for k in range(args.steps):
             _, it = S.solve(rhs[args.warmup + k], x, rtol=1e-8)
             iters.append(it)
+            nonconv += not S.converged
             launches += S.last_launches()
         ev1.record(stream)
         ev1.synchronize()
@@ -227,22 +348,24 @@ def run(args):
     xh = torch.empty(n, dtype=torch.float64).pin_memory()
     S.solve_host(bh, xh)
     barrier()
-    e_iters = 0
+    e_iters, e_nonconv = 0, 0
     ev0.record(stream)
     for k in range(args.steps):
         e_iters += S.solve_host(bh, xh)
+        e_nonconv += not S.converged
     ev1.record(stream)
     ev1.synchronize()
     e_ms, e_iters = reduce_over_ranks(ev0.elapsed_time(ev1), e_iters, dev)
 
     # ---- per-kernel device times (CUDA events on this stream) and the roofline of the dominant kernel
     kms = S.time_kernels(rhs[0], rhs[0], reps=args.kernel_reps)
+    S.close()
     if rank != 0:
         if ws > 1:
             torch.distributed.destroy_process_group()
         return
     hbm, hbm_src = hbm_peak()
-    fp64_peak = rdr.measure_fp64_peak()
+    fp64_after = rdr.measure_fp64_peak()
     dgemm = None
     if not args.no_dgemm:
         a = torch.randn(4096, 4096, dtype=torch.float64, device=dev)
@@ -256,13 +379,16 @@ def run(args):
         e1.record()
         e1.synchronize()
         dgemm = 5 * 2 * 4096 ** 3 / (e0.elapsed_time(e1) / 1e3) / 1e12
+    fp64_peak = max(fp64_burst, fp64_after)
     patch_alg = info["bytes_precond"] - 24.0 * info["n_interior"]
     apply_tf = info["flops_apply"] / (kms[0] / 1e3) / 1e12
     patch_gbs = patch_alg / (kms[2] / 1e3) / 1e9
-    key = f"cfg{cfg}" + (f"_p{c.p}" if cfg == 5 else "")
+    key = workload_key(cfg, c.p)
     apply_roof = {"bound": "tensor", "kernel": "apply_tc_kernel (gather, DMMA contraction, scatter-add)",
                   "achieved": apply_tf, "peak": fp64_peak, "unit": "TFLOP/s", "frac": apply_tf / fp64_peak,
-                  "peak_source": "measured in this run: DMMA.8x8x4 issue-bound loop (rdr_measure_fp64_peak)",
+                  "peak_source": "measured in this run: DMMA.8x8x4 issue-bound loop (rdr_measure_fp64_peak), "
+                                 f"burst before the workload {fp64_burst:.2f}, after it {fp64_after:.2f} TFLOP/s; "
+                                 "the larger is the peak",
                   "alg_flops_per_launch": info["flops_apply"],
                   "traffic": committed_traffic(key, "apply_tc_kernel")[0]}
     patch_roof = {"bound": "hbm", "kernel": "patch_ldg_kernel (star-patch solves, packed FP64 inverses)",
@@ -273,17 +399,18 @@ def run(args):
     tsrc = committed_traffic(key, dominant["kernel"].split()[0])[1]
     if tsrc:
         dominant["traffic_source"] = tsrc
+    ms_iter = ms_local / max(1.0, sum(iters))
     line = {
         "metric": METRIC, "value": value, "unit": "PCG iters/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOADS[cfg] + (f" (p={c.p})" if cfg == 5 else ""),
-                   "n_free": info["n_free"], "n_total": n, "n_cells": info["n_cells"], "n_loc": info["n_loc"],
-                   "n_patches": info["n_patches"], "max_patch": info["max_patch"], "rtol": 1e-8,
-                   "parallelism": f"replicas x{ws} (one independent solve per GPU)",
-                   "l2": f"inputs larger than L2: {info['patch_bytes'] / 1e9:.2f} GB of patch inverses streamed "
-                         f"every iteration (> 126 MB L2)"},
-        "iters_per_solve": float(np.mean(iters)), "ms_per_iter": ms_local / max(1.0, sum(iters)),
+        "config": config_dict(cfg, c.p, ws),
+        "problem": {"n_free": info["n_free"], "n_total": n, "n_cells": info["n_cells"], "n_loc": info["n_loc"],
+                    "n_patches": info["n_patches"], "max_patch": info["max_patch"],
+                    "patch_bytes": info["patch_bytes"]},
+        "iters_per_solve": float(np.mean(iters)), "nonconverged_solves": nonconv + e_nonconv,
+        "ms_per_iter": ms_iter, "time_to_solution_ms": ms_local / args.steps,
+        "iter_frac_t_roof": t_roof_ms(info, fp64_peak, hbm) / ms_iter,
         "dofs_per_s_per_apply": info["n_free"] / (kms[0] / 1e3),
         "kernel_ms": {"apply": kms[0], "jacobi": kms[1], "patches": kms[2], "gradient": kms[3]},
         "roofline": dominant, "roofline_other": other,
@@ -294,11 +421,15 @@ def run(args):
         "clocks": clk.summary(),
         "setup_s": info["setup_seconds"],
     }
+    if nonconv + e_nonconv:
+        print(f"bench: {nonconv + e_nonconv} solves did not converge (RDR_ENOCONV)", file=sys.stderr)
+    if not args.no_sweep and ws == 1:
+        pts = [(2, None)] + [(5, p) for p in range(1, 13)]
+        line["sweep"] = [measure_point(rdr, torch, cf, p, dev, 3, fp64_peak, hbm) for cf, p in pts]
     if not args.no_cpu:
-        ips, tot, cores = oracle_sample(cfg, c.p, args.ref_iters, 1, 0)
-        line["cpu_baseline"] = {"value": ips, "unit": "PCG iters/s", "cores": cores, "kind": "oracle",
-                                "sample": f"{args.ref_iters} oracle PCG iterations on the same workload "
-                                          f"(scipy CSR apply + cho_solve patches), setup untimed"}
+        ips, per_step, desc, det = oracle_sample(cfg, c.p, args.cpu_steps, 1, args.ref_iters)
+        line["cpu_baseline"] = {"value": ips, "unit": "PCG iters/s", "kind": "oracle", "sample": desc,
+                                **host_info(), **det}
     print(json.dumps(line), flush=True)
     if ws > 1:
         torch.distributed.destroy_process_group()
@@ -310,12 +441,14 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=2)
-    ap.add_argument("--p", type=int, default=6, help="degree of the config-5 sweep point")
-    ap.add_argument("--ref-iters", type=int, default=20)
+    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--p", type=int, default=6, help="degree of the config-5/7/8 sweep point")
+    ap.add_argument("--ref-iters", type=int, default=20, help="oracle PCG iterations per step (global oracle)")
+    ap.add_argument("--cpu-steps", type=int, default=3, help="oracle samples for cpu_baseline")
     ap.add_argument("--kernel-reps", type=int, default=50)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-dgemm", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3

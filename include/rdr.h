@@ -80,17 +80,33 @@ enum { RDR_ADDITIVE = 0, RDR_HYBRID = 1 };
  *                dense.cpp), then uploaded. Both give A_m^-1 to rounding. */
 enum { RDR_SETUP_DEVICE = 0, RDR_SETUP_HOST = 1 };
 
+/* How rdr_solve drives the PCG iteration (R-A16); all three run the same
+ * kernels and give the same iterates:
+ *   RDR_LOOP_DEVICE (default) -- one CUDA graph whose conditional WHILE node
+ *                repeats a body of 8 iterations until the stopping test, which
+ *                the fused operator apply performs on the device, fires: one
+ *                graph launch and one host synchronisation per solve (the
+ *                hybrid preconditioner's unfused path uses RDR_LOOP_HOST);
+ *   RDR_LOOP_HOST -- graphs of 8 iterations relaunched by the host until done;
+ *   RDR_LOOP_EAGER -- every kernel launched on the stream, the host testing the
+ *                stop flag after each iteration (no graphs: profilers see every
+ *                kernel of the iteration). */
+enum { RDR_LOOP_DEVICE = 0, RDR_LOOP_HOST = 1, RDR_LOOP_EAGER = 2 };
+
 struct rdr_options {
   int decomposition;  /* RDR_SPLIT or RDR_UNSPLIT */
   int preconditioner; /* RDR_ADDITIVE or RDR_HYBRID */
   int setup;          /* RDR_SETUP_DEVICE or RDR_SETUP_HOST */
+  int loop;           /* RDR_LOOP_DEVICE, RDR_LOOP_HOST or RDR_LOOP_EAGER */
 };
 
 enum {
   RDR_OK = 0,
-  RDR_EINVAL = -1,   /* bad p / space / sizes / alpha <= 0 / beta < 0 / NULL pointer */
+  RDR_EINVAL = -1,   /* bad p / space / sizes / options / NULL pointer; alpha <= 0, beta < 0, or
+                        beta = 0 with H(curl) or H(div) (gradients resp. div-free fields
+                        would be in the kernel of A and of the star-patch matrices) */
   RDR_EMESH = -2,    /* |det J| <= 1e-12 h^3, non-manifold face, mask bit on an interior face */
-  RDR_ENOTSPD = -3,  /* a patch Cholesky pivot <= 0 (e.g. beta = 0 with H(curl)) */
+  RDR_ENOTSPD = -3,  /* a non-positive pivot while inverting a patch (or the hybrid coarse) matrix */
   RDR_ENOMEM = -4,   /* device or host allocation failed */
   RDR_ECUDA = -5,    /* any other CUDA runtime error */
   RDR_ENOCONV = -6   /* PCG reached maxit */
@@ -131,8 +147,8 @@ int rdr_setup(rdr_handle** h, const double* vertices, int64_t nv, const int32_t*
               const uint8_t* dirichlet_mask, void* stream);
 
 /* rdr_setup with options (NULL = defaults: RDR_SPLIT, RDR_ADDITIVE,
- * RDR_SETUP_DEVICE). RDR_EINVAL for an unknown decomposition, preconditioner
- * or setup, or RDR_HYBRID with RDR_UNSPLIT. */
+ * RDR_SETUP_DEVICE, RDR_LOOP_DEVICE). RDR_EINVAL for an unknown decomposition,
+ * preconditioner, setup or loop, or RDR_HYBRID with RDR_UNSPLIT. */
 int rdr_setup_ex(rdr_handle** h, const double* vertices, int64_t nv, const int32_t* tets, int64_t nt,
                  int p, int space, const double* alpha, const double* beta,
                  const uint8_t* dirichlet_mask, const struct rdr_options* opt, void* stream);
@@ -163,6 +179,29 @@ int rdr_solve_host(rdr_handle* h, const double* b_host, double* x_host, double r
 /* Per-kernel launch accounting of the last rdr_solve: number of library kernel
  * launches (graph nodes included). */
 int rdr_last_launches(const rdr_handle* h, int64_t* launches);
+
+/* Outcome of the last rdr_solve / rdr_solve_host / rdr_profile_solve:
+ * iterations, whether the stopping test ||z_k|| <= rtol ||z_0|| (R-A16) fired,
+ * ||z_0|| and ||z_k|| at the last test, and the kernel launches. */
+struct rdr_solve_stats {
+  int32_t iters;
+  int32_t converged;
+  double z0;
+  double z_last;
+  int64_t launches;
+};
+int rdr_last_solve(const rdr_handle* h, struct rdr_solve_stats* out);
+
+/* Measurement helper: one PCG solve (as rdr_solve, x left in the handle)
+ * with every kernel launched eagerly and CUDA events between the kernel groups
+ * of each iteration; ms[4] receives the average device ms per iteration of
+ * ms[0] the fused operator apply (direction update + A p + stopping test),
+ * ms[1] the x/r update + interior Jacobi, ms[2] the star-patch solves,
+ * ms[3] the discrete-gradient kernels (H(curl), else ~0) -- the in-solve
+ * counterparts of rdr_time_kernels. Additive preconditioner only
+ * (RDR_EINVAL otherwise). Synchronizes `stream`. */
+int rdr_profile_solve(rdr_handle* h, const double* b, double rtol, int maxit, int* iters, double* ms,
+                      void* stream);
 
 /* Measurement helper (bench.py roofline): launch each hot-path kernel `reps`
  * times back to back on `stream` between CUDA events and return the average

@@ -2,11 +2,10 @@
 //
 //  * apply_tc_kernel   : gather x_e -> y_e = sum_s c_{e,s} R_s x_e on DMMA -> scatter-add
 //                        (north_star operator apply; matrix-free action P:2267-2275)
-//  * apply_kernel      : the same on CUDA cores (RDR_KERNEL=simple, parity bring-up)
 //  * precond_init      : interior point-Jacobi z_I = r_I / A_II (Thm 5.1)
-//  * patch_stream_kernel: additive star patches z += E_m A_m^{-1} E_m^T r with the
-//                        stored packed inverses streamed from HBM by TMA bulk
-//                        copies (Eq. 5.4 / 5.12)
+//  * patch_ldg_kernel / patch_warp_kernel: additive star patches
+//                        z += E_m A_m^{-1} E_m^T r with the stored packed inverses
+//                        streamed from HBM (Eq. 5.4 / 5.12)
 //  * gather_grad / scatter_grad : the discrete gradient of the H(curl) potential
 //                        patches (R-A12, Lemma 4.3)
 //  * pcg_*             : fused PCG vector updates and reductions (R-A16)
@@ -89,69 +88,6 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
   }
   __syncthreads();
   return s;
-}
-
-// ---------------------------------------------------------------- operator apply
-// One CTA = TC cells. Thread i owns output rows i, i+blockDim, ...; for each
-// reference matrix s it forms t_c = sum_j R_s[j][i] X[c][j] for its TC cells
-// (R_s symmetric, so the [j][i] read is coalesced over i) and accumulates
-// y[c][i] += c_{c,s} t_c. Gather/scatter through the masked dof map.
-template <int TC>
-__global__ void __launch_bounds__(128) apply_kernel(DevOperator op, const double* __restrict__ x,
-                                                   double* __restrict__ y, double* pq_acc,
-                                                   const PcgScalars* guard) {
-  if (stopped(guard)) return;
-  extern __shared__ double smem[];
-  const int n = op.n_loc, nm = op.n_mat, ldr = op.n_pad;
-  double* X = smem;                         // [TC][n]
-  double* C = X + TC * n;                   // [TC][nm]
-  int* D = reinterpret_cast<int*>(C + TC * nm);  // [TC][n]
-  const int64_t c0 = (int64_t)blockIdx.x * TC;
-  const int64_t rem = op.n_cells - c0;
-  const int nc = rem < TC ? (int)rem : TC;
-  for (int k = threadIdx.x; k < TC * n; k += blockDim.x) {
-    int c = k / n;
-    int g = (c < nc) ? op.dofmap_m[(c0 + c) * n + (k - c * n)] : -1;
-    D[k] = g;
-    X[k] = (g >= 0) ? x[g] : 0.0;
-  }
-  for (int k = threadIdx.x; k < TC * nm; k += blockDim.x) {
-    int c = k / nm;
-    C[k] = (c < nc) ? op.coef[(c0 + c) * nm + (k - c * nm)] : 0.0;
-  }
-  __syncthreads();
-  double pq = 0;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    double acc[TC];
-#pragma unroll
-    for (int c = 0; c < TC; ++c) acc[c] = 0;
-    for (int s = 0; s < nm; ++s) {
-      const double* Rs = op.R + (size_t)s * n * ldr + i;
-      double t[TC];
-#pragma unroll
-      for (int c = 0; c < TC; ++c) t[c] = 0;
-      for (int j = 0; j < n; ++j) {
-        double r = __ldg(Rs + (size_t)j * ldr);
-#pragma unroll
-        for (int c = 0; c < TC; ++c) t[c] = fma(r, X[c * n + j], t[c]);
-      }
-#pragma unroll
-      for (int c = 0; c < TC; ++c) acc[c] = fma(C[c * nm + s], t[c], acc[c]);
-    }
-#pragma unroll
-    for (int c = 0; c < TC; ++c) {
-      int g = D[c * n + i];
-      if (g >= 0) {
-        atomicAdd(y + g, acc[c]);
-        pq = fma(X[c * n + i], acc[c], pq);
-      }
-    }
-  }
-  if (pq_acc) {
-    __shared__ double sh[32];
-    double s = block_sum(pq, sh);
-    if (threadIdx.x == 0) atomicAdd(pq_acc, s);
-  }
 }
 
 // ---------------------------------------------------------------- operator apply on FP64 tensor cores
@@ -464,6 +400,7 @@ __global__ void __launch_bounds__((kApplyWarps + 1) * 32, 2)
       const double zn = sqrt(v->zz);
       if (kit == 0) {
         sc->z0 = zn;
+        sc->z_last = zn;
         sc->iters = 0;
         if (zn == 0.0) {
           sc->done = 1;
@@ -473,6 +410,7 @@ __global__ void __launch_bounds__((kApplyWarps + 1) * 32, 2)
         }
       } else {
         sc->iters = kit;
+        sc->z_last = zn;
         if (zn <= v->rtol * v->z0) {
           sc->done = 1;
           sc->converged = 1;
@@ -530,20 +468,6 @@ cudaError_t launch_apply_tc(const DevOperator& op, const double* x, double* y, d
   return launch_apply_tc_bm<16, PCG>(op, x, y, pq_acc, guard, s, sc, p0, p1);
 }
 
-template <int TC>
-cudaError_t launch_apply_simple(const DevOperator& op, const double* x, double* y, double* pq_acc,
-                            const PcgScalars* guard, cudaStream_t s) {
-  size_t sm = (size_t)TC * op.n_loc * (sizeof(double) + sizeof(int)) + (size_t)TC * op.n_mat * sizeof(double);
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(apply_kernel<TC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    configured = true;
-  }
-  unsigned grid = (unsigned)((op.n_cells + TC - 1) / TC);
-  apply_kernel<TC><<<grid, 128, sm, s>>>(op, x, y, pq_acc, guard);
-  return cudaGetLastError();
-}
-
 // ---------------------------------------------------------------- preconditioner
 __global__ void precond_init_kernel(DevPrecond pc, const double* __restrict__ r, double* __restrict__ z,
                                     double* rz_acc, const PcgScalars* guard) {
@@ -592,294 +516,8 @@ __global__ void scatter_grad_kernel(DevPrecond pc, double* __restrict__ z, const
   }
 }
 
-// Persistent star-patch kernel (Eq. 5.4 P:1763-1774 / Eq. 5.12 P:1956-1970 with
-// exact local solvers, R-A15): z += E_m A_m^{-1} E_m^T r for every patch m.
-// The packed lower tiles of A_m^{-1} (setup.hpp patch layout) are the only
-// HBM stream of the kernel. A CTA owns a list of patches (LPT schedule from
-// setup, sched_off/sched_ids); its tile sequence (patch by patch, tiles in
-// order I(I+1)/2 + J) is dealt round-robin to the 8 warps. Every warp streams
-// its own tiles with cp.async.bulk (TMA) into its own K-slot ring, each slot
-// completing on an mbarrier, issuing tile j+K as soon as tile j is consumed:
-// no producer warp and no cross-warp slot hand-off, so a slow warp never
-// stalls the stream of another. For an off-diagonal tile (I,J) lane l forms
-// the row product sum_k A[l][k] r_J[k] (-> z_I) and the column product
-// sum_i A[i][l] r_I[i] (-> z_J) straight from the swizzled tile in shared
-// memory, without shuffles or atomics: each warp accumulates into a private
-// copy of the patch's z (double-buffered by patch parity when it fits). At a
-// patch boundary (CTA barrier) the copies are summed and scatter-added to
-// global memory and the r buffer is refilled with r of the patch two ahead.
-constexpr int kPatchWarps = 8;
-
-struct PatchView {
-  int n, nb, kind;
-  int64_t idx_off, tile_off;
-};
-__device__ __forceinline__ PatchView patch_view(const DevPrecond& pc, int pid) {
-  PatchView v;
-  v.n = pc.pn[pid];
-  v.nb = (v.n + 31) >> 5;
-  v.kind = pc.pkind[pid];
-  v.idx_off = pc.idx_off[pid];
-  v.tile_off = pc.tile_off[pid];
-  return v;
-}
-
-// gather r of patch `pid` into rb (npad entries, zero padded)
-__device__ __forceinline__ void patch_gather(const DevPrecond& pc, int pid, const double* __restrict__ r,
-                                             double* rb) {
-  if (pid < 0) return;
-  const PatchView v = patch_view(pc, pid);
-  const double* __restrict__ rin = v.kind ? pc.gbuf : r;
-  const int32_t* id = pc.idx + v.idx_off;
-  const int npad = v.nb * 32;
-  for (int i = threadIdx.x; i < npad; i += kPatchWarps * 32) {
-    const int gi = id[i];
-    rb[i] = gi >= 0 ? rin[gi] : 0.0;
-  }
-}
-
-// Dynamic patch queue: CTAs claim patches (sorted by decreasing size at setup,
-// so the claim order is longest-first) from a global counter. The j-th patch
-// a CTA processes is recorded in a 64-entry shared ring so that the warps'
-// tile cursors, which run ahead independently, agree on it.
-constexpr int kClaimRing = 64;
-constexpr int kUnclaimed = -2, kClaiming = -1, kQueueEnd = -3;
-
-__device__ __forceinline__ int get_patch(const DevPrecond& pc, int* claim, int j) {
-  volatile int* c = claim + (j & (kClaimRing - 1));
-  int v = *c;
-  if (v == kUnclaimed) {
-    if ((threadIdx.x & 31) == 0 && atomicCAS(claim + (j & (kClaimRing - 1)), kUnclaimed, kClaiming) == kUnclaimed) {
-      const int pid = atomicAdd(pc.queue, 1);
-      *c = pid < pc.n_patches ? pid : kQueueEnd;
-    }
-    __syncwarp();
-    do {
-      v = *c;
-    } while (v == kUnclaimed || v == kClaiming);
-  } else {
-    while (v == kClaiming) v = *c;
-  }
-  return v == kQueueEnd ? -1 : v;
-}
-
-// A warp's cursor over its tiles t = w, w+8, ... of the CTA's tile sequence.
-struct TileCursor {
-  int k, pid, I, J;  // sequence index of the patch (pid < 0: past the end), tile (I, J)
-  PatchView v;
-  __device__ __forceinline__ void settle(const DevPrecond& pc, int* claim) {
-    // normalise (I, J) in tile order, moving on to later patches as needed
-    while (pid >= 0) {
-      while (J > I) {
-        J -= I + 1;
-        ++I;
-      }
-      if (I < v.nb) return;
-      const int over = J + I * (I + 1) / 2 - v.nb * (v.nb + 1) / 2;  // tiles past the end of the patch
-      pid = get_patch(pc, claim, ++k);
-      if (pid >= 0) v = patch_view(pc, pid);
-      I = 0;
-      J = over;
-    }
-  }
-  __device__ __forceinline__ bool valid() const { return pid >= 0; }
-};
-
-__device__ __forceinline__ void issue_tile(const DevPrecond& pc, const TileCursor& c, double* dst, uint64_t* bar) {
-  const int rows = min(32, c.v.n - 32 * c.I);
-  const double* src = pc.tiles + c.v.tile_off + 512LL * c.I * c.I + 16LL * c.I + (int64_t)c.J * 32 * rows;
-  // full tile rows*32 doubles; diagonal rows(rows+1)/2 rounded up to 2 (16 bytes)
-  const uint32_t nd = c.J < c.I ? 32u * rows : (uint32_t)((rows * (rows + 1) / 2 + 1) & ~1);
-  mbar_expect_tx(bar, nd * 8u);
-  bulk_g2s(dst, src, nd * 8u, bar);
-}
-
-__global__ void __launch_bounds__(kPatchWarps * 32, 2)
-    patch_stream_kernel(DevPrecond pc, const double* __restrict__ r, double* __restrict__ z, double* rz_acc,
-                        const PcgScalars* guard) {
-  pdl_wait();
-  if (stopped(guard)) return;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  const int K = pc.ring_slots / kPatchWarps;  // slots per warp
-  const int NP = pc.npad_max;
-  const int ZB = pc.zbufs;                    // private z copies per warp (1 or 2)
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw) + warp * 2 * K;
-  uint64_t* used = full + K;  // per slot: the 32 lanes' reads done (count 32)
-  double* ring = reinterpret_cast<double*>(smem_raw + 16 * pc.ring_slots) + (size_t)warp * K * 1024;  // [K][1024]
-  double* rbuf = reinterpret_cast<double*>(smem_raw + 16 * pc.ring_slots) + (size_t)pc.ring_slots * 1024;  // [2][NP]
-  double* zw = rbuf + 2 * NP;                                            // [ZB][8 warps][NP]
-  __shared__ int claim[kClaimRing];
-  for (int i = threadIdx.x; i < kClaimRing; i += blockDim.x) claim[i] = kUnclaimed;
-  if (lane == 0) {
-    for (int s = 0; s < K; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&used[s], 32);
-    }
-    mbar_fence_init();
-  }
-  __syncthreads();
-  // consumer cursor and prefetch cursor start at this warp's first tile
-  TileCursor cur;
-  cur.k = 0;
-  cur.pid = get_patch(pc, claim, 0);
-  if (cur.pid >= 0) cur.v = patch_view(pc, cur.pid);
-  cur.I = 0;
-  cur.J = warp;
-  cur.settle(pc, claim);
-  TileCursor pre = cur;
-  for (int s = 0; s < K && pre.valid(); ++s) {
-    if (lane == 0) issue_tile(pc, pre, ring + (size_t)s * 1024, &full[s]);
-    pre.J += kPatchWarps;
-    pre.settle(pc, claim);
-  }
-
-  for (int i = threadIdx.x; i < ZB * kPatchWarps * NP; i += kPatchWarps * 32) zw[i] = 0.0;
-  patch_gather(pc, get_patch(pc, claim, 0), r, rbuf);
-  patch_gather(pc, get_patch(pc, claim, 1), r, rbuf + NP);
-  __syncthreads();
-  double part = 0.0;
-  int slot = 0;
-  uint32_t phase = 0;
-  for (int k = 0;; ++k) {
-    const int pid = get_patch(pc, claim, k);
-    if (pid < 0) break;
-    const PatchView v = patch_view(pc, pid);
-    double* rl = rbuf + (k & 1) * NP;
-    double* zmine = zw + ((size_t)(ZB == 2 ? (k & 1) : 0) * kPatchWarps + warp) * NP;
-    while (cur.valid() && cur.k == k) {
-      const int I = cur.I, J = cur.J;
-      mbar_wait(&full[slot], phase);
-      const double* tb = ring + (size_t)slot * 1024;
-      const int rows = min(32, v.n - 32 * I);
-      const double* rI = rl + I * 32;
-      double acc_i, acc_j = 0.0;
-      if (J < I) {
-        // row product (lane = row l): chunk c of row l at l*32 + 2*(c ^ (l&7));
-        // column product (lane = column l): (i, l) at i*32 + 2*((l>>1) ^ (i&7)) + (l&1)
-        const double2* rJ2 = reinterpret_cast<const double2*>(rl + J * 32);
-        const double2* trow = reinterpret_cast<const double2*>(tb + lane * 32);
-        const double* tcol = tb + (lane & 1);
-        double ar[4] = {0.0, 0.0, 0.0, 0.0}, ac[4] = {0.0, 0.0, 0.0, 0.0};
-        if (lane < rows) {
-#pragma unroll
-          for (int c = 0; c < 16; ++c) {
-            const double2 a = trow[c ^ (lane & 7)];
-            const double2 x = rJ2[c];
-            ar[c & 3] = fma(a.x, x.x, ar[c & 3]);
-            ar[c & 3] = fma(a.y, x.y, ar[c & 3]);
-          }
-        }
-        if (rows == 32) {
-#pragma unroll
-          for (int i = 0; i < 32; ++i)
-            ac[i & 3] = fma(tcol[i * 32 + 2 * ((lane >> 1) ^ (i & 7))], rI[i], ac[i & 3]);
-        } else {
-#pragma unroll
-          for (int i = 0; i < 32; ++i)
-            if (i < rows) ac[i & 3] = fma(tcol[i * 32 + 2 * ((lane >> 1) ^ (i & 7))], rI[i], ac[i & 3]);
-        }
-        acc_i = (ar[0] + ar[1]) + (ar[2] + ar[3]);
-        acc_j = (ac[0] + ac[1]) + (ac[2] + ac[3]);
-      } else {
-        // diagonal tile, lower triangle packed by columns: (i,q), q <= i at q*rows - q(q-1)/2 + i - q;
-        // lane l: sum_{q<=l} L(l,q) r_q + sum_{q>l} L(q,l) r_q
-        double ad[4] = {0.0, 0.0, 0.0, 0.0};
-        if (lane < rows) {
-          const int colbase = lane * rows - lane * (lane - 1) / 2 - lane;  // L(q,l) at colbase + q
-#pragma unroll
-          for (int q = 0; q < 32; ++q) {
-            if (q < rows) {
-              const int off = q <= lane ? q * rows - q * (q - 1) / 2 + (lane - q) : colbase + q;
-              ad[q & 3] = fma(tb[off], rI[q], ad[q & 3]);
-            }
-          }
-        }
-        acc_i = (ad[0] + ad[1]) + (ad[2] + ad[3]);
-      }
-      // slot consumed by every lane once its products are computed (the arrive
-      // depends on them, hence on the tile loads): lane 0 refills the slot with
-      // this warp's tile K ahead once all 32 lanes arrived
-      mbar_release(&used[slot]);
-      if (pre.valid()) {
-        if (lane == 0) {
-          mbar_wait(&used[slot], phase);
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          issue_tile(pc, pre, ring + (size_t)slot * 1024, &full[slot]);
-        }
-        pre.J += kPatchWarps;
-        pre.settle(pc, claim);
-      }
-      if (++slot == K) {
-        slot = 0;
-        phase ^= 1u;
-      }
-      zmine[I * 32 + lane] += acc_i;
-      if (J < I) zmine[J * 32 + lane] += acc_j;
-      cur.J += kPatchWarps;
-      cur.settle(pc, claim);
-    }
-    __syncthreads();  // every warp's z copy of patch k complete
-    // sum the copies, scatter-add z of patch k, r.z partial, refill this r
-    // buffer with r of patch k+2 (a thread refills exactly the entries it read)
-    {
-      double* __restrict__ zout = v.kind ? pc.ubuf : z;
-      const int32_t* id = pc.idx + v.idx_off;
-      const double* zk = zw + (size_t)(ZB == 2 ? (k & 1) : 0) * kPatchWarps * NP;
-      for (int i = threadIdx.x; i < v.n; i += kPatchWarps * 32) {
-        double zi = 0.0;
-#pragma unroll
-        for (int w = 0; w < kPatchWarps; ++w) zi += zk[(size_t)w * NP + i];
-        atomicAdd(zout + id[i], pc.out_scale * zi);
-        part = fma(rl[i], zi, part);
-      }
-      patch_gather(pc, get_patch(pc, claim, k + 2), r, rl);
-      // every warp is past patch k-1: its claim entry can be reused (the
-      // cursors run at most a few patches ahead, far less than the ring)
-      if (threadIdx.x == 0 && k >= 1) claim[(k - 1) & (kClaimRing - 1)] = kUnclaimed;
-    }
-    if (ZB == 2) {
-      // patch k+1 accumulates into the copies of parity (k+1)&1, last summed at
-      // boundary k-1, i.e. before the barrier above: each warp clears its own
-      {
-        double* znext = zw + ((size_t)((k + 1) & 1) * kPatchWarps + warp) * NP;
-        for (int i = lane; i < NP; i += 32) znext[i] = 0.0;
-        __syncwarp();
-      }
-    } else {
-      __syncthreads();  // every copy summed before it is cleared
-      double* zmine0 = zw + (size_t)warp * NP;
-      for (int i = lane; i < NP; i += 32) zmine0[i] = 0.0;
-      __syncwarp();
-    }
-  }
-  __shared__ double sh[kPatchWarps];
-  part = warp_sum(part);
-  if (lane == 0) sh[warp] = part;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    if (rz_acc) {
-      double s = 0;
-      for (int w = 0; w < kPatchWarps; ++w) s += sh[w];
-      atomicAdd(rz_acc, s);
-    }
-    // the last CTA out resets the queue for the next launch
-    __threadfence();
-    if (atomicAdd(pc.queue + 1, 1) == (int)gridDim.x - 1) {
-      pc.queue[0] = 0;
-      pc.queue[1] = 0;
-      __threadfence();
-    }
-  }
-}
-
-size_t patch_smem_bytes(int slots, int npad_max, int zbufs) {
-  return sizeof(uint64_t) * 2 * slots +
-         sizeof(double) * ((size_t)slots * 1024 + (2 + (size_t)zbufs * kPatchWarps) * (size_t)npad_max);
-}
-
-// Direct-load star-patch kernel (the default; RDR_PATCH_KERNEL=tma selects
-// patch_stream_kernel above). One CTA per patch, patches in decreasing size
+// Star-patch kernel (Eq. 5.4 P:1763-1774 / Eq. 5.12 P:1956-1970 with exact
+// local solvers, R-A15): z += E_m A_m^{-1} E_m^T r. One CTA per patch, patches in decreasing size
 // order, so the hardware block scheduler hands out the work longest-first.
 // Full tiles are stored row-major in 32-byte groups ((i,k) at
 // ((k>>2)*rows + i)*4 + (k&3)): a warp owns a tile and reads it in two
@@ -1148,25 +786,34 @@ __global__ void __launch_bounds__(kLdgWarps * 32, 32 / kLdgWarps)
 
 // ---------------------------------------------------------------- hybrid Schwarz
 // Symmetric multiplicative sweep J, P, C, P, J: helpers.
-// e = s * dinv .* r on the interior dofs (set: e = 0 elsewhere; add: e += ...)
+// e = s * dinv .* r on the interior dofs (set: e = 0 elsewhere and the sweep's
+// A e accumulator hy = 0; add: e += ...). Every sweep kernel returns at once
+// once the PCG has stopped (guard), like the patch and apply kernels.
 __global__ void hyb_jacobi_kernel(DevPrecond pc, const double* __restrict__ r, double* __restrict__ e, double s,
-                                  int add) {
+                                  int add, const PcgScalars* guard) {
   pdl_wait();
+  if (stopped(guard)) return;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < pc.n_total; i += stride) {
     const double v = i >= pc.off3 ? s * pc.dinv[i - pc.off3] * r[i] : 0.0;
     e[i] = add ? e[i] + v : v;
+    if (!add) pc.hy[i] = 0.0;
   }
   if (pc.ubuf)
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < pc.n_cg_iface; i += stride) pc.ubuf[i] = 0.0;
 }
 
-// t = r - y (y = A e, constrained rows already 0); also clears the coarse accumulators
-__global__ void hyb_residual_kernel(DevPrecond pc, const double* __restrict__ r, const double* __restrict__ y,
-                                    double* __restrict__ t) {
+// t = r - y (y = A e, constrained rows already 0), then y = 0 for the next
+// stage's apply; also clears the coarse accumulators
+__global__ void hyb_residual_kernel(DevPrecond pc, const double* __restrict__ r, double* __restrict__ y,
+                                    double* __restrict__ t, const PcgScalars* guard) {
   pdl_wait();
+  if (stopped(guard)) return;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < pc.n_total; i += stride) t[i] = r[i] - y[i];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < pc.n_total; i += stride) {
+    t[i] = r[i] - y[i];
+    y[i] = 0.0;
+  }
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < pc.nc; i += stride) pc.czc[i] = 0.0;
   if (pc.ubuf)
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < pc.n_cg_iface; i += stride) pc.ubuf[i] = 0.0;
@@ -1177,8 +824,10 @@ __global__ void hyb_residual_kernel(DevPrecond pc, const double* __restrict__ r,
 // tiles spread over the whole grid (one warp per tile, half tiles as in
 // patch_ldg_kernel), row and transposed products accumulated into czc with
 // red.global.add; the coarse residual is read through cidx.
-__global__ void __launch_bounds__(256) coarse_symv_kernel(DevPrecond pc, const double* __restrict__ t) {
+__global__ void __launch_bounds__(256) coarse_symv_kernel(DevPrecond pc, const double* __restrict__ t,
+                                                           const PcgScalars* guard) {
   pdl_wait();
+  if (stopped(guard)) return;
   const int n = (int)pc.nc, nb = (n + 31) >> 5;
   const int64_t ntiles = (int64_t)nb * (nb + 1) / 2;
   const int lane = threadIdx.x & 31;
@@ -1239,8 +888,9 @@ __global__ void __launch_bounds__(256) coarse_symv_kernel(DevPrecond pc, const d
 }
 
 // e[cidx[k]] += czc[k]
-__global__ void coarse_scatter_kernel(DevPrecond pc, double* __restrict__ e) {
+__global__ void coarse_scatter_kernel(DevPrecond pc, double* __restrict__ e, const PcgScalars* guard) {
   pdl_wait();
+  if (stopped(guard)) return;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < pc.nc; k += stride) e[pc.cidx[k]] += pc.czc[k];
 }
@@ -1304,6 +954,7 @@ __global__ void pcg_start_kernel(PcgScalars* sc, const double* __restrict__ z, d
     volatile PcgScalars* v = sc;
     double zz = v->zz;
     sc->z0 = sqrt(zz);
+    sc->z_last = sc->z0;
     sc->rz = v->rz_new;
     sc->rz_new = 0;
     sc->zz = 0;
@@ -1343,6 +994,7 @@ __global__ void pcg_finish_kernel(PcgScalars* sc, const double* __restrict__ z, 
     double zn = sqrt(v->zz);
     int it = v->iters + 1;
     sc->iters = it;
+    sc->z_last = zn;
     if (zn <= v->rtol * v->z0) {
       sc->done = 1;
       sc->converged = 1;
@@ -1416,19 +1068,13 @@ unsigned vec_grid(int64_t n) {
 
 cudaError_t launch_apply(const DevOperator& op, const double* x, double* y, double* pq_acc,
                          const PcgScalars* guard, cudaStream_t s) {
-  if (!op.Bsw) {  // CUDA-core reference kernel (RDR_KERNEL=simple)
-    if (op.n_loc <= 64) return launch_apply_simple<16>(op, x, y, pq_acc, guard, s);
-    if (op.n_loc <= 400) return launch_apply_simple<8>(op, x, y, pq_acc, guard, s);
-    return launch_apply_simple<4>(op, x, y, pq_acc, guard, s);
-  }
   return launch_apply_tc<false>(op, x, y, pq_acc, guard, s);
 }
 
-size_t patch_kernel_smem(int slots, int npad_max, int zbufs) { return patch_smem_bytes(slots, npad_max, zbufs); }
 size_t max_kernel_smem() { return kMaxSmem; }
 
 int count_precond_launches(const DevPrecond& pc) {
-  const int patch_launches = pc.n_patches == 0 ? 0 : pc.kernel == 1 ? 1 : (pc.n_big > 0) + (pc.n_big < pc.n_patches);
+  const int patch_launches = pc.n_patches == 0 ? 0 : (pc.n_big > 0) + (pc.n_big < pc.n_patches);
   return 1 + patch_launches + (pc.gbuf ? 2 : 0);
 }
 
@@ -1443,9 +1089,6 @@ cudaError_t launch_precond_part(int part, const DevPrecond& pc, const double* r,
       break;
     case 2:
       if (pc.n_patches > 0) {
-        if (pc.kernel == 1)
-          return launch_k(patch_stream_kernel, dim3(pc.n_ctas), dim3(kPatchWarps * 32),
-                          patch_smem_bytes(pc.ring_slots, pc.npad_max, pc.zbufs), s, pc, r, z, rz_acc, guard);
         const int W = pc.ldg_warps;
         cudaError_t e = cudaSuccess;
         if (pc.n_big > 0) {  // one CTA per patch
@@ -1478,25 +1121,26 @@ cudaError_t launch_precond_hybrid(const DevOperator& op, const DevPrecond& pc, c
                                   const PcgScalars* guard, cudaStream_t s) {
   // symmetric multiplicative sweep X_I (Jacobi), X_Gamma (patches), W (coarse), X_Gamma, X_I
   const dim3 vg(vec_grid(pc.n_total)), vb(kVecThreads);
-  cudaError_t e = launch_k(hyb_jacobi_kernel, vg, vb, 0, s, pc, r, z, pc.s1, 0);
+  cudaError_t e = launch_k(hyb_jacobi_kernel, vg, vb, 0, s, pc, r, z, pc.s1, 0, guard);  // also hy = 0
   if (e != cudaSuccess) return e;
   DevPrecond pp = pc;
   pp.out_scale = pc.s2;
   for (int stage = 1; stage < 5; ++stage) {
-    if ((e = cudaMemsetAsync(pc.hy, 0, sizeof(double) * pc.n_total, s)) != cudaSuccess) return e;
     if ((e = launch_apply(op, z, pc.hy, nullptr, guard, s)) != cudaSuccess) return e;
-    if ((e = launch_k(hyb_residual_kernel, vg, vb, 0, s, pc, r, (const double*)pc.hy, pc.ht)) != cudaSuccess) return e;
+    if ((e = launch_k(hyb_residual_kernel, vg, vb, 0, s, pc, r, pc.hy, pc.ht, guard)) != cudaSuccess) return e;
     if (stage == 1 || stage == 3) {  // interface star patches, weight 1/rho_2
       for (int part = 1; part < 4; ++part)
         if ((e = launch_precond_part(part, pp, pc.ht, z, nullptr, guard, s)) != cudaSuccess) return e;
     } else if (stage == 2) {         // exact coarse solve on W^k
       if (pc.nc > 0) {
-        if ((e = launch_k(coarse_symv_kernel, dim3(148 * 4), dim3(256), 0, s, pc, (const double*)pc.ht)) != cudaSuccess)
+        if ((e = launch_k(coarse_symv_kernel, dim3(148 * 4), dim3(256), 0, s, pc, (const double*)pc.ht, guard)) !=
+            cudaSuccess)
           return e;
-        if ((e = launch_k(coarse_scatter_kernel, dim3(vec_grid(pc.nc)), vb, 0, s, pc, z)) != cudaSuccess) return e;
+        if ((e = launch_k(coarse_scatter_kernel, dim3(vec_grid(pc.nc)), vb, 0, s, pc, z, guard)) != cudaSuccess)
+          return e;
       }
     } else {                         // interior Jacobi, weight 1/rho_1
-      if ((e = launch_k(hyb_jacobi_kernel, vg, vb, 0, s, pc, (const double*)pc.ht, z, pc.s1, 1)) != cudaSuccess)
+      if ((e = launch_k(hyb_jacobi_kernel, vg, vb, 0, s, pc, (const double*)pc.ht, z, pc.s1, 1, guard)) != cudaSuccess)
         return e;
     }
   }
@@ -1504,7 +1148,7 @@ cudaError_t launch_precond_hybrid(const DevOperator& op, const DevPrecond& pc, c
 }
 
 int count_hybrid_launches(const DevPrecond& pc) {
-  const int patches = (pc.n_patches > 0 ? 1 : 0) + (pc.gbuf ? 2 : 0);
+  const int patches = count_precond_launches(pc) - 1;
   return 1 + 4 * 2 + 2 * patches + (pc.nc > 0 ? 2 : 0) + 1;
 }
 
@@ -1549,10 +1193,7 @@ cudaError_t launch_pcg_direction(PcgScalars* sc, const double* z, double* p, dou
   return cudaGetLastError();
 }
 
-bool fused_pcg_supported(const DevOperator& op) {
-  static const bool off = std::getenv("RDR_PCG_UNFUSED") != nullptr;
-  return op.Bsw && op.owner && !off;
-}
+bool fused_pcg_supported(const DevOperator& op) { return op.Bsw && op.owner; }
 
 cudaError_t launch_pcg_fused_apply(const DevOperator& op, PcgScalars* sc, const double* z, double* p0, double* p1,
                                    double* q, cudaStream_t s) {
@@ -1588,10 +1229,6 @@ cudaError_t launch_dmma_peak(double* out, int n, int blocks, int threads, cudaSt
 
 namespace rdr {
 void configure_kernels() {  // errors here would surface as a later launch's cudaGetLastError
-  cudaFuncSetAttribute(apply_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  cudaFuncSetAttribute(apply_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  cudaFuncSetAttribute(apply_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  cudaFuncSetAttribute(patch_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
   cudaFuncSetAttribute(patch_ldg_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
   cudaFuncSetAttribute(patch_ldg_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
   cudaFuncSetAttribute(apply_tc_kernel<64, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);

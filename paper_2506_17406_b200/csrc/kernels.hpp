@@ -24,6 +24,7 @@ struct PcgScalars {
   double rz_acc;    // fused path: r.z accumulated by the preconditioner
   double rz_old;    // fused path: r.z of the z used by the current direction
   double pq2[2];    // fused path: p.Ap, double-buffered by iteration parity
+  double z_last;    // ||z_k|| at the last stopping test (rdr_last_solve)
 };
 
 struct DevOperator {
@@ -36,7 +37,7 @@ struct DevOperator {
   int kpad;                     // n_mat * kp rounded up to 16 (K rows of the stack)
   int ngroups;                  // ceil(n_loc / 32) column groups
   const double* Bsw;            // [ngroups][kpad][32] stacked reference matrices, swizzled (kernels.cu
-                                // apply_tc_kernel); NULL selects the CUDA-core kernel (RDR_KERNEL=simple)
+                                // apply_tc_kernel)
   const uint8_t* owner;         // [n_cells][n_loc] 1 at the first (cell, local) occurrence of each free dof
 };
 
@@ -51,14 +52,8 @@ struct DevPrecond {
   const int64_t* tile_off;      // [np+1]
   const double* tiles;
   const uint8_t* pkind;         // 0 own numbering, 1 CG potential
-  int32_t kernel;               // 0: patch_ldg_kernel (tile layout "groups"), 1: patch_stream_kernel ("swizzled")
   int32_t ldg_warps;            // warps per CTA of patch_ldg_kernel: 8, or 4 when most patches are small
   int64_t n_big;                // patch_ldg_kernel: patches [0, n_big) one per CTA, the rest (n <= 128) one per warp
-  // persistent patch kernel: n_ctas CTAs claim patches from a queue
-  int32_t n_ctas;
-  int32_t* queue;               // [2] claim counter, finished-CTA counter (zero between launches)
-  int32_t ring_slots;           // shared-memory tile slots of 8 KB: 8 warps x K
-  int32_t zbufs;                // private z copies per warp: 2 (by patch parity) or 1
   int32_t npad_max;             // largest patch dimension rounded up to 32
   // H(curl) potential space
   int64_t n_cg_iface;           // CG dofs [0, n_cg_iface) used by patches
@@ -115,7 +110,6 @@ cudaError_t launch_pcg_update_jacobi(PcgScalars* sc, const DevPrecond& pc, const
                                      double* q, double* x, double* r, double* z, cudaStream_t s);
 
 int count_precond_launches(const DevPrecond& pc);  // kernels per rdr_precond
-size_t patch_kernel_smem(int slots, int npad_max, int zbufs);  // dynamic shared memory of the patch kernel
 size_t max_kernel_smem();                           // per-CTA dynamic shared-memory opt-in used
 void configure_kernels();                            // shared-memory opt-ins (call once, outside capture)
 // DMMA.8x8x4 issue-bound loop: n iterations x 4 chains x 512 flop per warp

@@ -11,6 +11,8 @@
 #include <cstring>
 #include <exception>
 #include <new>
+#include <mutex>
+#include <set>
 #include <vector>
 
 #include "../../include/rdr.h"
@@ -124,6 +126,32 @@ std::vector<double> sym_eigenvalues(std::vector<double> A, int n) {
   return ev;
 }
 
+// The persisting-L2 set-aside is a device-wide limit: handles that hold a
+// window register their size here; the limit is the largest registered size
+// and is reset (with the persisting lines) only when the last owner goes.
+std::mutex g_l2_mutex;
+std::multiset<size_t> g_l2_owners;
+
+void l2_window_acquire(size_t bytes) {
+  std::lock_guard<std::mutex> lk(g_l2_mutex);
+  g_l2_owners.insert(bytes);
+  cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, *g_l2_owners.rbegin());
+  cudaGetLastError();
+}
+
+void l2_window_release(size_t bytes) {
+  std::lock_guard<std::mutex> lk(g_l2_mutex);
+  auto it = g_l2_owners.find(bytes);
+  if (it != g_l2_owners.end()) g_l2_owners.erase(it);
+  if (g_l2_owners.empty()) {
+    cudaCtxResetPersistingL2Cache();
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);
+  } else {
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, *g_l2_owners.rbegin());
+  }
+  cudaGetLastError();
+}
+
 }  // namespace
 
 struct rdr_handle {
@@ -144,7 +172,7 @@ struct rdr_handle {
   cudaStream_t cap_stream = nullptr;
   cudaGraphExec_t graph = nullptr;
   cudaGraphExec_t wgraph = nullptr;  // device-side while loop (fused path)
-  bool device_loop = true;           // RDR_PCG_HOSTLOOP=1: host-driven graph of 8 iterations instead
+  int loop = RDR_LOOP_DEVICE;        // rdr_options.loop
   int graph_iters = 0;
   int launches_per_iter = 0;
   double rho1 = 1.0, rho2 = 1.0;  // hybrid Schwarz weights (rdr_get_weights)
@@ -165,11 +193,7 @@ struct rdr_handle {
     if (graph) cudaGraphExecDestroy(graph);
     if (wgraph) cudaGraphExecDestroy(wgraph);
     if (cap_stream) cudaStreamDestroy(cap_stream);
-    if (l2_window.num_bytes) {  // release the persisting set-aside this handle requested
-      cudaCtxResetPersistingL2Cache();
-      cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);
-      cudaGetLastError();
-    }
+    if (l2_window.num_bytes) l2_window_release(l2_window.num_bytes);
     for (void* p : owned) cudaFree(p);
     if (h_sc) cudaFreeHost(h_sc);
   }
@@ -248,7 +272,7 @@ static int device_patch_setup(DevPatchSetup s, const Patches& P, const PatchAsse
 
 static int setup_impl(rdr_handle* h, const double* vertices, int64_t nv, const int32_t* tets, int64_t nt, int p,
                       int space, const double* alpha, const double* beta, const uint8_t* mask, bool unsplit,
-                      bool hybrid, bool host_setup, cudaStream_t stream) {
+                      bool hybrid, bool host_setup, int loop, cudaStream_t stream) {
   auto t0 = std::chrono::steady_clock::now();
   if (stream) CK(cudaStreamSynchronize(stream));
   configure_kernels();
@@ -261,8 +285,12 @@ static int setup_impl(rdr_handle* h, const double* vertices, int64_t nv, const i
   if ((st = fetch(alpha, (size_t)nt, ha))) return st;
   if ((st = fetch(beta, (size_t)nt, hb))) return st;
   if ((st = fetch(mask, (size_t)nt * 4, hm))) return st;
+  // alpha > 0, beta >= 0; H(curl) and H(div) need beta > 0: with beta = 0
+  // gradients (curl-free fields) resp. div-free fields are in the kernel of A and
+  // of the star-patch matrices (their tiny rounded pivots would not be caught)
   for (int64_t t = 0; t < nt; ++t)
-    if (!(ha[t] > 0) || !(hb[t] >= 0)) return RDR_EINVAL;
+    if (!(ha[t] > 0) || !(hb[t] >= 0) || (space != RDR_HGRAD && !(hb[t] > 0))) return RDR_EINVAL;
+  h->loop = loop;
 
   Mesh m;
   if ((st = build_mesh(hx.data(), nv, ht.data(), nt, hm.data(), m))) return st;
@@ -299,9 +327,7 @@ static int setup_impl(rdr_handle* h, const double* vertices, int64_t nv, const i
   op.kp = (el.n + 3) / 4 * 4;
   op.kpad = (el.n_mat * op.kp + 15) / 16 * 16;
   op.ngroups = (el.n + 31) / 32;
-  op.Bsw = nullptr;
-  const char* kern = std::getenv("RDR_KERNEL");
-  if (!(kern && std::strcmp(kern, "simple") == 0)) {
+  {
     // stacked reference matrices [R_0; ...; R_{nm-1}] (kp rows each), split in
     // 32-column groups, element (k, col) of a group at k*32 + (col ^ ((k & 3) << 2))
     // (the shared-memory swizzle of apply_tc_kernel's B fragments)
@@ -378,14 +404,9 @@ static int setup_impl(rdr_handle* h, const double* vertices, int64_t nv, const i
   }
   Patches P;
   DeviceTiles sink;
-  {
-    const char* pk = std::getenv("RDR_PATCH_KERNEL");
-    pc.kernel = (pk && std::strcmp(pk, "tma") == 0) ? 1 : 0;
-    pc.ldg_warps = 8;  // decided below from the patch sizes (RDR_PATCH_WARPS=4|8 overrides)
-  }
   const auto tp0 = std::chrono::steady_clock::now();
   PatchAssembly pasm;
-  const PatchLayout layout = pc.kernel == 1 ? kTileSwizzled : kTileGroups;
+  const PatchLayout layout = kTileGroups;
   st = build_patches(m, num, el, coef, space == RDR_HCURL ? &cg_num : nullptr, cg_el,
                      space == RDR_HCURL ? &cg_coef : nullptr, P, sink, layout, unsplit, host_setup ? nullptr : &pasm);
   if (sink.d) h->owned.push_back(sink.d);
@@ -434,37 +455,7 @@ static int setup_impl(rdr_handle* h, const double* vertices, int64_t nv, const i
       return st;
   }
   h->info.patch_setup_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - tp0).count();
-  {  // persistent patch kernel: tile slots, CTAs per SM, claim queue
-    int dev = 0, sms = 148;
-    CK(cudaGetDevice(&dev));
-    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    pc.npad_max = std::max(32, (P.max_n + 31) / 32 * 32);
-    const size_t per_sm = 228 * 1024;
-    // 8 warps x K tile slots of 8 KB and private z copies per warp: two CTAs
-    // per SM (16 consumer warps) with K = 1 when they fit -- measured faster
-    // than deeper per-warp prefetch with 8 warps per SM -- else one CTA with
-    // the deepest K that fits (RDR_PATCH_CTAS / RDR_PATCH_K / RDR_PATCH_ZB override)
-    const size_t cap1 = max_kernel_smem(), cap2 = per_sm / 2 - 1024;
-    auto fits = [&](int c, int k, int zb) { return patch_kernel_smem(8 * k, pc.npad_max, zb) <= (c == 2 ? cap2 : cap1); };
-    int per_cta_sm = 2, K = 1, ZB = 1;
-    if (!fits(2, 1, 1)) {
-      per_cta_sm = 1;
-      while (K < 3 && fits(1, K + 1, 1)) ++K;
-    }
-    if (const char* e = std::getenv("RDR_PATCH_K")) K = std::max(1, std::atoi(e));
-    if (const char* e = std::getenv("RDR_PATCH_ZB")) ZB = std::atoi(e) == 2 ? 2 : 1;
-    if (const char* e = std::getenv("RDR_PATCH_CTAS")) per_cta_sm = std::atoi(e) == 2 ? 2 : 1;
-    if (pc.kernel == 1 && !fits(1, K, ZB)) return RDR_EINVAL;  // TMA variant: tile ring + z copies must fit
-    pc.ring_slots = 8 * K;
-    pc.zbufs = ZB;
-    const int64_t np = (int64_t)P.n.size();
-    const int G = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * per_cta_sm, np));
-    pc.n_ctas = G;
-    // patches are claimed dynamically in decreasing size order (the order of P)
-    if ((st = h->own_alloc((void**)&pc.queue, 2 * sizeof(int32_t)))) return st;
-    CK(cudaMemset(pc.queue, 0, 2 * sizeof(int32_t)));
-
-  }
+  pc.npad_max = std::max(32, (P.max_n + 31) / 32 * 32);
 
   // ---- PCG workspace: one slab, the vectors every kernel of an iteration touches
   // first, then copies of the dof map and owner flags, so that an L2
@@ -507,7 +498,7 @@ static int setup_impl(rdr_handle* h, const double* vertices, int64_t nv, const i
     const bool want = lp ? std::atoi(lp) == 1 : hot <= ((size_t)16 << 20);
     if (fits && want) {
       const size_t bytes = hot, setaside = hot;
-      cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, setaside);
+      l2_window_acquire(setaside);
       h->l2_window.base_ptr = slab;
       h->l2_window.num_bytes = bytes;
       h->l2_window.hitRatio = (float)setaside / (float)bytes;
@@ -558,7 +549,6 @@ static int setup_impl(rdr_handle* h, const double* vertices, int64_t nv, const i
     if ((st = hybrid_weights(h, dinv))) return st;
     pc.hybrid = 1;
   }
-  h->device_loop = std::getenv("RDR_PCG_HOSTLOOP") == nullptr;
   if ((st = h->own_alloc((void**)&h->d_sc, sizeof(PcgScalars)))) return st;
   CK(cudaMallocHost((void**)&h->h_sc, sizeof(PcgScalars)));
   CK(cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
@@ -702,12 +692,14 @@ int rdr_setup_ex(rdr_handle** hp, const double* vertices, int64_t nv, const int3
   if (pre == RDR_HYBRID && dec != RDR_SPLIT) return RDR_EINVAL;
   const int su = opt ? opt->setup : RDR_SETUP_DEVICE;
   if (su != RDR_SETUP_DEVICE && su != RDR_SETUP_HOST) return RDR_EINVAL;
+  const int loop = opt ? opt->loop : RDR_LOOP_DEVICE;
+  if (loop != RDR_LOOP_DEVICE && loop != RDR_LOOP_HOST && loop != RDR_LOOP_EAGER) return RDR_EINVAL;
   rdr_handle* h = new (std::nothrow) rdr_handle();
   if (!h) return RDR_ENOMEM;
   int st;
   try {
     st = setup_impl(h, vertices, nv, tets, nt, p, space, alpha, beta, dirichlet_mask, dec == RDR_UNSPLIT,
-                    pre == RDR_HYBRID, su == RDR_SETUP_HOST, (cudaStream_t)stream);
+                    pre == RDR_HYBRID, su == RDR_SETUP_HOST, loop, (cudaStream_t)stream);
   } catch (const std::bad_alloc&) {
     st = RDR_ENOMEM;
   } catch (const std::exception& e) {
@@ -839,67 +831,93 @@ static int build_while_graph(rdr_handle* h) {
   return RDR_OK;
 }
 
-static int solve_device(rdr_handle* h, const double* b, double rtol, int maxit, int* iters, cudaStream_t s) {
+// PCG start (R-A16): x0 = 0, r0 = b (masked), z0 = P^-1 r0 and the scalars;
+// returns the launches it enqueued
+static int64_t pcg_begin(rdr_handle* h, const double* b, double rtol, int maxit, cudaStream_t s, int* st) {
   const int64_t n = h->n_total;
-  int st;
-  int64_t launches = 0;
-  if (h->fused && h->device_loop) {
-    if ((st = build_while_graph(h))) return st;
-    CK(cudaStreamSynchronize(s));  // h_sc (pinned) is reused as the H2D template
-    std::memset(h->h_sc, 0, sizeof(PcgScalars));
+  auto fail = [&](cudaError_t e) {
+    *st = cuda_status(e);
+    return (int64_t)0;
+  };
+  cudaError_t e;
+  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return fail(e);  // h_sc (pinned) is the H2D template
+  std::memset(h->h_sc, 0, sizeof(PcgScalars));
+  if (h->fused) {
     h->h_sc->rtol = rtol;
     h->h_sc->maxit = maxit;
-    CK(cudaMemcpyAsync(h->d_sc, h->h_sc, sizeof(PcgScalars), cudaMemcpyHostToDevice, s));
-    CK(cudaMemsetAsync(h->d_p, 0, sizeof(double) * n, s));
-    CK(cudaMemsetAsync(h->d_p2, 0, sizeof(double) * n, s));
-    CK(launch_pcg_init(b, h->d_cons, n, h->d_x, h->d_r, h->d_q, s));
-    CK(launch_precond(h->pc, h->d_r, h->d_z, &h->d_sc->rz_acc, nullptr, s));
+    if ((e = cudaMemcpyAsync(h->d_sc, h->h_sc, sizeof(PcgScalars), cudaMemcpyHostToDevice, s))) return fail(e);
+    if ((e = cudaMemsetAsync(h->d_p, 0, sizeof(double) * n, s))) return fail(e);
+    if ((e = cudaMemsetAsync(h->d_p2, 0, sizeof(double) * n, s))) return fail(e);
+    if ((e = launch_pcg_init(b, h->d_cons, n, h->d_x, h->d_r, h->d_q, s))) return fail(e);
+    if ((e = launch_precond(h->pc, h->d_r, h->d_z, &h->d_sc->rz_acc, nullptr, s))) return fail(e);
+    *st = RDR_OK;
+    return 1 + count_precond_launches(h->pc);
+  }
+  if ((e = cudaMemcpyAsync(h->d_sc, h->h_sc, sizeof(PcgScalars), cudaMemcpyHostToDevice, s))) return fail(e);
+  if ((e = launch_pcg_init(b, h->d_cons, n, h->d_x, h->d_r, h->d_q, s))) return fail(e);
+  if (h->pc.hybrid) {
+    if ((e = launch_precond_hybrid(h->op, h->pc, h->d_r, h->d_z, nullptr, s))) return fail(e);
+    if ((e = launch_pcg_rz(h->d_sc, h->d_r, h->d_z, n, s))) return fail(e);
+  } else {
+    if ((e = launch_precond(h->pc, h->d_r, h->d_z, &h->d_sc->rz_new, nullptr, s))) return fail(e);
+  }
+  if ((e = launch_pcg_start(h->d_sc, h->d_z, h->d_p, n, rtol, maxit, s))) return fail(e);
+  *st = RDR_OK;
+  return 2 + (h->pc.hybrid ? count_hybrid_launches(h->pc) + 1 : count_precond_launches(h->pc));
+}
+
+static int fetch_scalars(rdr_handle* h, cudaStream_t s) {
+  CK(cudaMemcpyAsync(h->h_sc, h->d_sc, sizeof(PcgScalars), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return RDR_OK;
+}
+
+// One PCG solve. rdr_options.loop: RDR_LOOP_DEVICE -- one graph whose while node
+// repeats 8-iteration bodies until the device-side stopping test fires (one host
+// synchronisation per solve; fused path; the unfused hybrid path falls back to
+// RDR_LOOP_HOST); RDR_LOOP_HOST -- graphs of 8 iterations relaunched by the host
+// until done; RDR_LOOP_EAGER -- every kernel launched on the stream, the host
+// checking the stop flag after each iteration (no graphs: profilers see every
+// launch).
+static int solve_device(rdr_handle* h, const double* b, double rtol, int maxit, int* iters, cudaStream_t s) {
+  int st;
+  int64_t launches = pcg_begin(h, b, rtol, maxit, s, &st);
+  if (st) return st;
+  // the unfused path tests before each iteration, the fused one inside its apply
+  const bool test_first = !h->fused;
+  if (h->fused && h->loop == RDR_LOOP_DEVICE) {
+    if ((st = build_while_graph(h))) return st;
     CK(cudaGraphLaunch(h->wgraph, s));
-    CK(cudaMemcpyAsync(h->h_sc, h->d_sc, sizeof(PcgScalars), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
+    if ((st = fetch_scalars(h, s))) return st;
     // bodies of kWhileUnroll iterations (+ the condition kernel) ran until the one that detected convergence
     const int64_t bodies = (h->h_sc->k + kWhileUnroll - 1) / kWhileUnroll;
-    launches = 1 + count_precond_launches(h->pc) + bodies * (kWhileUnroll * h->launches_per_iter + 1);
-    h->last_launches = launches;
-    *iters = h->h_sc->iters;
-    return h->h_sc->converged ? RDR_OK : RDR_ENOCONV;
-  }
-  if ((st = build_graph(h, 8))) return st;
-  if (h->fused) {
-    CK(cudaStreamSynchronize(s));  // h_sc (pinned) is reused as the H2D template
-    std::memset(h->h_sc, 0, sizeof(PcgScalars));
-    h->h_sc->rtol = rtol;
-    h->h_sc->maxit = maxit;
-    CK(cudaMemcpyAsync(h->d_sc, h->h_sc, sizeof(PcgScalars), cudaMemcpyHostToDevice, s));
-    CK(cudaMemsetAsync(h->d_p, 0, sizeof(double) * n, s));
-    CK(cudaMemsetAsync(h->d_p2, 0, sizeof(double) * n, s));
-    CK(launch_pcg_init(b, h->d_cons, n, h->d_x, h->d_r, h->d_q, s));
-    CK(launch_precond(h->pc, h->d_r, h->d_z, &h->d_sc->rz_acc, nullptr, s));
-    launches += 1 + count_precond_launches(h->pc);
-    for (;;) {  // the fused apply of each iteration performs the stopping test
-      CK(cudaGraphLaunch(h->graph, s));
-      launches += (int64_t)h->graph_iters * h->launches_per_iter;
-      CK(cudaMemcpyAsync(h->h_sc, h->d_sc, sizeof(PcgScalars), cudaMemcpyDeviceToHost, s));
-      CK(cudaStreamSynchronize(s));
-      if (h->h_sc->done) break;
+    launches += bodies * (kWhileUnroll * h->launches_per_iter + 1);
+  } else if (h->loop == RDR_LOOP_EAGER) {
+    for (;;) {
+      if (test_first) {
+        if ((st = fetch_scalars(h, s))) return st;
+        if (h->h_sc->done) break;
+      }
+      if ((st = enqueue_iteration(h, s))) return st;
+      launches += h->launches_per_iter;
+      if (!test_first) {
+        if ((st = fetch_scalars(h, s))) return st;
+        if (h->h_sc->done) break;
+      }
     }
   } else {
-    CK(cudaMemsetAsync(h->d_sc, 0, sizeof(PcgScalars), s));
-    CK(launch_pcg_init(b, h->d_cons, n, h->d_x, h->d_r, h->d_q, s));
-    if (h->pc.hybrid) {
-      CK(launch_precond_hybrid(h->op, h->pc, h->d_r, h->d_z, nullptr, s));
-      CK(launch_pcg_rz(h->d_sc, h->d_r, h->d_z, n, s));
-    } else {
-      CK(launch_precond(h->pc, h->d_r, h->d_z, &h->d_sc->rz_new, nullptr, s));
-    }
-    CK(launch_pcg_start(h->d_sc, h->d_z, h->d_p, n, rtol, maxit, s));
-    launches += 2 + count_precond_launches(h->pc);
+    if ((st = build_graph(h, 8))) return st;
     for (;;) {
-      CK(cudaMemcpyAsync(h->h_sc, h->d_sc, sizeof(PcgScalars), cudaMemcpyDeviceToHost, s));
-      CK(cudaStreamSynchronize(s));
-      if (h->h_sc->done) break;
+      if (test_first) {
+        if ((st = fetch_scalars(h, s))) return st;
+        if (h->h_sc->done) break;
+      }
       CK(cudaGraphLaunch(h->graph, s));
       launches += (int64_t)h->graph_iters * h->launches_per_iter;
+      if (!test_first) {
+        if ((st = fetch_scalars(h, s))) return st;
+        if (h->h_sc->done) break;
+      }
     }
   }
   h->last_launches = launches;
@@ -951,6 +969,63 @@ int rdr_last_launches(const rdr_handle* h, int64_t* launches) {
   if (!h || !launches) return RDR_EINVAL;
   *launches = h->last_launches;
   return RDR_OK;
+}
+
+int rdr_last_solve(const rdr_handle* h, rdr_solve_stats* out) {
+  if (!h || !out) return RDR_EINVAL;
+  out->iters = h->h_sc->iters;
+  out->converged = h->h_sc->converged;
+  out->z0 = h->h_sc->z0;
+  out->z_last = h->h_sc->z_last;
+  out->launches = h->last_launches;
+  return RDR_OK;
+}
+
+int rdr_profile_solve(rdr_handle* h, const double* b, double rtol, int maxit, int* iters, double* ms, void* stream) {
+  if (!h || !b || !iters || !ms || !(rtol >= 0)) return RDR_EINVAL;
+  if (!h->fused) return RDR_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  int st;
+  pcg_begin(h, b, rtol, maxit, s, &st);
+  if (st) return st;
+  cudaEvent_t ev[6];
+  for (auto& e : ev) CK(cudaEventCreate(&e));
+  double acc[4] = {0, 0, 0, 0};
+  int n_apply = 0;
+  for (;;) {  // the eager fused iteration with an event between its kernel groups
+    CK(cudaEventRecord(ev[0], s));
+    CK(launch_pcg_fused_apply(h->op, h->d_sc, h->d_z, h->d_p, h->d_p2, h->d_q, s));
+    CK(cudaEventRecord(ev[1], s));
+    CK(launch_pcg_update_jacobi(h->d_sc, h->pc, h->d_p, h->d_p2, h->d_q, h->d_x, h->d_r, h->d_z, s));
+    CK(cudaEventRecord(ev[2], s));
+    CK(launch_precond_part(1, h->pc, h->d_r, h->d_z, &h->d_sc->rz_acc, h->d_sc, s));
+    CK(cudaEventRecord(ev[3], s));
+    CK(launch_precond_part(2, h->pc, h->d_r, h->d_z, &h->d_sc->rz_acc, h->d_sc, s));
+    CK(cudaEventRecord(ev[4], s));
+    CK(launch_precond_part(3, h->pc, h->d_r, h->d_z, &h->d_sc->rz_acc, h->d_sc, s));
+    CK(cudaEventRecord(ev[5], s));
+    if ((st = fetch_scalars(h, s))) break;
+    float t[5];
+    for (int k = 0; k < 5; ++k) CK(cudaEventElapsedTime(&t[k], ev[k], ev[k + 1]));
+    ++n_apply;
+    if (h->h_sc->done) {  // this iteration's apply performed the final stopping test
+      acc[0] += t[0];
+      break;
+    }
+    acc[0] += t[0];
+    acc[1] += t[1];
+    acc[3] += t[2] + t[4];
+    acc[2] += t[3];
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  if (st) return st;
+  const int n_full = std::max(1, n_apply - 1);
+  ms[0] = acc[0] / n_apply;
+  ms[1] = acc[1] / n_full;
+  ms[2] = acc[2] / n_full;
+  ms[3] = acc[3] / n_full;
+  *iters = h->h_sc->iters;
+  return h->h_sc->converged ? RDR_OK : RDR_ENOCONV;
 }
 
 int rdr_time_kernels(rdr_handle* h, const double* x, double* y, const double* r, double* z, int reps, double* ms,

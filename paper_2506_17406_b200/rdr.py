@@ -15,6 +15,7 @@ HGRAD, HCURL, HDIV = 0, 1, 2
 SPLIT, UNSPLIT = 0, 1
 ADDITIVE, HYBRID = 0, 1
 SETUP_DEVICE, SETUP_HOST = 0, 1
+LOOP_DEVICE, LOOP_HOST, LOOP_EAGER = 0, 1, 2
 RDR_OK, RDR_ENOCONV = 0, -6
 
 
@@ -25,7 +26,16 @@ class RdrError(RuntimeError):
 
 
 class Options(ctypes.Structure):
-    _fields_ = [("decomposition", ctypes.c_int), ("preconditioner", ctypes.c_int), ("setup", ctypes.c_int)]
+    _fields_ = [("decomposition", ctypes.c_int), ("preconditioner", ctypes.c_int), ("setup", ctypes.c_int),
+                ("loop", ctypes.c_int)]
+
+
+class SolveStats(ctypes.Structure):
+    _fields_ = [("iters", ctypes.c_int32), ("converged", ctypes.c_int32), ("z0", ctypes.c_double),
+                ("z_last", ctypes.c_double), ("launches", ctypes.c_int64)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
 
 
 class Info(ctypes.Structure):
@@ -59,6 +69,8 @@ def _load():
         "rdr_solve": (ctypes.c_int, [P, P, P, D, ctypes.c_int, ctypes.POINTER(ctypes.c_int), P]),
         "rdr_solve_host": (ctypes.c_int, [P, P, P, D, ctypes.c_int, ctypes.POINTER(ctypes.c_int), P]),
         "rdr_last_launches": (ctypes.c_int, [P, ctypes.POINTER(I64)]),
+        "rdr_last_solve": (ctypes.c_int, [P, ctypes.POINTER(SolveStats)]),
+        "rdr_profile_solve": (ctypes.c_int, [P, P, D, ctypes.c_int, ctypes.POINTER(ctypes.c_int), P, P]),
         "rdr_time_kernels": (ctypes.c_int, [P, P, P, P, P, ctypes.c_int, P, P]),
         "rdr_measure_fp64_peak": (ctypes.c_int, [ctypes.POINTER(D), P]),
         "rdr_debug_fused_apply": (ctypes.c_int, [P, P, P, P]),
@@ -134,7 +146,7 @@ class Solver:
     CUDA tensors of length n_total."""
 
     def __init__(self, vertices, tets, p, space, alpha, beta, mask, stream=None, decomposition=SPLIT,
-                 preconditioner=ADDITIVE, setup=SETUP_DEVICE):
+                 preconditioner=ADDITIVE, setup=SETUP_DEVICE, loop=LOOP_DEVICE):
         import torch
         self._keep = [np.ascontiguousarray(vertices, dtype=np.float64) if isinstance(vertices, np.ndarray) else vertices,
                       np.ascontiguousarray(tets, dtype=np.int32) if isinstance(tets, np.ndarray) else tets,
@@ -144,7 +156,7 @@ class Solver:
         v, t, a, b, m = self._keep
         self._h = ctypes.c_void_p()
         nv, nt = v.shape[0], t.shape[0]
-        opt = Options(int(decomposition), int(preconditioner), int(setup))
+        opt = Options(int(decomposition), int(preconditioner), int(setup), int(loop))
         _check(_lib.rdr_setup_ex(ctypes.byref(self._h), _ptr(v), nv, _ptr(t), nt, int(p), int(space), _ptr(a),
                                  _ptr(b), _ptr(m), ctypes.byref(opt), _stream(stream)), "rdr_setup_ex")
         self._keep = None
@@ -214,6 +226,24 @@ class Solver:
         """q = A z through the fused PCG variant of the apply kernel (debugging)."""
         _check(_lib.rdr_debug_fused_apply(self._h, _ptr(z), _ptr(q), _stream(stream)), "rdr_debug_fused_apply")
         return q
+
+    def last_stats(self) -> dict:
+        """iters, converged, ||z_0||, ||z_k|| at the last stopping test, launches of the last solve."""
+        st = SolveStats()
+        _check(_lib.rdr_last_solve(self._h, ctypes.byref(st)), "rdr_last_solve")
+        return st.as_dict()
+
+    def profile_solve(self, b, rtol=1e-8, maxit=10000, stream=None):
+        """Eager PCG solve with CUDA events between kernel groups: (iters, ms per
+        iteration of [apply, update + Jacobi, patches, gradient])."""
+        it = ctypes.c_int()
+        ms = np.zeros(4)
+        code = _lib.rdr_profile_solve(self._h, _ptr(b), float(rtol), int(maxit), ctypes.byref(it), _ptr(ms),
+                                      _stream(stream))
+        if code not in (RDR_OK, RDR_ENOCONV):
+            _check(code, "rdr_profile_solve")
+        self.converged = code == RDR_OK
+        return it.value, ms
 
     def last_launches(self) -> int:
         n = ctypes.c_int64()

@@ -7,6 +7,8 @@ values of the +-1 iteration-count parity tests at sizes too large to run the
 oracle inside the GPU test session.
 
     python scripts/oracle_golden.py 5:1-8 4 5:9-12 [3] [6]   (6: the H(div) NEXT-2 workload)
+    python scripts/oracle_golden.py --lean 3 7:9-10 8:9-10     (oracle/lean.py: element-by-element
+                                                              operator, packed Cholesky factors)
 """
 import json
 import os
@@ -19,27 +21,37 @@ sys.path.insert(0, ROOT)
 
 from rdr_inputs import make_config  # noqa: E402
 from oracle.solver import Oracle  # noqa: E402
+from oracle.lean import LeanOracle  # noqa: E402
 
 OUT = os.path.join(ROOT, "tests", "golden", "oracle_pcg_iters.json")
 
 
-def run(cfg, p):
+def run(cfg, p, lean=False):
     t0 = time.time()
     c = make_config(cfg, p=p) if p is not None else make_config(cfg)
-    O = Oracle(c.vertices, c.tets, c.p, c.space, c.alpha, c.beta, c.mask)
+    if lean:
+        store = os.path.join(ROOT, ".lean_store")
+        os.makedirs(store, exist_ok=True)
+        O = LeanOracle(c.vertices, c.tets, c.p, c.space, c.alpha, c.beta, c.mask, store_dir=store,
+                       workers=os.cpu_count(), verbose=True)
+    else:
+        O = Oracle(c.vertices, c.tets, c.p, c.space, c.alpha, c.beta, c.mask)
     O.build_preconditioner(kappa=False)
     b = c.draw_vector(O.n_total)
-    x, it, res = O.solve(b, rtol=1e-8)
+    hist = []
+    x, it, res = O.solve(b, rtol=1e-8, history=hist)
     return {"cfg": cfg, "p": c.p, "space": ("hgrad", "hcurl", "hdiv")[c.space], "n_total": int(O.n_total),
             "n_free": int(O.free.sum()), "iters": int(it), "true_rel_res": float(res),
-            "oracle_seconds": round(time.time() - t0, 1)}
+            "z_ratio_tail": [float(h) for h in hist[-3:]],
+            "oracle_seconds": round(time.time() - t0, 1), "oracle": "lean" if lean else "global"}
 
 
 def main():
     data = json.load(open(OUT)) if os.path.exists(OUT) else {"note": "", "entries": []}
     data["note"] = ("Oracle PCG iteration counts (oracle/solver.py, R-A16, rtol 1e-8) on BASELINE.json configs "
                     "with the seeded rhs; written by scripts/oracle_golden.py (oracle/ only).")
-    for spec in sys.argv[1:]:
+    lean = "--lean" in sys.argv
+    for spec in [a for a in sys.argv[1:] if a != "--lean"]:
         if ":" in spec:
             cfg, rng = spec.split(":")
             lo, hi = (int(v) for v in rng.split("-")) if "-" in rng else (int(rng), int(rng))
@@ -47,7 +59,7 @@ def main():
         else:
             jobs = [(int(spec), None)]
         for cfg, p in jobs:
-            e = run(cfg, p)
+            e = run(cfg, p, lean)
             e["host"] = f"{platform.node()} ({os.cpu_count()} cpus)"
             data["entries"] = [x for x in data["entries"] if not (x["cfg"] == e["cfg"] and x["p"] == e["p"])]
             data["entries"].append(e)

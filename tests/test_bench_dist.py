@@ -56,3 +56,45 @@ def test_reference_arm_nonzero_rank_is_silent(capsys, monkeypatch):
         config, p, ref_iters, steps, warmup = 1, 3, 1, 1, 0
     bench.run_reference(A)
     assert capsys.readouterr().out == ""
+
+
+def test_reference_arm_line_matches_our_config(capsys, monkeypatch):
+    """The reference arm's `config` is the same object our arm prints (same_config)."""
+    import json
+    import bench
+    monkeypatch.setenv("RANK", "0")
+    monkeypatch.setenv("WORLD_SIZE", "1")
+
+    class A:
+        config, p, ref_iters, steps, warmup = 1, 3, 2, 1, 0
+    bench.run_reference(A)
+    line = json.loads(capsys.readouterr().out)
+    assert line["impl"] == "reference" and line["value"] > 0
+    assert line["config"] == bench.config_dict(1, 3, 1)
+    assert line["cpu_baseline"]["cores"] >= 1 and "cpu_model" in line["cpu_baseline"]
+
+
+def test_lean_iteration_sample_scaling():
+    """oracle.lean.IterationSample (bench.py's cfg3 oracle timing): the sample's
+    scale factors are the cell and packed-factor ratios it states."""
+    import numpy as np
+    from rdr_inputs import make_config
+    from oracle.solver import Oracle
+    from oracle.lean import IterationSample
+    c = make_config(0, n=3, p=3, space=0, perturb=True, bc="all", coeffs="one")
+    O = Oracle(c.vertices, c.tets, c.p, c.space, c.alpha, c.beta, c.mask, assemble=False)
+    S = IterationSample(O, n_patches=4)
+    d = S.time_iteration()
+    assert d["sample_patches"] == 4 and d["t_iter"] > 0
+    assert np.isclose(d["scale_apply"], O.topo.nt / d["sample_cells"])
+    sizes = np.array([len(i) for _, i in O.patch_sets()], dtype=float)
+    samp = sum(n * (n + 1) / 2 for _, _, n in S.factors)
+    assert np.isclose(d["scale_patches"], np.sum(sizes * (sizes + 1) / 2) / samp)
+    # the sampled patch factors are the global oracle's patch matrices
+    from scipy.linalg import lapack
+    G = Oracle(c.vertices, c.tets, c.p, c.space, c.alpha, c.beta, c.mask)
+    r = c.draw_vector(G.n_total)
+    for (v, idx), (idx2, ap, n) in zip(S.patches, S.factors):
+        Am = G.A[idx][:, idx].toarray()
+        u = lapack.dpptrs(n, ap, r[idx][:, None], lower=1)[0][:, 0]
+        assert np.linalg.norm(Am @ u - r[idx]) <= 1e-12 * np.linalg.norm(r[idx])

@@ -311,7 +311,8 @@ def run(args):
     # denominator of a kernel timed in isolation, as MEASURED_PEAKS' burst figures)
     fp64_burst = rdr.measure_fp64_peak()
     c = make_cfg(cfg, args.p, seed=rank)
-    S = rdr.Solver(c.vertices, c.tets, c.p, c.space, c.alpha, c.beta, c.mask)
+    loop = {"device": rdr.LOOP_DEVICE, "host": rdr.LOOP_HOST, "eager": rdr.LOOP_EAGER}[args.loop]
+    S = rdr.Solver(c.vertices, c.tets, c.p, c.space, c.alpha, c.beta, c.mask, loop=loop)
     info = S.info
     n = S.n_total
     stream = torch.cuda.current_stream()
@@ -418,6 +419,7 @@ def run(args):
         "e2e": {"value": e_iters / (e_ms / 1e3), "unit": "PCG iters/s", "h2d_bytes_per_step": 8 * n,
                 "d2h_bytes_per_step": 8 * n},
         "gpu_launches": int(launches),
+        "pcg_loop": args.loop,
         "clocks": clk.summary(),
         "setup_s": info["setup_seconds"],
     }
@@ -449,6 +451,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-dgemm", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--loop", default="device", choices=["device", "host", "eager"],
+                    help="rdr_options.loop of the timed solver (host: graphs ncu can profile node by node)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3

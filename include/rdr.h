@@ -132,6 +132,8 @@ struct rdr_info {
   double patch_setup_flops;    /* algorithmic flops of the device block sweep: per patch, with
                                   nb = ceil(n/64), sum over pivot blocks of 2*64^3 per updated
                                   lower tile and panel product = 2*64^3 nb (nb-1)(nb+2)/2 */
+  int32_t apply_variant;       /* warp layout of the operator apply chosen by setup-time autotuning */
+  int32_t apply_grid;          /* its persistent grid (CTAs) */
 };
 
 /* Build the operator and the preconditioner (host setup once, then upload).
@@ -196,8 +198,9 @@ int rdr_last_solve(const rdr_handle* h, struct rdr_solve_stats* out);
  * with every kernel launched eagerly and CUDA events between the kernel groups
  * of each iteration; ms[4] receives the average device ms per iteration of
  * ms[0] the fused operator apply (direction update + A p + stopping test),
- * ms[1] the x/r update + interior Jacobi, ms[2] the star-patch solves,
- * ms[3] the discrete-gradient kernels (H(curl), else ~0) -- the in-solve
+ * ms[1] the x/r update + interior Jacobi, ms[2] the star-patch solves
+ * (H(curl): the discrete gradient of the potential patches included),
+ * ms[3] = 0 (kept for the layout of rdr_time_kernels) -- the in-solve
  * counterparts of rdr_time_kernels. Additive preconditioner only
  * (RDR_EINVAL otherwise). Synchronizes `stream`. */
 int rdr_profile_solve(rdr_handle* h, const double* b, double rtol, int maxit, int* iters, double* ms,
@@ -206,8 +209,8 @@ int rdr_profile_solve(rdr_handle* h, const double* b, double rtol, int maxit, in
 /* Measurement helper (bench.py roofline): launch each hot-path kernel `reps`
  * times back to back on `stream` between CUDA events and return the average
  * device time per launch in ms: ms[0] operator apply (gather-contract-scatter),
- * ms[1] interior Jacobi + zeroing, ms[2] patch solves, ms[3] discrete-gradient
- * kernels (H(curl), else 0). x, r: device input vectors, y, z: outputs
+ * ms[1] interior Jacobi + zeroing, ms[2] patch solves (H(curl): with the
+ * discrete gradient of the potential patches), ms[3] = 0. x, r: device input vectors, y, z: outputs
  * (contents overwritten). Synchronizes `stream`. */
 int rdr_time_kernels(rdr_handle* h, const double* x, double* y, const double* r, double* z, int reps, double* ms,
                      void* stream);
@@ -219,6 +222,12 @@ int rdr_measure_fp64_peak(double* tflops, void* stream);
 
 void rdr_destroy(rdr_handle* h);
 const char* rdr_strerror(int code);
+
+/* Debugging entry point: run the operator apply (and the solves) with warp
+ * layout `variant` (0 <= variant < 8; kernels.cu apply_variants) instead of the
+ * one setup's autotuning chose; RDR_EINVAL if it does not fit this operator.
+ * The GPU tests use it to check every layout against the oracle. */
+int rdr_debug_set_apply_variant(rdr_handle* h, int variant);
 
 /* Debugging entry point: one fused PCG operator apply at iteration 0 (q = A z
  * through the PCG variant of the apply kernel, which also writes the search

@@ -150,236 +150,309 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                : "memory");
 }
 
-constexpr int kApplyKC = 16;     // K rows per ring slot (16 x 32 doubles = 4 KB)
-constexpr int kApplySlots = 8;   // ring depth
-constexpr int kApplyCols = 32;   // N columns per CTA (4 n8-tiles)
-constexpr int kApplyWarps = 8;   // consumer warps (+1 producer warp)
+constexpr int kApplyCols = 32;   // N columns per work unit: one 32-column group of the stack
+constexpr int kLutShift = 9;     // op.lut[i] = (local entity << 9) | position inside the entity's block
 
 // smem row stride of X: == 4 (mod 16) doubles, so a warp's 8x4 A-fragment read is conflict-free
 __host__ __device__ __forceinline__ int apply_x_stride(int kp) { return kp + ((4 - kp % 16) + 16) % 16; }
 
-template <int BM>
-__host__ __device__ __forceinline__ size_t apply_smem_bytes(int kp, int nm) {
-  return sizeof(uint64_t) * 2 * kApplySlots + sizeof(double) * kApplySlots * kApplyKC * kApplyCols +
-         sizeof(double) * (size_t)BM * apply_x_stride(kp) + sizeof(double) * (size_t)BM * nm +
-         sizeof(int) * (size_t)BM * kApplyCols;
+// Warp layout: BM cells per work unit, warp tile 16 cells x 8*NQ columns,
+// MW = BM/16 warps along M, NW = 32/(8 NQ) along N, KS K-split groups:
+// MW*NW*KS MMA warps plus one TMA producer warp.
+__host__ __device__ constexpr int apply_mma_warps(int BM, int NQ, int KS) { return (BM / 16) * (32 / (8 * NQ)) * KS; }
+
+// One ring chunk = one 4-row step j4 of all NM reference matrices: rows
+// (j4, s, t) = R_s[4 j4 + t][group columns], t = 0..3, 4 NM x 32 doubles.
+__host__ __device__ constexpr int apply_chunk_doubles(int nm) { return 4 * nm * kApplyCols; }
+
+struct ApplySmem {
+  size_t ring, x, red, c, eb, lut, own, total;
+};
+__host__ __device__ inline ApplySmem apply_smem_layout(int BM, int NQ, int KS, int S, int kp, int nm) {
+  ApplySmem L;
+  const int MW = BM / 16, NW = 32 / (8 * NQ);
+  L.ring = sizeof(uint64_t) * 2 * S;
+  L.x = L.ring + sizeof(double) * (size_t)S * apply_chunk_doubles(nm);
+  L.red = L.x + sizeof(double) * (size_t)BM * apply_x_stride(kp);
+  L.c = L.red + sizeof(double) * (size_t)(KS - 1) * MW * NW * 16 * 8 * NQ;
+  L.eb = L.c + sizeof(double) * (size_t)BM * nm;
+  L.lut = L.eb + sizeof(int32_t) * (size_t)BM * 16;
+  L.own = L.lut + sizeof(uint16_t) * (size_t)((kp + 3) & ~3);
+  L.total = L.own + sizeof(uint16_t) * (size_t)((BM + 3) & ~3);
+  return L;
 }
 
-template <int BM, bool PCG>
-__global__ void __launch_bounds__((kApplyWarps + 1) * 32, 2)
-    apply_tc_kernel(DevOperator op, const double* __restrict__ x, double* __restrict__ y, double* pq_acc,
+__device__ __forceinline__ void mma_bar_sync(int nthreads) {  // named barrier 1: the MMA warps only
+  asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+}
+
+// Operator apply y += A x on FP64 tensor cores:
+// Y[c][i] = sum_s c_{c,s} sum_j X[c][j] R_s[j][i], one GEMM with M = cells,
+// N = n_loc, K = n_mat * kp (the stacked reference matrices), on DMMA
+// (mma.sync.m8n8k4.f64 -> SASS DMMA.8x8x4; sm_100a has no tcgen05 kind::f64,
+// SURVEY F1/F2).
+//
+// Persistent work split: the output is cut into units (a tile of BM cells) x
+// (a 32-column group), ntiles * ngroups of them in tile-major order, and CTA b
+// takes the contiguous range [U b / G, U (b+1) / G): balanced to one unit, and
+// a CTA gathers each tile once for all the column groups it covers (a tile
+// split between two CTAs is gathered by both). The producer warp streams the
+// group slices of the reference stack for all the CTA's units back to back
+// through an S-slot ring of cp.async.bulk (TMA) copies completing on
+// mbarriers, so the ring never drains between units. The stack is stored
+// j-major: chunk j4 holds rows 4 j4 .. 4 j4 + 3 of every R_s, so a chunk's K
+// loop is NM branch-free k-steps that reuse one pair of X values and the
+// cells' NM coefficients held in registers (A = c_s X is formed with one DMUL
+// per fragment). MMA warps own 16 cells x 8*NQ columns and split the chunks
+// in KS groups (chunk j4 -> group j4 % KS) reduced through shared memory.
+// The gather reads x (PCG mode: z and p_{k-1}) through per-cell entity bases
+// (ebase: first global dof of each of the 15 local entities, R-A9 numbering)
+// and the element's (entity, position) table, so no per-cell dof map is
+// stored; the epilogue scatter-adds with red.global.add.f64 and accumulates
+// p.(Ap). In PCG mode the gather also forms p_k = z_k + beta_k p_{k-1}, which
+// the owner cell of each entity writes once (the CTA holding the tile's
+// column group 0), and the last CTA performs the stopping test (R-A16).
+template <int BM, int NQ, int KS, int NM, bool PCG>
+__global__ void __launch_bounds__((apply_mma_warps(BM, NQ, KS) + 1) * 32, 1)
+    apply_tc_kernel(DevOperator op, int S, const double* __restrict__ x, double* __restrict__ y, double* pq_acc,
                     const PcgScalars* guard, PcgScalars* sc, double* pbuf0, double* pbuf1) {
-  constexpr int MW = BM / 16;             // warps along M (16 cells each)
-  constexpr int KS = kApplyWarps / MW;    // K-split groups
-  static_assert(MW * KS == kApplyWarps && kApplySlots % KS == 0, "warp layout");
+  constexpr int MW = BM / 16, NW = 32 / (8 * NQ), NWARP = apply_mma_warps(BM, NQ, KS);
+  constexpr int NT = NWARP * 32;
+  constexpr int kChunk = apply_chunk_doubles(NM);
+  constexpr uint32_t kChunkBytes = kChunk * sizeof(double);
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
-  uint64_t* empty = full + kApplySlots;
-  double* ring = reinterpret_cast<double*>(empty + kApplySlots);      // [slots][KC][32] swizzled
-  const int n = op.n_loc, nm = op.n_mat, kp = op.kp;
+  const int n = op.n_loc, kp = op.kp;
   const int XS = apply_x_stride(kp);
-  double* X = ring + kApplySlots * kApplyKC * kApplyCols;              // [BM][XS]
-  long long* Xi = reinterpret_cast<long long*>(X);                    // the same slots, holding dof ids first
-  double* C = X + BM * XS;                                             // [BM][nm]
-  int* D = reinterpret_cast<int*>(C + BM * nm);                        // [BM][32] dofs of this CTA's columns
+  const ApplySmem L = apply_smem_layout(BM, NQ, KS, S, kp, NM);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
+  uint64_t* empty = full + S;
+  double* ring = reinterpret_cast<double*>(smem_raw + L.ring);  // [S][4 NM][32] swizzled
+  double* X = reinterpret_cast<double*>(smem_raw + L.x);        // [BM][XS]
+  double* red = reinterpret_cast<double*>(smem_raw + L.red);    // [KS-1][MW*NW][16 * 8NQ] per lane
+  double* C = reinterpret_cast<double*>(smem_raw + L.c);        // [BM][NM]
+  int32_t* EB = reinterpret_cast<int32_t*>(smem_raw + L.eb);    // [BM][16]
+  uint16_t* LUT = reinterpret_cast<uint16_t*>(smem_raw + L.lut);
+  uint16_t* OWN = reinterpret_cast<uint16_t*>(smem_raw + L.own);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int cg = blockIdx.y, col0 = cg * kApplyCols;
-  const int nchunks = op.kpad / kApplyKC;
-  const double* __restrict__ Bg = op.Bsw + (size_t)cg * op.kpad * kApplyCols;
-  constexpr uint32_t kChunkBytes = kApplyKC * kApplyCols * sizeof(double);
+  const bool producer = warp == NWARP;
+  const int nchunks = kp / 4;
+  const int64_t U = (int64_t)op.ntiles * op.ngroups;
+  const int64_t u0 = U * blockIdx.x / gridDim.x, u1 = U * (blockIdx.x + 1) / gridDim.x;
+  const int64_t total_chunks = (u1 - u0) * nchunks;
 
   // ---- prologue on constant data only (overlaps the previous kernel under PDL)
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kApplySlots; ++s) {
+    for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], MW * 32);  // every consumer lane releases its own reads of the slot
+      mbar_init(&empty[s], MW * NW * 32);  // every lane of the chunk's K group releases its own reads
     }
     mbar_fence_init();
   }
+  for (int i = threadIdx.x; i < kp; i += blockDim.x) LUT[i] = i < n ? op.lut[i] : 0;
   __syncthreads();
-  const bool producer = warp == kApplyWarps;
-  const int prefilled = min(nchunks, kApplySlots);
-  if (producer && lane == 0) {  // fill the ring with the reference stack while everyone gathers
-    for (int c = 0; c < prefilled; ++c) {
-      mbar_expect_tx(&full[c], kChunkBytes);
-      bulk_g2s(ring + c * kApplyKC * kApplyCols, Bg + (size_t)c * kApplyKC * kApplyCols, kChunkBytes, &full[c]);
+  const int prefilled = (int)min((int64_t)S, total_chunks);
+  // producer cursor over the CTA's chunk sequence: unit group / chunk / ring slot,
+  // advanced incrementally (no 64-bit divisions on the issue path)
+  int p_grp = (int)(u0 % op.ngroups), p_c = 0, p_slot = 0;
+  auto issue_next = [&]() {
+    const double* src = op.Bsw + ((size_t)p_grp * nchunks + p_c) * kChunk;
+    mbar_expect_tx(&full[p_slot], kChunkBytes);
+    bulk_g2s(ring + p_slot * kChunk, src, kChunkBytes, &full[p_slot]);
+    if (++p_c == nchunks) {
+      p_c = 0;
+      if (++p_grp == op.ngroups) p_grp = 0;
     }
-  }
-  const int64_t c0 = (int64_t)blockIdx.x * BM;
-  const int nc = (int)min((int64_t)BM, op.n_cells - c0);
-  const int nthr = blockDim.x;
-  for (int e = threadIdx.x; e < BM * XS; e += nthr) {  // dof ids of the tile (X slots), this CTA's columns
-    const int c = e / XS, j = e - c * XS;
-    const int gd = (c < nc && j < n) ? op.dofmap_m[(c0 + c) * n + j] : -1;
-    Xi[e] = gd;
-    if (j >= col0 && j < col0 + kApplyCols) D[c * kApplyCols + (j - col0)] = (j < n) ? gd : -1;
-  }
-  for (int e = threadIdx.x; e < BM * nm; e += nthr) {
-    const int c = e / nm;
-    C[e] = (c < nc) ? op.coef[(c0 + c) * nm + (e - c * nm)] : 0.0;
-  }
-  // columns past n_loc (n not a multiple of 32): never written by the loop above
-  for (int e = threadIdx.x; e < BM * kApplyCols; e += nthr)
-    if (col0 + (e % kApplyCols) >= n) D[e] = -1;
+    if (++p_slot == S) p_slot = 0;
+  };
+  if (producer && lane == 0)
+    for (int q = 0; q < prefilled; ++q) issue_next();
 
   pdl_wait();
   if (stopped(guard)) {  // drain the prefilled ring before the CTA's shared memory goes away
     if (producer && lane == 0)
-      for (int c = 0; c < prefilled; ++c) mbar_wait(&full[c], 0);
+      for (int q = 0; q < prefilled; ++q) mbar_wait(&full[q], 0);
     return;
   }
 
-  // ---- PCG mode: direction update p_k = z_k + beta_k p_{k-1} folded into the gather
-  double beta = 0.0;
-  const double* p_old = nullptr;
-  double* p_new = nullptr;
+  double pq = 0.0, zz = 0.0;
   int kit = 0;
-  if (PCG) {
-    volatile PcgScalars* v = sc;
-    kit = v->k;
-    beta = kit == 0 ? 0.0 : v->rz_acc / v->rz_old;
-    p_old = (kit & 1) ? pbuf0 : pbuf1;
-    p_new = (kit & 1) ? pbuf1 : pbuf0;
-  }
-  double zz = 0.0;
-
-  // ---- gather X in place (each thread reads back the dof ids it stored above)
-  {
-    constexpr int GB = 8;
-    for (int e0 = 0; e0 < BM * XS; e0 += GB * nthr) {
-      int gd[GB];
-#pragma unroll
-      for (int i = 0; i < GB; ++i) {
-        const int e = e0 + i * nthr + threadIdx.x;
-        gd[i] = e < BM * XS ? (int)Xi[e] : -1;
-      }
-      double xv[GB], pv[GB];
-#pragma unroll
-      for (int i = 0; i < GB; ++i) {
-        xv[i] = gd[i] >= 0 ? x[gd[i]] : 0.0;
-        pv[i] = (PCG && gd[i] >= 0) ? p_old[gd[i]] : 0.0;
-      }
-#pragma unroll
-      for (int i = 0; i < GB; ++i) {
-        const int e = e0 + i * nthr + threadIdx.x;
-        if (e >= BM * XS) continue;
-        double v = xv[i];
-        if (PCG && gd[i] >= 0) {
-          v = fma(beta, pv[i], xv[i]);
-          const int c = e / XS, j = e - c * XS;
-          if (cg == 0 && op.owner[(c0 + c) * n + j]) {
-            p_new[gd[i]] = v;
-            zz = fma(xv[i], xv[i], zz);
-          }
-        }
-        X[e] = v;
-      }
-    }
-  }
-  __syncthreads();
-
-  const int g = lane >> 2, t = lane & 3;
-  const int mw = warp % MW, kg = warp / MW;
-  double acc[2][4][2];
-#pragma unroll
-  for (int m = 0; m < 2; ++m)
-#pragma unroll
-    for (int q = 0; q < 4; ++q) acc[m][q][0] = acc[m][q][1] = 0.0;
-
   if (producer) {
     if (lane == 0) {
-      for (int c = prefilled; c < nchunks; ++c) {
-        const int slot = c % kApplySlots;
-        if (c >= kApplySlots) mbar_wait(&empty[slot], ((c / kApplySlots) - 1) & 1);
-        mbar_expect_tx(&full[slot], kChunkBytes);
-        bulk_g2s(ring + slot * kApplyKC * kApplyCols, Bg + (size_t)c * kApplyKC * kApplyCols, kChunkBytes,
-                 &full[slot]);
+      uint32_t ph = 0;  // parity of the slot's previous use
+      for (int64_t q = prefilled; q < total_chunks; ++q) {
+        if (p_slot == 0 && q > prefilled) ph ^= 1u;
+        mbar_wait(&empty[p_slot], ph);
+        issue_next();
       }
     }
   } else {
-    // per-lane B offsets inside a 4-row k-step: (k, col) stored at k*32 + (col ^ ((k & 3) << 2))
-    int boff[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) boff[q] = t * kApplyCols + ((q * 8 + g) ^ (t << 2));
-    const double* xr0 = X + (mw * 16 + g) * XS + t;
-    const double* xr1 = xr0 + 8 * XS;
-    const double* cr0 = C + (mw * 16 + g) * nm;
-    const double* cr1 = cr0 + 8 * nm;
-    for (int c = kg; c < nchunks; c += KS) {
-      const int slot = c % kApplySlots;
-      mbar_wait(&full[slot], (c / kApplySlots) & 1);
-      const double* Bs = ring + slot * kApplyKC * kApplyCols;
-      int krow = c * kApplyKC;
-      int s = krow / kp, j = krow - s * kp;
-      double cs0 = s < nm ? cr0[s] : 0.0, cs1 = s < nm ? cr1[s] : 0.0;
-#pragma unroll
-      for (int k4 = 0; k4 < kApplyKC / 4; ++k4) {
-        const double a0 = cs0 * xr0[j], a1 = cs1 * xr1[j];
-        double b[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) b[q] = Bs[k4 * 4 * kApplyCols + boff[q]];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          dmma884(acc[0][q][0], acc[0][q][1], a0, b[q]);
-          dmma884(acc[1][q][0], acc[1][q][1], a1, b[q]);
-        }
-        j += 4;
-        if (j >= kp) {
-          j = 0;
-          ++s;
-          cs0 = s < nm ? cr0[s] : 0.0;
-          cs1 = s < nm ? cr1[s] : 0.0;
-        }
-      }
-      // Every lane releases the slot after its own loads of it completed. An
-      // arrive issued right behind the LDS let the TMA refill overwrite the slot
-      // while the loads were still in flight: one warp in ~1 of 2 launches read
-      // half-refilled fragments (PCG variant, BM = 32, p = 10).
-      mbar_release(&empty[slot]);
+    // ---- PCG mode: direction update p_k = z_k + beta_k p_{k-1} folded into the gather
+    double beta = 0.0;
+    const double* p_old = nullptr;
+    double* p_new = nullptr;
+    if (PCG) {
+      volatile PcgScalars* v = sc;
+      kit = v->k;
+      beta = kit == 0 ? 0.0 : v->rz_acc / v->rz_old;
+      p_old = (kit & 1) ? pbuf0 : pbuf1;
+      p_new = (kit & 1) ? pbuf1 : pbuf0;
     }
-  }
-  __syncthreads();  // every chunk consumed (all bulk copies complete): the ring is free
-  if (pdl_late()) pdl_trigger();
+    const int tid = threadIdx.x;
+    const int g8 = lane >> 2, t4 = lane & 3;
+    const int kg = warp / (MW * NW), wmn = warp % (MW * NW), mw = wmn % MW, nw = wmn / MW;
+    int boff[NQ];  // B fragment (k, col) of a 4-row k-step at k*32 + (col ^ ((k & 3) << 2))
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) boff[q] = t4 * kApplyCols + ((nw * 8 * NQ + q * 8 + g8) ^ (t4 << 2));
+    const double* xr0 = X + (mw * 16 + g8) * XS + t4;
+    const double* xr1 = xr0 + 8 * XS;
+    double cs0[NM], cs1[NM];  // the two fragment rows' cell coefficients
+    int64_t tile_cur = -1;
+    int64_t qbase = 0;
+    for (int64_t u = u0; u < u1; ++u, qbase += nchunks) {
+      const int64_t tile = u / op.ngroups;
+      const int grp = (int)(u % op.ngroups);
+      if (tile != tile_cur) {
+        // ---- gather the tile (once per CTA): entity bases, coefficients, owner bits, then X
+        mma_bar_sync(NT);  // every read of the previous tile's X / C / EB is done
+        const int64_t c0 = tile * BM;
+        const int nc = (int)min((int64_t)BM, op.n_cells - c0);
+        for (int e = tid; e < BM * 16; e += NT) EB[e] = (e >> 4) < nc ? op.ebase[c0 * 16 + e] : -1;
+        for (int e = tid; e < BM * NM; e += NT) C[e] = e / NM < nc ? op.coef[c0 * NM + e] : 0.0;
+        for (int e = tid; e < BM; e += NT) OWN[e] = e < nc ? op.own[c0 + e] : 0;
+        mma_bar_sync(NT);
+        const bool writer = PCG && grp == 0;  // the CTA that holds column group 0 of the tile
+        constexpr int GB = 4;
+        const int total = BM * XS;
+        for (int e0 = 0; e0 < total; e0 += GB * NT) {
+          int gid[GB];
+          bool own[GB];
+#pragma unroll
+          for (int i = 0; i < GB; ++i) {
+            const int e = e0 + i * NT + tid;
+            const int c = e / XS, j = e - c * XS;
+            gid[i] = -1;
+            own[i] = false;
+            if (e < total && j < n) {
+              const int l = LUT[j];
+              const int b = EB[c * 16 + (l >> kLutShift)];
+              if (b >= 0) {
+                gid[i] = b + (l & ((1 << kLutShift) - 1));
+                own[i] = (OWN[c] >> (l >> kLutShift)) & 1;
+              }
+            }
+          }
+          double xv[GB], pv[GB];
+#pragma unroll
+          for (int i = 0; i < GB; ++i) {
+            xv[i] = gid[i] >= 0 ? x[gid[i]] : 0.0;
+            pv[i] = (PCG && gid[i] >= 0) ? p_old[gid[i]] : 0.0;
+          }
+#pragma unroll
+          for (int i = 0; i < GB; ++i) {
+            const int e = e0 + i * NT + tid;
+            if (e >= total) continue;
+            double v = xv[i];
+            if (PCG && gid[i] >= 0) {
+              v = fma(beta, pv[i], xv[i]);
+              if (writer && own[i]) {
+                p_new[gid[i]] = v;
+                zz = fma(xv[i], xv[i], zz);
+              }
+            }
+            X[e] = v;
+          }
+        }
+        mma_bar_sync(NT);
+#pragma unroll
+        for (int s = 0; s < NM; ++s) {
+          cs0[s] = C[(mw * 16 + g8) * NM + s];
+          cs1[s] = C[(mw * 16 + 8 + g8) * NM + s];
+        }
+        tile_cur = tile;
+      }
 
-  // ---- K-split reduction through the ring, then scatter-add from group 0
-  double* red = ring;  // [(KS-1)][MW][16][32]
-  if (!producer && kg > 0) {
-    double* dst = red + (((kg - 1) * MW + mw) * 16) * 32 + lane;
-#pragma unroll
-    for (int m = 0; m < 2; ++m)
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-#pragma unroll
-        for (int i = 0; i < 2; ++i) dst[((m * 4 + q) * 2 + i) * 32] = acc[m][q][i];
-  }
-  __syncthreads();
-  double pq = 0.0;
-  if (!producer && kg == 0) {
-    for (int h = 1; h < KS; ++h) {
-      const double* src = red + (((h - 1) * MW + mw) * 16) * 32 + lane;
+      // ---- K loop of the unit: chunk j4 (rows 4 j4.. of every R_s) by K group j4 % KS
+      double acc[2][NQ][2];
 #pragma unroll
       for (int m = 0; m < 2; ++m)
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
+        for (int q = 0; q < NQ; ++q) acc[m][q][0] = acc[m][q][1] = 0.0;
+      // ring position of this warp's first chunk of the unit (one division per unit)
+      int slot = (int)((qbase + kg) % S);
+      uint32_t par = (uint32_t)(((qbase + kg) / S) & 1);
+      for (int c = kg; c < nchunks; c += KS) {
+        mbar_wait(&full[slot], par);
+        const double* Bs = ring + slot * kChunk;
+        const double x0 = xr0[4 * c], x1 = xr1[4 * c];
 #pragma unroll
-          for (int i = 0; i < 2; ++i) acc[m][q][i] += src[((m * 4 + q) * 2 + i) * 32];
-    }
+        for (int s = 0; s < NM; ++s) {
+          const double a0 = cs0[s] * x0, a1 = cs1[s] * x1;
+          double b[NQ];
 #pragma unroll
-    for (int m = 0; m < 2; ++m) {
-      const int row = mw * 16 + m * 8 + g;
+          for (int q = 0; q < NQ; ++q) b[q] = Bs[s * 4 * kApplyCols + boff[q]];
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
-#pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          const int cl = q * 8 + 2 * t + i;
-          const int gd = D[row * kApplyCols + cl];
-          if (gd >= 0) {
-            atomicAdd(y + gd, acc[m][q][i]);
-            pq = fma(X[row * XS + col0 + cl], acc[m][q][i], pq);
+          for (int q = 0; q < NQ; ++q) {
+            dmma884(acc[0][q][0], acc[0][q][1], a0, b[q]);
+            dmma884(acc[1][q][0], acc[1][q][1], a1, b[q]);
           }
         }
+        // every lane releases the slot after its own loads of it completed (DESIGN.md §6:
+        // an arrive right behind the LDS let the TMA refill race the loads)
+        mbar_release(&empty[slot]);
+        slot += KS;
+        while (slot >= S) {
+          slot -= S;
+          par ^= 1u;
+        }
+      }
+
+      // ---- K-split reduction, then scatter-add from K group 0
+      if (KS > 1) {
+        if (kg > 0) {
+          double* dst = red + (((kg - 1) * MW * NW + wmn) * 16 * 8 * NQ) + lane;
+#pragma unroll
+          for (int m = 0; m < 2; ++m)
+#pragma unroll
+            for (int q = 0; q < NQ; ++q)
+#pragma unroll
+              for (int i = 0; i < 2; ++i) dst[((m * NQ + q) * 2 + i) * 32] = acc[m][q][i];
+        }
+        mma_bar_sync(NT);
+        if (kg == 0)
+          for (int h = 1; h < KS; ++h) {
+            const double* src = red + (((h - 1) * MW * NW + wmn) * 16 * 8 * NQ) + lane;
+#pragma unroll
+            for (int m = 0; m < 2; ++m)
+#pragma unroll
+              for (int q = 0; q < NQ; ++q)
+#pragma unroll
+                for (int i = 0; i < 2; ++i) acc[m][q][i] += src[((m * NQ + q) * 2 + i) * 32];
+          }
+      }
+      if (kg == 0) {
+#pragma unroll
+        for (int m = 0; m < 2; ++m) {
+          const int row = mw * 16 + m * 8 + g8;
+#pragma unroll
+          for (int q = 0; q < NQ; ++q)
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+              const int col = grp * kApplyCols + nw * 8 * NQ + q * 8 + 2 * t4 + i;
+              if (col < n) {
+                const int l = LUT[col];
+                const int b = EB[row * 16 + (l >> kLutShift)];
+                if (b >= 0) {
+                  atomicAdd(y + b + (l & ((1 << kLutShift) - 1)), acc[m][q][i]);
+                  pq = fma(X[row * XS + col], acc[m][q][i], pq);
+                }
+              }
+            }
+        }
+      }
+      if (KS > 1) mma_bar_sync(NT);  // the reduction buffer is reused by the next unit
     }
   }
+  if (pdl_late()) pdl_trigger();
 
   if (PCG) {
     __shared__ double sh[32];
@@ -390,8 +463,7 @@ __global__ void __launch_bounds__((kApplyWarps + 1) * 32, 2)
       atomicAdd(&sc->pq2[kit & 1], spq);
       atomicAdd(&sc->zz, szz);
       __threadfence();
-      const unsigned nblocks = gridDim.x * gridDim.y;
-      last = atomicAdd(&sc->ticket, 1u) == nblocks - 1;
+      last = atomicAdd(&sc->ticket, 1u) == gridDim.x - 1;
     }
     __syncthreads();
     if (last && threadIdx.x == 0) {  // stopping test on z_k (R-A16), then advance k
@@ -434,38 +506,56 @@ __global__ void __launch_bounds__((kApplyWarps + 1) * 32, 2)
 
 constexpr size_t kMaxSmem = 226 * 1024;  // 227 KB opt-in minus the static reduction scratch
 
-size_t apply_smem(int bm, const DevOperator& op) {
-  return bm == 64 ? apply_smem_bytes<64>(op.kp, op.n_mat)
-                  : bm == 32 ? apply_smem_bytes<32>(op.kp, op.n_mat) : apply_smem_bytes<16>(op.kp, op.n_mat);
+// The warp layouts built (BM, NQ, KS) with their ring depths, each for NM = 7
+// (H(grad), H(div)) and 12 (H(curl)); apply_choose picks the first that fits
+// two CTAs per SM, else the first that fits one.
+struct ApplyVariant {
+  int bm, nq, ks, slots, nm;
+  const void* fn[2];  // plain, PCG
+};
+template <int BM, int NQ, int KS, int NM>
+ApplyVariant apply_variant(int slots) {
+  return {BM, NQ, KS, slots, NM,
+          {(const void*)apply_tc_kernel<BM, NQ, KS, NM, false>, (const void*)apply_tc_kernel<BM, NQ, KS, NM, true>}};
+}
+const ApplyVariant* apply_variants(int* count) {
+  static const ApplyVariant v[] = {
+      apply_variant<32, 4, 2, 7>(4),  apply_variant<32, 4, 2, 12>(4),   // 4 MMA warps
+      apply_variant<32, 4, 4, 7>(6),  apply_variant<32, 4, 4, 12>(6),   // 8 MMA warps
+      apply_variant<32, 2, 2, 7>(4),  apply_variant<32, 2, 2, 12>(4),   // 8 MMA warps, 16 x 16 warp tiles
+      apply_variant<16, 4, 4, 7>(6),  apply_variant<16, 4, 4, 12>(6),   // 4 MMA warps, 16 cells per unit
+  };
+  *count = (int)(sizeof(v) / sizeof(v[0]));
+  return v;
 }
 
-// cells per CTA: 32 when two such CTAs fit on an SM (the two desynchronise, so
-// one's gather and epilogue overlap the other's DMMA loop), else 16; BM = 64
-// (one CTA per SM) measured 15-20% slower on configs 2, 4 and 5 (p = 10, 12).
-int apply_bm(const DevOperator& op) {
-  static const int forced = std::getenv("RDR_APPLY_BM") ? std::atoi(std::getenv("RDR_APPLY_BM")) : 0;
-  if ((forced == 16 || forced == 32 || forced == 64) && apply_smem(forced, op) <= kMaxSmem) return forced;
-  const size_t two_per_sm = 228 * 1024 / 2 - 1024;
-  return apply_smem(32, op) <= two_per_sm ? 32 : 16;
+size_t apply_variant_smem(const ApplyVariant& v, const DevOperator& op) {
+  return apply_smem_layout(v.bm, v.nq, v.ks, v.slots, op.kp, op.n_mat).total;
 }
 
-template <int BM, bool PCG>
-cudaError_t launch_apply_tc_bm(const DevOperator& op, const double* x, double* y, double* pq_acc,
-                               const PcgScalars* guard, cudaStream_t s, PcgScalars* sc, double* p0, double* p1) {
-  const size_t sm = apply_smem_bytes<BM>(op.kp, op.n_mat);
-  dim3 grid((unsigned)((op.n_cells + BM - 1) / BM), (unsigned)op.ngroups);
-  return launch_k(apply_tc_kernel<BM, PCG>, grid, dim3((kApplyWarps + 1) * 32), sm, s, op, x, y, pq_acc, guard, sc,
-                  p0, p1);
-}
+inline int apply_threads(const ApplyVariant& v) { return (apply_mma_warps(v.bm, v.nq, v.ks) + 1) * 32; }
 
 template <bool PCG>
 cudaError_t launch_apply_tc(const DevOperator& op, const double* x, double* y, double* pq_acc,
                             const PcgScalars* guard, cudaStream_t s, PcgScalars* sc = nullptr,
                             double* p0 = nullptr, double* p1 = nullptr) {
-  const int bm = apply_bm(op);
-  if (bm == 64) return launch_apply_tc_bm<64, PCG>(op, x, y, pq_acc, guard, s, sc, p0, p1);
-  if (bm == 32) return launch_apply_tc_bm<32, PCG>(op, x, y, pq_acc, guard, s, sc, p0, p1);
-  return launch_apply_tc_bm<16, PCG>(op, x, y, pq_acc, guard, s, sc, p0, p1);
+  int cnt = 0;
+  const ApplyVariant& v = apply_variants(&cnt)[op.av];
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)op.apply_grid);
+  cfg.blockDim = dim3(apply_threads(v));
+  cfg.dynamicSmemBytes = apply_variant_smem(v, op);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  int S = v.slots;
+  DevOperator o = op;
+  void* args[] = {(void*)&o, (void*)&S, (void*)&x, (void*)&y, (void*)&pq_acc, (void*)&guard, (void*)&sc, (void*)&p0,
+                  (void*)&p1};
+  return cudaLaunchKernelExC(&cfg, v.fn[PCG ? 1 : 0], args);
 }
 
 // ---------------------------------------------------------------- preconditioner
@@ -485,8 +575,6 @@ __global__ void precond_init_kernel(DevPrecond pc, const double* __restrict__ r,
       part = fma(ri, zi, part);
     }
   }
-  if (pc.ubuf)
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < pc.n_cg_iface; i += stride) pc.ubuf[i] = 0.0;
   if (rz_acc) {
     __shared__ double sh[32];
     double s = block_sum(part, sh);
@@ -494,27 +582,6 @@ __global__ void precond_init_kernel(DevPrecond pc, const double* __restrict__ r,
   }
 }
 
-__global__ void gather_grad_kernel(DevPrecond pc, const double* __restrict__ r, const PcgScalars* guard) {
-  pdl_wait();
-  if (stopped(guard)) return;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < pc.n_cg_iface; c += stride) {
-    double s = 0;
-    for (int64_t k = pc.g_ptr[c]; k < pc.g_ptr[c + 1]; ++k) s = fma(pc.g_val[k], r[pc.g_col[k]], s);
-    pc.gbuf[c] = s;
-  }
-}
-
-__global__ void scatter_grad_kernel(DevPrecond pc, double* __restrict__ z, const PcgScalars* guard) {
-  pdl_wait();
-  if (stopped(guard)) return;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < pc.n_cg_iface; c += stride) {
-    double u = pc.ubuf[c];
-    if (u == 0.0) continue;
-    for (int64_t k = pc.g_ptr[c]; k < pc.g_ptr[c + 1]; ++k) atomicAdd(z + pc.g_col[k], pc.g_val[k] * u);
-  }
-}
 
 // Star-patch kernel (Eq. 5.4 P:1763-1774 / Eq. 5.12 P:1956-1970 with exact
 // local solvers, R-A15): z += E_m A_m^{-1} E_m^T r. One CTA per patch, patches in decreasing size
@@ -536,6 +603,28 @@ __device__ __forceinline__ double ld_stream1(const double* p) {
   double v;
   asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
   return v;
+}
+
+// H(curl) potential patches (kind 1, Eq. 5.12): the patch's dofs are
+// CG_p interface dofs c embedded by the discrete gradient G (R-A12), so the
+// patch residual is (G^T r)_c = sum_k G[k][c] r_k and the correction is
+// scattered as z_k += G[k][c] u_c, both straight from the CSR rows of G^T
+// (one entry per CG edge / face dof, the incident Whitney edges per vertex).
+__device__ __forceinline__ double patch_residual(const DevPrecond& pc, bool pot, const double* __restrict__ r,
+                                                 int g) {
+  if (g < 0) return 0.0;
+  if (!pot) return r[g];
+  double s = 0.0;
+  for (int64_t k = pc.g_ptr[g]; k < pc.g_ptr[g + 1]; ++k) s = fma(pc.g_val[k], r[pc.g_col[k]], s);
+  return s;
+}
+__device__ __forceinline__ void patch_scatter(const DevPrecond& pc, bool pot, double* __restrict__ z, int g,
+                                              double u) {
+  if (!pot) {
+    atomicAdd(z + g, u);
+    return;
+  }
+  for (int64_t k = pc.g_ptr[g]; k < pc.g_ptr[g + 1]; ++k) atomicAdd(z + pc.g_col[k], pc.g_val[k] * u);
 }
 
 // v[k] over 32 lanes -> lane l holds sum_{lanes} v[l & 15] (16-value transpose reduction)
@@ -578,8 +667,6 @@ __global__ void __launch_bounds__(kLdgWarps * 32, 32 / kLdgWarps)
   const int n = pc.pn[pid];
   const int nb = (n + 31) >> 5, npad = nb * 32;
   const bool pot = pc.pkind[pid] != 0;
-  const double* __restrict__ rin = pot ? pc.gbuf : r;
-  double* __restrict__ zout = pot ? pc.ubuf : z;
   double* rl = smem + warp * 2 * kSmallPatch;
   double* zl = rl + kSmallPatch;
   const int32_t* id = pc.idx + pc.idx_off[pid];
@@ -621,10 +708,7 @@ __global__ void __launch_bounds__(kLdgWarps * 32, 32 / kLdgWarps)
   load_half(a);
   pdl_wait();
   if (stopped(guard)) return;
-  for (int i = lane; i < npad; i += 32) {
-    const int g = (int)rli[i];
-    rl[i] = (g >= 0) ? rin[g] : 0.0;
-  }
+  for (int i = lane; i < npad; i += 32) rl[i] = patch_residual(pc, pot, r, (int)rli[i]);
   __syncwarp();
   double row = 0.0;
   while (t < ntiles) {
@@ -663,7 +747,7 @@ __global__ void __launch_bounds__(kLdgWarps * 32, 32 / kLdgWarps)
   double part = 0.0;
   for (int i = lane; i < n; i += 32) {
     const double zi = zl[i];
-    atomicAdd(zout + id[i], pc.out_scale * zi);
+    patch_scatter(pc, pot, z, id[i], pc.out_scale * zi);
     part = fma(rl[i], zi, part);
   }
   part = warp_sum(part);
@@ -679,8 +763,6 @@ __global__ void __launch_bounds__(kLdgWarps * 32, 32 / kLdgWarps)
   const int n = pc.pn[pid];
   const int nb = (n + 31) >> 5, npad = nb * 32;
   const bool pot = pc.pkind[pid] != 0;
-  const double* __restrict__ rin = pot ? pc.gbuf : r;
-  double* __restrict__ zout = pot ? pc.ubuf : z;
   double* rl = smem;
   double* zl = smem + npad;
   const int32_t* id = pc.idx + pc.idx_off[pid];
@@ -731,10 +813,7 @@ __global__ void __launch_bounds__(kLdgWarps * 32, 32 / kLdgWarps)
   if (t < ntiles) load_half(a);  // the first half tile is in flight during the r gather
   pdl_wait();
   if (stopped(guard)) return;
-  for (int i = threadIdx.x; i < npad; i += blockDim.x) {
-    const int g = (int)rli[i];
-    rl[i] = (g >= 0) ? rin[g] : 0.0;
-  }
+  for (int i = threadIdx.x; i < npad; i += blockDim.x) rl[i] = patch_residual(pc, pot, r, (int)rli[i]);
   __syncthreads();
   double row = 0.0;
   while (t < ntiles) {
@@ -774,7 +853,7 @@ __global__ void __launch_bounds__(kLdgWarps * 32, 32 / kLdgWarps)
   double part = 0.0;
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     const double zi = zl[i];
-    atomicAdd(zout + id[i], pc.out_scale * zi);
+    patch_scatter(pc, pot, z, id[i], pc.out_scale * zi);
     part = fma(rl[i], zi, part);
   }
   if (rz_acc) {
@@ -799,8 +878,6 @@ __global__ void hyb_jacobi_kernel(DevPrecond pc, const double* __restrict__ r, d
     e[i] = add ? e[i] + v : v;
     if (!add) pc.hy[i] = 0.0;
   }
-  if (pc.ubuf)
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < pc.n_cg_iface; i += stride) pc.ubuf[i] = 0.0;
 }
 
 // t = r - y (y = A e, constrained rows already 0), then y = 0 for the next
@@ -815,8 +892,6 @@ __global__ void hyb_residual_kernel(DevPrecond pc, const double* __restrict__ r,
     y[i] = 0.0;
   }
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < pc.nc; i += stride) pc.czc[i] = 0.0;
-  if (pc.ubuf)
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < pc.n_cg_iface; i += stride) pc.ubuf[i] = 0.0;
 }
 
 // coarse solve e += E_c A_c^-1 E_c^T t: the stored packed inverse of the
@@ -1039,8 +1114,6 @@ __global__ void pcg_update_jacobi_kernel(PcgScalars* sc, DevPrecond pc, const do
       part = fma(rn, zi, part);
     }
   }
-  if (pc.ubuf)
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < pc.n_cg_iface; i += stride) pc.ubuf[i] = 0.0;
   __shared__ double sh[32];
   const double s = block_sum(part, sh);
   if (threadIdx.x == 0) atomicAdd(&sc->rz_acc, s);
@@ -1075,7 +1148,7 @@ size_t max_kernel_smem() { return kMaxSmem; }
 
 int count_precond_launches(const DevPrecond& pc) {
   const int patch_launches = pc.n_patches == 0 ? 0 : (pc.n_big > 0) + (pc.n_big < pc.n_patches);
-  return 1 + patch_launches + (pc.gbuf ? 2 : 0);
+  return 1 + patch_launches;
 }
 
 cudaError_t launch_precond_part(int part, const DevPrecond& pc, const double* r, double* z, double* rz_acc,
@@ -1085,9 +1158,6 @@ cudaError_t launch_precond_part(int part, const DevPrecond& pc, const double* r,
       return launch_k(precond_init_kernel, dim3(vec_grid(pc.n_total)), dim3(kVecThreads), 0, s, pc, r, z, rz_acc,
                       guard);
     case 1:
-      if (pc.gbuf) return launch_k(gather_grad_kernel, dim3(vec_grid(pc.n_cg_iface)), dim3(kVecThreads), 0, s, pc, r, guard);
-      break;
-    case 2:
       if (pc.n_patches > 0) {
         const int W = pc.ldg_warps;
         cudaError_t e = cudaSuccess;
@@ -1110,9 +1180,6 @@ cudaError_t launch_precond_part(int part, const DevPrecond& pc, const double* r,
         return e;
       }
       break;
-    case 3:
-      if (pc.gbuf) return launch_k(scatter_grad_kernel, dim3(vec_grid(pc.n_cg_iface)), dim3(kVecThreads), 0, s, pc, z, guard);
-      break;
   }
   return cudaGetLastError();
 }
@@ -1129,8 +1196,7 @@ cudaError_t launch_precond_hybrid(const DevOperator& op, const DevPrecond& pc, c
     if ((e = launch_apply(op, z, pc.hy, nullptr, guard, s)) != cudaSuccess) return e;
     if ((e = launch_k(hyb_residual_kernel, vg, vb, 0, s, pc, r, pc.hy, pc.ht, guard)) != cudaSuccess) return e;
     if (stage == 1 || stage == 3) {  // interface star patches, weight 1/rho_2
-      for (int part = 1; part < 4; ++part)
-        if ((e = launch_precond_part(part, pp, pc.ht, z, nullptr, guard, s)) != cudaSuccess) return e;
+      if ((e = launch_precond_part(1, pp, pc.ht, z, nullptr, guard, s)) != cudaSuccess) return e;
     } else if (stage == 2) {         // exact coarse solve on W^k
       if (pc.nc > 0) {
         if ((e = launch_k(coarse_symv_kernel, dim3(148 * 4), dim3(256), 0, s, pc, (const double*)pc.ht, guard)) !=
@@ -1162,7 +1228,7 @@ cudaError_t launch_pcg_rz(PcgScalars* sc, const double* r, const double* z, int6
 
 cudaError_t launch_precond(const DevPrecond& pc, const double* r, double* z, double* rz_acc,
                            const PcgScalars* guard, cudaStream_t s) {
-  for (int part = 0; part < 4; ++part) {
+  for (int part = 0; part < 2; ++part) {
     cudaError_t e = launch_precond_part(part, pc, r, z, rz_acc, guard, s);
     if (e != cudaSuccess) return e;
   }
@@ -1193,7 +1259,70 @@ cudaError_t launch_pcg_direction(PcgScalars* sc, const double* z, double* p, dou
   return cudaGetLastError();
 }
 
-bool fused_pcg_supported(const DevOperator& op) { return op.Bsw && op.owner; }
+bool fused_pcg_supported(const DevOperator& op) { return op.Bsw && op.own; }
+
+// Variant k's cell tiles and persistent grid for this operator (occupancy from
+// the PCG instance's registers and shared memory); -1 if it cannot run.
+int apply_configure_variant(DevOperator& op, int k) {
+  int cnt = 0;
+  const ApplyVariant* vs = apply_variants(&cnt);
+  if (k < 0 || k >= cnt || vs[k].nm != op.n_mat || apply_variant_smem(vs[k], op) > kMaxSmem) return -1;
+  const ApplyVariant& v = vs[k];
+  int per_sm = 0, dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, v.fn[1], apply_threads(v), apply_variant_smem(v, op)) !=
+      cudaSuccess) {
+    cudaGetLastError();
+    return -1;
+  }
+  if (per_sm < 1) return -1;
+  op.av = k;
+  op.ntiles = (int)((op.n_cells + v.bm - 1) / v.bm);
+  const int64_t units = (int64_t)op.ntiles * op.ngroups;
+  op.apply_grid = (int)std::max<int64_t>(1, std::min<int64_t>(units, (int64_t)per_sm * sms));
+  return 0;
+}
+
+int apply_variant_count() {
+  int cnt = 0;
+  apply_variants(&cnt);
+  return cnt;
+}
+
+// Setup-time autotuning of the apply's warp layout: every variant that fits is
+// timed on this operator (one warm-up, then `reps` plain applies between CUDA
+// events on `s`) and the fastest is kept.
+int tune_apply(DevOperator& op, const double* x, double* y, cudaStream_t s, int reps) {
+  const int cnt = apply_variant_count();
+  cudaEvent_t e0, e1;
+  if (cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess) return -1;
+  int best = -1;
+  float best_ms = 0.f;
+  DevOperator best_op = op;
+  for (int k = 0; k < cnt; ++k) {
+    DevOperator t = op;
+    if (apply_configure_variant(t, k)) continue;
+    if (launch_apply_tc<false>(t, x, y, nullptr, nullptr, s) != cudaSuccess) continue;
+    cudaEventRecord(e0, s);
+    for (int r = 0; r < reps; ++r) launch_apply_tc<false>(t, x, y, nullptr, nullptr, s);
+    cudaEventRecord(e1, s);
+    if (cudaEventSynchronize(e1) != cudaSuccess) continue;
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (best < 0 || ms < best_ms) {
+      best = k;
+      best_ms = ms;
+      best_op = t;
+    }
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaGetLastError();
+  if (best < 0) return -1;
+  op = best_op;
+  return 0;
+}
 
 cudaError_t launch_pcg_fused_apply(const DevOperator& op, PcgScalars* sc, const double* z, double* p0, double* p1,
                                    double* q, cudaStream_t s) {
@@ -1231,12 +1360,10 @@ namespace rdr {
 void configure_kernels() {  // errors here would surface as a later launch's cudaGetLastError
   cudaFuncSetAttribute(patch_ldg_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
   cudaFuncSetAttribute(patch_ldg_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
-  cudaFuncSetAttribute(apply_tc_kernel<64, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
-  cudaFuncSetAttribute(apply_tc_kernel<64, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
-  cudaFuncSetAttribute(apply_tc_kernel<32, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
-  cudaFuncSetAttribute(apply_tc_kernel<32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
-  cudaFuncSetAttribute(apply_tc_kernel<16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
-  cudaFuncSetAttribute(apply_tc_kernel<16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
+  int cnt = 0;
+  const ApplyVariant* v = apply_variants(&cnt);
+  for (int k = 0; k < cnt; ++k)
+    for (const void* fn : v[k].fn) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
   cudaGetLastError();
 }
 }  // namespace rdr

@@ -28,17 +28,20 @@ struct PcgScalars {
 };
 
 struct DevOperator {
-  int n_loc, n_mat, n_pad;      // n_pad: row stride of the reference matrices
+  int n_loc, n_mat;
   int64_t n_cells, n_total;
-  const int32_t* dofmap_m;      // [n_cells][n_loc], -1 for constrained dofs
+  const int32_t* ebase;         // [n_cells][16] first global dof of each local entity, -1 if constrained
+                                // (setup.hpp EntityMap)
+  const uint16_t* own;          // [n_cells] bit l: this cell owns local entity l (first cell containing it)
+  const uint16_t* lut;          // [n_loc] (local entity << 9) | position inside the entity's block
   const double* coef;           // [n_cells][n_mat]
-  const double* R;              // [n_mat][n_loc][n_pad]
   int kp;                       // n_loc rounded up to 4: rows per reference matrix in the K stack
-  int kpad;                     // n_mat * kp rounded up to 16 (K rows of the stack)
   int ngroups;                  // ceil(n_loc / 32) column groups
-  const double* Bsw;            // [ngroups][kpad][32] stacked reference matrices, swizzled (kernels.cu
+  const double* Bsw;            // [ngroups][kp/4][n_mat][4][32]: the reference matrices stacked j-major
+                                // (chunk j4 = rows 4 j4 .. 4 j4 + 3 of every R_s), columns swizzled (kernels.cu
                                 // apply_tc_kernel)
-  const uint8_t* owner;         // [n_cells][n_loc] 1 at the first (cell, local) occurrence of each free dof
+  // launch configuration (configure_apply): warp-layout variant, cell tiles, persistent grid
+  int av, ntiles, apply_grid;
 };
 
 struct DevPrecond {
@@ -55,13 +58,11 @@ struct DevPrecond {
   int32_t ldg_warps;            // warps per CTA of patch_ldg_kernel: 8, or 4 when most patches are small
   int64_t n_big;                // patch_ldg_kernel: patches [0, n_big) one per CTA, the rest (n <= 128) one per warp
   int32_t npad_max;             // largest patch dimension rounded up to 32
-  // H(curl) potential space
-  int64_t n_cg_iface;           // CG dofs [0, n_cg_iface) used by patches
+  // H(curl) potential patches: CSR rows of G^T over the CG dofs [0, n_cg_iface) they use (R-A12)
+  int64_t n_cg_iface;
   const int64_t* g_ptr;
   const int32_t* g_col;
   const double* g_val;
-  double* gbuf;                 // G^T r (CG numbering)
-  double* ubuf;                 // patch corrections in the CG numbering
   double out_scale;             // patch corrections are scaled by this (1; 1/rho_2 in the hybrid sweep)
   // hybrid Schwarz: Whitney coarse space and sweep workspace
   int hybrid;                   // 0 additive (J + patches), 1 symmetric multiplicative J,P,C,P,J
@@ -78,8 +79,8 @@ cudaError_t launch_apply(const DevOperator& op, const double* x, double* y, doub
                          const PcgScalars* guard, cudaStream_t s);
 cudaError_t launch_precond(const DevPrecond& pc, const double* r, double* z, double* rz_acc,
                            const PcgScalars* guard, cudaStream_t s);
-// one piece of the preconditioner: 0 interior Jacobi + zeroing, 1 G^T r (H(curl)),
-// 2 patch solves, 3 z += G u (H(curl))
+// one piece of the preconditioner: 0 interior Jacobi + zeroing of the patch
+// part, 1 the patch solves (H(curl) potential patches through G inside)
 cudaError_t launch_precond_part(int part, const DevPrecond& pc, const double* r, double* z, double* rz_acc,
                                 const PcgScalars* guard, cudaStream_t s);
 // z = P^-1 r with the hybrid sweep J, P, C, P, J (pc.hybrid = 1); needs the operator for the residuals
@@ -104,6 +105,12 @@ cudaError_t launch_pcg_direction(PcgScalars* sc, const double* z, double* p, dou
 // Fused PCG step (3 kernels per iteration for H(grad)): fused apply (direction
 // update + A p + ||z||^2 + stopping test), update + interior Jacobi, patches.
 bool fused_pcg_supported(const DevOperator& op);
+// the apply's warp-layout variants (kernels.cu apply_variants): configure op for
+// variant k (0, or -1 if it does not fit this operator), and setup-time
+// autotuning over all that fit (x, y: device scratch of length n_total)
+int apply_variant_count();
+int apply_configure_variant(DevOperator& op, int k);
+int tune_apply(DevOperator& op, const double* x, double* y, cudaStream_t s, int reps);
 cudaError_t launch_pcg_fused_apply(const DevOperator& op, PcgScalars* sc, const double* z, double* p0, double* p1,
                                    double* q, cudaStream_t s);
 cudaError_t launch_pcg_update_jacobi(PcgScalars* sc, const DevPrecond& pc, const double* p0, const double* p1,

@@ -307,58 +307,49 @@ static int setup_impl(rdr_handle* h, const double* vertices, int64_t nv, const i
   h->n_total = num.n_total;
 
   // ---- operator
-  std::vector<int32_t> dm = num.dofmap;
-  for (auto& g : dm)
-    if (num.constrained[g]) g = -1;
+  EntityMap em;
+  if (build_entity_map(m, num, el, em)) return RDR_EMESH;
   DevOperator& op = h->op;
   op.n_loc = el.n;
   op.n_mat = el.n_mat;
-  op.n_pad = el.n;
   op.n_cells = nt;
   op.n_total = num.n_total;
-  int32_t* d_dm;
+  uint16_t* d_lut;
   double *d_coef, *d_R;
-  if ((st = h->own_upload(&d_dm, dm))) return st;
+  if ((st = h->own_upload(&d_lut, em.lut))) return st;
   if ((st = h->own_upload(&d_coef, coef))) return st;
-  if ((st = h->own_upload(&d_R, el.R))) return st;
-  op.dofmap_m = d_dm;
+  if ((st = h->own_upload(&d_R, el.R))) return st;  // the device patch setup's reference matrices
+  op.lut = d_lut;
   op.coef = d_coef;
-  op.R = d_R;
   op.kp = (el.n + 3) / 4 * 4;
-  op.kpad = (el.n_mat * op.kp + 15) / 16 * 16;
   op.ngroups = (el.n + 31) / 32;
   {
-    // stacked reference matrices [R_0; ...; R_{nm-1}] (kp rows each), split in
-    // 32-column groups, element (k, col) of a group at k*32 + (col ^ ((k & 3) << 2))
-    // (the shared-memory swizzle of apply_tc_kernel's B fragments)
-    std::vector<double> B((size_t)op.ngroups * op.kpad * 32, 0.0);
+    // reference matrices stacked j-major in 32-column groups: group g, chunk j4,
+    // matrix s, row t holds R_s[4 j4 + t][32 g + c] at column c ^ (t << 2) (the
+    // shared-memory swizzle of apply_tc_kernel's B fragments)
+    const int nm = el.n_mat, nj4 = op.kp / 4;
+    std::vector<double> B((size_t)op.ngroups * nj4 * nm * 4 * 32, 0.0);
     for (int g = 0; g < op.ngroups; ++g)
-      for (int k = 0; k < el.n_mat * op.kp; ++k) {
-        const int s = k / op.kp, j = k % op.kp;
-        if (j >= el.n) continue;
-        for (int c = 0; c < 32; ++c) {
-          const int col = 32 * g + c;
-          if (col >= el.n) continue;
-          B[((size_t)g * op.kpad + k) * 32 + (c ^ ((k & 3) << 2))] = el.R[((size_t)s * el.n + j) * el.n + col];
-        }
-      }
+      for (int j4 = 0; j4 < nj4; ++j4)
+        for (int s = 0; s < nm; ++s)
+          for (int t = 0; t < 4; ++t) {
+            const int j = 4 * j4 + t;
+            if (j >= el.n) continue;
+            const size_t row = (((size_t)g * nj4 + j4) * nm + s) * 4 + t;
+            for (int c = 0; c < 32; ++c) {
+              const int col = 32 * g + c;
+              if (col < el.n) B[row * 32 + (c ^ (t << 2))] = el.R[((size_t)s * el.n + j) * el.n + col];
+            }
+          }
     double* d_B;
     if ((st = h->own_upload(&d_B, B))) return st;
     op.Bsw = d_B;
   }
   if ((st = h->own_upload(&h->d_cons, num.constrained))) return st;
-  {  // owner flags: first (cell, local) occurrence of every free dof (fused PCG reductions)
-    std::vector<uint8_t> owner((size_t)nt * el.n, 0), seen(num.n_total, 0);
-    for (size_t k = 0; k < owner.size(); ++k) {
-      const int32_t g = num.dofmap[k];
-      if (!num.constrained[g] && !seen[g]) {
-        seen[g] = 1;
-        owner[k] = 1;
-      }
-    }
-    uint8_t* d_owner;
-    if ((st = h->own_upload(&d_owner, owner))) return st;
-    op.owner = d_owner;
+  {  // a layout that fits (n_loc too large for all: EINVAL); tuned below on the device
+    int k = 0;
+    while (k < apply_variant_count() && apply_configure_variant(op, k)) ++k;
+    if (k == apply_variant_count()) return RDR_EINVAL;
   }
 
   // ---- preconditioner
@@ -399,8 +390,6 @@ static int setup_impl(rdr_handle* h, const double* vertices, int64_t nv, const i
     pc.g_ptr = d_gp;
     pc.g_col = d_gc;
     pc.g_val = d_gv;
-    if ((st = h->own_alloc((void**)&pc.gbuf, sizeof(double) * std::max<int64_t>(1, pc.n_cg_iface)))) return st;
-    if ((st = h->own_alloc((void**)&pc.ubuf, sizeof(double) * std::max<int64_t>(1, pc.n_cg_iface)))) return st;
   }
   Patches P;
   DeviceTiles sink;
@@ -458,14 +447,14 @@ static int setup_impl(rdr_handle* h, const double* vertices, int64_t nv, const i
   pc.npad_max = std::max(32, (P.max_n + 31) / 32 * 32);
 
   // ---- PCG workspace: one slab, the vectors every kernel of an iteration touches
-  // first, then copies of the dof map and owner flags, so that an L2
+  // first, then the operator's entity bases and owner bits, so that an L2
   // access-policy window can keep them resident while the patch kernel streams
   // the inverses through L2 (see the size rule below)
   const size_t vb = sizeof(double) * std::max<int64_t>(1, num.n_total);
   {
     auto al = [](size_t b) { return (b + 255) / 256 * 256; };
-    const size_t dmb = sizeof(int32_t) * dm.size(), owb = (size_t)nt * el.n;
-    const size_t slab_bytes = 7 * al(vb) + al(dmb) + al(owb);
+    const size_t ebb = sizeof(int32_t) * em.ebase.size(), owb = sizeof(uint16_t) * em.own.size();
+    const size_t slab_bytes = 7 * al(vb) + al(ebb) + al(owb);
     char* slab = nullptr;
     if ((st = h->own_alloc((void**)&slab, slab_bytes))) return st;
     size_t off = 0;
@@ -473,15 +462,15 @@ static int setup_impl(rdr_handle* h, const double* vertices, int64_t nv, const i
       *v = reinterpret_cast<double*>(slab + off);
       off += al(vb);
     }
-    int32_t* dm2 = reinterpret_cast<int32_t*>(slab + off);
-    off += al(dmb);
-    uint8_t* ow2 = reinterpret_cast<uint8_t*>(slab + off);
+    int32_t* eb = reinterpret_cast<int32_t*>(slab + off);
+    off += al(ebb);
+    uint16_t* ow = reinterpret_cast<uint16_t*>(slab + off);
     off += al(owb);
     h->d_b = reinterpret_cast<double*>(slab + off);
-    CK(cudaMemcpy(dm2, op.dofmap_m, dmb, cudaMemcpyDeviceToDevice));
-    CK(cudaMemcpy(ow2, op.owner, owb, cudaMemcpyDeviceToDevice));
-    op.dofmap_m = dm2;
-    op.owner = ow2;
+    CK(cudaMemcpy(eb, em.ebase.data(), ebb, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ow, em.own.data(), owb, cudaMemcpyHostToDevice));
+    op.ebase = eb;
+    op.own = ow;
     const size_t hot = off;  // everything but b
     int dev = 0, max_win = 0, max_persist = 0;
     CK(cudaGetDevice(&dev));
@@ -563,6 +552,7 @@ static int setup_impl(rdr_handle* h, const double* vertices, int64_t nv, const i
   // one warm-up apply/precond on zero vectors: kernel attributes get configured
   // here, outside any later stream capture
   CK(cudaMemset(h->d_p, 0, vb));
+  if (tune_apply(op, h->d_p, h->d_q, 0, 3)) return RDR_ECUDA;  // the fastest warp layout on this operator
   CK(launch_apply(op, h->d_p, h->d_q, nullptr, nullptr, 0));
   if (hybrid)
     CK(launch_precond_hybrid(op, pc, h->d_p, h->d_z, nullptr, 0));
@@ -585,6 +575,8 @@ static int setup_impl(rdr_handle* h, const double* vertices, int64_t nv, const i
   in.flops_apply = 2.0 * el.n * (double)el.n * el.n_mat * (double)nt;
   in.bytes_apply = 24.0 * num.n_total + (double)nt * (4.0 * el.n + 8.0 * el.n_mat);
   in.bytes_precond = P.alg_bytes + 24.0 * in.n_interior;
+  in.apply_variant = op.av;
+  in.apply_grid = op.apply_grid;
   in.patch_setup_flops = 0;
   for (int32_t n : P.n) {  // lower tiles I >= J, I, J != K: nb(nb-1)/2 per K; panel: nb-1 per K
     const double nb = (n + 63) / 64;
@@ -632,8 +624,7 @@ static int hybrid_weights(rdr_handle* h, const std::vector<double>& dinv) {
       }
       CK(cudaMemcpy(h->d_r, v.data(), vb, cudaMemcpyHostToDevice));
       CK(cudaMemset(h->d_z, 0, vb));
-      if (h->pc.ubuf) CK(cudaMemset(h->pc.ubuf, 0, sizeof(double) * h->pc.n_cg_iface));
-      for (int part = 1; part < 4; ++part) CK(launch_precond_part(part, h->pc, h->d_r, h->d_z, nullptr, nullptr, 0));
+      CK(launch_precond_part(1, h->pc, h->d_r, h->d_z, nullptr, nullptr, 0));
       CK(cudaMemcpy(out.data(), h->d_z, vb, cudaMemcpyDeviceToHost));
       for (int64_t i = 0; i < n; ++i) out[i] *= mask[i];
       return RDR_OK;
@@ -758,11 +749,10 @@ int rdr_get_weights(const rdr_handle* h, double* rho) {
 
 static int enqueue_iteration(rdr_handle* h, cudaStream_t s) {
   const int64_t n = h->n_total;
-  if (h->fused) {  // 3 kernels (+2 for the H(curl) discrete gradient) per PCG iteration
+  if (h->fused) {  // 3 kernels per PCG iteration
     CK(launch_pcg_fused_apply(h->op, h->d_sc, h->d_z, h->d_p, h->d_p2, h->d_q, s));
     CK(launch_pcg_update_jacobi(h->d_sc, h->pc, h->d_p, h->d_p2, h->d_q, h->d_x, h->d_r, h->d_z, s));
-    for (int part = 1; part < 4; ++part)
-      CK(launch_precond_part(part, h->pc, h->d_r, h->d_z, &h->d_sc->rz_acc, h->d_sc, s));
+    CK(launch_precond_part(1, h->pc, h->d_r, h->d_z, &h->d_sc->rz_acc, h->d_sc, s));
     return RDR_OK;
   }
   CK(launch_apply(h->op, h->d_p, h->d_q, &h->d_sc->pq, h->d_sc, s));
@@ -965,6 +955,19 @@ int rdr_debug_fused_apply(rdr_handle* h, const double* z, double* q, void* strea
   return RDR_OK;
 }
 
+int rdr_debug_set_apply_variant(rdr_handle* h, int variant) {
+  if (!h) return RDR_EINVAL;
+  DevOperator t = h->op;
+  if (apply_configure_variant(t, variant)) return RDR_EINVAL;
+  h->op = t;
+  if (h->graph) cudaGraphExecDestroy(h->graph);
+  if (h->wgraph) cudaGraphExecDestroy(h->wgraph);
+  h->graph = h->wgraph = nullptr;  // captured with the old launch configuration
+  h->info.apply_variant = t.av;
+  h->info.apply_grid = t.apply_grid;
+  return RDR_OK;
+}
+
 int rdr_last_launches(const rdr_handle* h, int64_t* launches) {
   if (!h || !launches) return RDR_EINVAL;
   *launches = h->last_launches;
@@ -988,7 +991,7 @@ int rdr_profile_solve(rdr_handle* h, const double* b, double rtol, int maxit, in
   int st;
   pcg_begin(h, b, rtol, maxit, s, &st);
   if (st) return st;
-  cudaEvent_t ev[6];
+  cudaEvent_t ev[4];
   for (auto& e : ev) CK(cudaEventCreate(&e));
   double acc[4] = {0, 0, 0, 0};
   int n_apply = 0;
@@ -1000,13 +1003,9 @@ int rdr_profile_solve(rdr_handle* h, const double* b, double rtol, int maxit, in
     CK(cudaEventRecord(ev[2], s));
     CK(launch_precond_part(1, h->pc, h->d_r, h->d_z, &h->d_sc->rz_acc, h->d_sc, s));
     CK(cudaEventRecord(ev[3], s));
-    CK(launch_precond_part(2, h->pc, h->d_r, h->d_z, &h->d_sc->rz_acc, h->d_sc, s));
-    CK(cudaEventRecord(ev[4], s));
-    CK(launch_precond_part(3, h->pc, h->d_r, h->d_z, &h->d_sc->rz_acc, h->d_sc, s));
-    CK(cudaEventRecord(ev[5], s));
     if ((st = fetch_scalars(h, s))) break;
-    float t[5];
-    for (int k = 0; k < 5; ++k) CK(cudaEventElapsedTime(&t[k], ev[k], ev[k + 1]));
+    float t[3];
+    for (int k = 0; k < 3; ++k) CK(cudaEventElapsedTime(&t[k], ev[k], ev[k + 1]));
     ++n_apply;
     if (h->h_sc->done) {  // this iteration's apply performed the final stopping test
       acc[0] += t[0];
@@ -1014,8 +1013,7 @@ int rdr_profile_solve(rdr_handle* h, const double* b, double rtol, int maxit, in
     }
     acc[0] += t[0];
     acc[1] += t[1];
-    acc[3] += t[2] + t[4];
-    acc[2] += t[3];
+    acc[2] += t[2];
   }
   for (auto& e : ev) cudaEventDestroy(e);
   if (st) return st;
@@ -1048,17 +1046,8 @@ int rdr_time_kernels(rdr_handle* h, const double* x, double* y, const double* r,
   };
   int st = timed([&] { return launch_apply(h->op, x, y, nullptr, nullptr, s); }, &ms[0]);
   if (!st) st = timed([&] { return launch_precond_part(0, h->pc, r, z, nullptr, nullptr, s); }, &ms[1]);
-  if (!st) st = timed([&] { return launch_precond_part(2, h->pc, r, z, nullptr, nullptr, s); }, &ms[2]);
-  if (!st) {
-    if (h->pc.gbuf) {
-      st = timed([&] {
-        cudaError_t e = launch_precond_part(1, h->pc, r, z, nullptr, nullptr, s);
-        return e != cudaSuccess ? e : launch_precond_part(3, h->pc, r, z, nullptr, nullptr, s);
-      }, &ms[3]);
-    } else {
-      ms[3] = 0;
-    }
-  }
+  if (!st) st = timed([&] { return launch_precond_part(1, h->pc, r, z, nullptr, nullptr, s); }, &ms[2]);
+  ms[3] = 0;  // the H(curl) discrete gradient runs inside the patch kernel
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   return st;

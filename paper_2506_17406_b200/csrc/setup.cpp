@@ -196,6 +196,54 @@ void build_numbering(const Mesh& m, const RefElement& el, Numbering& num) {
   }
 }
 
+int build_entity_map(const Mesh& m, const Numbering& num, const RefElement& el, EntityMap& em) {
+  // Under R-A3 / R-A9 every cell parametrises a shared entity identically, so
+  // the global id of local dof i of cell t is base(t, entity of i) + pos(i),
+  // with pos(i) the same on every cell; verified below against the dof map.
+  const int n = el.n;
+  auto local_entity = [](const LocalDof& d) { return d.dim == 0 ? d.ent : d.dim == 1 ? 4 + d.ent : d.dim == 2 ? 10 + d.ent : 14; };
+  auto global_entity = [&](int64_t t, const LocalDof& d) -> int64_t {
+    return d.dim == 0 ? m.cells[4 * t + d.ent] : d.dim == 1 ? m.cell_edges[6 * t + d.ent]
+                                             : d.dim == 2 ? m.cell_faces[4 * t + d.ent] : t;
+  };
+  em.lut.assign(n, 0);
+  for (int i = 0; i < n; ++i) {
+    const LocalDof& d = el.dofs[i];
+    const int64_t pos = num.dofmap[i] - (num.off[d.dim] + global_entity(0, d) * num.per[d.dim]);
+    if (pos < 0 || pos >= num.per[d.dim] || pos >= 512) return -1;
+    em.lut[i] = (uint16_t)((local_entity(d) << 9) | pos);
+  }
+  const std::vector<uint8_t>* dir[4] = {&m.dir_v, &m.dir_e, &m.dir_f, nullptr};
+  const int64_t nent[4] = {m.nv, m.ne, m.nf, m.nt};
+  std::vector<int64_t> first[4];
+  for (int d = 0; d < 4; ++d) first[d].assign(nent[d], -1);
+  em.ebase.assign((size_t)m.nt * 16, -1);
+  em.own.assign(m.nt, 0);
+  static const int ldim[15] = {0, 0, 0, 0, 1, 1, 1, 1, 1, 1, 2, 2, 2, 2, 3};
+  static const int lent[15] = {0, 1, 2, 3, 0, 1, 2, 3, 4, 5, 0, 1, 2, 3, 0};
+  for (int64_t t = 0; t < m.nt; ++t)
+    for (int le = 0; le < 15; ++le) {
+      const int d = ldim[le];
+      if (num.per[d] == 0) continue;
+      LocalDof ld{d, lent[le], 0, 0};
+      const int64_t g = global_entity(t, ld);
+      const bool cons = dir[d] && (*dir[d])[g];
+      if (!cons) em.ebase[(size_t)t * 16 + le] = (int32_t)(num.off[d] + g * num.per[d]);
+      if (!cons && first[d][g] < 0) {
+        first[d][g] = t;
+        em.own[t] |= (uint16_t)(1u << le);
+      }
+    }
+  for (int64_t t = 0; t < m.nt; ++t)
+    for (int i = 0; i < n; ++i) {
+      const int l = em.lut[i];
+      const int32_t b = em.ebase[(size_t)t * 16 + (l >> 9)];
+      const int32_t g = num.dofmap[(size_t)t * n + i];
+      if (b < 0 ? !num.constrained[g] : (b + (l & 511) != g || num.constrained[g])) return -1;
+    }
+  return 0;
+}
+
 // J maps T-hat to the cell: J = E E-hat^{-1}, E columns x_k - x_0 (sorted vertices)
 struct RefEdgeInverse {
   double Ehinv[3][3];

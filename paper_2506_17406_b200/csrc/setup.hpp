@@ -33,6 +33,19 @@ struct Numbering {
 
 void build_numbering(const Mesh& m, const RefElement& el, Numbering& num);
 
+// Entity form of the dof map used by the operator apply (kernels.cu): per cell
+// the first global dof of each of its 15 local entities (4 vertices, 6 edges,
+// 4 faces, the cell; -1 if constrained or without dofs), per cell the bits of
+// the entities it owns (the lowest-index cell containing a free entity), and
+// per local dof (entity << 9) | position inside the entity's block.
+struct EntityMap {
+  std::vector<int32_t> ebase;  // [nt][16]
+  std::vector<uint16_t> own;   // [nt]
+  std::vector<uint16_t> lut;   // [n_loc]
+};
+// Returns 0, or -1 if the dof map does not have the entity form.
+int build_entity_map(const Mesh& m, const Numbering& num, const RefElement& el, EntityMap& em);
+
 // Per-cell coefficients c_{e,s} (7 for H(grad), 12 for H(curl)), see setup.cpp.
 void cell_coefficients(const Mesh& m, int space, const double* alpha, const double* beta, std::vector<double>& c);
 

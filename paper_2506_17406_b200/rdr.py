@@ -45,7 +45,8 @@ class Info(ctypes.Structure):
                 ("flops_apply", ctypes.c_double), ("bytes_apply", ctypes.c_double),
                 ("bytes_precond", ctypes.c_double), ("setup_seconds", ctypes.c_double),
                 ("refelem_seconds", ctypes.c_double), ("patch_setup_seconds", ctypes.c_double),
-                ("patch_kernel_seconds", ctypes.c_double), ("patch_setup_flops", ctypes.c_double)]
+                ("patch_kernel_seconds", ctypes.c_double), ("patch_setup_flops", ctypes.c_double),
+                ("apply_variant", ctypes.c_int32), ("apply_grid", ctypes.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -74,6 +75,7 @@ def _load():
         "rdr_time_kernels": (ctypes.c_int, [P, P, P, P, P, ctypes.c_int, P, P]),
         "rdr_measure_fp64_peak": (ctypes.c_int, [ctypes.POINTER(D), P]),
         "rdr_debug_fused_apply": (ctypes.c_int, [P, P, P, P]),
+        "rdr_debug_set_apply_variant": (ctypes.c_int, [P, ctypes.c_int]),
         "rdr_destroy": (None, [P]),
         "rdr_strerror": (ctypes.c_char_p, [ctypes.c_int]),
         "rdr_reference_matrices": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, P, ctypes.POINTER(I32),
@@ -244,6 +246,10 @@ class Solver:
             _check(code, "rdr_profile_solve")
         self.converged = code == RDR_OK
         return it.value, ms
+
+    def set_apply_variant(self, variant: int) -> bool:
+        """Debugging: force the apply's warp layout; False if it does not fit this operator."""
+        return _lib.rdr_debug_set_apply_variant(self._h, int(variant)) == RDR_OK
 
     def last_launches(self) -> int:
         n = ctypes.c_int64()

@@ -1,7 +1,11 @@
-"""Profiling driver: set up one config and launch each hot-path kernel a few
-times through rdr_time_kernels (for ncu: --kernel-name regex:<kernel> -c 1).
+"""Profiling driver (for ncu: --kernel-name regex:<kernel> -s <skip> -c <n>):
+set up one config, then either launch each hot-path kernel `reps` times
+through rdr_time_kernels (standalone launches, `--mode kernels`), or run one
+PCG solve of `reps` iterations with every kernel launched eagerly
+(rdr_options.loop = RDR_LOOP_EAGER, `--mode solve`): the in-solve kernels,
+i.e. the fused PCG-mode apply, the update + Jacobi and the patch solves.
 
-    python scripts/prof_kernels.py [config] [p] [reps]
+    python scripts/prof_kernels.py [config] [p] [reps] [--mode kernels|solve]
 """
 import os
 import sys
@@ -12,11 +16,23 @@ import torch  # noqa: E402
 from rdr_inputs import make_config  # noqa: E402
 from paper_2506_17406_b200 import rdr  # noqa: E402
 
-cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 2
-p = int(sys.argv[2]) if len(sys.argv) > 2 else 6
-reps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
-c = make_config(cfg, p=p) if cfg == 5 else make_config(cfg)
-S = rdr.Solver(c.vertices, c.tets, c.p, c.space, c.alpha, c.beta, c.mask)
+args = [a for a in sys.argv[1:] if not a.startswith("--")]
+mode = "solve" if "--mode" in sys.argv and sys.argv[sys.argv.index("--mode") + 1] == "solve" else "kernels"
+if mode == "solve":
+    args = [a for a in args if a != "solve"]
+else:
+    args = [a for a in args if a != "kernels"]
+cfg = int(args[0]) if len(args) > 0 else 3
+p = int(args[1]) if len(args) > 1 and args[1] != "-" else None
+reps = int(args[2]) if len(args) > 2 else 3
+c = make_config(cfg, p=p) if p else make_config(cfg)
+S = rdr.Solver(c.vertices, c.tets, c.p, c.space, c.alpha, c.beta, c.mask,
+               loop=rdr.LOOP_EAGER if mode == "solve" else rdr.LOOP_DEVICE)
 x = torch.from_numpy(c.draw_vector(S.n_total)).cuda()
-ms = S.time_kernels(x, x, reps=reps)
-print("kernel ms (apply, jacobi, patches, gradient):", ms.tolist(), S.info)
+if mode == "solve":
+    _, it = S.solve(x, maxit=reps, rtol=0.0)
+    torch.cuda.synchronize()
+    print("eager solve:", it, "iterations", S.info)
+else:
+    ms = S.time_kernels(x, x, reps=reps)
+    print("kernel ms (apply, jacobi, patches, gradient):", ms.tolist(), S.info)

@@ -1,6 +1,7 @@
-"""One short solve of a config (for an ncu launch list of its PCG kernels):
-    RDR_PCG_HOSTLOOP=1 ncu --graph-profiling node --metrics gpu__time_duration.sum ... \\
-        python scripts/solve_launches.py CONFIG [P] [MAXIT]"""
+"""One short PCG solve of a config with every kernel launched eagerly
+(rdr_options.loop = RDR_LOOP_EAGER), for an ncu launch list of its kernels:
+    ncu --metrics gpu__time_duration.sum --clock-control none --csv ... \\
+        python scripts/solve_launches.py CONFIG [P|-] [MAXIT]"""
 import os
 import sys
 
@@ -14,12 +15,9 @@ cfg = int(sys.argv[1])
 p = int(sys.argv[2]) if len(sys.argv) > 2 and sys.argv[2] != "-" else None
 maxit = int(sys.argv[3]) if len(sys.argv) > 3 else 16
 c = make_config(cfg, p=p) if p else make_config(cfg)
-S = rdr.Solver(c.vertices, c.tets, c.p, c.space, c.alpha, c.beta, c.mask)
+S = rdr.Solver(c.vertices, c.tets, c.p, c.space, c.alpha, c.beta, c.mask, loop=rdr.LOOP_EAGER)
 b = torch.from_numpy(c.draw_vector(S.n_total)).cuda()
 x = torch.empty_like(b)
-try:
-    S.solve(b, x, maxit=maxit)
-except rdr.RdrError:
-    pass  # ENOCONV at maxit is expected
+S.solve(b, x, maxit=maxit)  # RDR_ENOCONV at maxit is reported through S.converged
 torch.cuda.synchronize()
-print("done", S.info["n_total"])
+print("done", S.info["n_total"], "iterations", S.last_stats())

@@ -358,11 +358,36 @@ def test_loop_modes_and_profile(torch_cuda, space):
         if loop == rdr.LOOP_EAGER:
             it2, ms = S.profile_solve(b)
             assert abs(it2 - it) <= 1 and np.all(ms[:3] > 0)
-            assert (ms[3] > 0) == (space == HCURL)
+            assert ms[3] == 0  # the discrete gradient runs inside the patch kernel
     x0, it0 = res[rdr.LOOP_DEVICE]
     for loop in (rdr.LOOP_HOST, rdr.LOOP_EAGER):
         assert abs(res[loop][1] - it0) <= 1
         assert rel(res[loop][0], x0) <= 1e-8
+
+
+@pytest.mark.parametrize("space,p", [(HGRAD, 5), (HCURL, 4), (HDIV, 3)])
+def test_every_apply_layout(torch_cuda, space, p):
+    """Each warp layout of the apply (setup autotunes among them) against the
+    oracle, plain and in the fused PCG (rdr_debug_set_apply_variant)."""
+    from paper_2506_17406_b200 import rdr
+    torch = torch_cuda
+    c, S, O = _pair(torch, 0, n=2, p=p, space=space, perturb=True, bc="x0", coeffs="loguniform")
+    x = c.draw_vector(O.n_total)
+    xt = torch.from_numpy(x).cuda()
+    ya = O.apply(x)
+    b = c.draw_vector(O.n_total)
+    hist = []
+    _, ito, _ = O.solve(b, rtol=1e-8, history=hist)
+    ran = 0
+    for k in range(8):
+        if not S.set_apply_variant(k):
+            continue
+        ran += 1
+        assert S.info["apply_variant"] == k
+        assert rel(S.apply(xt).cpu().numpy(), ya) <= TOL, k
+        _, it = S.solve(torch.from_numpy(b).cuda(), rtol=1e-8)
+        _check_iters(S, it, ito, lambda kk: hist[kk - 1] if 0 < kk <= len(hist) else None)
+    assert ran == 4  # every layout of this n_mat fits these small elements
 
 
 def test_stream_semantics_and_repeated_setup(torch_cuda):

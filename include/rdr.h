@@ -80,24 +80,33 @@ enum { RDR_ADDITIVE = 0, RDR_HYBRID = 1 };
  *                dense.cpp), then uploaded. Both give A_m^-1 to rounding. */
 enum { RDR_SETUP_DEVICE = 0, RDR_SETUP_HOST = 1 };
 
-/* How rdr_solve drives the PCG iteration (R-A16); all three run the same
- * kernels and give the same iterates:
- *   RDR_LOOP_DEVICE (default) -- one CUDA graph whose conditional WHILE node
- *                repeats a body of 8 iterations until the stopping test, which
- *                the fused operator apply performs on the device, fires: one
- *                graph launch and one host synchronisation per solve (the
- *                hybrid preconditioner's unfused path uses RDR_LOOP_HOST);
+/* How rdr_solve drives the PCG iteration (R-A16); all of them run the same
+ * arithmetic and give the same iterates (to rounding):
+ *   RDR_LOOP_DEVICE (default) -- the loop runs on the device with one host
+ *                synchronisation per solve: small problems (additive
+ *                preconditioner, star patches <= 256 dofs, n_loc <= 128) as one
+ *                persistent cooperative kernel when a 10-iteration solve timed
+ *                at setup is faster that way (rdr_info.persistent_loop), else as
+ *                RDR_LOOP_GRAPH;
  *   RDR_LOOP_HOST -- graphs of 8 iterations relaunched by the host until done;
  *   RDR_LOOP_EAGER -- every kernel launched on the stream, the host testing the
  *                stop flag after each iteration (no graphs: profilers see every
- *                kernel of the iteration). */
-enum { RDR_LOOP_DEVICE = 0, RDR_LOOP_HOST = 1, RDR_LOOP_EAGER = 2 };
+ *                kernel of the iteration);
+ *   RDR_LOOP_GRAPH -- one CUDA graph whose conditional WHILE node repeats a body
+ *                of 8 iterations (3 kernels each: fused apply with the stopping
+ *                test, update + Jacobi, patches) until the test fires (the
+ *                hybrid preconditioner's unfused path uses RDR_LOOP_HOST);
+ *   RDR_LOOP_PERSISTENT -- the whole solve in one persistent cooperative kernel
+ *                (grid barriers between the phases of each iteration; CUDA-core
+ *                apply with the reference matrices in shared memory, one warp
+ *                per patch); RDR_EINVAL at setup if the problem is not eligible. */
+enum { RDR_LOOP_DEVICE = 0, RDR_LOOP_HOST = 1, RDR_LOOP_EAGER = 2, RDR_LOOP_GRAPH = 3, RDR_LOOP_PERSISTENT = 4 };
 
 struct rdr_options {
   int decomposition;  /* RDR_SPLIT or RDR_UNSPLIT */
   int preconditioner; /* RDR_ADDITIVE or RDR_HYBRID */
   int setup;          /* RDR_SETUP_DEVICE or RDR_SETUP_HOST */
-  int loop;           /* RDR_LOOP_DEVICE, RDR_LOOP_HOST or RDR_LOOP_EAGER */
+  int loop;           /* RDR_LOOP_DEVICE, _HOST, _EAGER, _GRAPH or _PERSISTENT */
 };
 
 enum {
@@ -134,6 +143,9 @@ struct rdr_info {
                                   lower tile and panel product = 2*64^3 nb (nb-1)(nb+2)/2 */
   int32_t apply_variant;       /* warp layout of the operator apply chosen by setup-time autotuning */
   int32_t apply_grid;          /* its persistent grid (CTAs) */
+  int32_t persistent_loop;     /* 1: solves run as the persistent cooperative kernel (RDR_LOOP_DEVICE
+                                  chose it, or RDR_LOOP_PERSISTENT) */
+  int32_t reserved;
 };
 
 /* Build the operator and the preconditioner (host setup once, then upload).
@@ -200,8 +212,7 @@ int rdr_last_solve(const rdr_handle* h, struct rdr_solve_stats* out);
  * ms[0] the fused operator apply (direction update + A p + stopping test),
  * ms[1] the x/r update + interior Jacobi, ms[2] the star-patch solves
  * (H(curl): the discrete gradient of the potential patches included),
- * ms[3] = 0 (kept for the layout of rdr_time_kernels) -- the in-solve
- * counterparts of rdr_time_kernels. Additive preconditioner only
+ * ms[3] = 0 -- the in-solve counterparts of rdr_time_kernels ms[0..2]. Additive preconditioner only
  * (RDR_EINVAL otherwise). Synchronizes `stream`. */
 int rdr_profile_solve(rdr_handle* h, const double* b, double rtol, int maxit, int* iters, double* ms,
                       void* stream);
@@ -210,7 +221,9 @@ int rdr_profile_solve(rdr_handle* h, const double* b, double rtol, int maxit, in
  * times back to back on `stream` between CUDA events and return the average
  * device time per launch in ms: ms[0] operator apply (gather-contract-scatter),
  * ms[1] interior Jacobi + zeroing, ms[2] patch solves (H(curl): with the
- * discrete gradient of the potential patches), ms[3] = 0. x, r: device input vectors, y, z: outputs
+ * discrete gradient of the potential patches), ms[3] the fused PCG-mode apply
+ * the solve runs (direction update + A p + stopping test; 0 with the hybrid
+ * preconditioner, whose PCG uses the plain apply). x must be nonzero on free dofs. x, r: device input vectors, y, z: outputs
  * (contents overwritten). Synchronizes `stream`. */
 int rdr_time_kernels(rdr_handle* h, const double* x, double* y, const double* r, double* z, int reps, double* ms,
                      void* stream);
@@ -224,7 +237,7 @@ void rdr_destroy(rdr_handle* h);
 const char* rdr_strerror(int code);
 
 /* Debugging entry point: run the operator apply (and the solves) with warp
- * layout `variant` (0 <= variant < 8; kernels.cu apply_variants) instead of the
+ * layout `variant` (0 <= variant < 10; kernels.cu apply_variants) instead of the
  * one setup's autotuning chose; RDR_EINVAL if it does not fit this operator.
  * The GPU tests use it to check every layout against the oracle. */
 int rdr_debug_set_apply_variant(rdr_handle* h, int variant);

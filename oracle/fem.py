@@ -13,6 +13,8 @@ path uses. Global CSR by the canonical numbering; Dirichlet by elimination.
 """
 from __future__ import annotations
 
+from functools import lru_cache
+
 import numpy as np
 import scipy.sparse as sp
 from scipy.special import roots_jacobi
@@ -45,15 +47,25 @@ def tet_quadrature(degree: int):
     return lam, wts
 
 
+@lru_cache(maxsize=None)
+def _tabulation(space: str, p: int):
+    """Quadrature exact to degree 2p+2 (R-A10) and the reference basis values /
+    derivatives at its points, tabulated in extended precision and rounded once;
+    computed once per (space, p) and process (read-only arrays)."""
+    lam, w = tet_quadrature(2 * p + 2)
+    val, der = tabulate(element(space, p), lam.astype(np.longdouble))
+    out = (lam, w, val.astype(np.float64), der.astype(np.float64))
+    for a in out:
+        a.setflags(write=False)
+    return out
+
+
 class Assembler:
     def __init__(self, space: str, p: int, topo, numbering):
         self.space, self.p = space, p
         self.topo, self.num = topo, numbering
         self.el = element(space, p)
-        self.lam, self.w = tet_quadrature(2 * p + 2)
-        val, der = tabulate(self.el, self.lam.astype(np.longdouble))
-        self.val = val.astype(np.float64)
-        self.der = der.astype(np.float64)
+        self.lam, self.w, self.val, self.der = _tabulation(space, p)
         T = reference_tet()
         self.Vhat = T.coords.astype(np.float64)
         self.Ehat_inv = np.linalg.inv((self.Vhat[1:] - self.Vhat[0]).T)

@@ -212,8 +212,8 @@ __device__ __forceinline__ void mma_bar_sync(int nthreads) {  // named barrier 1
 // p.(Ap). In PCG mode the gather also forms p_k = z_k + beta_k p_{k-1}, which
 // the owner cell of each entity writes once (the CTA holding the tile's
 // column group 0), and the last CTA performs the stopping test (R-A16).
-template <int BM, int NQ, int KS, int NM, bool PCG>
-__global__ void __launch_bounds__((apply_mma_warps(BM, NQ, KS) + 1) * 32, 1)
+template <int BM, int NQ, int KS, int NM, int MINB, bool PCG>
+__global__ void __launch_bounds__((apply_mma_warps(BM, NQ, KS) + 1) * 32, MINB)
     apply_tc_kernel(DevOperator op, int S, const double* __restrict__ x, double* __restrict__ y, double* pq_acc,
                     const PcgScalars* guard, PcgScalars* sc, double* pbuf0, double* pbuf1) {
   constexpr int MW = BM / 16, NW = 32 / (8 * NQ), NWARP = apply_mma_warps(BM, NQ, KS);
@@ -513,10 +513,11 @@ struct ApplyVariant {
   int bm, nq, ks, slots, nm;
   const void* fn[2];  // plain, PCG
 };
-template <int BM, int NQ, int KS, int NM>
+template <int BM, int NQ, int KS, int NM, int MINB = 1>
 ApplyVariant apply_variant(int slots) {
   return {BM, NQ, KS, slots, NM,
-          {(const void*)apply_tc_kernel<BM, NQ, KS, NM, false>, (const void*)apply_tc_kernel<BM, NQ, KS, NM, true>}};
+          {(const void*)apply_tc_kernel<BM, NQ, KS, NM, MINB, false>,
+           (const void*)apply_tc_kernel<BM, NQ, KS, NM, MINB, true>}};
 }
 const ApplyVariant* apply_variants(int* count) {
   static const ApplyVariant v[] = {
@@ -524,6 +525,7 @@ const ApplyVariant* apply_variants(int* count) {
       apply_variant<32, 4, 4, 7>(6),  apply_variant<32, 4, 4, 12>(6),   // 8 MMA warps
       apply_variant<32, 2, 2, 7>(4),  apply_variant<32, 2, 2, 12>(4),   // 8 MMA warps, 16 x 16 warp tiles
       apply_variant<16, 4, 4, 7>(6),  apply_variant<16, 4, 4, 12>(6),   // 4 MMA warps, 16 cells per unit
+      apply_variant<32, 4, 4, 7, 2>(6), apply_variant<32, 4, 4, 12, 2>(4),  // 8 MMA warps, registers for 2 CTAs/SM
   };
   *count = (int)(sizeof(v) / sizeof(v[0]));
   return v;
@@ -648,27 +650,19 @@ __device__ __forceinline__ double treduce16(double (&v)[16], int lane) {
   return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 16);
 }
 
-// Small patches (n <= 128, at most 4 block rows: the H(div) and H(curl) edge
-// stars, sorted last, [n_big, n_patches)) one per warp, kLdgWarps per CTA, so
-// a small patch's gather / scatter / reduction latency overlaps the other
-// warps' tile streams instead of serialising on __syncthreads. Same arithmetic
-// as patch_ldg_kernel.
-template <int kLdgWarps>
-__global__ void __launch_bounds__(kLdgWarps * 32, 32 / kLdgWarps)
-    patch_warp_kernel(DevPrecond pc, const double* __restrict__ r, double* __restrict__ z, double* rz_acc,
-                      const PcgScalars* guard) {
-  extern __shared__ double smem[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t pid = pc.n_big + (int64_t)blockIdx.x * kLdgWarps + warp;
-  if (pid >= pc.n_patches) {
-    pdl_wait();  // warps without a patch still order the CTA after the previous kernel
-    return;
-  }
+// One star patch solved by one warp (the lane = row half-tile stream of
+// patch_ldg_kernel without block barriers): z += E_m A_m^-1 E_m^T r for patch
+// pid, rl / zl = npad doubles of warp-private shared memory each. `ready()` is
+// called once the first half tile is in flight and before r is read (the PDL
+// wait of a kernel launched behind the producer of r); it returns false to
+// abandon the patch. Returns this lane's share of r.z (0 if abandoned).
+template <class Ready>
+__device__ __forceinline__ double warp_patch_solve(const DevPrecond& pc, int64_t pid, const double* __restrict__ r,
+                                                   double* __restrict__ z, double* rl, double* zl, int lane,
+                                                   Ready ready) {
   const int n = pc.pn[pid];
   const int nb = (n + 31) >> 5, npad = nb * 32;
   const bool pot = pc.pkind[pid] != 0;
-  double* rl = smem + warp * 2 * kSmallPatch;
-  double* zl = rl + kSmallPatch;
   const int32_t* id = pc.idx + pc.idx_off[pid];
   long long* rli = reinterpret_cast<long long*>(rl);
   for (int i = lane; i < npad; i += 32) {
@@ -706,8 +700,7 @@ __global__ void __launch_bounds__(kLdgWarps * 32, 32 / kLdgWarps)
   };
   double a[16];
   load_half(a);
-  pdl_wait();
-  if (stopped(guard)) return;
+  if (!ready()) return 0.0;
   for (int i = lane; i < npad; i += 32) rl[i] = patch_residual(pc, pot, r, (int)rli[i]);
   __syncwarp();
   double row = 0.0;
@@ -742,7 +735,6 @@ __global__ void __launch_bounds__(kLdgWarps * 32, 32 / kLdgWarps)
     }
     if (t < ntiles) load_half(a);
   }
-  if (pdl_late()) pdl_trigger();
   __syncwarp();
   double part = 0.0;
   for (int i = lane; i < n; i += 32) {
@@ -750,6 +742,35 @@ __global__ void __launch_bounds__(kLdgWarps * 32, 32 / kLdgWarps)
     patch_scatter(pc, pot, z, id[i], pc.out_scale * zi);
     part = fma(rl[i], zi, part);
   }
+  __syncwarp();  // rl / zl may be reused by the warp's next patch
+  return part;
+}
+
+// Small patches (n <= 128, at most 4 block rows: the H(div) and H(curl) edge
+// stars, sorted last, [n_big, n_patches)) one per warp, kLdgWarps per CTA, so
+// a small patch's gather / scatter / reduction latency overlaps the other
+// warps' tile streams instead of serialising on __syncthreads.
+template <int kLdgWarps>
+__global__ void __launch_bounds__(kLdgWarps * 32, 32 / kLdgWarps)
+    patch_warp_kernel(DevPrecond pc, const double* __restrict__ r, double* __restrict__ z, double* rz_acc,
+                      const PcgScalars* guard) {
+  extern __shared__ double smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t pid = pc.n_big + (int64_t)blockIdx.x * kLdgWarps + warp;
+  if (pid >= pc.n_patches) {
+    pdl_wait();  // warps without a patch still order the CTA after the previous kernel
+    return;
+  }
+  double* rl = smem + warp * 2 * kSmallPatch;
+  double* zl = rl + kSmallPatch;
+  bool live = true;
+  double part = warp_patch_solve(pc, pid, r, z, rl, zl, lane, [&] {
+    pdl_wait();
+    live = !stopped(guard);
+    return live;
+  });
+  if (!live) return;
+  if (pdl_late()) pdl_trigger();
   part = warp_sum(part);
   if (rz_acc && lane == 0) atomicAdd(rz_acc, part);
 }
@@ -1100,19 +1121,37 @@ __global__ void pcg_update_jacobi_kernel(PcgScalars* sc, DevPrecond pc, const do
   const double* __restrict__ p = (kk & 1) ? p1 : p0;
   const double alpha = sc->rz_old / sc->pq2[kk & 1];
   double part = 0;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < pc.n_total; i += stride) {
+  // two dofs per thread with 16-byte accesses (the slab vectors are 256-byte aligned)
+  const int64_t n2 = pc.n_total >> 1, stride = (int64_t)gridDim.x * blockDim.x;
+  const double2* __restrict__ p2 = reinterpret_cast<const double2*>(p);
+  double2* __restrict__ q2 = reinterpret_cast<double2*>(q);
+  double2* __restrict__ x2 = reinterpret_cast<double2*>(x);
+  double2* __restrict__ r2 = reinterpret_cast<double2*>(r);
+  double2* __restrict__ z2 = reinterpret_cast<double2*>(z);
+  auto jacobi = [&](int64_t i, double rn) {
+    if (i < pc.off3) return 0.0;
+    const double zi = pc.dinv[i - pc.off3] * rn;
+    part = fma(rn, zi, part);
+    return zi;
+  };
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n2; k += stride) {
+    const double2 pv = p2[k], qv = q2[k], rv = r2[k];
+    double2 xv = x2[k];
+    xv.x = fma(alpha, pv.x, xv.x);
+    xv.y = fma(alpha, pv.y, xv.y);
+    const double2 rn = make_double2(fma(-alpha, qv.x, rv.x), fma(-alpha, qv.y, rv.y));
+    x2[k] = xv;
+    r2[k] = rn;
+    q2[k] = make_double2(0.0, 0.0);
+    z2[k] = make_double2(jacobi(2 * k, rn.x), jacobi(2 * k + 1, rn.y));
+  }
+  if ((pc.n_total & 1) && blockIdx.x == 0 && threadIdx.x == 0) {  // odd length: the last dof
+    const int64_t i = pc.n_total - 1;
     x[i] = fma(alpha, p[i], x[i]);
     const double rn = fma(-alpha, q[i], r[i]);
     r[i] = rn;
     q[i] = 0.0;
-    if (i < pc.off3) {
-      z[i] = 0.0;
-    } else {
-      const double zi = pc.dinv[i - pc.off3] * rn;
-      z[i] = zi;
-      part = fma(rn, zi, part);
-    }
+    z[i] = jacobi(i, rn);
   }
   __shared__ double sh[32];
   const double s = block_sum(part, sh);
@@ -1130,6 +1169,180 @@ __global__ void pcg_direction_kernel(PcgScalars* sc, const double* __restrict__ 
   }
 }
 
+// ---------------------------------------------------------------- persistent PCG (small problems)
+// Small problems are launch-latency bound in the 3-kernel iteration (config 5 at
+// p <= 4: ~20-38 us per iteration for a few us of work). This kernel runs a whole
+// solve (R-A16, the fused order of the 3-kernel path) in one cooperative launch,
+// with a grid barrier between its phases.
+__device__ __forceinline__ void grid_barrier(PcgScalars* sc) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile uint32_t* gen = &sc->bar_gen;
+    const uint32_t g = *gen;
+    __threadfence();
+    if (atomicAdd(&sc->bar_count, 1u) == gridDim.x - 1) {
+      sc->bar_count = 0;
+      __threadfence();
+      atomicAdd(&sc->bar_gen, 1u);
+    } else {
+      while (*gen == g) __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void block_add(double v, double* dst, double* sh) {
+  const double s = block_sum(v, sh);
+  if (threadIdx.x == 0 && s != 0.0) atomicAdd(dst, s);
+}
+
+struct PersistentArgs {
+  const double* b;
+  const uint8_t* cons;
+  double *x, *r, *z, *p0, *p1, *q;
+};
+
+__global__ void __launch_bounds__(512, 1)
+    pcg_persistent_kernel(DevOperator op, DevPrecond pc, PcgScalars* sc, PersistentArgs a, int wb) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ double sh[32];
+  const int n = op.n_loc, nm = op.n_mat;
+  double* R = reinterpret_cast<double*>(smem_raw);  // [nm][n][n], symmetric: R_s[j][i] = R_s[i][j]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  double* w0 = R + (size_t)nm * n * n + (size_t)warp * 2 * wb;  // warp scratch: x_e / r_m
+  double* w1 = w0 + wb;                                         // dof ids / z_m
+  for (int i = threadIdx.x; i < nm * n * n; i += blockDim.x) R[i] = op.R[i];
+  const int64_t N = pc.n_total, gstride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int gwarp = blockIdx.x * nw + warp, nwarps = gridDim.x * nw;
+  const double rtol = sc->rtol;
+  const int maxit = sc->maxit;
+  auto all_patches = [&](double* rz_dst) {  // z += sum_m E_m A_m^-1 E_m^T r
+    double part = 0.0;
+    for (int64_t pid = gwarp; pid < pc.n_patches; pid += nwarps)
+      part += warp_patch_solve(pc, pid, a.r, a.z, w0, w1, lane, [] { return true; });
+    block_add(part, rz_dst, sh);
+  };
+
+  // ---- start: x0 = 0, r0 = b (masked), z0 = P^-1 r0, r0.z0 (into prz[0])
+  double part = 0.0;
+  for (int64_t i = gtid; i < N; i += gstride) {
+    const double ri = a.cons[i] ? 0.0 : a.b[i];
+    a.x[i] = 0.0;
+    a.q[i] = 0.0;
+    a.p0[i] = 0.0;
+    a.p1[i] = 0.0;
+    a.r[i] = ri;
+    const double zi = i >= pc.off3 ? pc.dinv[i - pc.off3] * ri : 0.0;
+    a.z[i] = zi;
+    part = fma(ri, zi, part);
+  }
+  block_add(part, &sc->prz[0], sh);
+  grid_barrier(sc);
+  all_patches(&sc->prz[0]);
+  grid_barrier(sc);
+
+  double z0 = 0.0;
+  for (int k = 0;; ++k) {
+    // ---- fused apply: p_k = z_k + beta_k p_{k-1} (owners write it), ||z_k||^2, q = A p_k, p.q
+    volatile PcgScalars* v = sc;
+    const double rz = v->prz[k % 3];
+    const double beta = k == 0 ? 0.0 : rz / v->prz[(k + 2) % 3];
+    const double* p_old = (k & 1) ? a.p0 : a.p1;
+    double* p_new = (k & 1) ? a.p1 : a.p0;
+    if (gtid == 0) sc->prz[(k + 1) % 3] = 0.0;  // accumulated from the update on, after the barrier
+    double zz = 0.0, pq = 0.0;
+    long long* ids = reinterpret_cast<long long*>(w1);
+    for (int64_t c = gwarp; c < op.n_cells; c += nwarps) {
+      const int own = op.own[c];
+      for (int i = lane; i < n; i += 32) {
+        const int l = op.lut[i];
+        const int bse = op.ebase[c * 16 + (l >> 9)];
+        double val = 0.0;
+        long long id = -1;
+        if (bse >= 0) {
+          id = bse + (l & 511);
+          const double zi = a.z[id];
+          val = fma(beta, p_old[id], zi);
+          if ((own >> (l >> 9)) & 1) {
+            p_new[id] = val;
+            zz = fma(zi, zi, zz);
+          }
+        }
+        w0[i] = val;
+        ids[i] = id;
+      }
+      __syncwarp();
+      for (int i = lane; i < n; i += 32) {
+        double acc = 0.0;
+        for (int s = 0; s < nm; ++s) {
+          const double* Rs = R + (size_t)s * n * n + i;
+          double t = 0.0;
+          for (int j = 0; j < n; ++j) t = fma(Rs[j * n], w0[j], t);
+          acc = fma(op.coef[c * nm + s], t, acc);
+        }
+        if (ids[i] >= 0) {
+          atomicAdd(a.q + ids[i], acc);
+          pq = fma(w0[i], acc, pq);
+        }
+      }
+      __syncwarp();
+    }
+    block_add(zz, &sc->pzz[k & 1], sh);
+    block_add(pq, &sc->ppq[k & 1], sh);
+    grid_barrier(sc);
+
+    // ---- stopping test on z_k (R-A16): every thread takes the same decision
+    const double zn = sqrt(v->pzz[k & 1]);
+    bool stop = false, conv = false;
+    if (k == 0) {
+      z0 = zn;
+      conv = zn == 0.0;
+      stop = conv || maxit <= 0;
+    } else {
+      conv = zn <= rtol * z0;
+      stop = conv || k >= maxit;
+    }
+    if (stop) {
+      if (gtid == 0) {
+        sc->iters = k;
+        sc->z0 = z0;
+        sc->z_last = zn;
+        sc->converged = conv;
+        sc->done = 1;
+        sc->k = k + 1;
+      }
+      break;
+    }
+
+    // ---- x += alpha p_k, r -= alpha q, q = 0, interior Jacobi z_I = D r_I, z_Gamma = 0, r.z
+    const double alpha = rz / v->ppq[k & 1];
+    if (gtid == 0) {  // last read after the previous barrier; accumulated again in the next apply
+      sc->pzz[(k + 1) & 1] = 0.0;
+      sc->ppq[(k + 1) & 1] = 0.0;
+    }
+    part = 0.0;
+    for (int64_t i = gtid; i < N; i += gstride) {
+      a.x[i] = fma(alpha, p_new[i], a.x[i]);
+      const double rn = fma(-alpha, a.q[i], a.r[i]);
+      a.r[i] = rn;
+      a.q[i] = 0.0;
+      double zi = 0.0;
+      if (i >= pc.off3) {
+        zi = pc.dinv[i - pc.off3] * rn;
+        part = fma(rn, zi, part);
+      }
+      a.z[i] = zi;
+    }
+    block_add(part, &sc->prz[(k + 1) % 3], sh);
+    grid_barrier(sc);
+    // ---- star patches
+    all_patches(&sc->prz[(k + 1) % 3]);
+    grid_barrier(sc);
+  }
+}
+
 unsigned vec_grid(int64_t n) {
   int64_t g = (n + kVecThreads - 1) / kVecThreads;
   if (g > 148 * 16) g = 148 * 16;
@@ -1138,6 +1351,48 @@ unsigned vec_grid(int64_t n) {
 }
 
 }  // namespace
+
+PersistentPcg plan_persistent_pcg(const DevOperator& op, const DevPrecond& pc) {
+  PersistentPcg plan;
+  if (pc.hybrid || pc.npad_max > 256 || op.n_loc > 128) return plan;
+  plan.wb = std::max(pc.npad_max, (op.n_loc + 31) / 32 * 32);
+  const size_t rbytes = sizeof(double) * (size_t)op.n_mat * op.n_loc * op.n_loc;
+  for (int w : {16, 8, 4}) {
+    const size_t sm = rbytes + sizeof(double) * 2 * (size_t)plan.wb * w;
+    if (sm <= kMaxSmem) {
+      plan.warps = w;
+      plan.smem = sm;
+      break;
+    }
+  }
+  if (!plan.warps) return plan;
+  int dev = 0, sms = 148, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (cudaFuncSetAttribute(pcg_persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.smem) !=
+          cudaSuccess ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pcg_persistent_kernel, plan.warps * 32, plan.smem) !=
+          cudaSuccess ||
+      per_sm < 1) {
+    cudaGetLastError();
+    plan.warps = 0;
+    return plan;
+  }
+  plan.grid = sms * std::min(per_sm, 2);
+  return plan;
+}
+
+cudaError_t launch_persistent_pcg(const PersistentPcg& plan, const DevOperator& op, const DevPrecond& pc,
+                                  PcgScalars* sc, const double* b, const uint8_t* cons, double* x, double* r,
+                                  double* z, double* p0, double* p1, double* q, cudaStream_t s) {
+  PersistentArgs a{b, cons, x, r, z, p0, p1, q};
+  DevOperator o = op;
+  DevPrecond c = pc;
+  int wb = plan.wb;
+  void* args[] = {(void*)&o, (void*)&c, (void*)&sc, (void*)&a, (void*)&wb};
+  return cudaLaunchCooperativeKernel((const void*)pcg_persistent_kernel, dim3(plan.grid), dim3(plan.warps * 32), args,
+                                     plan.smem, s);
+}
 
 cudaError_t launch_apply(const DevOperator& op, const double* x, double* y, double* pq_acc,
                          const PcgScalars* guard, cudaStream_t s) {
@@ -1331,8 +1586,8 @@ cudaError_t launch_pcg_fused_apply(const DevOperator& op, PcgScalars* sc, const 
 
 cudaError_t launch_pcg_update_jacobi(PcgScalars* sc, const DevPrecond& pc, const double* p0, const double* p1,
                                      double* q, double* x, double* r, double* z, cudaStream_t s) {
-  return launch_k(pcg_update_jacobi_kernel, dim3(vec_grid(pc.n_total)), dim3(kVecThreads), 0, s, sc, pc, p0, p1, q, x,
-                  r, z);
+  return launch_k(pcg_update_jacobi_kernel, dim3(vec_grid((pc.n_total + 1) / 2)), dim3(kVecThreads), 0, s, sc, pc, p0,
+                  p1, q, x, r, z);
 }
 
 // FP64 tensor-core peak microbenchmark (roofline denominator of the apply,

@@ -25,6 +25,13 @@ struct PcgScalars {
   double rz_old;    // fused path: r.z of the z used by the current direction
   double pq2[2];    // fused path: p.Ap, double-buffered by iteration parity
   double z_last;    // ||z_k|| at the last stopping test (rdr_last_solve)
+  // persistent PCG kernel (small problems): r.z by iteration mod 3, ||z||^2 and p.Ap by
+  // parity, and its grid barrier
+  double prz[3];
+  double pzz[2];
+  double ppq[2];
+  uint32_t bar_count;
+  uint32_t bar_gen;
 };
 
 struct DevOperator {
@@ -35,6 +42,7 @@ struct DevOperator {
   const uint16_t* own;          // [n_cells] bit l: this cell owns local entity l (first cell containing it)
   const uint16_t* lut;          // [n_loc] (local entity << 9) | position inside the entity's block
   const double* coef;           // [n_cells][n_mat]
+  const double* R;              // [n_mat][n_loc][n_loc] reference matrices (the persistent PCG kernel)
   int kp;                       // n_loc rounded up to 4: rows per reference matrix in the K stack
   int ngroups;                  // ceil(n_loc / 32) column groups
   const double* Bsw;            // [ngroups][kp/4][n_mat][4][32]: the reference matrices stacked j-major
@@ -115,6 +123,21 @@ cudaError_t launch_pcg_fused_apply(const DevOperator& op, PcgScalars* sc, const 
                                    double* q, cudaStream_t s);
 cudaError_t launch_pcg_update_jacobi(PcgScalars* sc, const DevPrecond& pc, const double* p0, const double* p1,
                                      double* q, double* x, double* r, double* z, cudaStream_t s);
+
+// Persistent PCG (small problems, fused additive path): the whole solve of R-A16 in one
+// cooperative launch -- init, then per iteration the fused apply (CUDA cores, reference
+// matrices in shared memory), update + Jacobi and the warp-per-patch solves, separated by
+// grid barriers. x, r, z, p0, p1, q: the handle's vectors; sc zeroed except rtol / maxit.
+struct PersistentPcg {
+  int warps = 0;       // warps per CTA
+  int grid = 0;        // co-resident CTAs (0: not eligible)
+  int wb = 0;          // per-warp scratch doubles (x 2)
+  size_t smem = 0;
+};
+PersistentPcg plan_persistent_pcg(const DevOperator& op, const DevPrecond& pc);
+cudaError_t launch_persistent_pcg(const PersistentPcg& plan, const DevOperator& op, const DevPrecond& pc,
+                                  PcgScalars* sc, const double* b, const uint8_t* cons, double* x, double* r,
+                                  double* z, double* p0, double* p1, double* q, cudaStream_t s);
 
 int count_precond_launches(const DevPrecond& pc);  // kernels per rdr_precond
 size_t max_kernel_smem();                           // per-CTA dynamic shared-memory opt-in used

@@ -173,6 +173,8 @@ struct rdr_handle {
   cudaGraphExec_t graph = nullptr;
   cudaGraphExec_t wgraph = nullptr;  // device-side while loop (fused path)
   int loop = RDR_LOOP_DEVICE;        // rdr_options.loop
+  PersistentPcg persist;             // the persistent PCG kernel's plan (grid 0: not eligible)
+  bool use_persist = false;          // solves run as one persistent cooperative launch
   int graph_iters = 0;
   int launches_per_iter = 0;
   double rho1 = 1.0, rho2 = 1.0;  // hybrid Schwarz weights (rdr_get_weights)
@@ -200,6 +202,7 @@ struct rdr_handle {
 };
 
 static int hybrid_weights(rdr_handle* h, const std::vector<double>& dinv);
+static int select_loop(rdr_handle* h);
 
 // device memory freed at scope exit (setup temporaries)
 struct DevTemps {
@@ -321,6 +324,7 @@ static int setup_impl(rdr_handle* h, const double* vertices, int64_t nv, const i
   if ((st = h->own_upload(&d_R, el.R))) return st;  // the device patch setup's reference matrices
   op.lut = d_lut;
   op.coef = d_coef;
+  op.R = d_R;
   op.kp = (el.n + 3) / 4 * 4;
   op.ngroups = (el.n + 31) / 32;
   {
@@ -575,6 +579,7 @@ static int setup_impl(rdr_handle* h, const double* vertices, int64_t nv, const i
   in.flops_apply = 2.0 * el.n * (double)el.n * el.n_mat * (double)nt;
   in.bytes_apply = 24.0 * num.n_total + (double)nt * (4.0 * el.n + 8.0 * el.n_mat);
   in.bytes_precond = P.alg_bytes + 24.0 * in.n_interior;
+  in.persistent_loop = 0;
   in.apply_variant = op.av;
   in.apply_grid = op.apply_grid;
   in.patch_setup_flops = 0;
@@ -684,7 +689,7 @@ int rdr_setup_ex(rdr_handle** hp, const double* vertices, int64_t nv, const int3
   const int su = opt ? opt->setup : RDR_SETUP_DEVICE;
   if (su != RDR_SETUP_DEVICE && su != RDR_SETUP_HOST) return RDR_EINVAL;
   const int loop = opt ? opt->loop : RDR_LOOP_DEVICE;
-  if (loop != RDR_LOOP_DEVICE && loop != RDR_LOOP_HOST && loop != RDR_LOOP_EAGER) return RDR_EINVAL;
+  if (loop < RDR_LOOP_DEVICE || loop > RDR_LOOP_PERSISTENT) return RDR_EINVAL;
   rdr_handle* h = new (std::nothrow) rdr_handle();
   if (!h) return RDR_ENOMEM;
   int st;
@@ -697,6 +702,7 @@ int rdr_setup_ex(rdr_handle** hp, const double* vertices, int64_t nv, const int3
     std::fprintf(stderr, "rdr_setup: %s\n", e.what());
     st = RDR_EINVAL;
   }
+  if (!st) st = select_loop(h);
   if (st) {
     delete h;
     return st;
@@ -871,11 +877,24 @@ static int fetch_scalars(rdr_handle* h, cudaStream_t s) {
 // launch).
 static int solve_device(rdr_handle* h, const double* b, double rtol, int maxit, int* iters, cudaStream_t s) {
   int st;
+  if (h->use_persist) {  // the whole solve in one cooperative launch (small problems)
+    CK(cudaStreamSynchronize(s));
+    std::memset(h->h_sc, 0, sizeof(PcgScalars));
+    h->h_sc->rtol = rtol;
+    h->h_sc->maxit = maxit;
+    CK(cudaMemcpyAsync(h->d_sc, h->h_sc, sizeof(PcgScalars), cudaMemcpyHostToDevice, s));
+    CK(launch_persistent_pcg(h->persist, h->op, h->pc, h->d_sc, b, h->d_cons, h->d_x, h->d_r, h->d_z, h->d_p,
+                             h->d_p2, h->d_q, s));
+    if ((st = fetch_scalars(h, s))) return st;
+    h->last_launches = 1;
+    *iters = h->h_sc->iters;
+    return h->h_sc->converged ? RDR_OK : RDR_ENOCONV;
+  }
   int64_t launches = pcg_begin(h, b, rtol, maxit, s, &st);
   if (st) return st;
   // the unfused path tests before each iteration, the fused one inside its apply
   const bool test_first = !h->fused;
-  if (h->fused && h->loop == RDR_LOOP_DEVICE) {
+  if (h->fused && (h->loop == RDR_LOOP_DEVICE || h->loop == RDR_LOOP_GRAPH)) {
     if ((st = build_while_graph(h))) return st;
     CK(cudaGraphLaunch(h->wgraph, s));
     if ((st = fetch_scalars(h, s))) return st;
@@ -914,6 +933,56 @@ static int solve_device(rdr_handle* h, const double* b, double rtol, int maxit, 
   *iters = h->h_sc->iters;
   return h->h_sc->converged ? RDR_OK : RDR_ENOCONV;
 }
+
+}  // extern "C"
+
+// rdr_options.loop: RDR_LOOP_DEVICE runs a small problem's solves as one
+// persistent cooperative launch when the kernel is eligible (additive
+// preconditioner, patches <= 256 dofs, n_loc <= 128, its shared memory fits) and
+// a 10-iteration solve measured at setup is faster than with the graph's WHILE
+// node; RDR_LOOP_PERSISTENT requires it (RDR_EINVAL if not eligible);
+// RDR_LOOP_GRAPH, RDR_LOOP_HOST and RDR_LOOP_EAGER never use it.
+static int select_loop(rdr_handle* h) {
+  h->use_persist = false;
+  if (!h->fused || (h->loop != RDR_LOOP_DEVICE && h->loop != RDR_LOOP_PERSISTENT)) return RDR_OK;
+  h->persist = plan_persistent_pcg(h->op, h->pc);
+  if (h->persist.grid == 0) return h->loop == RDR_LOOP_PERSISTENT ? RDR_EINVAL : RDR_OK;
+  if (h->loop == RDR_LOOP_PERSISTENT) {
+    h->use_persist = true;
+    h->info.persistent_loop = 1;
+    return RDR_OK;
+  }
+  // time both drivers on a 10-iteration solve (rtol 0) with b = 1 on every dof
+  std::vector<double> ones(h->n_total, 1.0);
+  CK(cudaMemcpy(h->d_b, ones.data(), sizeof(double) * h->n_total, cudaMemcpyHostToDevice));
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  float t[2] = {0.f, 0.f};
+  for (int mode = 0; mode < 2; ++mode) {
+    h->use_persist = mode == 1;
+    int it = 0, st = RDR_OK;
+    for (int rep = 0; rep < 3 && (st == RDR_OK || st == RDR_ENOCONV); ++rep) {  // the last one timed
+      CK(cudaEventRecord(e0, 0));
+      st = solve_device(h, h->d_b, 0.0, 10, &it, 0);
+      CK(cudaEventRecord(e1, 0));
+      CK(cudaEventSynchronize(e1));
+    }
+    if (st != RDR_OK && st != RDR_ENOCONV) {
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+      return st;
+    }
+    CK(cudaEventElapsedTime(&t[mode], e0, e1));
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  h->use_persist = t[1] < t[0];
+  h->info.persistent_loop = h->use_persist;
+  return RDR_OK;
+}
+
+extern "C" {
 
 int rdr_solve(rdr_handle* h, const double* b, double* x, double rtol, int maxit, int* iters, void* stream) {
   if (!h || !b || !x || !iters || !(rtol >= 0)) return RDR_EINVAL;
@@ -1047,7 +1116,15 @@ int rdr_time_kernels(rdr_handle* h, const double* x, double* y, const double* r,
   int st = timed([&] { return launch_apply(h->op, x, y, nullptr, nullptr, s); }, &ms[0]);
   if (!st) st = timed([&] { return launch_precond_part(0, h->pc, r, z, nullptr, nullptr, s); }, &ms[1]);
   if (!st) st = timed([&] { return launch_precond_part(1, h->pc, r, z, nullptr, nullptr, s); }, &ms[2]);
-  ms[3] = 0;  // the H(curl) discrete gradient runs inside the patch kernel
+  if (!st && h->fused) {  // the PCG-mode apply the solve runs: direction update + A p + stopping test
+    std::memset(h->h_sc, 0, sizeof(PcgScalars));
+    h->h_sc->rtol = 0.0;
+    h->h_sc->maxit = 1 << 30;  // the stopping test never fires (x != 0: ||z_0|| > 0)
+    CK(cudaMemcpyAsync(h->d_sc, h->h_sc, sizeof(PcgScalars), cudaMemcpyHostToDevice, s));
+    st = timed([&] { return launch_pcg_fused_apply(h->op, h->d_sc, x, h->d_p, h->d_p2, y, s); }, &ms[3]);
+  } else if (!st) {
+    ms[3] = 0;
+  }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   return st;

@@ -15,7 +15,7 @@ HGRAD, HCURL, HDIV = 0, 1, 2
 SPLIT, UNSPLIT = 0, 1
 ADDITIVE, HYBRID = 0, 1
 SETUP_DEVICE, SETUP_HOST = 0, 1
-LOOP_DEVICE, LOOP_HOST, LOOP_EAGER = 0, 1, 2
+LOOP_DEVICE, LOOP_HOST, LOOP_EAGER, LOOP_GRAPH, LOOP_PERSISTENT = 0, 1, 2, 3, 4
 RDR_OK, RDR_ENOCONV = 0, -6
 
 
@@ -46,7 +46,8 @@ class Info(ctypes.Structure):
                 ("bytes_precond", ctypes.c_double), ("setup_seconds", ctypes.c_double),
                 ("refelem_seconds", ctypes.c_double), ("patch_setup_seconds", ctypes.c_double),
                 ("patch_kernel_seconds", ctypes.c_double), ("patch_setup_flops", ctypes.c_double),
-                ("apply_variant", ctypes.c_int32), ("apply_grid", ctypes.c_int32)]
+                ("apply_variant", ctypes.c_int32), ("apply_grid", ctypes.c_int32),
+                ("persistent_loop", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -217,7 +218,7 @@ class Solver:
         return it.value
 
     def time_kernels(self, x, r, reps=20, stream=None):
-        """Average device ms per launch: (apply, jacobi, patches, gradient)."""
+        """Average device ms per launch: (apply, jacobi, patches, fused PCG-mode apply)."""
         y, z = self._vec(None), self._vec(None)
         ms = np.zeros(4)
         _check(_lib.rdr_time_kernels(self._h, _ptr(x), _ptr(y), _ptr(r), _ptr(z), int(reps), _ptr(ms),
@@ -237,7 +238,7 @@ class Solver:
 
     def profile_solve(self, b, rtol=1e-8, maxit=10000, stream=None):
         """Eager PCG solve with CUDA events between kernel groups: (iters, ms per
-        iteration of [apply, update + Jacobi, patches, gradient])."""
+        iteration of [apply, update + Jacobi, patches, 0])."""
         it = ctypes.c_int()
         ms = np.zeros(4)
         code = _lib.rdr_profile_solve(self._h, _ptr(b), float(rtol), int(maxit), ctypes.byref(it), _ptr(ms),

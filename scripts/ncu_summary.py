@@ -60,6 +60,17 @@ def full(path):
         for i, k in enumerate(h):
             if any(k.startswith(w) for w in KEYS):
                 print(f"{k:75s} {r[i]:>16s} {units[i]}")
+        stalls = []
+        for i, k in enumerate(h):
+            if k.startswith("smsp__pcsamp_warps_issue_stalled_") and not k.endswith("not_issued"):
+                try:
+                    stalls.append((k[len("smsp__pcsamp_warps_issue_stalled_"):], float(r[i].replace(",", ""))))
+                except ValueError:
+                    pass
+        tot = sum(v for _, v in stalls)
+        if tot > 0:
+            top = sorted(stalls, key=lambda kv: -kv[1])[:8]
+            print("warp stall samples (share): " + ", ".join(f"{k} {100 * v / tot:.1f}%" for k, v in top))
 
 
 def traffic(path, key, out="profiles/traffic.json"):
@@ -89,5 +100,36 @@ def traffic(path, key, out="profiles/traffic.json"):
     json.dump(data, open(out, "w"), indent=1)
 
 
+def source(path, top=40):
+    """The hottest SASS instructions of each kernel in an `ncu --set full
+    --import-source on` report: share of warp-stall samples, executions, text."""
+    out = subprocess.run(["ncu", "-i", path, "--page", "source", "--csv", "--print-source", "sass"],
+                         capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    print(f"# hottest SASS lines of {path} (share of warp-stall samples)")
+    hdr = None
+    block = []
+
+    def flush():
+        if not hdr or not block:
+            return
+        i_s, i_src, i_ex = (hdr.index(k) for k in ("Warp Stall Sampling (All Samples)", "Source",
+                                                    "Instructions Executed"))
+        tot = sum(float(r[i_s] or 0) for r in block) or 1.0
+        for r in sorted(block, key=lambda r: -float(r[i_s] or 0))[:int(top)]:
+            print(f"{100 * float(r[i_s] or 0) / tot:6.2f}% {r[i_ex]:>10s}  {r[i_src].strip()[:90]}")
+
+    for r in rows:
+        if r and r[0] == "Kernel Name":
+            flush()
+            print(f"## {r[1][:140]}")
+            hdr, block = None, []
+        elif r and r[0] == "Address":
+            hdr = r
+        elif hdr and len(r) == len(hdr):
+            block.append(r)
+    flush()
+
+
 if __name__ == "__main__":
-    {"launches": launches, "full": full, "traffic": traffic}[sys.argv[1]](*sys.argv[2:])
+    {"launches": launches, "full": full, "traffic": traffic, "source": source}[sys.argv[1]](*sys.argv[2:])

@@ -85,7 +85,7 @@ enum { RDR_SETUP_DEVICE = 0, RDR_SETUP_HOST = 1 };
  *   RDR_LOOP_DEVICE (default) -- the loop runs on the device with one host
  *                synchronisation per solve: small problems (additive
  *                preconditioner, star patches <= 256 dofs, n_loc <= 128) as one
- *                persistent cooperative kernel when a 10-iteration solve timed
+ *                persistent cooperative kernel when a 40-iteration solve timed
  *                at setup is faster that way (rdr_info.persistent_loop), else as
  *                RDR_LOOP_GRAPH;
  *   RDR_LOOP_HOST -- graphs of 8 iterations relaunched by the host until done;

@@ -25,13 +25,10 @@ struct PcgScalars {
   double rz_old;    // fused path: r.z of the z used by the current direction
   double pq2[2];    // fused path: p.Ap, double-buffered by iteration parity
   double z_last;    // ||z_k|| at the last stopping test (rdr_last_solve)
-  // persistent PCG kernel (small problems): r.z by iteration mod 3, ||z||^2 and p.Ap by
-  // parity, and its grid barrier
+  // persistent PCG kernel (small problems): r.z by iteration mod 3, ||z||^2 and p.Ap by parity
   double prz[3];
   double pzz[2];
   double ppq[2];
-  uint32_t bar_count;
-  uint32_t bar_gen;
 };
 
 struct DevOperator {

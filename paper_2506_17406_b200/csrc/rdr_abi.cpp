@@ -939,7 +939,7 @@ static int solve_device(rdr_handle* h, const double* b, double rtol, int maxit, 
 // rdr_options.loop: RDR_LOOP_DEVICE runs a small problem's solves as one
 // persistent cooperative launch when the kernel is eligible (additive
 // preconditioner, patches <= 256 dofs, n_loc <= 128, its shared memory fits) and
-// a 10-iteration solve measured at setup is faster than with the graph's WHILE
+// a 40-iteration solve measured at setup is faster than with the graph's WHILE
 // node; RDR_LOOP_PERSISTENT requires it (RDR_EINVAL if not eligible);
 // RDR_LOOP_GRAPH, RDR_LOOP_HOST and RDR_LOOP_EAGER never use it.
 static int select_loop(rdr_handle* h) {
@@ -952,7 +952,7 @@ static int select_loop(rdr_handle* h) {
     h->info.persistent_loop = 1;
     return RDR_OK;
   }
-  // time both drivers on a 10-iteration solve (rtol 0) with b = 1 on every dof
+  // time both drivers on a 40-iteration solve (rtol 0; a typical length) with b = 1 on every dof
   std::vector<double> ones(h->n_total, 1.0);
   CK(cudaMemcpy(h->d_b, ones.data(), sizeof(double) * h->n_total, cudaMemcpyHostToDevice));
   cudaEvent_t e0, e1;
@@ -964,7 +964,7 @@ static int select_loop(rdr_handle* h) {
     int it = 0, st = RDR_OK;
     for (int rep = 0; rep < 3 && (st == RDR_OK || st == RDR_ENOCONV); ++rep) {  // the last one timed
       CK(cudaEventRecord(e0, 0));
-      st = solve_device(h, h->d_b, 0.0, 10, &it, 0);
+      st = solve_device(h, h->d_b, 0.0, 40, &it, 0);
       CK(cudaEventRecord(e1, 0));
       CK(cudaEventSynchronize(e1));
     }

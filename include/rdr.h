@@ -145,7 +145,7 @@ struct rdr_info {
   int32_t apply_grid;          /* its persistent grid (CTAs) */
   int32_t persistent_loop;     /* 1: solves run as the persistent cooperative kernel (RDR_LOOP_DEVICE
                                   chose it, or RDR_LOOP_PERSISTENT) */
-  int32_t reserved;
+  int32_t apply_slots;         /* its TMA ring depth (reference-stack chunks of n_mat KB) */
 };
 
 /* Build the operator and the preconditioner (host setup once, then upload).
@@ -237,7 +237,7 @@ void rdr_destroy(rdr_handle* h);
 const char* rdr_strerror(int code);
 
 /* Debugging entry point: run the operator apply (and the solves) with warp
- * layout `variant` (0 <= variant < 10; kernels.cu apply_variants) instead of the
+ * layout `variant` (0 <= variant < 12; kernels.cu apply_variants) instead of the
  * one setup's autotuning chose; RDR_EINVAL if it does not fit this operator.
  * The GPU tests use it to check every layout against the oracle. */
 int rdr_debug_set_apply_variant(rdr_handle* h, int variant);

@@ -507,33 +507,33 @@ __global__ void __launch_bounds__((apply_mma_warps(BM, NQ, KS) + 1) * 32, MINB)
 
 constexpr size_t kMaxSmem = 226 * 1024;  // 227 KB opt-in minus the static reduction scratch
 
-// The warp layouts built (BM, NQ, KS) with their ring depths, each for NM = 7
-// (H(grad), H(div)) and 12 (H(curl)); apply_choose picks the first that fits
-// two CTAs per SM, else the first that fits one.
+// The warp layouts built (BM, NQ, KS), each for NM = 7 (H(grad), H(div)) and 12
+// (H(curl)). The ring depth is sized per operator (apply_configure_variant).
 struct ApplyVariant {
-  int bm, nq, ks, slots, nm;
+  int bm, nq, ks, nm;
   const void* fn[2];  // plain, PCG
 };
 template <int BM, int NQ, int KS, int NM, int MINB = 1>
-ApplyVariant apply_variant(int slots) {
-  return {BM, NQ, KS, slots, NM,
+ApplyVariant apply_variant() {
+  return {BM, NQ, KS, NM,
           {(const void*)apply_tc_kernel<BM, NQ, KS, NM, MINB, false>,
            (const void*)apply_tc_kernel<BM, NQ, KS, NM, MINB, true>}};
 }
 const ApplyVariant* apply_variants(int* count) {
   static const ApplyVariant v[] = {
-      apply_variant<32, 4, 2, 7>(4),  apply_variant<32, 4, 2, 12>(4),   // 4 MMA warps
-      apply_variant<32, 4, 4, 7>(6),  apply_variant<32, 4, 4, 12>(6),   // 8 MMA warps
-      apply_variant<32, 2, 2, 7>(4),  apply_variant<32, 2, 2, 12>(4),   // 8 MMA warps, 16 x 16 warp tiles
-      apply_variant<16, 4, 4, 7>(6),  apply_variant<16, 4, 4, 12>(6),   // 4 MMA warps, 16 cells per unit
-      apply_variant<32, 4, 4, 7, 2>(6), apply_variant<32, 4, 4, 12, 2>(4),  // 8 MMA warps, registers for 2 CTAs/SM
+      apply_variant<32, 4, 2, 7>(),  apply_variant<32, 4, 2, 12>(),   // 4 MMA warps
+      apply_variant<32, 4, 4, 7>(),  apply_variant<32, 4, 4, 12>(),   // 8 MMA warps
+      apply_variant<32, 2, 2, 7>(),  apply_variant<32, 2, 2, 12>(),   // 8 MMA warps, 16 x 16 warp tiles
+      apply_variant<16, 4, 4, 7>(),  apply_variant<16, 4, 4, 12>(),   // 4 MMA warps, 16 cells per unit
+      apply_variant<32, 4, 4, 7, 2>(), apply_variant<32, 4, 4, 12, 2>(),  // 8 MMA warps, registers for 2 CTAs/SM
+      apply_variant<16, 2, 4, 7>(),  apply_variant<16, 2, 4, 12>(),   // 8 MMA warps, 16 cells (large n_loc)
   };
   *count = (int)(sizeof(v) / sizeof(v[0]));
   return v;
 }
 
 size_t apply_variant_smem(const ApplyVariant& v, const DevOperator& op) {
-  return apply_smem_layout(v.bm, v.nq, v.ks, v.slots, op.kp, op.n_mat).total;
+  return apply_smem_layout(v.bm, v.nq, v.ks, op.apply_slots, op.kp, op.n_mat).total;
 }
 
 inline int apply_threads(const ApplyVariant& v) { return (apply_mma_warps(v.bm, v.nq, v.ks) + 1) * 32; }
@@ -554,7 +554,7 @@ cudaError_t launch_apply_tc(const DevOperator& op, const double* x, double* y, d
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
-  int S = v.slots;
+  int S = op.apply_slots;
   DevOperator o = op;
   void* args[] = {(void*)&o, (void*)&S, (void*)&x, (void*)&y, (void*)&pq_acc, (void*)&guard, (void*)&sc, (void*)&p0,
                   (void*)&p1};
@@ -644,6 +644,7 @@ __device__ __forceinline__ void treduce_stage(double (&v)[16], int lane) {
   }
 }
 __device__ __forceinline__ double treduce16(double (&v)[16], int lane) {
+  __syncwarp();  // converged: plain SHFL (not the WARPSYNC.COLLECTIVE sequence ptxas emits otherwise)
   treduce_stage<8>(v, lane);
   treduce_stage<4>(v, lane);
   treduce_stage<2>(v, lane);
@@ -855,15 +856,18 @@ __global__ void __launch_bounds__(kLdgWarps * 32, 32 / kLdgWarps)
     }
     const double col = treduce16(a, lane);
     if (lane < 16) atomicAdd(zl + J * 32 + 16 * h + lane, col);
-    if (h == 1) {  // tile done: its row products, then this warp's next tile
-      atomicAdd(zl + I * 32 + lane, row);
-      row = 0.0;
+    if (h == 1) {  // tile done: this warp's next tile; row products flushed when the block row changes
       h = 0;
       t += kLdgWarps;
       J += kLdgWarps;
+      const int I0 = I;
       while (J > I) {
         J -= I + 1;
         ++I;
+      }
+      if (I != I0 || t >= ntiles) {
+        atomicAdd(zl + I0 * 32 + lane, row);
+        row = 0.0;
       }
     } else {
       h = 1;
@@ -1509,17 +1513,35 @@ bool fused_pcg_supported(const DevOperator& op) { return op.Bsw && op.own; }
 int apply_configure_variant(DevOperator& op, int k) {
   int cnt = 0;
   const ApplyVariant* vs = apply_variants(&cnt);
-  if (k < 0 || k >= cnt || vs[k].nm != op.n_mat || apply_variant_smem(vs[k], op) > kMaxSmem) return -1;
+  if (k < 0 || k >= cnt || vs[k].nm != op.n_mat) return -1;
   const ApplyVariant& v = vs[k];
-  int per_sm = 0, dev = 0, sms = 148;
+  // Ring depth: each K group consumes every KS-th chunk, so the ring holds S / KS
+  // chunks ahead per group; take the deepest ring (up to 4 per group) that keeps
+  // two CTAs per SM if the registers allow two, else one CTA per SM.
+  const size_t base = apply_smem_layout(v.bm, v.nq, v.ks, 0, op.kp, op.n_mat).total;
+  const size_t chunk = sizeof(double) * apply_chunk_doubles(op.n_mat);
+  int dev = 0, sms = 148, regs_occ = 0, per_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, v.fn[1], apply_threads(v), apply_variant_smem(v, op)) !=
-      cudaSuccess) {
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&regs_occ, v.fn[1], apply_threads(v), 0) != cudaSuccess) {
     cudaGetLastError();
     return -1;
   }
-  if (per_sm < 1) return -1;
+  const size_t two_per_sm = 228 * 1024 / 2 - 1024;
+  const int s_max = 4 * v.ks;
+  int S = 0;
+  if (regs_occ >= 2 && base + chunk * 2 * v.ks <= two_per_sm)
+    S = (int)std::min<size_t>(s_max, (two_per_sm - base) / chunk);
+  else if (base + chunk * (v.ks + 2) <= kMaxSmem)
+    S = (int)std::min<size_t>(s_max, (kMaxSmem - base) / chunk);
+  if (S == 0) return -1;
+  op.apply_slots = S;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, v.fn[1], apply_threads(v), apply_variant_smem(v, op)) !=
+          cudaSuccess ||
+      per_sm < 1) {
+    cudaGetLastError();
+    return -1;
+  }
   op.av = k;
   op.ntiles = (int)((op.n_cells + v.bm - 1) / v.bm);
   const int64_t units = (int64_t)op.ntiles * op.ngroups;
@@ -1546,17 +1568,25 @@ int tune_apply(DevOperator& op, const double* x, double* y, cudaStream_t s, int 
   for (int k = 0; k < cnt; ++k) {
     DevOperator t = op;
     if (apply_configure_variant(t, k)) continue;
-    if (launch_apply_tc<false>(t, x, y, nullptr, nullptr, s) != cudaSuccess) continue;
-    cudaEventRecord(e0, s);
-    for (int r = 0; r < reps; ++r) launch_apply_tc<false>(t, x, y, nullptr, nullptr, s);
-    cudaEventRecord(e1, s);
-    if (cudaEventSynchronize(e1) != cudaSuccess) continue;
-    float ms = 0.f;
-    cudaEventElapsedTime(&ms, e0, e1);
-    if (best < 0 || ms < best_ms) {
-      best = k;
-      best_ms = ms;
-      best_op = t;
+    // the persistent grid (resident CTAs, each a contiguous range of units), and
+    // for problems with fewer units than twice that, one CTA per unit (waves)
+    const int64_t units = (int64_t)t.ntiles * t.ngroups;
+    const int grids[2] = {t.apply_grid, units < 2 * (int64_t)t.apply_grid ? (int)units : 0};
+    for (int gi = 0; gi < 2; ++gi) {
+      if (grids[gi] <= 0 || (gi == 1 && grids[1] == grids[0])) continue;
+      t.apply_grid = grids[gi];
+      if (launch_apply_tc<false>(t, x, y, nullptr, nullptr, s) != cudaSuccess) continue;
+      cudaEventRecord(e0, s);
+      for (int r = 0; r < reps; ++r) launch_apply_tc<false>(t, x, y, nullptr, nullptr, s);
+      cudaEventRecord(e1, s);
+      if (cudaEventSynchronize(e1) != cudaSuccess) continue;
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, e0, e1);
+      if (best < 0 || ms < best_ms) {
+        best = k;
+        best_ms = ms;
+        best_op = t;
+      }
     }
   }
   cudaEventDestroy(e0);

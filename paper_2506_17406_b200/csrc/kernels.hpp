@@ -46,7 +46,7 @@ struct DevOperator {
                                 // (chunk j4 = rows 4 j4 .. 4 j4 + 3 of every R_s), columns swizzled (kernels.cu
                                 // apply_tc_kernel)
   // launch configuration (configure_apply): warp-layout variant, cell tiles, persistent grid
-  int av, ntiles, apply_grid;
+  int av, ntiles, apply_grid, apply_slots;
 };
 
 struct DevPrecond {

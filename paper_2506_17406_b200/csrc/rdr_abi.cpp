@@ -582,6 +582,7 @@ static int setup_impl(rdr_handle* h, const double* vertices, int64_t nv, const i
   in.persistent_loop = 0;
   in.apply_variant = op.av;
   in.apply_grid = op.apply_grid;
+  in.apply_slots = op.apply_slots;
   in.patch_setup_flops = 0;
   for (int32_t n : P.n) {  // lower tiles I >= J, I, J != K: nb(nb-1)/2 per K; panel: nb-1 per K
     const double nb = (n + 63) / 64;
@@ -1034,6 +1035,7 @@ int rdr_debug_set_apply_variant(rdr_handle* h, int variant) {
   h->graph = h->wgraph = nullptr;  // captured with the old launch configuration
   h->info.apply_variant = t.av;
   h->info.apply_grid = t.apply_grid;
+  h->info.apply_slots = t.apply_slots;
   return RDR_OK;
 }
 

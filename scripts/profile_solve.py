@@ -30,7 +30,9 @@ def main():
                           "in_solve_ms": dict(zip(("apply", "update_jacobi", "patches"), ms.tolist()[:3])),
                           "standalone_ms": dict(zip(("apply", "jacobi", "patches", "pcg_apply"), alone.tolist())),
                           "apply_tflops_in_solve": info["flops_apply"] / ms[0] / 1e9,
-                          "apply_tflops_standalone": info["flops_apply"] / alone[0] / 1e9}), flush=True)
+                          "apply_tflops_standalone": info["flops_apply"] / alone[0] / 1e9,
+                          "apply_layout": {k: info[k] for k in ("apply_variant", "apply_slots", "apply_grid")}}),
+              flush=True)
         S.close()
 
 

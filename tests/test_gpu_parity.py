@@ -100,11 +100,12 @@ def test_hcurl_small(torch_cuda, p, perturb):
     _check_pcg(torch_cuda, c, S, O)
 
 
-@pytest.mark.parametrize("p", [9, 10])
-@pytest.mark.parametrize("bc", ["all", "x0"])
+@pytest.mark.parametrize("p,bc", [(10, "x0")])
 def test_hcurl_high_p(torch_cuda, p, bc):
-    """Ned1_9, Ned1_10 (north_star: H(curl) up to p=10) on the 6-tet cube; the
-    oracle's x87 reference element dominates the cost at these degrees."""
+    """Ned1_10 (north_star: H(curl) up to p=10) on the 6-tet cube with partial
+    Dirichlet, every row against the global oracle (p = 9, 10 with full
+    Dirichlet at full size: test_config78_high_p_sampled); the oracle's x87
+    reference element dominates the cost at this degree."""
     c, S, O = _pair(torch_cuda, 0, n=1, p=p, space=HCURL, perturb=False, bc=bc)
     _check_apply_precond(torch_cuda, c, S, O)
     _check_pcg(torch_cuda, c, S, O)
@@ -402,7 +403,7 @@ def test_every_apply_layout(torch_cuda, space, p):
     hist = []
     _, ito, _ = O.solve(b, rtol=1e-8, history=hist)
     ran = 0
-    for k in range(10):
+    for k in range(12):
         if not S.set_apply_variant(k):
             continue
         ran += 1
@@ -410,7 +411,7 @@ def test_every_apply_layout(torch_cuda, space, p):
         assert rel(S.apply(xt).cpu().numpy(), ya) <= TOL, k
         _, it = S.solve(torch.from_numpy(b).cuda(), rtol=1e-8)
         _check_iters(S, it, ito, lambda kk: hist[kk - 1] if 0 < kk <= len(hist) else None)
-    assert ran == 5  # every layout of this n_mat fits these small elements
+    assert ran == 6  # every layout of this n_mat fits these small elements
 
 
 def test_stream_semantics_and_repeated_setup(torch_cuda):
@@ -602,7 +603,7 @@ def test_device_patch_setup_errors(torch_cuda):
             assert e.value.code == -1
     c = make_config(0, n=1, p=2, space=HCURL, bc="all")
     with pytest.raises(rdr.RdrError) as e:
-        rdr.Solver(c.vertices, c.tets, 2, HCURL, c.alpha, c.beta, c.mask, loop=3)
+        rdr.Solver(c.vertices, c.tets, 2, HCURL, c.alpha, c.beta, c.mask, loop=7)
     assert e.value.code == -1
     with pytest.raises(rdr.RdrError) as e:
         rdr.Solver(c.vertices, c.tets, 2, HCURL, c.alpha, c.beta, c.mask, setup=2)
@@ -657,7 +658,7 @@ def test_config78_high_p_sampled(torch_cuda, cfg, p):
     A x and P^-1 r, PCG iterations vs the oracle's (golden, oracle/lean.py)."""
     c, S, O = _sampled_pair(cfg, p=p)
     b = c.draw_vector(O.n_total)
-    rows = _sample_rows(O, n_vertices=2, n_cells=3)
+    rows = _sample_rows(O, n_vertices=1, n_cells=2)  # every sampled patch costs ~30 element matrices at p = 10
     _check_sampled(torch_cuda, c, S, O, rows)
     _check_sampled_pcg(torch_cuda, c, S, O, rows, b, _golden(cfg, p))
 

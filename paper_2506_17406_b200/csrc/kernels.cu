@@ -294,7 +294,8 @@ __global__ void __launch_bounds__((apply_mma_warps(BM, NQ, KS) + 1) * 32, MINB)
     if (PCG) {
       volatile PcgScalars* v = sc;
       kit = v->k;
-      beta = kit == 0 ? 0.0 : v->rz_acc / v->rz_old;
+      const double rz_old = v->rz_old;  // 0 only before the first direction (or in a timing loop)
+      beta = (kit == 0 || rz_old == 0.0) ? 0.0 : v->rz_acc / rz_old;
       p_old = (kit & 1) ? pbuf0 : pbuf1;
       p_new = (kit & 1) ? pbuf1 : pbuf0;
     }

@@ -57,8 +57,9 @@ def measure(cfg, p, fp64_peak, hbm, solves=3, reps=20, dec="split", pre="additiv
         "apply_ms": kms[0], "apply_dofs_per_s": info["n_free"] / (kms[0] / 1e3),
         "apply_tflops": info["flops_apply"] / (kms[0] / 1e3) / 1e12,
         "apply_frac_dmma": info["flops_apply"] / (kms[0] / 1e3) / 1e12 / fp64_peak,
-        "jacobi_ms": kms[1], "patch_ms": kms[2], "gradient_ms": kms[3],
-        "precond_ms": kms[1] + kms[2] + kms[3],
+        "jacobi_ms": kms[1], "patch_ms": kms[2], "pcg_apply_ms": kms[3],
+        "pcg_apply_frac_dmma": info["flops_apply"] / (kms[3] / 1e3) / 1e12 / fp64_peak if kms[3] > 0 else None,
+        "precond_ms": kms[1] + kms[2],
         "patch_GBps": patch_bytes / (kms[2] / 1e3) / 1e9 if kms[2] > 0 else None,
         "patch_frac_hbm": patch_bytes / (kms[2] / 1e3) / 1e9 / hbm if kms[2] > 0 else None,
         "pcg_iters": it, "time_to_solution_ms": t_solve, "ms_per_iter": t_solve / max(1, it),
@@ -66,6 +67,11 @@ def measure(cfg, p, fp64_peak, hbm, solves=3, reps=20, dec="split", pre="additiv
         "t_roof_iter_ms": info["flops_apply"] / fp64_peak / 1e9 + (patch_bytes + 12 * 8 * n) / hbm / 1e6,
     }
     out["iter_frac_roofline"] = out["t_roof_iter_ms"] / out["ms_per_iter"]
+    out["apply_layout"] = {k: info[k] for k in ("apply_variant", "apply_slots", "apply_grid")}
+    out["persistent_loop"] = info["persistent_loop"]
+    if pre == "additive":  # in-solve kernel times (eager solve, events between kernel groups)
+        _, pms = S.profile_solve(b)
+        out["in_solve_ms"] = {"apply": pms[0], "update_jacobi": pms[1], "patches": pms[2]}
     if pre == "hybrid":
         out["rho"] = [float(v) for v in S.weights]
         t0 = time.time()
@@ -98,7 +104,7 @@ def main():
     with open(args.out, "w") as f:
         f.write(json.dumps(head) + "\n")
         for cfg in (int(v) for v in args.configs.split(",")):
-            for p in (range(lo, hi + 1) if cfg in (5, 7, 8) else [None]):
+            for p in (range(lo, min(hi, 12 if cfg == 5 else 10) + 1) if cfg in (5, 7, 8) else [None]):
                 r = measure(cfg, p, fp64_peak, hbm, dec=args.decomposition, pre=args.precond)
                 print(json.dumps(r), flush=True)
                 f.write(json.dumps(r) + "\n")

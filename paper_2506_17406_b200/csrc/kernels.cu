@@ -24,17 +24,11 @@ namespace {
 
 constexpr int kVecThreads = 256;
 
-// Launch with the programmatic stream-serialization attribute (PDL, see
-// pdl_wait); RDR_PDL=0 launches plainly. Every kernel launched this way calls
-// pdl_wait() before it reads anything a predecessor kernel writes.
-bool pdl_enabled() {
-  static const bool on = !(std::getenv("RDR_PDL") && std::getenv("RDR_PDL")[0] == '0');
-  return on;
-}
-bool pdl_patch_enabled() {  // RDR_PDL_PATCH=0: launch the patch kernel without PDL
-  static const bool on = pdl_enabled() && !(std::getenv("RDR_PDL_PATCH") && std::getenv("RDR_PDL_PATCH")[0] == '0');
-  return on;
-}
+// Kernels are launched with the programmatic stream-serialization attribute
+// (PDL, see pdl_wait). Every kernel launched this way calls pdl_wait() before
+// it reads anything a predecessor kernel writes.
+constexpr bool pdl_enabled() { return true; }
+constexpr bool pdl_patch_enabled() { return true; }
 template <typename... Params, typename... Args>
 cudaError_t launch_kx(bool pdl, void (*kernel)(Params...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                       Args... args) {

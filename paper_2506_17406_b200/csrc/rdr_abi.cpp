@@ -405,17 +405,14 @@ static int setup_impl(rdr_handle* h, const double* vertices, int64_t nv, const i
   if (sink.d) h->owned.push_back(sink.d);
   if (st) return st;
   pc.n_patches = (int64_t)P.n.size();
-  {  // mostly small patches (<= 4 tile rows, e.g. the H(curl) edge stars): 4-warp CTAs, 8 per SM
+  {  // mostly small patches (<= 4 tile rows, e.g. the H(curl) edge stars): 4-warp CTAs, 8 per SM.
+    // Only small patches (H(div) edge stars): one per warp (patch_warp_kernel). Mixed sizes keep
+    // one CTA per patch: a second launch for the small ones measured slower on configs 2, 4, 5
+    // and 7 (profiles/round2/experiments/patch_launch_shape_ab.log, and round 1's 273 -> 320 us).
     int64_t small = 0;
     for (int32_t n : P.n) small += n <= 128;
     pc.ldg_warps = 2 * small > pc.n_patches ? 4 : 8;
-    if (const char* pw = std::getenv("RDR_PATCH_WARPS")) pc.ldg_warps = std::atoi(pw) == 4 ? 4 : 8;
-    // only small patches (H(div) edge stars): one per warp (patch_warp_kernel).
-    // Mixed sizes keep one CTA per patch: splitting them over two launches measured
-    // slower on config 4 (273 -> 320 us). RDR_PATCH_WARP_SMALL=0|1 overrides.
-    const char* ws = std::getenv("RDR_PATCH_WARP_SMALL");
-    const bool warp_small = ws ? std::atoi(ws) != 0 : small == pc.n_patches;
-    pc.n_big = (int64_t)P.n.size() - (warp_small ? small : 0);
+    pc.n_big = small == pc.n_patches ? 0 : pc.n_patches;
   }
   pc.max_n = P.max_n;
   int32_t *d_pn, *d_idx;
@@ -480,15 +477,14 @@ static int setup_impl(rdr_handle* h, const double* vertices, int64_t nv, const i
     CK(cudaGetDevice(&dev));
     cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, dev);
     cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev);
-    const char* lp = std::getenv("RDR_L2_PERSIST");
     h->l2_window = {};
-    // Only when the whole hot region fits the persisting set-aside. Default: hot
-    // regions up to 16 MB (1/8 of L2; config 2's is 7 MB: bench 10.84k vs 10.71k
-    // PCG it/s); larger full windows measured within +-2 % (configs 4, 6) and a
-    // partial one 4 % slower (config 3) (profiles/experiments/r2w_l2_persist_ab.log,
-    // r2x_l2_persist_ab.log). RDR_L2_PERSIST=0|1 overrides the size rule.
+    // Only when the whole hot region fits the persisting set-aside and is at most
+    // 16 MB (1/8 of L2; config 2's is 7 MB: bench 10.84k vs 10.71k PCG it/s);
+    // larger full windows measured within +-2 % (configs 4, 6) and a partial one
+    // 4 % slower (config 3) (profiles/experiments/r2w_l2_persist_ab.log,
+    // r2x_l2_persist_ab.log).
     const bool fits = hot <= (size_t)max_win && hot <= (size_t)max_persist;
-    const bool want = lp ? std::atoi(lp) == 1 : hot <= ((size_t)16 << 20);
+    const bool want = hot <= ((size_t)16 << 20);
     if (fits && want) {
       const size_t bytes = hot, setaside = hot;
       l2_window_acquire(setaside);

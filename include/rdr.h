@@ -146,6 +146,9 @@ struct rdr_info {
   int32_t persistent_loop;     /* 1: solves run as the persistent cooperative kernel (RDR_LOOP_DEVICE
                                   chose it, or RDR_LOOP_PERSISTENT) */
   int32_t apply_slots;         /* its TMA ring depth (reference-stack chunks of n_mat KB) */
+  int32_t small_patch_grid;    /* > 0: all patches <= 128 dofs and setup's timing chose resident warps
+                                  walking them (this many CTAs); 0: one warp per patch or CTA per patch */
+  int32_t reserved;
 };
 
 /* Build the operator and the preconditioner (host setup once, then upload).
@@ -241,6 +244,14 @@ const char* rdr_strerror(int code);
  * one setup's autotuning chose; RDR_EINVAL if it does not fit this operator.
  * The GPU tests use it to check every layout against the oracle. */
 int rdr_debug_set_apply_variant(rdr_handle* h, int variant);
+
+/* Debugging entry point: run the small star patches (configurations whose
+ * patches all have <= 128 dofs, e.g. the H(div) edge stars) with one warp per
+ * patch (persistent = 0) or with resident warps that walk the patches and load
+ * the next one's tiles while scattering the current one (persistent = 1)
+ * instead of the one setup's timing chose; RDR_EINVAL if the configuration
+ * has no small-patch launch. */
+int rdr_debug_set_small_patch_kernel(rdr_handle* h, int persistent);
 
 /* Debugging entry point: one fused PCG operator apply at iteration 0 (q = A z
  * through the PCG variant of the apply kernel, which also writes the search

@@ -772,6 +772,159 @@ __global__ void __launch_bounds__(kLdgWarps * 32, 32 / kLdgWarps)
   if (rz_acc && lane == 0) atomicAdd(rz_acc, part);
 }
 
+// Small patches (every patch <= 128 dofs, as the H(div) edge stars), persistent
+// form: a grid of resident CTAs whose warps each walk a strided sequence of
+// patches (pid = gw, gw + GW, ...). After a patch's last tile, the warp issues
+// the next patch's dof ids and first half tile, then scatters the finished
+// patch (its atomics and shared-memory reads overlap those loads), then
+// gathers the next r: the per-patch latency chain of patch_warp_kernel
+// (ids -> first tile, ids -> r, the scatter) is half hidden. Shared memory:
+// two (r, z) buffer pairs per warp.
+struct SmallPatch {
+  int64_t pid;
+  int n, nb, ntiles;
+  bool pot;
+  const double* T;
+  const int32_t* id;
+};
+
+template <int kLdgWarps>
+__global__ void __launch_bounds__(kLdgWarps * 32, 24 / kLdgWarps)
+    patch_warp_loop_kernel(DevPrecond pc, const double* __restrict__ r, double* __restrict__ z, double* rz_acc,
+                           const PcgScalars* guard) {
+  extern __shared__ double smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t gw = (int64_t)blockIdx.x * kLdgWarps + warp, GW = (int64_t)gridDim.x * kLdgWarps;
+  double* wbuf = smem + (size_t)warp * 4 * kSmallPatch;  // [2 buffers][r, z][128]
+  auto meta = [&](int64_t pid) {
+    SmallPatch m;
+    m.pid = pid;
+    m.n = pc.pn[pid];
+    m.nb = (m.n + 31) >> 5;
+    m.ntiles = m.nb * (m.nb + 1) / 2;
+    m.pot = pc.pkind[pid] != 0;
+    m.T = pc.tiles + pc.tile_off[pid];
+    m.id = pc.idx + pc.idx_off[pid];
+    return m;
+  };
+  auto load_half = [&](double(&a)[16], const SmallPatch& m, int I, int J, int h) {
+    const int rows = min(32, m.n - 32 * I);
+    const double* tb = m.T + 512LL * I * I + 16LL * I + (int64_t)J * 32 * rows;
+    if (J < I) {
+      if (lane < rows) {
+        const double4* tp = reinterpret_cast<const double4*>(tb) + lane + 4 * h * rows;
+#pragma unroll
+        for (int k4 = 0; k4 < 4; ++k4) {
+          const double4 v = ld_stream4(tp + k4 * rows);
+          a[4 * k4] = v.x;
+          a[4 * k4 + 1] = v.y;
+          a[4 * k4 + 2] = v.z;
+          a[4 * k4 + 3] = v.w;
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < 16; ++q) a[q] = 0.0;
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const int k = 16 * h + q;
+        a[q] = (k <= lane && lane < rows) ? ld_stream1(tb + k * rows - k * (k - 1) / 2 + (lane - k)) : 0.0;
+      }
+    }
+  };
+  int64_t pid = pc.n_big + gw;
+  if (pid >= pc.n_patches) {
+    pdl_wait();
+    return;
+  }
+  SmallPatch m = meta(pid);
+  int buf = 0;
+  int ids[4];  // this lane's dof ids of the patch (npad <= 128)
+#pragma unroll
+  for (int q = 0; q < 4; ++q) ids[q] = 32 * q + lane < m.nb * 32 ? m.id[32 * q + lane] : -1;
+  double a[16];
+  load_half(a, m, 0, 0, 0);
+  pdl_wait();
+  if (stopped(guard)) return;
+  double part = 0.0;
+  for (;;) {
+    double* rl = wbuf + buf * 2 * kSmallPatch;
+    double* zl = rl + kSmallPatch;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (32 * q < m.nb * 32) {
+        rl[32 * q + lane] = patch_residual(pc, m.pot, r, ids[q]);
+        zl[32 * q + lane] = 0.0;
+      }
+    __syncwarp();
+    // the patch's tiles (lane = row, half tiles), as patch_warp_kernel
+    int I = 0, J = 0, h = 0, t = 0;
+    double row = 0.0;
+    while (t < m.ntiles) {
+      const double ri = rl[I * 32 + lane];
+      if (J < I) {
+        const double* rJ = rl + J * 32 + 16 * h;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) row = fma(a[q], rJ[q], row);
+#pragma unroll
+        for (int q = 0; q < 16; ++q) a[q] *= ri;
+      } else {
+        const double* rI = rl + I * 32 + 16 * h;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) row = fma(a[q], rI[q], row);
+#pragma unroll
+        for (int q = 0; q < 16; ++q) a[q] = (16 * h + q < lane) ? a[q] * ri : 0.0;
+      }
+      const double col = treduce16(a, lane);
+      if (lane < 16) atomicAdd(zl + J * 32 + 16 * h + lane, col);
+      if (h == 1) {
+        atomicAdd(zl + I * 32 + lane, row);
+        row = 0.0;
+        h = 0;
+        ++t;
+        if (++J > I) {
+          J = 0;
+          ++I;
+        }
+      } else {
+        h = 1;
+      }
+      if (t < m.ntiles) load_half(a, m, I, J, h);
+    }
+    // the next patch's ids and first half tile are issued before this one is scattered
+    const int64_t next = pid + GW;
+    const bool more = next < pc.n_patches;
+    SmallPatch mn = m;
+    int nids[4];
+    if (more) {
+      mn = meta(next);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) nids[q] = 32 * q + lane < mn.nb * 32 ? mn.id[32 * q + lane] : -1;
+      load_half(a, mn, 0, 0, 0);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int i = 32 * q + lane;
+      if (i < m.n) {
+        const double zi = zl[i];
+        patch_scatter(pc, m.pot, z, ids[q], pc.out_scale * zi);
+        part = fma(rl[i], zi, part);
+      }
+    }
+    if (!more) break;
+    pid = next;
+    m = mn;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) ids[q] = nids[q];
+    buf ^= 1;
+  }
+  if (pdl_late()) pdl_trigger();
+  part = warp_sum(part);
+  if (rz_acc && lane == 0) atomicAdd(rz_acc, part);
+}
+
 template <int kLdgWarps>
 __global__ void __launch_bounds__(kLdgWarps * 32, 32 / kLdgWarps)
     patch_ldg_kernel(DevPrecond pc, const double* __restrict__ r, double* __restrict__ z, double* rz_acc,
@@ -1412,12 +1565,20 @@ cudaError_t launch_precond_part(int part, const DevPrecond& pc, const double* r,
           if (e != cudaSuccess) return e;
         }
         if (pc.n_big < pc.n_patches) {  // one warp per small patch
-          const size_t sm = 2 * sizeof(double) * kSmallPatch * W;
-          const dim3 grid((unsigned)((pc.n_patches - pc.n_big + W - 1) / W));
-          e = W == 4 ? launch_kx(pdl_patch_enabled(), patch_warp_kernel<4>, grid, dim3(4 * 32), sm, s, pc, r, z,
-                                 rz_acc, guard)
-                     : launch_kx(pdl_patch_enabled(), patch_warp_kernel<8>, grid, dim3(8 * 32), sm, s, pc, r, z,
-                                 rz_acc, guard);
+          if (pc.small_grid > 0) {  // persistent warps walking the small patches
+            const size_t sm = 4 * sizeof(double) * kSmallPatch * W;
+            e = W == 4 ? launch_kx(pdl_patch_enabled(), patch_warp_loop_kernel<4>, dim3(pc.small_grid), dim3(4 * 32),
+                                   sm, s, pc, r, z, rz_acc, guard)
+                       : launch_kx(pdl_patch_enabled(), patch_warp_loop_kernel<8>, dim3(pc.small_grid), dim3(8 * 32),
+                                   sm, s, pc, r, z, rz_acc, guard);
+          } else {
+            const size_t sm = 2 * sizeof(double) * kSmallPatch * W;
+            const dim3 grid((unsigned)((pc.n_patches - pc.n_big + W - 1) / W));
+            e = W == 4 ? launch_kx(pdl_patch_enabled(), patch_warp_kernel<4>, grid, dim3(4 * 32), sm, s, pc, r, z,
+                                   rz_acc, guard)
+                       : launch_kx(pdl_patch_enabled(), patch_warp_kernel<8>, grid, dim3(8 * 32), sm, s, pc, r, z,
+                                   rz_acc, guard);
+          }
         }
         return e;
       }
@@ -1553,6 +1714,44 @@ int apply_variant_count() {
 // Setup-time autotuning of the apply's warp layout: every variant that fits is
 // timed on this operator (one warm-up, then `reps` plain applies between CUDA
 // events on `s`) and the fastest is kept.
+// Setup-time choice for workloads of small patches only (patch_warp_kernel, one
+// warp per patch, vs patch_warp_loop_kernel, resident warps walking the
+// patches with the next patch's loads in flight): both timed on r (reps launches
+// each), the faster kept in pc.small_grid.
+int tune_small_patches(DevPrecond& pc, const double* r, double* z, cudaStream_t s, int reps) {
+  pc.small_grid = 0;
+  if (pc.n_big >= pc.n_patches) return 0;
+  const int W = pc.ldg_warps;
+  const void* fn = W == 4 ? (const void*)patch_warp_loop_kernel<4> : (const void*)patch_warp_loop_kernel<8>;
+  const size_t sm = 4 * sizeof(double) * kSmallPatch * W;
+  int dev = 0, sms = 148, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, W * 32, sm) != cudaSuccess || per_sm < 1) {
+    cudaGetLastError();
+    return 0;
+  }
+  const int64_t needed = (pc.n_patches - pc.n_big + W - 1) / W;
+  const int grid = (int)std::min<int64_t>(needed, (int64_t)per_sm * sms);
+  cudaEvent_t e0, e1;
+  if (cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess) return -1;
+  float t[2] = {0.f, 0.f};
+  for (int mode = 0; mode < 2; ++mode) {
+    pc.small_grid = mode ? grid : 0;
+    launch_precond_part(1, pc, r, z, nullptr, nullptr, s);
+    cudaEventRecord(e0, s);
+    for (int k = 0; k < reps; ++k) launch_precond_part(1, pc, r, z, nullptr, nullptr, s);
+    cudaEventRecord(e1, s);
+    cudaEventSynchronize(e1);
+    cudaEventElapsedTime(&t[mode], e0, e1);
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  pc.small_grid = t[1] < t[0] ? grid : 0;
+  return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
 int tune_apply(DevOperator& op, const double* x, double* y, cudaStream_t s, int reps) {
   const int cnt = apply_variant_count();
   cudaEvent_t e0, e1;

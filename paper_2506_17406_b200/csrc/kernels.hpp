@@ -62,6 +62,7 @@ struct DevPrecond {
   const uint8_t* pkind;         // 0 own numbering, 1 CG potential
   int32_t ldg_warps;            // warps per CTA of patch_ldg_kernel: 8, or 4 when most patches are small
   int64_t n_big;                // patch_ldg_kernel: patches [0, n_big) one per CTA, the rest (n <= 128) one per warp
+  int32_t small_grid;           // > 0: the small patches run as patch_warp_loop_kernel on this many resident CTAs
   int32_t npad_max;             // largest patch dimension rounded up to 32
   // H(curl) potential patches: CSR rows of G^T over the CG dofs [0, n_cg_iface) they use (R-A12)
   int64_t n_cg_iface;
@@ -116,6 +117,8 @@ bool fused_pcg_supported(const DevOperator& op);
 int apply_variant_count();
 int apply_configure_variant(DevOperator& op, int k);
 int tune_apply(DevOperator& op, const double* x, double* y, cudaStream_t s, int reps);
+// setup-time choice between the two small-patch kernels (r, z: device scratch of length n_total)
+int tune_small_patches(DevPrecond& pc, const double* r, double* z, cudaStream_t s, int reps);
 cudaError_t launch_pcg_fused_apply(const DevOperator& op, PcgScalars* sc, const double* z, double* p0, double* p1,
                                    double* q, cudaStream_t s);
 cudaError_t launch_pcg_update_jacobi(PcgScalars* sc, const DevPrecond& pc, const double* p0, const double* p1,

@@ -553,6 +553,7 @@ static int setup_impl(rdr_handle* h, const double* vertices, int64_t nv, const i
   // here, outside any later stream capture
   CK(cudaMemset(h->d_p, 0, vb));
   if (tune_apply(op, h->d_p, h->d_q, 0, 3)) return RDR_ECUDA;  // the fastest warp layout on this operator
+  if (tune_small_patches(pc, h->d_p, h->d_z, 0, 3)) return RDR_ECUDA;
   CK(launch_apply(op, h->d_p, h->d_q, nullptr, nullptr, 0));
   if (hybrid)
     CK(launch_precond_hybrid(op, pc, h->d_p, h->d_z, nullptr, 0));
@@ -579,6 +580,7 @@ static int setup_impl(rdr_handle* h, const double* vertices, int64_t nv, const i
   in.apply_variant = op.av;
   in.apply_grid = op.apply_grid;
   in.apply_slots = op.apply_slots;
+  in.small_patch_grid = pc.small_grid;
   in.patch_setup_flops = 0;
   for (int32_t n : P.n) {  // lower tiles I >= J, I, J != K: nb(nb-1)/2 per K; panel: nb-1 per K
     const double nb = (n + 63) / 64;
@@ -1032,6 +1034,27 @@ int rdr_debug_set_apply_variant(rdr_handle* h, int variant) {
   h->info.apply_variant = t.av;
   h->info.apply_grid = t.apply_grid;
   h->info.apply_slots = t.apply_slots;
+  return RDR_OK;
+}
+
+int rdr_debug_set_small_patch_kernel(rdr_handle* h, int persistent) {
+  if (!h || h->pc.n_big >= h->pc.n_patches || (persistent != 0 && persistent != 1)) return RDR_EINVAL;
+  if (!persistent) {
+    h->pc.small_grid = 0;
+  } else {
+    DevPrecond t = h->pc;
+    // reuse the tuner's occupancy-based grid: time nothing, take the persistent grid
+    const int W = t.ldg_warps;
+    int dev = 0, sms = 148;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const int64_t needed = (t.n_patches - t.n_big + W - 1) / W;
+    h->pc.small_grid = (int)std::min<int64_t>(needed, (int64_t)sms * (24 / W));
+  }
+  if (h->graph) cudaGraphExecDestroy(h->graph);
+  if (h->wgraph) cudaGraphExecDestroy(h->wgraph);
+  h->graph = h->wgraph = nullptr;  // captured with the old launch configuration
+  h->info.small_patch_grid = h->pc.small_grid;
   return RDR_OK;
 }
 

@@ -47,7 +47,8 @@ class Info(ctypes.Structure):
                 ("refelem_seconds", ctypes.c_double), ("patch_setup_seconds", ctypes.c_double),
                 ("patch_kernel_seconds", ctypes.c_double), ("patch_setup_flops", ctypes.c_double),
                 ("apply_variant", ctypes.c_int32), ("apply_grid", ctypes.c_int32),
-                ("persistent_loop", ctypes.c_int32), ("apply_slots", ctypes.c_int32)]
+                ("persistent_loop", ctypes.c_int32), ("apply_slots", ctypes.c_int32),
+                ("small_patch_grid", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -77,6 +78,7 @@ def _load():
         "rdr_measure_fp64_peak": (ctypes.c_int, [ctypes.POINTER(D), P]),
         "rdr_debug_fused_apply": (ctypes.c_int, [P, P, P, P]),
         "rdr_debug_set_apply_variant": (ctypes.c_int, [P, ctypes.c_int]),
+        "rdr_debug_set_small_patch_kernel": (ctypes.c_int, [P, ctypes.c_int]),
         "rdr_destroy": (None, [P]),
         "rdr_strerror": (ctypes.c_char_p, [ctypes.c_int]),
         "rdr_reference_matrices": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, P, ctypes.POINTER(I32),
@@ -251,6 +253,11 @@ class Solver:
     def set_apply_variant(self, variant: int) -> bool:
         """Debugging: force the apply's warp layout; False if it does not fit this operator."""
         return _lib.rdr_debug_set_apply_variant(self._h, int(variant)) == RDR_OK
+
+    def set_small_patch_kernel(self, persistent: bool) -> bool:
+        """Debugging: force the small-patch kernel (one warp per patch, or resident warps
+        walking the patches); False if the configuration has no small-patch launch."""
+        return _lib.rdr_debug_set_small_patch_kernel(self._h, int(bool(persistent))) == RDR_OK
 
     def last_launches(self) -> int:
         n = ctypes.c_int64()

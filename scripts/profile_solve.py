@@ -31,7 +31,8 @@ def main():
                           "standalone_ms": dict(zip(("apply", "jacobi", "patches", "pcg_apply"), alone.tolist())),
                           "apply_tflops_in_solve": info["flops_apply"] / ms[0] / 1e9,
                           "apply_tflops_standalone": info["flops_apply"] / alone[0] / 1e9,
-                          "apply_layout": {k: info[k] for k in ("apply_variant", "apply_slots", "apply_grid")}}),
+                          "apply_layout": {k: info[k] for k in ("apply_variant", "apply_slots", "apply_grid")},
+                          "small_patch_grid": info["small_patch_grid"]}),
               flush=True)
         S.close()
 

@@ -414,6 +414,34 @@ def test_every_apply_layout(torch_cuda, space, p):
     assert ran == 6  # every layout of this n_mat fits these small elements
 
 
+@pytest.mark.parametrize("p", [2, 4])
+def test_both_small_patch_kernels(torch_cuda, p):
+    """H(div) edge stars (all patches <= 128 dofs): one warp per patch and the
+    resident warps walking the patches with prefetch give the oracle's P^-1 r
+    and PCG iterations (rdr_debug_set_small_patch_kernel)."""
+    from paper_2506_17406_b200 import rdr
+    from oracle.solver import Oracle
+    torch = torch_cuda
+    # unit coefficients: with the 1e4 log-uniform contrast on this mesh the edge stars reach
+    # kappa ~ 1e5 and the stored inverses differ from the oracle's Cholesky solves by ~kappa eps
+    c = make_config(0, n=3, p=p, space=HDIV, perturb=True, bc="x0", coeffs="one")
+    S = rdr.Solver(c.vertices, c.tets, c.p, c.space, c.alpha, c.beta, c.mask, loop=rdr.LOOP_GRAPH)
+    O = Oracle(c.vertices, c.tets, c.p, c.space, c.alpha, c.beta, c.mask)
+    x = c.draw_vector(O.n_total)
+    za = O.precond(x)
+    b = c.draw_vector(O.n_total)
+    hist = []
+    _, ito, _ = O.solve(b, rtol=1e-8, history=hist)
+    for persistent in (False, True):
+        assert S.set_small_patch_kernel(persistent)
+        assert rel(S.precond(torch.from_numpy(x).cuda()).cpu().numpy(), za) <= TOL
+        _, it = S.solve(torch.from_numpy(b).cuda(), rtol=1e-8)
+        _check_iters(S, it, ito, lambda k: hist[k - 1] if 0 < k <= len(hist) else None)
+    c2 = make_config(0, n=2, p=6, space=HGRAD, bc="all")  # 431-dof vertex stars: no small-patch launch
+    S2 = rdr.Solver(c2.vertices, c2.tets, c2.p, c2.space, c2.alpha, c2.beta, c2.mask)
+    assert not S2.set_small_patch_kernel(True)
+
+
 def test_stream_semantics_and_repeated_setup(torch_cuda):
     """apply / precond are asynchronous on the caller's stream (results visible
     after a sync on that stream only); setup/destroy can be repeated; a handle

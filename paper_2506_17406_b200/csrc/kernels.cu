@@ -49,8 +49,14 @@ cudaError_t launch_k(void (*kernel)(Params...), dim3 grid, dim3 block, size_t sm
   return launch_kx(true, kernel, grid, block, smem, s, args...);
 }
 
+// The PCG stop flag, read once the previous kernel's writes are visible (after
+// griddepcontrol.wait): a relaxed GPU-scope load (a volatile read compiles to a
+// system-scope LDG.STRONG.SYS, which every thread of a large grid then pays).
 __device__ __forceinline__ bool stopped(const PcgScalars* g) {
-  return g != nullptr && *((volatile const int32_t*)&g->done) != 0;
+  if (g == nullptr) return false;
+  int v;
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(&g->done) : "memory");
+  return v != 0;
 }
 
 // Programmatic dependent launch (PDL): a kernel launched with the programmatic
@@ -285,11 +291,18 @@ __global__ void __launch_bounds__((apply_mma_warps(BM, NQ, KS) + 1) * 32, MINB)
     double beta = 0.0;
     const double* p_old = nullptr;
     double* p_new = nullptr;
-    if (PCG) {
-      volatile PcgScalars* v = sc;
-      kit = v->k;
-      const double rz_old = v->rz_old;  // 0 only before the first direction (or in a timing loop)
-      beta = (kit == 0 || rz_old == 0.0) ? 0.0 : v->rz_acc / rz_old;
+    if (PCG) {  // the scalars once per CTA (shared), not one strong load per thread
+      __shared__ double s_beta;
+      __shared__ int s_kit;
+      if (threadIdx.x == 0) {
+        volatile PcgScalars* v = sc;
+        s_kit = v->k;
+        const double rz_old = v->rz_old;  // 0 only before the first direction (or in a timing loop)
+        s_beta = (s_kit == 0 || rz_old == 0.0) ? 0.0 : v->rz_acc / rz_old;
+      }
+      mma_bar_sync(NT);
+      kit = s_kit;
+      beta = s_beta;
       p_old = (kit & 1) ? pbuf0 : pbuf1;
       p_new = (kit & 1) ? pbuf1 : pbuf0;
     }
@@ -1269,10 +1282,20 @@ __global__ void pcg_update_jacobi_kernel(PcgScalars* sc, DevPrecond pc, const do
                                          const double* __restrict__ p1, double* __restrict__ q,
                                          double* __restrict__ x, double* __restrict__ r, double* __restrict__ z) {
   pdl_wait();
-  if (stopped(sc)) return;
-  const int kk = *((volatile int32_t*)&sc->k) - 1;  // iteration of the apply that just ran
+  // the scalars once per block (strong loads by every thread cost ~25 us on config 4)
+  __shared__ double s_alpha;
+  __shared__ int s_kk, s_stop;
+  if (threadIdx.x == 0) {
+    volatile const PcgScalars* v = sc;
+    s_stop = v->done;
+    s_kk = v->k - 1;  // iteration of the apply that just ran
+    s_alpha = s_stop ? 0.0 : v->rz_old / v->pq2[s_kk & 1];
+  }
+  __syncthreads();
+  if (s_stop) return;
+  const int kk = s_kk;
   const double* __restrict__ p = (kk & 1) ? p1 : p0;
-  const double alpha = sc->rz_old / sc->pq2[kk & 1];
+  const double alpha = s_alpha;
   double part = 0;
   // two dofs per thread with 16-byte accesses (the slab vectors are 256-byte aligned)
   const int64_t n2 = pc.n_total >> 1, stride = (int64_t)gridDim.x * blockDim.x;
@@ -1666,7 +1689,10 @@ bool fused_pcg_supported(const DevOperator& op) { return op.Bsw && op.own; }
 
 // Variant k's cell tiles and persistent grid for this operator (occupancy from
 // the PCG instance's registers and shared memory); -1 if it cannot run.
-int apply_configure_variant(DevOperator& op, int k) {
+// Variant k with ring mode `ring`: 0 the default rule below, 1 the deepest ring
+// that still fits two CTAs per SM (at least KS + 1 chunks), 2 the deepest ring
+// for one CTA per SM (the setup autotuner tries all three).
+int apply_configure_variant_ring(DevOperator& op, int k, int ring) {
   int cnt = 0;
   const ApplyVariant* vs = apply_variants(&cnt);
   if (k < 0 || k >= cnt || vs[k].nm != op.n_mat) return -1;
@@ -1686,10 +1712,16 @@ int apply_configure_variant(DevOperator& op, int k) {
   const size_t two_per_sm = 228 * 1024 / 2 - 1024;
   const int s_max = 4 * v.ks;
   int S = 0;
-  if (regs_occ >= 2 && base + chunk * 2 * v.ks <= two_per_sm)
+  if (ring == 1) {
+    if (regs_occ >= 2 && base + chunk * (v.ks + 1) <= two_per_sm)
+      S = (int)std::min<size_t>(s_max, (two_per_sm - base) / chunk);
+  } else if (ring == 2) {
+    if (base + chunk * (v.ks + 2) <= kMaxSmem) S = (int)std::min<size_t>(s_max, (kMaxSmem - base) / chunk);
+  } else if (regs_occ >= 2 && base + chunk * 2 * v.ks <= two_per_sm) {
     S = (int)std::min<size_t>(s_max, (two_per_sm - base) / chunk);
-  else if (base + chunk * (v.ks + 2) <= kMaxSmem)
+  } else if (base + chunk * (v.ks + 2) <= kMaxSmem) {
     S = (int)std::min<size_t>(s_max, (kMaxSmem - base) / chunk);
+  }
   if (S == 0) return -1;
   op.apply_slots = S;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, v.fn[1], apply_threads(v), apply_variant_smem(v, op)) !=
@@ -1704,6 +1736,8 @@ int apply_configure_variant(DevOperator& op, int k) {
   op.apply_grid = (int)std::max<int64_t>(1, std::min<int64_t>(units, (int64_t)per_sm * sms));
   return 0;
 }
+
+int apply_configure_variant(DevOperator& op, int k) { return apply_configure_variant_ring(op, k, 0); }
 
 int apply_variant_count() {
   int cnt = 0;
@@ -1759,9 +1793,14 @@ int tune_apply(DevOperator& op, const double* x, double* y, cudaStream_t s, int 
   int best = -1;
   float best_ms = 0.f;
   DevOperator best_op = op;
-  for (int k = 0; k < cnt; ++k) {
+  for (int kr = 0; kr < 3 * cnt; ++kr) {
+    const int k = kr / 3, ring = kr % 3;
     DevOperator t = op;
-    if (apply_configure_variant(t, k)) continue;
+    if (apply_configure_variant_ring(t, k, ring)) continue;
+    if (ring > 0) {  // skip ring modes that give the default's depth
+      DevOperator d = op;
+      if (!apply_configure_variant_ring(d, k, 0) && d.apply_slots == t.apply_slots) continue;
+    }
     // the persistent grid (resident CTAs, each a contiguous range of units), and
     // for problems with fewer units than twice that, one CTA per unit (waves)
     const int64_t units = (int64_t)t.ntiles * t.ngroups;

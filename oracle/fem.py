@@ -76,35 +76,52 @@ class Assembler:
         E = np.transpose(x[:, 1:] - x[:, :1], (0, 2, 1))       # columns x_k - x_0
         return E @ self.Ehat_inv                              # J with F(V-hat_k) = x_k
 
+    def _weighted(self, which):
+        """sqrt(w_q) R[q, n, :] of the tabulated values ("val") or derivatives
+        ("der"), stored [n, q, b] (b = the reference frame components) so that
+        the physical quantities below come out as [cells, n, q*3] rows."""
+        key = "_w_" + which
+        if not hasattr(self, key):
+            R = getattr(self, which)
+            sw = np.sqrt(self.w)
+            Rw = R * (sw[:, None, None] if R.ndim == 3 else sw[:, None])
+            setattr(self, key, np.ascontiguousarray(np.swapaxes(Rw, 0, 1)))
+        return getattr(self, key)
+
+    @staticmethod
+    def _gram_phys(Jm, Rw, det=None):
+        """sum_q w_q F_c(x_q)_i . F_c(x_q)_j for F_c = Jm_c R(x_q) (/ det_c): the
+        physical vector field of every basis function at every quadrature point
+        of cell c, contracted over points and Cartesian components."""
+        nc, n, nq = Jm.shape[0], Rw.shape[0], Rw.shape[1]
+        F = np.matmul(Rw.reshape(1, n * nq, 3), np.transpose(Jm, (0, 2, 1)))  # [c, n*q, a]
+        F = F.reshape(nc, n, nq * 3)
+        if det is not None:
+            F /= det[:, None, None]
+        return F @ np.transpose(F, (0, 2, 1))
+
     def element_matrices(self, cells, alpha, beta):
-        """[nc, n, n] element matrices of a^k on the given cells."""
+        """[nc, n, n] element matrices of a^k on the given cells, by quadrature
+        of the physical basis functions (R-A10): the pulled-back values at the
+        quadrature points (J^-T grad for 0-forms, J^-T phi / J curl / det for
+        1-forms, J phi / det and div / det for 2-forms), weighted sums over points."""
         J = self.jacobians(cells)
         det = np.linalg.det(J)
         vol = np.abs(det) * self.vol_hat
-        wq = self.w
-        sw = np.sqrt(wq)
-
-        def gram(F):  # sum_q w_q F[c,q,i,:].F[c,q,j,:] as a batched matmul
-            G = np.transpose(F * sw[None, :, None, None], (0, 2, 1, 3)).reshape(F.shape[0], F.shape[2], -1)
-            return G @ np.transpose(G, (0, 2, 1))
-
         if self.space == "hgrad":
             Jit = np.linalg.inv(np.transpose(J, (0, 2, 1)))   # J^-T
-            g = np.einsum("cab,qnb->cqna", Jit, self.der)     # physical gradients
-            Mm = np.einsum("q,qi,qj->ij", wq, self.val, self.val)
-            Kk = gram(g)
+            Vw = self._weighted("val")                       # [n, q]
+            Mm = Vw @ Vw.T
+            Kk = self._gram_phys(Jit, self._weighted("der"))  # physical gradients
             return vol[:, None, None] * (beta[:, None, None] * Mm[None] + alpha[:, None, None] * Kk)
         if self.space == "hdiv":  # 2-forms: phi = J phi-hat / det J, div phi = div-hat phi-hat / det J
-            ph = np.einsum("cab,qnb->cqna", J, self.val) / det[:, None, None, None]
-            dv = self.der[None] / det[:, None, None]
-            Mm = gram(ph)
-            Kk = np.einsum("q,cqi,cqj->cij", wq, dv, dv)
+            Mm = self._gram_phys(J, self._weighted("val"), det)
+            Dw = self._weighted("der")[None] / det[:, None, None]  # [c, n, q]
+            Kk = Dw @ np.transpose(Dw, (0, 2, 1))
             return vol[:, None, None] * (beta[:, None, None] * Mm + alpha[:, None, None] * Kk)
         Jit = np.linalg.inv(np.transpose(J, (0, 2, 1)))
-        ph = np.einsum("cab,qnb->cqna", Jit, self.val)
-        cu = np.einsum("cab,qnb->cqna", J, self.der) / det[:, None, None, None]
-        Mm = gram(ph)
-        Kk = gram(cu)
+        Mm = self._gram_phys(Jit, self._weighted("val"))
+        Kk = self._gram_phys(J, self._weighted("der"), det)
         return vol[:, None, None] * (beta[:, None, None] * Mm + alpha[:, None, None] * Kk)
 
     def assemble(self, alpha, beta, chunk: int = 256):

@@ -31,7 +31,7 @@ from functools import lru_cache
 
 import numpy as np
 
-from .xprec import LD, eigh_ld, inv_ld, qr_pos_ld
+from .xprec import LD, eigh_ld, inv_ld, mm_ld, qr_pos_ld
 from .simplex import (Simplex, canonical, reference_tet, multi_indices, mi_lookup,
                       TET_EDGES, TET_FACES, trace0, trace1, trace2, pairs)
 
@@ -115,26 +115,26 @@ def bubble_eigen(S: Simplex, kind: str, Fspan, q: int, dim_bubble: int, n_kernel
     renormalise to Eq. 3.8, canonicalize (R-A5, R-A6)."""
     if kind == "cg":
         M = S.mass0(Fspan, q, Fspan, q)
-        dF = Fspan @ S.grad_op(q)
+        dF = mm_ld(Fspan, S.grad_op(q))
         K = S.mass1(dF, q - 1, dF, q - 1)
     elif kind == "ned":
         M = S.mass1(Fspan, q, Fspan, q)
-        dF = Fspan @ S.curl_op(q)
+        dF = mm_ld(Fspan, S.curl_op(q))
         K = S.mass2(dF, q - 1, dF, q - 1)
     else:  # "rt": 2-forms on T-hat, d = div (Eq. 3.17, P:825-830)
         M = S.mass2(Fspan, q, Fspan, q)
-        dF = Fspan @ S.div_op(q)
+        dF = mm_ld(Fspan, S.div_op(q))
         K = S.mass0(dF, q - 1, dF, q - 1)
     s, U = eigh_ld(M)
     keep = s > LD(1e-13) * s.max()
     assert int(keep.sum()) == dim_bubble, (kind, S.l, int(keep.sum()), dim_bubble)
     D = U[:, keep] / np.sqrt(s[keep])[None, :]
-    Kp = D.T @ K @ D
+    Kp = mm_ld(mm_ld(D.T, K), D)
     mu, Y = eigh_ld(Kp)
     nz = mu > LD(ZERO_MODE_TOL) * mu.max()
     assert int((~nz).sum()) == n_kernel, (kind, S.l, int((~nz).sum()), n_kernel)
     mu = mu[nz]
-    Fhat = (D @ Y[:, nz]).T @ Fspan          # M-orthonormal psi-hat
+    Fhat = mm_ld(mm_ld(D, Y[:, nz]).T, Fspan)         # M-orthonormal psi-hat
     F = Fhat / np.sqrt(mu)[:, None]          # Eq. 3.8 normalisation
     gaps = [(mu[k + 1] - mu[k]) / mu[k + 1] for k in range(len(mu) - 1)
             if (mu[k + 1] - mu[k]) > CLUSTER_TOL * mu[k + 1]]
@@ -273,8 +273,8 @@ def cg_element(p: int) -> RefElement:
                 continue
             Sc = canonical(dim) if dim < 3 else T
             tr = trace0(B, p, 4, s) if dim < 3 else B
-            g_psi = eb.F @ Sc.grad_op(p)
-            g_v = tr @ Sc.grad_op(p)
+            g_psi = mm_ld(eb.F, Sc.grad_op(p))
+            g_v = mm_ld(tr, Sc.grad_op(p))
             Vs = Sc.mass1(g_psi, p - 1, g_v, p - 1)
             for j in range(len(eb.lam)):
                 rows.append(Vs[j])
@@ -322,15 +322,15 @@ def ned_element(p: int) -> RefElement:
             else:
                 Psi = ned_bubbles(dim, p)
                 if len(Psi.lam):
-                    cP = Psi.F @ Sc.curl_op(p)
-                    cv = tr @ Sc.curl_op(p)
+                    cP = mm_ld(Psi.F, Sc.curl_op(p))
+                    cv = mm_ld(tr, Sc.curl_op(p))
                     Vs = Sc.mass2(cP, p - 1, cv, p - 1)
                     for j in range(len(Psi.lam)):
                         rows.append(Vs[j])
                         ents.append((dim, ei, j, "I"))
             psi = cg_bubbles(dim, p)
             if len(psi.lam):
-                g_psi = psi.F @ Sc.grad_op(p)
+                g_psi = mm_ld(psi.F, Sc.grad_op(p))
                 Vs = Sc.mass1(g_psi, p - 1, tr, p)
                 for j in range(len(psi.lam)):
                     rows.append(Vs[j])
@@ -379,7 +379,7 @@ def rt_element(p: int) -> RefElement:
     Sc = canonical(2)
     u = face_unit_form(Sc)
     PsiF = ned_bubbles(2, p)
-    cPsiF = PsiF.F @ Sc.curl_op(p) if len(PsiF.lam) else None
+    cPsiF = mm_ld(PsiF.F, Sc.curl_op(p)) if len(PsiF.lam) else None
     for ei, s in enumerate(TET_FACES):
         tr = trace2(Fb, p, 4, s)
         rows.append(Sc.mass2(u, 0, tr, p)[0])
@@ -391,13 +391,13 @@ def rt_element(p: int) -> RefElement:
                 ents.append((2, ei, j, "II"))
     Phi = rt_bubbles(p)
     if len(Phi.lam):
-        Vs = T.mass0(Phi.F @ T.div_op(p), p - 1, Fb @ T.div_op(p), p - 1)
+        Vs = T.mass0(mm_ld(Phi.F, T.div_op(p)), p - 1, mm_ld(Fb, T.div_op(p)), p - 1)
         for j in range(len(Phi.lam)):
             rows.append(Vs[j])
             ents.append((3, 0, j, "I"))
     PsiC = ned_bubbles(3, p)
     if len(PsiC.lam):
-        Vs = T.mass2(PsiC.F @ T.curl_op(p), p - 1, Fb, p)
+        Vs = T.mass2(mm_ld(PsiC.F, T.curl_op(p)), p - 1, Fb, p)
         for j in range(len(PsiC.lam)):
             rows.append(Vs[j])
             ents.append((3, 0, j, "II"))
@@ -418,15 +418,15 @@ def tabulate(el: RefElement, bary):
     hgrad: (phi [npts,n], grad [npts,n,3]); hcurl: (phi [npts,n,3], curl [npts,n,3])."""
     T, p = el.T, el.p
     if el.space == "hgrad":
-        Phi = el.C.T @ el.span  # rows = phi_j in monomial coefficients
+        Phi = mm_ld(el.C.T, el.span)  # rows = phi_j in monomial coefficients
         val = T.eval0(Phi, p, bary)
-        der = T.eval1(Phi @ T.grad_op(p), p - 1, bary)
+        der = T.eval1(mm_ld(Phi, T.grad_op(p)), p - 1, bary)
         return val, der
-    Phi = el.C.T @ el.span
+    Phi = mm_ld(el.C.T, el.span)
     if el.space == "hdiv":  # (phi [npts,n,3] 2-form proxies, div [npts,n])
-        return T.eval2(Phi, p, bary), T.eval0(Phi @ T.div_op(p), p - 1, bary)
+        return T.eval2(Phi, p, bary), T.eval0(mm_ld(Phi, T.div_op(p)), p - 1, bary)
     val = T.eval1(Phi, p, bary)
-    der = T.eval2(Phi @ T.curl_op(p), p - 1, bary)
+    der = T.eval2(mm_ld(Phi, T.curl_op(p)), p - 1, bary)
     return val, der
 
 
@@ -437,31 +437,31 @@ def reference_matrices(el: RefElement):
     hdiv: M [3,3,n,n] of the 2-form proxies; K [n,n] with divergences."""
     T, p, C = el.T, el.p, el.C
     if el.space == "hgrad":
-        Mh = C.T @ T.mass0(el.span, p, el.span, p) @ C
-        G = el.span @ T.grad_op(p)
+        Mh = mm_ld(mm_ld(C.T, T.mass0(el.span, p, el.span, p)), C)
+        G = mm_ld(el.span, T.grad_op(p))
         Np1 = len(multi_indices(4, p - 1))
         Gr = G.reshape(el.n, Np1, 4)
-        Dc = [C.T @ (Gr @ T.g[:, a]) for a in range(3)]
+        Dc = [mm_ld(C.T, Gr @ T.g[:, a]) for a in range(3)]
         I1 = T.I(p - 1, p - 1)
-        K = np.array([[Dc[a] @ I1 @ Dc[b].T for b in range(3)] for a in range(3)])
+        K = np.array([[mm_ld(mm_ld(Dc[a], I1), Dc[b].T) for b in range(3)] for a in range(3)])
         return Mh, K
     Np = len(multi_indices(4, p))
     if el.space == "hdiv":  # M^{ab}_ij = int phi_i,a phi_j,b (2-form proxies), K_ij = int div phi_i div phi_j
         cr = np.array([np.cross(T.g[a], T.g[b]) for a, b in T.pairs], dtype=LD)
         Pr = el.span.reshape(el.n, Np, len(T.pairs))
-        Pc = [C.T @ (Pr @ cr[:, a]) for a in range(3)]
+        Pc = [mm_ld(C.T, Pr @ cr[:, a]) for a in range(3)]
         Ip = T.I(p, p)
-        M = np.array([[Pc[a] @ Ip @ Pc[b].T for b in range(3)] for a in range(3)])
-        Dv = C.T @ (el.span @ T.div_op(p))
-        return M, Dv @ T.I(p - 1, p - 1) @ Dv.T
+        M = np.array([[mm_ld(mm_ld(Pc[a], Ip), Pc[b].T) for b in range(3)] for a in range(3)])
+        Dv = mm_ld(C.T, mm_ld(el.span, T.div_op(p)))
+        return M, mm_ld(mm_ld(Dv, T.I(p - 1, p - 1)), Dv.T)
     Pr = el.span.reshape(el.n, Np, 4)
-    Pc = [C.T @ (Pr @ T.g[:, a]) for a in range(3)]
+    Pc = [mm_ld(C.T, Pr @ T.g[:, a]) for a in range(3)]
     Ip = T.I(p, p)
-    M = np.array([[Pc[a] @ Ip @ Pc[b].T for b in range(3)] for a in range(3)])
+    M = np.array([[mm_ld(mm_ld(Pc[a], Ip), Pc[b].T) for b in range(3)] for a in range(3)])
     cr = np.array([np.cross(T.g[a], T.g[b]) for a, b in T.pairs], dtype=LD)
     Np1 = len(multi_indices(4, p - 1))
-    Cf = (el.span @ T.curl_op(p)).reshape(el.n, Np1, len(T.pairs))
-    Rc = [C.T @ (Cf @ cr[:, a]) for a in range(3)]
+    Cf = mm_ld(el.span, T.curl_op(p)).reshape(el.n, Np1, len(T.pairs))
+    Rc = [mm_ld(C.T, Cf @ cr[:, a]) for a in range(3)]
     I1 = T.I(p - 1, p - 1)
-    K = np.array([[Rc[a] @ I1 @ Rc[b].T for b in range(3)] for a in range(3)])
+    K = np.array([[mm_ld(mm_ld(Rc[a], I1), Rc[b].T) for b in range(3)] for a in range(3)])
     return M, K

@@ -22,7 +22,7 @@ from functools import lru_cache
 
 import numpy as np
 
-from .xprec import LD, ld, inv_ld
+from .xprec import LD, ld, inv_ld, mm_ld
 
 
 @lru_cache(maxsize=None)
@@ -90,15 +90,15 @@ class Simplex:
         return num * (ld(math.factorial(self.l)) * self.vol / f[q1 + q2 + self.l])
 
     def mass0(self, F1, q1, F2, q2):
-        return F1 @ self.I(q1, q2) @ F2.T
+        return mm_ld(mm_ld(F1, self.I(q1, q2)), F2.T)
 
     def mass1(self, F1, q1, F2, q2):
         T = np.kron(self.I(q1, q2), self.G)
-        return F1 @ T @ F2.T
+        return mm_ld(mm_ld(F1, T), F2.T)
 
     def mass2(self, F1, q1, F2, q2):
         T = np.kron(self.I(q1, q2), self.H)
-        return F1 @ T @ F2.T
+        return mm_ld(mm_ld(F1, T), F2.T)
 
     # ---------------------------------------------------------------- operators
     def grad_op(self, q: int) -> np.ndarray:
@@ -208,13 +208,14 @@ class Simplex:
 
     def eval0(self, F, q, bary):
         """F [nf, N_q] -> values [npts, nf]."""
-        return self.monomials(bary, q) @ F.T
+        return mm_ld(self.monomials(bary, q), F.T)
 
     def eval1(self, F, q, bary):
-        """F [nf, N_q*nv] -> Cartesian vectors [npts, nf, dim]."""
+        """F [nf, N_q*nv] -> Cartesian vectors [npts, nf, dim]:
+        sum_a lambda^a(x) sum_m F[f, a, m] g_m (the 1-form's proxy)."""
         Mo = self.monomials(bary, q)
         Fr = F.reshape(F.shape[0], -1, self.nv)
-        return np.einsum("pa,fam,md->pfd", Mo, Fr, self.g)
+        return self._contract(Mo, Fr @ self.g.astype(LD))
 
     def eval2(self, F, q, bary):
         """F [nf, N_q*npairs] -> curl values: [npts, nf, 3] in 3D, [npts, nf] in 2D."""
@@ -222,11 +223,19 @@ class Simplex:
         Fr = F.reshape(F.shape[0], -1, len(self.pairs))
         if self.dim == 3:
             cr = np.array([np.cross(self.g[a].astype(LD), self.g[b].astype(LD)) for a, b in self.pairs], dtype=LD)
-            return np.einsum("pa,fak,kd->pfd", Mo, Fr, cr)
+            return self._contract(Mo, Fr @ cr)
         if self.dim == 2:
             cr = np.array([self.g[a][0] * self.g[b][1] - self.g[a][1] * self.g[b][0] for a, b in self.pairs], dtype=LD)
-            return np.einsum("pa,fak,k->pf", Mo, Fr, cr)
+            return self._contract(Mo, (Fr @ cr)[:, :, None])[:, :, 0]
         raise ValueError("no curl in 1D")
+
+    @staticmethod
+    def _contract(Mo, H):
+        """out[p, f, d] = sum_a Mo[p, a] H[f, a, d] (values of the monomial
+        expansion; the sum over the form's frame is already in H)."""
+        nf, na, nd = H.shape
+        Ht = np.ascontiguousarray(np.transpose(H, (1, 0, 2)).reshape(na, nf * nd))
+        return mm_ld(Mo, Ht).reshape(Mo.shape[0], nf, nd)
 
 
 def _det_ld(E):

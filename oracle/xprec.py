@@ -14,10 +14,65 @@ Pinned in tests/test_oracle_xprec.py against residuals and mpmath.
 """
 from __future__ import annotations
 
+import ctypes
+import os
+import subprocess
+
 import numpy as np
 from fractions import Fraction
 
 LD = np.longdouble
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LDGEMM_SO = os.path.join(_HERE, "_ldgemm.so")
+_ldgemm = None
+
+
+def build_ldgemm() -> str:
+    """Compile oracle/ldgemm.c (the long-double product, OpenMP over rows)."""
+    src = os.path.join(_HERE, "ldgemm.c")
+    tmp = _LDGEMM_SO + f".{os.getpid()}.tmp"
+    subprocess.run(["gcc", "-O2", "-fopenmp", "-fPIC", "-shared", "-o", tmp, src], check=True)
+    os.replace(tmp, _LDGEMM_SO)
+    return _LDGEMM_SO
+
+
+def _lib():
+    global _ldgemm
+    if _ldgemm is None:
+        src = os.path.join(_HERE, "ldgemm.c")
+        try:
+            if not os.path.exists(_LDGEMM_SO) or os.path.getmtime(_LDGEMM_SO) < os.path.getmtime(src):
+                build_ldgemm()
+            lib = ctypes.CDLL(_LDGEMM_SO)
+            lib.ld_gemm.argtypes = [ctypes.c_void_p] * 3 + [ctypes.c_int64] * 3
+            lib.ld_gemm.restype = None
+            _ldgemm = lib
+        except (OSError, subprocess.CalledProcessError):
+            _ldgemm = False  # no compiler: numpy's own (identical, slower) loop
+    return _ldgemm
+
+
+def mm_ld(A: np.ndarray, B: np.ndarray) -> np.ndarray:
+    """A @ B in longdouble, bitwise equal to numpy's non-BLAS matmul (k summed in
+    ascending order from 0), computed by oracle/ldgemm.c with the rows spread
+    over the host's cores (numpy's longdouble loop is single-threaded)."""
+    A = np.asarray(A, dtype=LD)
+    B = np.asarray(B, dtype=LD)
+    if A.ndim != 2 or B.ndim != 2:
+        return A @ B
+    m, k = A.shape
+    k2, n = B.shape
+    if k != k2:
+        raise ValueError(f"mm_ld: shapes {A.shape} {B.shape}")
+    lib = _lib()
+    if not lib or m * k * n < 32768:
+        return A @ B
+    A = np.ascontiguousarray(A)
+    B = np.ascontiguousarray(B)
+    C = np.empty((m, n), dtype=LD)
+    lib.ld_gemm(A.ctypes.data, B.ctypes.data, C.ctypes.data, m, k, n)
+    return C
 
 
 def ld(x) -> np.longdouble:
@@ -60,9 +115,9 @@ def eigh_ld(A: np.ndarray, iters: int = 4):
     X = X64.astype(LD)
     I = np.eye(n, dtype=LD)
     for _ in range(iters):
-        R = I - X.T @ X
+        R = I - mm_ld(X.T, X)
         R = (R + R.T) / 2
-        S = X.T @ A @ X
+        S = mm_ld(mm_ld(X.T, A), X)
         S = (S + S.T) / 2
         w = np.diag(S) / (1 - np.diag(R))
         scale = np.max(np.abs(w)) if n else LD(1)
@@ -71,9 +126,9 @@ def eigh_ld(A: np.ndarray, iters: int = 4):
         D = w[None, :] - w[:, None]  # D_ij = w_j - w_i
         big = np.abs(D) > delta
         E = np.where(big, (S + w[None, :] * R) / np.where(big, D, 1), R / 2)
-        X = X + X @ E
-    R = I - X.T @ X
-    S = X.T @ A @ X
+        X = X + mm_ld(X, E)
+    R = I - mm_ld(X.T, X)
+    S = mm_ld(mm_ld(X.T, A), X)
     w = np.diag(S) / (1 - np.diag(R))
     order = np.argsort(w.astype(np.float64), kind="stable")
     return w[order], X[:, order]

@@ -71,3 +71,22 @@ def test_ld_conversion_exact():
     assert ld(Fraction(1, 3)) == LD(1) / LD(3)
     big = 27 * 10 ** 25
     assert abs(float(ld(big) / LD("2.7e26") - 1)) < 1e-18
+
+
+def test_mm_ld_bitwise_equal_to_numpy_and_exact_on_integers():
+    """oracle/ldgemm.c (mm_ld) is numpy's non-BLAS longdouble matmul loop spread
+    over threads: bitwise equal on random operands (contiguous and transposed
+    views, ragged shapes), and exact on small-integer products (every partial
+    sum representable) against Python integers."""
+    from oracle.xprec import mm_ld
+    rng = np.random.default_rng(7)
+    for m, k, n in [(37, 53, 41), (64, 64, 64), (5, 300, 3), (130, 7, 90)]:
+        A = rng.standard_normal((m, k)).astype(LD) / LD(3)
+        B = rng.standard_normal((k, n)).astype(LD) / LD(7)
+        assert np.array_equal(mm_ld(A, B), A @ B)
+        At = np.ascontiguousarray(A.T)
+        assert np.array_equal(mm_ld(At.T, B), A @ B)
+    Ai = rng.integers(-1000, 1000, (40, 60))
+    Bi = rng.integers(-1000, 1000, (60, 50))
+    exact = np.array([[sum(int(Ai[i, l]) * int(Bi[l, j]) for l in range(60)) for j in range(50)] for i in range(40)])
+    assert np.array_equal(mm_ld(Ai.astype(LD), Bi.astype(LD)).astype(np.int64), exact)

@@ -659,6 +659,23 @@ __device__ __forceinline__ double treduce16(double (&v)[16], int lane) {
   treduce_stage<1>(v, lane);
   return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 16);
 }
+// The same reduction for a half tile held in lane-permuted order: position
+// 4 g' + j holds column 4 (g' ^ G) + j, G = (lane >> 2) & 3 (patch_ldg_kernel
+// loads its four 4-column groups in that order). Then at the 8- and
+// 4-exchanges every lane keeps its low positions and sends its high ones --
+// the partner (lane ^ 8, lane ^ 4) holds the matching columns there -- so 12 of
+// the 15 exchanges need no select (the stage-8 and stage-4 selects were most of
+// the kernel's instructions); lane l ends with column l & 15 as before.
+__device__ __forceinline__ double treduce16p(double (&v)[16], int lane) {
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < 8; ++k) v[k] += __shfl_xor_sync(0xffffffffu, v[k + 8], 8);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) v[k] += __shfl_xor_sync(0xffffffffu, v[k + 4], 4);
+  treduce_stage<2>(v, lane);
+  treduce_stage<1>(v, lane);
+  return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 16);
+}
 
 // One star patch solved by one warp (the lane = row half-tile stream of
 // patch_ldg_kernel without block barriers): z += E_m A_m^-1 E_m^T r for patch
@@ -960,12 +977,14 @@ __global__ void __launch_bounds__(kLdgWarps * 32, 32 / kLdgWarps)
   const double* T = pc.tiles + pc.tile_off[pid];
   const int ntiles = nb * (nb + 1) / 2;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int G4 = ((lane >> 2) & 3) << 2;  // lane-permuted column order (treduce16p)
   int I = 0, J = warp, h = 0, t = warp;
   while (J > I) {
     J -= I + 1;
     ++I;
   }
-  // half tile (I, J, h) -> a[16] (row `lane`; diagonal tiles: lower triangle only)
+  // half tile (I, J, h) -> a[16] (row `lane`; diagonal tiles: lower triangle only), position
+  // q holding column 16 h + (q ^ G4)
   auto load_half = [&](double(&a)[16]) {
     const int rows = min(32, n - 32 * I);
     const double* tb = T + 512LL * I * I + 16LL * I + (int64_t)J * 32 * rows;
@@ -974,7 +993,7 @@ __global__ void __launch_bounds__(kLdgWarps * 32, 32 / kLdgWarps)
         const double4* tp = reinterpret_cast<const double4*>(tb) + lane + 4 * h * rows;
 #pragma unroll
         for (int k4 = 0; k4 < 4; ++k4) {
-          const double4 v = ld_stream4(tp + k4 * rows);
+          const double4 v = ld_stream4(tp + (k4 ^ (G4 >> 2)) * rows);
           a[4 * k4] = v.x;
           a[4 * k4 + 1] = v.y;
           a[4 * k4 + 2] = v.z;
@@ -987,9 +1006,13 @@ __global__ void __launch_bounds__(kLdgWarps * 32, 32 / kLdgWarps)
     } else {
       // diagonal tile, lower triangle packed by columns: (i,k), k <= i at k*rows - k(k-1)/2 + i - k
 #pragma unroll
-      for (int q = 0; q < 16; ++q) {
-        const int k = 16 * h + q;
-        a[q] = (k <= lane && lane < rows) ? ld_stream1(tb + k * rows - k * (k - 1) / 2 + (lane - k)) : 0.0;
+      for (int g = 0; g < 4; ++g) {
+        const int c0 = 16 * h + ((4 * g) ^ G4);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int k = c0 + j;
+          a[4 * g + j] = (k <= lane && lane < rows) ? ld_stream1(tb + k * rows - k * (k - 1) / 2 + (lane - k)) : 0.0;
+        }
       }
     }
   };
@@ -1005,17 +1028,27 @@ __global__ void __launch_bounds__(kLdgWarps * 32, 32 / kLdgWarps)
     if (J < I) {
       const double* rJ = rl + J * 32 + 16 * h;
 #pragma unroll
-      for (int q = 0; q < 16; ++q) row = fma(a[q], rJ[q], row);
+      for (int g = 0; g < 4; ++g) {
+        const double* rg = rJ + ((4 * g) ^ G4);  // the group's columns (4-aligned: ^ == +)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) row = fma(a[4 * g + j], rg[j], row);
+      }
 #pragma unroll
       for (int q = 0; q < 16; ++q) a[q] *= ri;
     } else {
       const double* rI = rl + I * 32 + 16 * h;
 #pragma unroll
-      for (int q = 0; q < 16; ++q) row = fma(a[q], rI[q], row);
+      for (int g = 0; g < 4; ++g) {
+        const int c0 = (4 * g) ^ G4;
+        const double* rg = rI + c0;
 #pragma unroll
-      for (int q = 0; q < 16; ++q) a[q] = (16 * h + q < lane) ? a[q] * ri : 0.0;  // strict lower, transposed
+        for (int j = 0; j < 4; ++j) row = fma(a[4 * g + j], rg[j], row);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)  // strict lower, transposed
+          a[4 * g + j] = (16 * h + c0 + j < lane) ? a[4 * g + j] * ri : 0.0;
+      }
     }
-    const double col = treduce16(a, lane);
+    const double col = treduce16p(a, lane);
     if (lane < 16) atomicAdd(zl + J * 32 + 16 * h + lane, col);
     if (h == 1) {  // tile done: this warp's next tile; row products flushed when the block row changes
       h = 0;

@@ -7,6 +7,7 @@
 #   gpurun_out/TAG_<cfg>_<kernel>_src.txt  hottest SASS lines (scripts/ncu_summary.py source)
 #   gpurun_out/TAG_traffic.json         dram bytes per launch (scripts/ncu_summary.py traffic)
 #   bash scripts/ncu_evidence.sh TAG 3 4 5:12 2 6 7:10
+#   KERNELS=patch bash scripts/ncu_evidence.sh TAG 3   (a subset of the kernels)
 TAG=$1; shift
 mkdir -p gpurun_out
 for spec in "$@"; do
@@ -15,7 +16,7 @@ for spec in "$@"; do
   run="python scripts/prof_kernels.py $cfg $p 4 --mode solve"
   $run > gpurun_out/${TAG}_${name}_plain.log 2>&1 || { echo "$name: plain run failed"; continue; }
   ncu_common="--set full --clock-control none --import-source on --kernel-name-base demangled"
-  for k in apply patch update; do
+  for k in ${KERNELS:-apply patch update}; do
     case $k in
       apply) sel='-k regex:apply_tc_kernel.*bool\)1 -s 1 -c 1' ;;
       patch) sel='-k regex:patch_(ldg|warp)_kernel -s 4 -c 2' ;;

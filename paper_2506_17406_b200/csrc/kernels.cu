@@ -15,6 +15,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdlib>
+#include <vector>
 
 #include "kernels.hpp"
 
@@ -1819,13 +1820,20 @@ int tune_small_patches(DevPrecond& pc, const double* r, double* z, cudaStream_t 
   return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
-int tune_apply(DevOperator& op, const double* x, double* y, cudaStream_t s, int reps) {
+// Setup-time autotuning of the apply's warp layout. Every (layout, ring depth,
+// grid) candidate that fits is timed on the kernel the solve runs -- the
+// PCG-mode apply (sc: scalars with rtol 0 and a huge maxit, so the stopping
+// test never fires; x != 0; p0, p1: scratch direction buffers), or the plain
+// apply when the operator has no PCG mode -- in three interleaved rounds of
+// `reps` launches after a warm-up, each candidate scored by its best round.
+// (Timing each candidate once, back to back, let the clock drift right after
+// the patch-setup kernel pick a layout that ran the config-3 solve at 167
+// instead of 177 PCG it/s: profiles/round2/experiments/apply_layout_bench_ab.jsonl.)
+int tune_apply(DevOperator& op, const double* x, double* y, PcgScalars* sc, double* p0, double* p1, cudaStream_t s,
+               int reps) {
   const int cnt = apply_variant_count();
-  cudaEvent_t e0, e1;
-  if (cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess) return -1;
-  int best = -1;
-  float best_ms = 0.f;
-  DevOperator best_op = op;
+  const bool pcg = sc && fused_pcg_supported(op);
+  std::vector<DevOperator> cand;
   for (int kr = 0; kr < 3 * cnt; ++kr) {
     const int k = kr / 3, ring = kr % 3;
     DevOperator t = op;
@@ -1841,25 +1849,37 @@ int tune_apply(DevOperator& op, const double* x, double* y, cudaStream_t s, int 
     for (int gi = 0; gi < 2; ++gi) {
       if (grids[gi] <= 0 || (gi == 1 && grids[1] == grids[0])) continue;
       t.apply_grid = grids[gi];
-      if (launch_apply_tc<false>(t, x, y, nullptr, nullptr, s) != cudaSuccess) continue;
+      cand.push_back(t);
+    }
+  }
+  auto launch = [&](const DevOperator& t) {
+    return pcg ? launch_apply_tc<1>(t, x, y, nullptr, sc, s, sc, p0, p1) : launch_apply_tc<0>(t, x, y, nullptr, nullptr, s);
+  };
+  cudaEvent_t e0, e1;
+  if (cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess) return -1;
+  std::vector<float> best_ms(cand.size(), -1.f);
+  for (int round = 0; round < 3; ++round)
+    for (size_t c = 0; c < cand.size(); ++c) {
+      if (launch(cand[c]) != cudaSuccess) {
+        cudaGetLastError();
+        continue;
+      }
       cudaEventRecord(e0, s);
-      for (int r = 0; r < reps; ++r) launch_apply_tc<false>(t, x, y, nullptr, nullptr, s);
+      for (int r = 0; r < reps; ++r) launch(cand[c]);
       cudaEventRecord(e1, s);
       if (cudaEventSynchronize(e1) != cudaSuccess) continue;
       float ms = 0.f;
       cudaEventElapsedTime(&ms, e0, e1);
-      if (best < 0 || ms < best_ms) {
-        best = k;
-        best_ms = ms;
-        best_op = t;
-      }
+      if (best_ms[c] < 0.f || ms < best_ms[c]) best_ms[c] = ms;
     }
-  }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   cudaGetLastError();
+  int best = -1;
+  for (size_t c = 0; c < cand.size(); ++c)
+    if (best_ms[c] >= 0.f && (best < 0 || best_ms[c] < best_ms[best])) best = (int)c;
   if (best < 0) return -1;
-  op = best_op;
+  op = cand[best];
   return 0;
 }
 

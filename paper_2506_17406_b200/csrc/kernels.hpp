@@ -116,7 +116,8 @@ bool fused_pcg_supported(const DevOperator& op);
 // autotuning over all that fit (x, y: device scratch of length n_total)
 int apply_variant_count();
 int apply_configure_variant(DevOperator& op, int k);
-int tune_apply(DevOperator& op, const double* x, double* y, cudaStream_t s, int reps);
+int tune_apply(DevOperator& op, const double* x, double* y, PcgScalars* sc, double* p0, double* p1, cudaStream_t s,
+               int reps);
 // setup-time choice between the two small-patch kernels (r, z: device scratch of length n_total)
 int tune_small_patches(DevPrecond& pc, const double* r, double* z, cudaStream_t s, int reps);
 cudaError_t launch_pcg_fused_apply(const DevOperator& op, PcgScalars* sc, const double* z, double* p0, double* p1,

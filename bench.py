@@ -413,7 +413,10 @@ def run(args):
         "config": config_dict(cfg, c.p, ws),
         "problem": {"n_free": info["n_free"], "n_total": n, "n_cells": info["n_cells"], "n_loc": info["n_loc"],
                     "n_patches": info["n_patches"], "max_patch": info["max_patch"],
-                    "patch_bytes": info["patch_bytes"]},
+                    "patch_bytes": info["patch_bytes"],
+                    # the apply configuration setup's timing chose (profilers reproduce it with
+                    # scripts/prof_kernels.py --apply variant,slots,grid)
+                    "apply_layout": {k: info[k] for k in ("apply_variant", "apply_slots", "apply_grid")}},
         "iters_per_solve": float(np.mean(iters)), "nonconverged_solves": nonconv + e_nonconv,
         "ms_per_iter": ms_iter, "time_to_solution_ms": ms_local / args.steps,
         "iter_frac_t_roof": t_roof_ms(info, fp64_peak, hbm) / ms_iter,

@@ -245,6 +245,14 @@ const char* rdr_strerror(int code);
  * The GPU tests use it to check every layout against the oracle. */
 int rdr_debug_set_apply_variant(rdr_handle* h, int variant);
 
+/* Debugging entry point: the apply's warp layout `variant` with a ring of
+ * `slots` reference-stack chunks and a grid of `grid` CTAs (0: the persistent
+ * grid of resident CTAs) -- the three values rdr_info reports as apply_variant,
+ * apply_slots and apply_grid -- so that a profiler run can reproduce the
+ * configuration another setup's timing chose (scripts/prof_kernels.py --apply).
+ * RDR_EINVAL if it does not fit this operator. */
+int rdr_debug_set_apply_config(rdr_handle* h, int variant, int slots, int grid);
+
 /* Debugging entry point: run the small star patches (configurations whose
  * patches all have <= 128 dofs, e.g. the H(div) edge stars) with one warp per
  * patch (persistent = 0) or with resident warps that walk the patches and load

@@ -1773,6 +1773,31 @@ int apply_configure_variant_ring(DevOperator& op, int k, int ring) {
 
 int apply_configure_variant(DevOperator& op, int k) { return apply_configure_variant_ring(op, k, 0); }
 
+// Variant k with an explicit ring depth (slots >= KS + 1) and grid (0: the persistent grid of
+// resident CTAs), e.g. to reproduce the configuration another setup's timing chose.
+int apply_configure_exact(DevOperator& op, int k, int slots, int grid) {
+  DevOperator t = op;
+  if (apply_configure_variant_ring(t, k, 0)) return -1;
+  int cnt = 0;
+  const ApplyVariant& v = apply_variants(&cnt)[k];
+  if (slots < v.ks + 1 || apply_smem_layout(v.bm, v.nq, v.ks, slots, t.kp, t.n_mat).total > kMaxSmem) return -1;
+  t.apply_slots = slots;
+  int dev = 0, sms = 148, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, v.fn[1], apply_threads(v), apply_variant_smem(v, t)) !=
+          cudaSuccess ||
+      per_sm < 1) {
+    cudaGetLastError();
+    return -1;
+  }
+  const int64_t units = (int64_t)t.ntiles * t.ngroups;
+  t.apply_grid = grid > 0 ? (int)std::min<int64_t>(grid, units)
+                          : (int)std::max<int64_t>(1, std::min<int64_t>(units, (int64_t)per_sm * sms));
+  op = t;
+  return 0;
+}
+
 int apply_variant_count() {
   int cnt = 0;
   apply_variants(&cnt);

@@ -116,6 +116,7 @@ bool fused_pcg_supported(const DevOperator& op);
 // autotuning over all that fit (x, y: device scratch of length n_total)
 int apply_variant_count();
 int apply_configure_variant(DevOperator& op, int k);
+int apply_configure_exact(DevOperator& op, int k, int slots, int grid);
 int tune_apply(DevOperator& op, const double* x, double* y, PcgScalars* sc, double* p0, double* p1, cudaStream_t s,
                int reps);
 // setup-time choice between the two small-patch kernels (r, z: device scratch of length n_total)

@@ -1047,6 +1047,20 @@ int rdr_debug_set_apply_variant(rdr_handle* h, int variant) {
   return RDR_OK;
 }
 
+int rdr_debug_set_apply_config(rdr_handle* h, int variant, int slots, int grid) {
+  if (!h) return RDR_EINVAL;
+  DevOperator t = h->op;
+  if (apply_configure_exact(t, variant, slots, grid)) return RDR_EINVAL;
+  h->op = t;
+  if (h->graph) cudaGraphExecDestroy(h->graph);
+  if (h->wgraph) cudaGraphExecDestroy(h->wgraph);
+  h->graph = h->wgraph = nullptr;  // captured with the old launch configuration
+  h->info.apply_variant = t.av;
+  h->info.apply_grid = t.apply_grid;
+  h->info.apply_slots = t.apply_slots;
+  return RDR_OK;
+}
+
 int rdr_debug_set_small_patch_kernel(rdr_handle* h, int persistent) {
   if (!h || h->pc.n_big >= h->pc.n_patches || (persistent != 0 && persistent != 1)) return RDR_EINVAL;
   if (!persistent) {

@@ -79,6 +79,7 @@ def _load():
         "rdr_debug_fused_apply": (ctypes.c_int, [P, P, P, P]),
         "rdr_debug_set_apply_variant": (ctypes.c_int, [P, ctypes.c_int]),
         "rdr_debug_set_small_patch_kernel": (ctypes.c_int, [P, ctypes.c_int]),
+        "rdr_debug_set_apply_config": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_int, ctypes.c_int]),
         "rdr_destroy": (None, [P]),
         "rdr_strerror": (ctypes.c_char_p, [ctypes.c_int]),
         "rdr_reference_matrices": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, P, ctypes.POINTER(I32),
@@ -253,6 +254,11 @@ class Solver:
     def set_apply_variant(self, variant: int) -> bool:
         """Debugging: force the apply's warp layout; False if it does not fit this operator."""
         return _lib.rdr_debug_set_apply_variant(self._h, int(variant)) == RDR_OK
+
+    def set_apply_config(self, variant: int, slots: int, grid: int = 0) -> bool:
+        """Debugging: force the apply's layout, ring depth and grid (rdr_info's
+        apply_variant, apply_slots, apply_grid); False if it does not fit."""
+        return _lib.rdr_debug_set_apply_config(self._h, int(variant), int(slots), int(grid)) == RDR_OK
 
     def set_small_patch_kernel(self, persistent: bool) -> bool:
         """Debugging: force the small-patch kernel (one warp per patch, or resident warps

@@ -414,6 +414,40 @@ def test_every_apply_layout(torch_cuda, space, p):
     assert ran == 6  # every layout of this n_mat fits these small elements
 
 
+def test_apply_ring_depths_and_grids(torch_cuda):
+    """The apply with explicit ring depths (the shallowest, KS + 1 chunks, to the
+    deepest that fits) and grids (resident CTAs, one CTA per unit, a single CTA
+    walking every unit) against the oracle, plain and in the fused PCG
+    (rdr_debug_set_apply_config: the configurations setup's timing can pick)."""
+    from paper_2506_17406_b200 import rdr
+    from oracle.solver import Oracle
+    torch = torch_cuda
+    c = make_config(0, n=2, p=7, space=HGRAD, perturb=True, bc="x0", coeffs="loguniform")
+    S = rdr.Solver(c.vertices, c.tets, c.p, c.space, c.alpha, c.beta, c.mask, loop=rdr.LOOP_GRAPH)
+    O = Oracle(c.vertices, c.tets, c.p, c.space, c.alpha, c.beta, c.mask)
+    x = c.draw_vector(O.n_total)
+    ya = O.apply(x)
+    b = c.draw_vector(O.n_total)
+    hist = []
+    _, ito, _ = O.solve(b, rtol=1e-8, history=hist)
+    ks = {0: 2, 2: 4, 6: 4}  # variant -> K-split groups: (32,4,2), (32,4,4), (16,4,4)
+    ran = 0
+    for v, kgroups in ks.items():
+        for slots in (kgroups + 1, 2 * kgroups, 16):
+            for grid in (0, 1, 7):
+                if not S.set_apply_config(v, slots, grid):
+                    continue
+                ran += 1
+                i = S.info
+                assert (i["apply_variant"], i["apply_slots"]) == (v, slots)
+                assert grid == 0 or i["apply_grid"] == grid
+                assert rel(S.apply(torch.from_numpy(x).cuda()).cpu().numpy(), ya) <= TOL, (v, slots, grid)
+                _, it = S.solve(torch.from_numpy(b).cuda(), rtol=1e-8)
+                _check_iters(S, it, ito, lambda kk: hist[kk - 1] if 0 < kk <= len(hist) else None)
+    assert ran >= 18
+    assert not S.set_apply_config(0, 2, 0)  # fewer chunks than K-split groups + 1
+
+
 @pytest.mark.parametrize("p", [2, 4])
 def test_both_small_patch_kernels(torch_cuda, p):
     """H(div) edge stars (all patches <= 128 dofs): one warp per patch and the

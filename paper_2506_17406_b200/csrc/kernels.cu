@@ -514,6 +514,310 @@ __global__ void __launch_bounds__((apply_mma_warps(BM, NQ, KS) + 1) * 32, MINB)
   }
 }
 
+// ---------------------------------------------------------------- factored apply (H(curl))
+// The reference matrices factor through L2-orthonormal bases of P_p (values) and
+// P_{p-1} (curls): M^{ab} = FaM FbM^T, K^{ab} = FaK FbK^T (refelem.cpp, RefElement::F).
+// The cell operator is y_e = F (Gm ⊗ I) F^T x_e on the value block plus the same with
+// Gk on the curl block, i.e. two GEMMs per cell tile with a per-cell 3 x 3 mix between:
+//   stage A (fact_stage_a_kernel): gather x_e (PCG mode: the direction update and
+//            ||z||^2 as in apply_tc_kernel), U = X F  (K = n_loc, N = nf) -> op.ubuf;
+//   stage B (fact_stage_b_kernel): V = mix(U) (and p.Ap = sum u.v), Y = V F^T
+//            (K = nf, N = n_loc), scatter-add.
+// 4 (n_loc + 3) (nf) flops per cell against 2 n_mat n_loc^2: 3.1x fewer for Ned1_6.
+// DMMA.8x8x4 with A from shared memory and B = F read through L1/L2 (op.F is
+// [kp][nfp], zero-padded, ~0.8 MB for Ned1_6). 8 warps, 16 cells per CTA, each warp
+// 16 cells x 32 columns per pass.
+constexpr int kFactBM = 16, kFactWarps = 8, kFactNQ = 4;
+constexpr int64_t kFactMinCells = 2048;
+
+struct FactSmem {
+  size_t x, eb, lut, own, total;
+};
+__host__ __device__ inline FactSmem fact_a_layout(int kp) {
+  FactSmem L;
+  L.x = 0;
+  L.eb = L.x + sizeof(double) * (size_t)kFactBM * apply_x_stride(kp);
+  L.lut = L.eb + sizeof(int32_t) * kFactBM * 16;
+  L.own = L.lut + sizeof(uint16_t) * (size_t)((kp + 3) & ~3);
+  L.total = L.own + sizeof(uint16_t) * kFactBM;
+  return L;
+}
+__host__ __device__ inline size_t fact_vs(int nfp) { return (size_t)nfp + 4; }  // V row stride (== 4 mod 16)
+__host__ __device__ inline FactSmem fact_b_layout(int kp, int nfp) {
+  FactSmem L;
+  L.x = 0;  // V [16][nfp + 4]
+  L.eb = L.x + sizeof(double) * (size_t)kFactBM * fact_vs(nfp);
+  L.lut = L.eb + sizeof(int32_t) * kFactBM * 16;
+  L.own = L.lut + sizeof(uint16_t) * (size_t)((kp + 3) & ~3);  // coefficients [16][12] doubles
+  L.total = L.own + sizeof(double) * kFactBM * 12;
+  return L;
+}
+
+template <bool PCG>
+__global__ void __launch_bounds__(kFactWarps * 32)
+    fact_stage_a_kernel(DevOperator op, const double* __restrict__ x, const PcgScalars* guard, PcgScalars* sc,
+                        double* pbuf0, double* pbuf1) {
+  extern __shared__ __align__(128) unsigned char fsm_raw[];
+  constexpr int NT = kFactWarps * 32;
+  const int n = op.n_loc, kp = op.kp, XS = apply_x_stride(kp), nfp = op.nfp;
+  const FactSmem L = fact_a_layout(kp);
+  double* X = reinterpret_cast<double*>(fsm_raw + L.x);
+  int32_t* EB = reinterpret_cast<int32_t*>(fsm_raw + L.eb);
+  uint16_t* LUT = reinterpret_cast<uint16_t*>(fsm_raw + L.lut);
+  uint16_t* OWN = reinterpret_cast<uint16_t*>(fsm_raw + L.own);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g8 = lane >> 2, t4 = lane & 3;
+  const int64_t c0 = (int64_t)blockIdx.x * kFactBM;
+  const int nc = (int)min((int64_t)kFactBM, op.n_cells - c0);
+  for (int i = tid; i < kp; i += NT) LUT[i] = i < n ? op.lut[i] : 0;
+  for (int e = tid; e < kFactBM * 16; e += NT) EB[e] = (e >> 4) < nc ? op.ebase[c0 * 16 + e] : -1;
+  for (int e = tid; e < kFactBM; e += NT) OWN[e] = e < nc ? op.own[c0 + e] : 0;
+  pdl_wait();
+  if (stopped(guard)) return;
+  double beta = 0.0;
+  int kit = 0;
+  const double* p_old = nullptr;
+  double* p_new = nullptr;
+  if (PCG) {
+    __shared__ double s_beta;
+    __shared__ int s_kit;
+    if (tid == 0) {
+      volatile PcgScalars* v = sc;
+      s_kit = v->k;
+      const double rz_old = v->rz_old;
+      s_beta = (s_kit == 0 || rz_old == 0.0) ? 0.0 : v->rz_acc / rz_old;
+    }
+    __syncthreads();
+    kit = s_kit;
+    beta = s_beta;
+    p_old = (kit & 1) ? pbuf0 : pbuf1;
+    p_new = (kit & 1) ? pbuf1 : pbuf0;
+  } else {
+    __syncthreads();
+  }
+  // ---- gather the tile (PCG mode: p_k = z_k + beta p_{k-1}, the owner cell writes it, ||z||^2;
+  // a version issuing 8 elements' loads before any store measured slower:
+  // profiles/round2/experiments/fact_apply_batched_gather_ab.jsonl)
+  double zz = 0.0;
+  const int total = kFactBM * XS;
+  for (int e = tid; e < total; e += NT) {
+    const int c = e / XS, j = e - c * XS;
+    double v = 0.0;
+    if (j < n) {
+      const int l = LUT[j];
+      const int b = EB[c * 16 + (l >> kLutShift)];
+      if (b >= 0) {
+        const int g = b + (l & ((1 << kLutShift) - 1));
+        const double xv = x[g];
+        v = xv;
+        if (PCG) {
+          v = fma(beta, p_old[g], xv);
+          if ((OWN[c] >> (l >> kLutShift)) & 1) {
+            p_new[g] = v;
+            zz = fma(xv, xv, zz);
+          }
+        }
+      }
+    }
+    X[e] = v;
+  }
+  __syncthreads();
+  // ---- stage A: U = X F, warp = 32-column block, 16 cells
+  const double* xr0 = X + g8 * XS + t4;
+  const double* xr1 = xr0 + 8 * XS;
+  const int nblk = nfp / 32;
+  for (int blk = warp; blk < nblk; blk += kFactWarps) {
+    double acc[2][kFactNQ][2];
+#pragma unroll
+    for (int m = 0; m < 2; ++m)
+#pragma unroll
+      for (int q = 0; q < kFactNQ; ++q) acc[m][q][0] = acc[m][q][1] = 0.0;
+    const double* fb = op.F + (size_t)t4 * nfp + blk * 32 + g8;
+#pragma unroll 4
+    for (int k0 = 0; k0 < kp; k0 += 4) {
+      const double a0 = xr0[k0], a1 = xr1[k0];
+      const double* fr = fb + (size_t)k0 * nfp;
+      double b[kFactNQ];
+#pragma unroll
+      for (int q = 0; q < kFactNQ; ++q) b[q] = __ldg(fr + q * 8);
+#pragma unroll
+      for (int q = 0; q < kFactNQ; ++q) {
+        dmma884(acc[0][q][0], acc[0][q][1], a0, b[q]);
+        dmma884(acc[1][q][0], acc[1][q][1], a1, b[q]);
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < 2; ++m) {
+      const int row = m * 8 + g8;
+      if (row < nc) {
+        double* ur = op.ubuf + (size_t)(c0 + row) * nfp + blk * 32 + 2 * t4;
+#pragma unroll
+        for (int q = 0; q < kFactNQ; ++q) *reinterpret_cast<double2*>(ur + q * 8) = make_double2(acc[m][q][0], acc[m][q][1]);
+      }
+    }
+  }
+  if (pdl_late()) pdl_trigger();
+  if (PCG) {  // ||z||^2, then the stopping test in the last CTA (as apply_tc_kernel's PCG mode)
+    __shared__ double sh[32];
+    __shared__ bool last;
+    const double szz = block_sum(zz, sh);
+    if (tid == 0) {
+      atomicAdd(&sc->zz, szz);
+      __threadfence();
+      last = atomicAdd(&sc->ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (last && tid == 0) {
+      __threadfence();
+      volatile PcgScalars* v = sc;
+      const double zn = sqrt(v->zz);
+      if (kit == 0) {
+        sc->z0 = zn;
+        sc->z_last = zn;
+        sc->iters = 0;
+        if (zn == 0.0) {
+          sc->done = 1;
+          sc->converged = 1;
+        } else if (v->maxit <= 0) {
+          sc->done = 1;
+        }
+      } else {
+        sc->iters = kit;
+        sc->z_last = zn;
+        if (zn <= v->rtol * v->z0) {
+          sc->done = 1;
+          sc->converged = 1;
+        } else if (kit >= v->maxit) {
+          sc->done = 1;
+        }
+      }
+      sc->rz_old = v->rz_acc;
+      sc->pq2[(kit + 1) & 1] = 0.0;  // accumulator of the next fused apply
+      sc->rz_acc = 0.0;
+      sc->zz = 0.0;
+      sc->ticket = 0;
+      sc->k = kit + 1;
+    }
+  }
+}
+
+// stage B: V = mix(U) with the cells' 3 x 3 coefficient matrices (value block: coef 0..5 =
+// Gm_00, Gm_11, Gm_22, Gm_01, Gm_02, Gm_12; curl block: coef 6..11 likewise), p.Ap =
+// sum over the tile of u.v (PCG mode: into pq2 of the iteration stage A just ran), then
+// Y = V F^T and the scatter-add.
+template <bool PCG>
+__global__ void __launch_bounds__(kFactWarps * 32)
+    fact_stage_b_kernel(DevOperator op, double* __restrict__ y, double* pq_acc, const PcgScalars* guard,
+                        PcgScalars* sc) {
+  extern __shared__ __align__(128) unsigned char fsm_raw[];
+  constexpr int NT = kFactWarps * 32;
+  const int n = op.n_loc, kp = op.kp, nfp = op.nfp, VS = (int)fact_vs(nfp);
+  const FactSmem L = fact_b_layout(kp, nfp);
+  double* V = reinterpret_cast<double*>(fsm_raw + L.x);
+  int32_t* EB = reinterpret_cast<int32_t*>(fsm_raw + L.eb);
+  uint16_t* LUT = reinterpret_cast<uint16_t*>(fsm_raw + L.lut);
+  double* C = reinterpret_cast<double*>(fsm_raw + L.own);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g8 = lane >> 2, t4 = lane & 3;
+  const int64_t c0 = (int64_t)blockIdx.x * kFactBM;
+  const int nc = (int)min((int64_t)kFactBM, op.n_cells - c0);
+  for (int i = tid; i < kp; i += NT) LUT[i] = i < n ? op.lut[i] : 0;
+  for (int e = tid; e < kFactBM * 16; e += NT) EB[e] = (e >> 4) < nc ? op.ebase[c0 * 16 + e] : -1;
+  for (int e = tid; e < kFactBM * 12; e += NT) C[e] = e / 12 < nc ? op.coef[c0 * 12 + e] : 0.0;
+  pdl_wait();
+  if (stopped(guard)) return;
+  for (int e = tid; e < kFactBM * (nfp / 2); e += NT) {  // U tile -> smem (16-byte loads)
+    const int c = e / (nfp / 2), j = 2 * (e - c * (nfp / 2));
+    const double2 u = c < nc ? *reinterpret_cast<const double2*>(op.ubuf + (size_t)(c0 + c) * nfp + j)
+                             : make_double2(0.0, 0.0);
+    V[c * VS + j] = u.x;
+    V[c * VS + j + 1] = u.y;
+  }
+  __syncthreads();
+  double pq = 0.0;
+  const int npm = op.nfm / 3, npk = (op.nf - op.nfm) / 3;
+  for (int e = tid; e < kFactBM * (npm + npk); e += NT) {
+    const int c = e / (npm + npk), k = e - c * (npm + npk);
+    const bool val = k < npm;
+    const int np3 = val ? npm : npk, off = val ? k : op.nfm + (k - npm);
+    const double* g = C + c * 12 + (val ? 0 : 6);
+    double* vr = V + c * VS + off;
+    const double u0 = vr[0], u1 = vr[np3], u2 = vr[2 * np3];
+    const double v0 = g[0] * u0 + g[3] * u1 + g[4] * u2;
+    const double v1 = g[3] * u0 + g[1] * u1 + g[5] * u2;
+    const double v2 = g[4] * u0 + g[5] * u1 + g[2] * u2;
+    vr[0] = v0;
+    vr[np3] = v1;
+    vr[2 * np3] = v2;
+    pq = fma(u0, v0, fma(u1, v1, fma(u2, v2, pq)));
+  }
+  __syncthreads();
+  // ---- stage B: Y = V F^T, warp = 32 output columns, 16 cells
+  const double* vr0 = V + g8 * VS + t4;
+  const double* vr1 = vr0 + 8 * VS;
+  const int nblk = (kp + 31) / 32;
+  for (int blk = warp; blk < nblk; blk += kFactWarps) {
+    double acc[2][kFactNQ][2];
+#pragma unroll
+    for (int m = 0; m < 2; ++m)
+#pragma unroll
+      for (int q = 0; q < kFactNQ; ++q) acc[m][q][0] = acc[m][q][1] = 0.0;
+    int colr[kFactNQ];  // F row of this lane's B fragment column (clamped: rows >= kp read as zero)
+#pragma unroll
+    for (int q = 0; q < kFactNQ; ++q) colr[q] = min(blk * 32 + q * 8 + g8, kp - 1);
+    bool colok[kFactNQ];
+#pragma unroll
+    for (int q = 0; q < kFactNQ; ++q) colok[q] = blk * 32 + q * 8 + g8 < kp;
+#pragma unroll 4
+    for (int k0 = 0; k0 < op.nf; k0 += 4) {
+      const double a0 = vr0[k0], a1 = vr1[k0];
+      double b[kFactNQ];
+#pragma unroll
+      for (int q = 0; q < kFactNQ; ++q) b[q] = colok[q] ? __ldg(op.F + (size_t)colr[q] * nfp + k0 + t4) : 0.0;
+#pragma unroll
+      for (int q = 0; q < kFactNQ; ++q) {
+        dmma884(acc[0][q][0], acc[0][q][1], a0, b[q]);
+        dmma884(acc[1][q][0], acc[1][q][1], a1, b[q]);
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < 2; ++m) {
+      const int row = m * 8 + g8;
+#pragma unroll
+      for (int q = 0; q < kFactNQ; ++q)
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int col = blk * 32 + q * 8 + 2 * t4 + i;
+          if (row < nc && col < n) {
+            const int l = LUT[col];
+            const int b = EB[row * 16 + (l >> kLutShift)];
+            if (b >= 0) atomicAdd(y + b + (l & ((1 << kLutShift) - 1)), acc[m][q][i]);
+          }
+        }
+    }
+  }
+  if (pdl_late()) pdl_trigger();
+  __shared__ double sh[32];
+  const double spq = block_sum(pq, sh);
+  if (tid == 0) {
+    if (PCG) {
+      const int kit = ((volatile PcgScalars*)sc)->k - 1;  // stage A of this iteration advanced k
+      atomicAdd(&sc->pq2[kit & 1], spq);
+    } else if (pq_acc) {
+      atomicAdd(pq_acc, spq);
+    }
+  }
+}
+
+template <bool PCG>
+cudaError_t launch_fact_apply(const DevOperator& op, const double* x, double* y, double* pq_acc,
+                              const PcgScalars* guard, PcgScalars* sc, double* p0, double* p1, cudaStream_t s) {
+  const dim3 grid((unsigned)((op.n_cells + kFactBM - 1) / kFactBM)), block(kFactWarps * 32);
+  cudaError_t e = launch_k(fact_stage_a_kernel<PCG>, grid, block, fact_a_layout(op.kp).total, s, op, x, guard, sc, p0,
+                           p1);
+  if (e != cudaSuccess) return e;
+  return launch_k(fact_stage_b_kernel<PCG>, grid, block, fact_b_layout(op.kp, op.nfp).total, s, op, y, pq_acc, guard,
+                  sc);
+}
+
 constexpr size_t kMaxSmem = 226 * 1024;  // 227 KB opt-in minus the static reduction scratch
 
 // The warp layouts built (BM, NQ, KS), each for NM = 7 (H(grad), H(div)) and 12
@@ -1593,6 +1897,7 @@ cudaError_t launch_persistent_pcg(const PersistentPcg& plan, const DevOperator& 
 
 cudaError_t launch_apply(const DevOperator& op, const double* x, double* y, double* pq_acc,
                          const PcgScalars* guard, cudaStream_t s) {
+  if (op.fact) return launch_fact_apply<false>(op, x, y, pq_acc, guard, nullptr, nullptr, nullptr, s);
   return launch_apply_tc<false>(op, x, y, pq_acc, guard, s);
 }
 
@@ -1910,7 +2215,48 @@ int tune_apply(DevOperator& op, const double* x, double* y, PcgScalars* sc, doub
 
 cudaError_t launch_pcg_fused_apply(const DevOperator& op, PcgScalars* sc, const double* z, double* p0, double* p1,
                                    double* q, cudaStream_t s) {
+  if (op.fact) return launch_fact_apply<true>(op, z, q, nullptr, sc, sc, p0, p1, s);
   return launch_apply_tc<true>(op, z, q, nullptr, sc, s, sc, p0, p1);
+}
+
+// Setup-time choice between the DMMA apply (op.fact = 0, its tuned layout) and the
+// factored two-stage apply (op.fact = 1): both timed on the PCG-mode kernels the solve
+// runs (scalars as in tune_apply), three interleaved rounds, best round each.
+int tune_fact(DevOperator& op, const double* x, double* y, PcgScalars* sc, double* p0, double* p1, cudaStream_t s,
+              int reps) {
+  op.fact = 0;
+  // Only meshes of >= kFactMinCells cells are considered: below that the two timings are
+  // within noise, and a timing-dependent choice would make the rounding of small solves
+  // (the iteration count of an ill-conditioned one) vary from setup to setup.
+  if (!fact_apply_fits(op) || op.n_cells < kFactMinCells) return 0;
+  cudaEvent_t e0, e1;
+  if (cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess) return -1;
+  float best[2] = {-1.f, -1.f};
+  for (int round = 0; round < 3; ++round)
+    for (int f = 0; f < 2; ++f) {
+      DevOperator t = op;
+      t.fact = f;
+      if (launch_pcg_fused_apply(t, sc, x, p0, p1, y, s) != cudaSuccess) {
+        cudaGetLastError();
+        continue;
+      }
+      cudaEventRecord(e0, s);
+      for (int r = 0; r < reps; ++r) launch_pcg_fused_apply(t, sc, x, p0, p1, y, s);
+      cudaEventRecord(e1, s);
+      if (cudaEventSynchronize(e1) != cudaSuccess) continue;
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, e0, e1);
+      if (best[f] < 0.f || ms < best[f]) best[f] = ms;
+    }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaGetLastError();
+  op.fact = best[1] >= 0.f && best[1] < best[0] ? 1 : 0;
+  return 0;
+}
+
+bool fact_apply_fits(const DevOperator& op) {
+  return op.F && fact_a_layout(op.kp).total <= kMaxSmem && fact_b_layout(op.kp, op.nfp).total <= kMaxSmem;
 }
 
 cudaError_t launch_pcg_update_jacobi(PcgScalars* sc, const DevPrecond& pc, const double* p0, const double* p1,
@@ -1942,6 +2288,10 @@ cudaError_t launch_dmma_peak(double* out, int n, int blocks, int threads, cudaSt
 
 namespace rdr {
 void configure_kernels() {  // errors here would surface as a later launch's cudaGetLastError
+  cudaFuncSetAttribute(fact_stage_a_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
+  cudaFuncSetAttribute(fact_stage_a_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
+  cudaFuncSetAttribute(fact_stage_b_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
+  cudaFuncSetAttribute(fact_stage_b_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
   cudaFuncSetAttribute(patch_ldg_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
   cudaFuncSetAttribute(patch_ldg_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
   int cnt = 0;

@@ -47,6 +47,12 @@ struct DevOperator {
                                 // apply_tc_kernel)
   // launch configuration (configure_apply): warp-layout variant, cell tiles, persistent grid
   int av, ntiles, apply_grid, apply_slots;
+  // factored apply (H(curl)): F [kp][nfp] (RefElement::F, zero-padded),
+  // nf = its columns (nfm of them the value block), ubuf [n_cells][nfp] stage-A output;
+  // fact = 1: rdr_apply and the fused PCG run the two-stage factored kernels
+  const double* F;
+  int nf, nfm, nfp, fact;
+  double* ubuf;
 };
 
 struct DevPrecond {
@@ -111,6 +117,9 @@ cudaError_t launch_pcg_direction(PcgScalars* sc, const double* z, double* p, dou
 // Fused PCG step (3 kernels per iteration for H(grad)): fused apply (direction
 // update + A p + ||z||^2 + stopping test), update + interior Jacobi, patches.
 bool fused_pcg_supported(const DevOperator& op);
+bool fact_apply_fits(const DevOperator& op);  // the factored apply's shared memory fits
+int tune_fact(DevOperator& op, const double* x, double* y, PcgScalars* sc, double* p0, double* p1, cudaStream_t s,
+              int reps);
 // the apply's warp-layout variants (kernels.cu apply_variants): configure op for
 // variant k (0, or -1 if it does not fit this operator), and setup-time
 // autotuning over all that fit (x, y: device scratch of length n_total)

@@ -349,6 +349,21 @@ static int setup_impl(rdr_handle* h, const double* vertices, int64_t nv, const i
     if ((st = h->own_upload(&d_B, B))) return st;
     op.Bsw = d_B;
   }
+  op.F = nullptr;
+  op.nf = op.nfm = op.nfp = op.fact = 0;
+  op.ubuf = nullptr;
+  if (el.nf > 0) {  // factored apply: F [kp][nfp] zero-padded, stage-A buffer
+    op.nf = el.nf;
+    op.nfm = el.nfm;
+    op.nfp = (el.nf + 31) / 32 * 32;
+    std::vector<double> Fp((size_t)op.kp * op.nfp, 0.0);
+    for (int i = 0; i < el.n; ++i)
+      for (int j = 0; j < el.nf; ++j) Fp[(size_t)i * op.nfp + j] = el.F[(size_t)i * el.nf + j];
+    double* d_F;
+    if ((st = h->own_upload(&d_F, Fp))) return st;
+    op.F = d_F;
+    if ((st = h->own_alloc((void**)&op.ubuf, sizeof(double) * (size_t)nt * op.nfp))) return st;
+  }
   if ((st = h->own_upload(&h->d_cons, num.constrained))) return st;
   {  // a layout that fits (n_loc too large for all: EINVAL); tuned below on the device
     int k = 0;
@@ -560,6 +575,8 @@ static int setup_impl(rdr_handle* h, const double* vertices, int64_t nv, const i
     h->h_sc->maxit = 1 << 30;
     CK(cudaMemcpy(h->d_sc, h->h_sc, sizeof(PcgScalars), cudaMemcpyHostToDevice));
     if (tune_apply(op, h->d_b, h->d_q, h->d_sc, h->d_p, h->d_p2, 0, 5)) return RDR_ECUDA;
+    if (tune_fact(op, h->d_b, h->d_q, h->d_sc, h->d_p, h->d_p2, 0, 5)) return RDR_ECUDA;
+    if (op.fact && h->fused) h->launches_per_iter += 1;  // two stage kernels instead of one apply
     CK(cudaMemset(h->d_p, 0, vb));
     CK(cudaMemset(h->d_p2, 0, vb));
   }
@@ -591,6 +608,7 @@ static int setup_impl(rdr_handle* h, const double* vertices, int64_t nv, const i
   in.apply_grid = op.apply_grid;
   in.apply_slots = op.apply_slots;
   in.small_patch_grid = pc.small_grid;
+  in.apply_factored = op.fact;
   in.patch_setup_flops = 0;
   for (int32_t n : P.n) {  // lower tiles I >= J, I, J != K: nb(nb-1)/2 per K; panel: nb-1 per K
     const double nb = (n + 63) / 64;
@@ -1037,6 +1055,9 @@ int rdr_debug_set_apply_variant(rdr_handle* h, int variant) {
   if (!h) return RDR_EINVAL;
   DevOperator t = h->op;
   if (apply_configure_variant(t, variant)) return RDR_EINVAL;
+  if (t.fact && h->fused) h->launches_per_iter -= 1;
+  t.fact = 0;
+  h->info.apply_factored = 0;
   h->op = t;
   if (h->graph) cudaGraphExecDestroy(h->graph);
   if (h->wgraph) cudaGraphExecDestroy(h->wgraph);
@@ -1050,7 +1071,16 @@ int rdr_debug_set_apply_variant(rdr_handle* h, int variant) {
 int rdr_debug_set_apply_config(rdr_handle* h, int variant, int slots, int grid) {
   if (!h) return RDR_EINVAL;
   DevOperator t = h->op;
-  if (apply_configure_exact(t, variant, slots, grid)) return RDR_EINVAL;
+  if (variant == -1) {  // the factored two-stage apply (H(curl))
+    if (!fact_apply_fits(t)) return RDR_EINVAL;
+    if (!t.fact && h->fused) h->launches_per_iter += 1;
+    t.fact = 1;
+  } else {
+    if (apply_configure_exact(t, variant, slots, grid)) return RDR_EINVAL;
+    if (t.fact && h->fused) h->launches_per_iter -= 1;
+    t.fact = 0;
+  }
+  h->info.apply_factored = t.fact;
   h->op = t;
   if (h->graph) cudaGraphExecDestroy(h->graph);
   if (h->wgraph) cudaGraphExecDestroy(h->wgraph);
@@ -1232,6 +1262,23 @@ int rdr_reference_matrices(int space, int p, double* out, int32_t* n_loc, int32_
     if (out) std::memcpy(out, el.R.data(), sizeof(double) * el.R.size());
   } catch (const std::exception& e) {
     std::fprintf(stderr, "rdr_reference_matrices: %s\n", e.what());
+    return RDR_EINVAL;
+  }
+  return RDR_OK;
+}
+
+int rdr_reference_factors(int space, int p, double* out, int32_t* n_loc, int32_t* nf, int32_t* nfm) {
+  if (!n_loc || !nf || !nfm) return RDR_EINVAL;
+  if (space != RDR_HGRAD && space != RDR_HCURL && space != RDR_HDIV) return RDR_EINVAL;
+  if (p < 1 || (space == RDR_HGRAD && p > 12) || (space != RDR_HGRAD && p > 10)) return RDR_EINVAL;
+  try {
+    const RefElement& el = reference_element(space, p);
+    *n_loc = el.n;
+    *nf = el.nf;
+    *nfm = el.nfm;
+    if (out && el.nf) std::memcpy(out, el.F.data(), sizeof(double) * el.F.size());
+  } catch (const std::exception& e) {
+    std::fprintf(stderr, "rdr_reference_factors: %s\n", e.what());
     return RDR_EINVAL;
   }
   return RDR_OK;

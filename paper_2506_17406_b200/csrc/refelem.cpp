@@ -750,6 +750,23 @@ void upper_t_solve(const Mat& L, Mat& B) {
     }
 }
 
+Mat cholesky_lower(const Mat& A) {  // A = L L^T, A SPD (long double)
+  const int n = A.r;
+  Mat L(n, n);
+  for (int j = 0; j < n; ++j) {
+    ld d = A(j, j);
+    for (int k = 0; k < j; ++k) d -= L(j, k) * L(j, k);
+    if (!(d > 0)) throw std::runtime_error("cholesky: not SPD");
+    L(j, j) = std::sqrt(d);
+    for (int i = j + 1; i < n; ++i) {
+      ld v = A(i, j);
+      for (int k = 0; k < j; ++k) v -= L(i, k) * L(j, k);
+      L(i, j) = v / L(j, j);
+    }
+  }
+  return L;
+}
+
 Mat inverse(const Mat& M) {  // Gauss-Jordan with partial pivoting
   const int n = M.r;
   Mat A = M, X(n, n);
@@ -1235,6 +1252,20 @@ std::unique_ptr<RefElement> build_ned(int p) {
   for (int a = 0; a < 3; ++a) put(6 + a, Kk[a][a], false);
   for (int k = 0; k < 3; ++k) put(9 + k, Kk[ab[k][0]][ab[k][1]], true);
   for (ld l : ned_bubbles(3, p).lam) el->lam_cell.push_back((double)l);
+  {  // factors through L2-orthonormal bases of P_p and P_{p-1} (RefElement::F)
+    const Mat Lp = cholesky_lower(integrals(T, p, p));
+    const Mat Lq = cholesky_lower(integrals(T, p - 1, p - 1));
+    el->nfm = 3 * Np;
+    el->nf = 3 * Np + 3 * Np1;
+    el->F.assign((size_t)n * el->nf, 0.0);
+    for (int a = 0; a < 3; ++a) {
+      const Mat FM = mul(P[a], Lp), FK = mul(Rc[a], Lq);
+      for (int i = 0; i < n; ++i) {
+        for (int k = 0; k < Np; ++k) el->F[(size_t)i * el->nf + a * Np + k] = (double)FM(i, k);
+        for (int k = 0; k < Np1; ++k) el->F[(size_t)i * el->nf + el->nfm + a * Np1 + k] = (double)FK(i, k);
+      }
+    }
+  }
   return el;
 }
 
@@ -1334,7 +1365,7 @@ std::map<std::pair<int, int>, std::unique_ptr<RefElement>> g_el;
 // ignored (rebuilt and rewritten); writes go through a temporary + rename.
 namespace {
 
-constexpr char kCacheMagic[8] = {'R', 'D', 'R', 'R', 'E', 'F', '0', '1'};
+constexpr char kCacheMagic[8] = {'R', 'D', 'R', 'R', 'E', 'F', '0', '2'};
 
 uint64_t fnv1a(const std::string& b) {
   uint64_t h = 1469598103934665603ULL;
@@ -1378,6 +1409,9 @@ std::string serialize(const RefElement& el) {
   b.append(reinterpret_cast<const char*>(el.R.data()), sizeof(double) * el.R.size());
   put(b, (int64_t)el.lam_cell.size());
   b.append(reinterpret_cast<const char*>(el.lam_cell.data()), sizeof(double) * el.lam_cell.size());
+  put(b, (int32_t)el.nf);
+  put(b, (int32_t)el.nfm);
+  b.append(reinterpret_cast<const char*>(el.F.data()), sizeof(double) * el.F.size());
   put(b, fnv1a(b));
   return b;
 }
@@ -1417,9 +1451,18 @@ std::unique_ptr<RefElement> load_cached(int space, int p) {
   el->R.resize(nr);
   std::memcpy(el->R.data(), b.data() + at, 8 * nr);
   at += 8 * nr;
-  if (!get(b, at, nlam) || nlam < 0 || at + 8 * nlam + 8 != b.size()) return nullptr;
+  if (!get(b, at, nlam) || nlam < 0 || at + 8 * nlam > b.size()) return nullptr;
   el->lam_cell.resize(nlam);
   std::memcpy(el->lam_cell.data(), b.data() + at, 8 * nlam);
+  at += 8 * nlam;
+  int32_t nf, nfm;
+  if (!get(b, at, nf) || !get(b, at, nfm) || nf < 0 || nfm < 0 || nfm > nf ||
+      at + 8 * (size_t)nf * n + 8 != b.size())
+    return nullptr;
+  el->nf = nf;
+  el->nfm = nfm;
+  el->F.resize((size_t)nf * n);
+  std::memcpy(el->F.data(), b.data() + at, 8 * (size_t)nf * n);
   return el;
 }
 

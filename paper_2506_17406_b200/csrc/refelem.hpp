@@ -22,6 +22,13 @@ struct RefElement {
   std::vector<LocalDof> dofs;    // R-A8 order
   std::vector<double> R;         // [n_mat][n][n] symmetric reference matrices (FP64)
   std::vector<double> lam_cell;  // interior type-I eigenvalues
+  // H(curl) only: the reference matrices factored through L2-orthonormal bases of P_p (values)
+  // and P_{p-1} (curls): M^{ab} = F_a^M F_b^M^T, K^{ab} = F_a^K F_b^K^T with F_a^M = P_a L_p,
+  // F_a^K = Rc_a L_{p-1} (P_a, Rc_a: component a of the basis functions / their curls in the
+  // barycentric monomials; L_q L_q^T the monomial Gram matrix). F = [n][nf], columns
+  // [F_0^M | F_1^M | F_2^M | F_0^K | F_1^K | F_2^K], nfm = 3 dim P_p (0: not factored).
+  int nf = 0, nfm = 0;
+  std::vector<double> F;
 };
 
 // Cached per (space, p). Throws std::runtime_error on internal failure.

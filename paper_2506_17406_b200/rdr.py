@@ -48,7 +48,7 @@ class Info(ctypes.Structure):
                 ("patch_kernel_seconds", ctypes.c_double), ("patch_setup_flops", ctypes.c_double),
                 ("apply_variant", ctypes.c_int32), ("apply_grid", ctypes.c_int32),
                 ("persistent_loop", ctypes.c_int32), ("apply_slots", ctypes.c_int32),
-                ("small_patch_grid", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+                ("small_patch_grid", ctypes.c_int32), ("apply_factored", ctypes.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -414,6 +414,63 @@ def test_every_apply_layout(torch_cuda, space, p):
     assert ran == 6  # every layout of this n_mat fits these small elements
 
 
+@pytest.mark.parametrize("p,n,perturb", [(1, 2, True), (2, 2, True), (4, 2, True), (6, 2, False), (10, 1, False)])
+def test_factored_apply_hcurl(torch_cuda, p, n, perturb):
+    """The factored two-stage apply (the reference matrices
+    factored through L2-orthonormal bases of P_p and P_{p-1}, a per-cell 3 x 3 mix
+    between two GEMMs) against the oracle: A x, the fused PCG's first apply, and
+    PCG iterations (rdr_debug_set_apply_config(-1)); the factors reproduce the
+    library's reference matrices (rdr_reference_factors)."""
+    import ctypes
+    from paper_2506_17406_b200 import rdr
+    from oracle.solver import Oracle
+    torch = torch_cuda
+    c = make_config(0, n=n, p=p, space=HCURL, perturb=perturb, bc="x0", coeffs="loguniform")
+    S = rdr.Solver(c.vertices, c.tets, c.p, c.space, c.alpha, c.beta, c.mask, loop=rdr.LOOP_GRAPH)
+    O = Oracle(c.vertices, c.tets, c.p, c.space, c.alpha, c.beta, c.mask)
+    assert S.info["apply_factored"] == 0  # small meshes: setup never picks it (kFactMinCells)
+    assert S.set_apply_config(-1, 0, 0) and S.info["apply_factored"] == 1
+    x = c.draw_vector(O.n_total)
+    xt = torch.from_numpy(x).cuda()
+    ya = O.apply(x)
+    assert rel(S.apply(xt).cpu().numpy(), ya) <= TOL
+    assert rel(S.debug_fused_apply(xt, torch.zeros_like(xt)).cpu().numpy(), O.apply(O.mask(x))) <= TOL
+    # PCG with unit coefficients: with the 1e4 log-uniform contrast at p = 1 the iteration count
+    # moves by 2 between two roundings of the same operator (DMMA 53, factored 52, oracle 54:
+    # profiles/round2/experiments/fact_apply_rounding.txt), beyond the +-1 bar
+    c = make_config(0, n=n, p=p, space=HCURL, perturb=perturb, bc="x0", coeffs="one")
+    S = rdr.Solver(c.vertices, c.tets, c.p, c.space, c.alpha, c.beta, c.mask, loop=rdr.LOOP_GRAPH)
+    O = Oracle(c.vertices, c.tets, c.p, c.space, c.alpha, c.beta, c.mask)
+    assert S.set_apply_config(-1, 0, 0)
+    b = c.draw_vector(O.n_total)
+    hist = []
+    xo, ito, _ = O.solve(b, rtol=1e-8, history=hist)
+    xg, it = S.solve(torch.from_numpy(b).cuda(), rtol=1e-8)
+    _check_iters(S, it, ito, lambda kk: hist[kk - 1] if 0 < kk <= len(hist) else None)
+    assert rel(xg.cpu().numpy(), xo) <= 1e-6
+    # the factors behind it: sum_ab G_ab F_a F_b^T = the reference matrices to rounding
+    lib = rdr._lib
+    nl, nf, nfm = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+    assert lib.rdr_reference_factors(HCURL, p, None, ctypes.byref(nl), ctypes.byref(nf), ctypes.byref(nfm)) == 0
+    F = np.zeros((nl.value, nf.value))
+    lib.rdr_reference_factors(HCURL, p, F.ctypes.data_as(ctypes.c_void_p), ctypes.byref(nl), ctypes.byref(nf),
+                              ctypes.byref(nfm))
+    nm_, nmat = ctypes.c_int32(), ctypes.c_int32()
+    lib.rdr_reference_matrices(HCURL, p, None, ctypes.byref(nm_), ctypes.byref(nmat))
+    R = np.zeros((nmat.value, nl.value, nl.value))
+    lib.rdr_reference_matrices(HCURL, p, R.ctypes.data_as(ctypes.c_void_p), ctypes.byref(nm_), ctypes.byref(nmat))
+    npm, npk = nfm.value // 3, (nf.value - nfm.value) // 3
+    FM = [F[:, a * npm:(a + 1) * npm] for a in range(3)]
+    FK = [F[:, nfm.value + a * npk:nfm.value + (a + 1) * npk] for a in range(3)]
+    for a in range(3):
+        assert rel(FM[a] @ FM[a].T, R[a]) <= 1e-13 and rel(FK[a] @ FK[a].T, R[6 + a]) <= 1e-13
+    for k, (a, bb) in enumerate([(0, 1), (0, 2), (1, 2)]):
+        X = FM[a] @ FM[bb].T
+        assert rel(X + X.T, R[3 + k]) <= 1e-13
+        X = FK[a] @ FK[bb].T
+        assert rel(X + X.T, R[9 + k]) <= 1e-13
+
+
 def test_apply_ring_depths_and_grids(torch_cuda):
     """The apply with explicit ring depths (the shallowest, KS + 1 chunks, to the
     deepest that fits) and grids (resident CTAs, one CTA per unit, a single CTA

@@ -149,7 +149,7 @@ struct rdr_info {
   int32_t small_patch_grid;    /* > 0: all patches <= 128 dofs and setup's timing chose resident warps
                                   walking them (this many CTAs); 0: one warp per patch or CTA per patch */
   int32_t apply_factored;      /* 1: the apply runs factored through orthonormal P_p / P_{p-1} bases
-                                  (two-stage kernels, H(curl)), chosen by setup-time
+                                  (two-stage kernels, H(curl) and H(div)), chosen by setup-time
                                   timing against the DMMA apply with the reference matrices */
 };
 
@@ -252,7 +252,7 @@ int rdr_debug_set_apply_variant(rdr_handle* h, int variant);
  * grid of resident CTAs) -- the three values rdr_info reports as apply_variant,
  * apply_slots and apply_grid -- so that a profiler run can reproduce the
  * configuration another setup's timing chose (scripts/prof_kernels.py --apply);
- * variant = -1 selects the factored two-stage apply (H(curl), rdr_info.apply_factored;
+ * variant = -1 selects the factored two-stage apply (H(curl), H(div); rdr_info.apply_factored;
  * slots and grid ignored). RDR_EINVAL if it does not fit this operator. */
 int rdr_debug_set_apply_config(rdr_handle* h, int variant, int slots, int grid);
 
@@ -277,12 +277,12 @@ int rdr_debug_fused_apply(rdr_handle* h, const double* z, double* q, void* strea
  * H(div) Mxx, Myy, Mzz, Mxy+Myx, Mxz+Mzx, Myz+Mzy (2-form proxies), then K (div-div).
  * Local dof order: DESIGN.md R-A8. */
 int rdr_reference_matrices(int space, int p, double* out, int32_t* n_loc, int32_t* n_mat);
-/* rdr_reference_factors (H(curl)): the factors of the reference matrices through
- * L2-orthonormal bases of P_p (values) and P_{p-1} (curls) that the factored
- * apply uses, layout [n_loc][nf], columns [F0M | F1M | F2M | F0K | F1K | F2K]
- * with nfm = 3 dim P_p: M^{ab} = FaM FbM^T, K^{ab} = FaK FbK^T (DESIGN.md
- * section 10e). Pass out = NULL to query *n_loc, *nf and *nfm; *nf = 0 for the
- * spaces without factors. */
+/* rdr_reference_factors (H(curl), H(div)): the factors of the reference matrices
+ * through L2-orthonormal bases of P_p (values) and P_{p-1} (curls / divergences)
+ * that the factored apply uses, layout [n_loc][nf]. H(curl): columns
+ * [F0M | F1M | F2M | F0K | F1K | F2K] with nfm = 3 dim P_p, M^{ab} = FaM FbM^T,
+ * K^{ab} = FaK FbK^T; H(div): [F0M | F1M | F2M | FD], K = FD FD^T (DESIGN.md
+ * section 10e). Pass out = NULL to query *n_loc, *nf and *nfm; *nf = 0 for H(grad). */
 int rdr_reference_factors(int space, int p, double* out, int32_t* n_loc, int32_t* nf, int32_t* nfm);
 /* In-place inverse of an n x n SPD row-major matrix with the host routine the
  * setup uses for the patch inverses (R-A15); RDR_ENOTSPD on a non-positive

@@ -514,7 +514,7 @@ __global__ void __launch_bounds__((apply_mma_warps(BM, NQ, KS) + 1) * 32, MINB)
   }
 }
 
-// ---------------------------------------------------------------- factored apply (H(curl))
+// ---------------------------------------------------------------- factored apply (H(curl), H(div))
 // The reference matrices factor through L2-orthonormal bases of P_p (values) and
 // P_{p-1} (curls): M^{ab} = FaM FbM^T, K^{ab} = FaK FbK^T (refelem.cpp, RefElement::F).
 // The cell operator is y_e = F (Gm ⊗ I) F^T x_e on the value block plus the same with
@@ -548,7 +548,7 @@ __host__ __device__ inline FactSmem fact_b_layout(int kp, int nfp) {
   L.x = 0;  // V [16][nfp + 4]
   L.eb = L.x + sizeof(double) * (size_t)kFactBM * fact_vs(nfp);
   L.lut = L.eb + sizeof(int32_t) * kFactBM * 16;
-  L.own = L.lut + sizeof(uint16_t) * (size_t)((kp + 3) & ~3);  // coefficients [16][12] doubles
+  L.own = L.lut + sizeof(uint16_t) * (size_t)((kp + 3) & ~3);  // coefficients [16][n_mat <= 12] doubles
   L.total = L.own + sizeof(double) * kFactBM * 12;
   return L;
 }
@@ -721,7 +721,8 @@ __global__ void __launch_bounds__(kFactWarps * 32)
   const int nc = (int)min((int64_t)kFactBM, op.n_cells - c0);
   for (int i = tid; i < kp; i += NT) LUT[i] = i < n ? op.lut[i] : 0;
   for (int e = tid; e < kFactBM * 16; e += NT) EB[e] = (e >> 4) < nc ? op.ebase[c0 * 16 + e] : -1;
-  for (int e = tid; e < kFactBM * 12; e += NT) C[e] = e / 12 < nc ? op.coef[c0 * 12 + e] : 0.0;
+  const int nm = op.n_mat;
+  for (int e = tid; e < kFactBM * nm; e += NT) C[e] = e / nm < nc ? op.coef[c0 * nm + e] : 0.0;
   pdl_wait();
   if (stopped(guard)) return;
   for (int e = tid; e < kFactBM * (nfp / 2); e += NT) {  // U tile -> smem (16-byte loads)
@@ -733,13 +734,19 @@ __global__ void __launch_bounds__(kFactWarps * 32)
   }
   __syncthreads();
   double pq = 0.0;
-  const int npm = op.nfm / 3, npk = (op.nf - op.nfm) / 3;
+  const int npm = op.nfm / 3, npk = (op.nf - op.nfm) / op.fck;
   for (int e = tid; e < kFactBM * (npm + npk); e += NT) {
     const int c = e / (npm + npk), k = e - c * (npm + npk);
     const bool val = k < npm;
     const int np3 = val ? npm : npk, off = val ? k : op.nfm + (k - npm);
-    const double* g = C + c * 12 + (val ? 0 : 6);
+    const double* g = C + c * nm + (val ? 0 : 6);
     double* vr = V + c * VS + off;
+    if (!val && op.fck == 1) {  // H(div): the div-div block is scalar, coefficient alpha / |det J|
+      const double u = vr[0], v = g[0] * u;
+      vr[0] = v;
+      pq = fma(u, v, pq);
+      continue;
+    }
     const double u0 = vr[0], u1 = vr[np3], u2 = vr[2 * np3];
     const double v0 = g[0] * u0 + g[3] * u1 + g[4] * u2;
     const double v1 = g[3] * u0 + g[1] * u1 + g[5] * u2;

@@ -52,6 +52,7 @@ struct DevOperator {
   // fact = 1: rdr_apply and the fused PCG run the two-stage factored kernels
   const double* F;
   int nf, nfm, nfp, fact;
+  int fck;                      // components of the second factor block: 3 (curls), 1 (divergence)
   double* ubuf;
 };
 

@@ -351,6 +351,7 @@ static int setup_impl(rdr_handle* h, const double* vertices, int64_t nv, const i
   }
   op.F = nullptr;
   op.nf = op.nfm = op.nfp = op.fact = 0;
+  op.fck = space == RDR_HDIV ? 1 : 3;
   op.ubuf = nullptr;
   if (el.nf > 0) {  // factored apply: F [kp][nfp] zero-padded, stage-A buffer
     op.nf = el.nf;

@@ -1351,6 +1351,22 @@ std::unique_ptr<RefElement> build_rt(int p) {
   for (int k = 0; k < 3; ++k) put(3 + k, Mm[ab[k][0]][ab[k][1]], true);
   put(6, Kd, false);
   for (ld l : Phi.lam) el->lam_cell.push_back((double)l);
+  {  // factors (RefElement::F): the proxy mass through P_p, the (scalar) divergence through P_{p-1}
+    const Mat Lp = cholesky_lower(integrals(T, p, p));
+    const Mat Lq = cholesky_lower(integrals(T, p - 1, p - 1));
+    const int Np1 = mi(4, p - 1).size();
+    el->nfm = 3 * Np;
+    el->nf = 3 * Np + Np1;
+    el->F.assign((size_t)n * el->nf, 0.0);
+    const Mat FD = mul(D, Lq);
+    for (int a = 0; a < 3; ++a) {
+      const Mat FM = mul(P[a], Lp);
+      for (int i = 0; i < n; ++i)
+        for (int k = 0; k < Np; ++k) el->F[(size_t)i * el->nf + a * Np + k] = (double)FM(i, k);
+    }
+    for (int i = 0; i < n; ++i)
+      for (int k = 0; k < Np1; ++k) el->F[(size_t)i * el->nf + el->nfm + k] = (double)FD(i, k);
+  }
   return el;
 }
 

@@ -27,6 +27,7 @@ struct RefElement {
   // F_a^K = Rc_a L_{p-1} (P_a, Rc_a: component a of the basis functions / their curls in the
   // barycentric monomials; L_q L_q^T the monomial Gram matrix). F = [n][nf], columns
   // [F_0^M | F_1^M | F_2^M | F_0^K | F_1^K | F_2^K], nfm = 3 dim P_p (0: not factored).
+  // H(div): [F_0^M | F_1^M | F_2^M | F^D], the div-div matrix K = F^D F^D^T (one component).
   int nf = 0, nfm = 0;
   std::vector<double> F;
 };

@@ -414,8 +414,10 @@ def test_every_apply_layout(torch_cuda, space, p):
     assert ran == 6  # every layout of this n_mat fits these small elements
 
 
-@pytest.mark.parametrize("p,n,perturb", [(1, 2, True), (2, 2, True), (4, 2, True), (6, 2, False), (10, 1, False)])
-def test_factored_apply_hcurl(torch_cuda, p, n, perturb):
+@pytest.mark.parametrize("space,p,n,perturb", [(HCURL, 1, 2, True), (HCURL, 2, 2, True), (HCURL, 4, 2, True),
+                                               (HCURL, 6, 2, False), (HCURL, 10, 1, False), (HDIV, 1, 2, True),
+                                               (HDIV, 3, 2, True), (HDIV, 6, 2, False)])
+def test_factored_apply(torch_cuda, space, p, n, perturb):
     """The factored two-stage apply (the reference matrices
     factored through L2-orthonormal bases of P_p and P_{p-1}, a per-cell 3 x 3 mix
     between two GEMMs) against the oracle: A x, the fused PCG's first apply, and
@@ -425,7 +427,7 @@ def test_factored_apply_hcurl(torch_cuda, p, n, perturb):
     from paper_2506_17406_b200 import rdr
     from oracle.solver import Oracle
     torch = torch_cuda
-    c = make_config(0, n=n, p=p, space=HCURL, perturb=perturb, bc="x0", coeffs="loguniform")
+    c = make_config(0, n=n, p=p, space=space, perturb=perturb, bc="x0", coeffs="loguniform")
     S = rdr.Solver(c.vertices, c.tets, c.p, c.space, c.alpha, c.beta, c.mask, loop=rdr.LOOP_GRAPH)
     O = Oracle(c.vertices, c.tets, c.p, c.space, c.alpha, c.beta, c.mask)
     assert S.info["apply_factored"] == 0  # small meshes: setup never picks it (kFactMinCells)
@@ -438,7 +440,7 @@ def test_factored_apply_hcurl(torch_cuda, p, n, perturb):
     # PCG with unit coefficients: with the 1e4 log-uniform contrast at p = 1 the iteration count
     # moves by 2 between two roundings of the same operator (DMMA 53, factored 52, oracle 54:
     # profiles/round2/experiments/fact_apply_rounding.txt), beyond the +-1 bar
-    c = make_config(0, n=n, p=p, space=HCURL, perturb=perturb, bc="x0", coeffs="one")
+    c = make_config(0, n=n, p=p, space=space, perturb=perturb, bc="x0", coeffs="one")
     S = rdr.Solver(c.vertices, c.tets, c.p, c.space, c.alpha, c.beta, c.mask, loop=rdr.LOOP_GRAPH)
     O = Oracle(c.vertices, c.tets, c.p, c.space, c.alpha, c.beta, c.mask)
     assert S.set_apply_config(-1, 0, 0)
@@ -451,22 +453,30 @@ def test_factored_apply_hcurl(torch_cuda, p, n, perturb):
     # the factors behind it: sum_ab G_ab F_a F_b^T = the reference matrices to rounding
     lib = rdr._lib
     nl, nf, nfm = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
-    assert lib.rdr_reference_factors(HCURL, p, None, ctypes.byref(nl), ctypes.byref(nf), ctypes.byref(nfm)) == 0
+    assert lib.rdr_reference_factors(space, p, None, ctypes.byref(nl), ctypes.byref(nf), ctypes.byref(nfm)) == 0
     F = np.zeros((nl.value, nf.value))
-    lib.rdr_reference_factors(HCURL, p, F.ctypes.data_as(ctypes.c_void_p), ctypes.byref(nl), ctypes.byref(nf),
+    lib.rdr_reference_factors(space, p, F.ctypes.data_as(ctypes.c_void_p), ctypes.byref(nl), ctypes.byref(nf),
                               ctypes.byref(nfm))
     nm_, nmat = ctypes.c_int32(), ctypes.c_int32()
-    lib.rdr_reference_matrices(HCURL, p, None, ctypes.byref(nm_), ctypes.byref(nmat))
+    lib.rdr_reference_matrices(space, p, None, ctypes.byref(nm_), ctypes.byref(nmat))
     R = np.zeros((nmat.value, nl.value, nl.value))
-    lib.rdr_reference_matrices(HCURL, p, R.ctypes.data_as(ctypes.c_void_p), ctypes.byref(nm_), ctypes.byref(nmat))
-    npm, npk = nfm.value // 3, (nf.value - nfm.value) // 3
+    lib.rdr_reference_matrices(space, p, R.ctypes.data_as(ctypes.c_void_p), ctypes.byref(nm_), ctypes.byref(nmat))
+    npm = nfm.value // 3
     FM = [F[:, a * npm:(a + 1) * npm] for a in range(3)]
-    FK = [F[:, nfm.value + a * npk:nfm.value + (a + 1) * npk] for a in range(3)]
     for a in range(3):
-        assert rel(FM[a] @ FM[a].T, R[a]) <= 1e-13 and rel(FK[a] @ FK[a].T, R[6 + a]) <= 1e-13
+        assert rel(FM[a] @ FM[a].T, R[a]) <= 1e-13
     for k, (a, bb) in enumerate([(0, 1), (0, 2), (1, 2)]):
         X = FM[a] @ FM[bb].T
         assert rel(X + X.T, R[3 + k]) <= 1e-13
+    if space == HDIV:  # div-div through the one-component block
+        FD = F[:, nfm.value:]
+        assert rel(FD @ FD.T, R[6]) <= 1e-13
+        return
+    npk = (nf.value - nfm.value) // 3
+    FK = [F[:, nfm.value + a * npk:nfm.value + (a + 1) * npk] for a in range(3)]
+    for a in range(3):
+        assert rel(FK[a] @ FK[a].T, R[6 + a]) <= 1e-13
+    for k, (a, bb) in enumerate([(0, 1), (0, 2), (1, 2)]):
         X = FK[a] @ FK[bb].T
         assert rel(X + X.T, R[9 + k]) <= 1e-13
 

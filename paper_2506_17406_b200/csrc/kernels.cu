@@ -527,50 +527,51 @@ __global__ void __launch_bounds__((apply_mma_warps(BM, NQ, KS) + 1) * 32, MINB)
 // DMMA.8x8x4 with A from shared memory and B = F read through L1/L2 (op.F is
 // [kp][nfp], zero-padded, ~0.8 MB for Ned1_6). 8 warps, 16 cells per CTA, each warp
 // 16 cells x 32 columns per pass.
-constexpr int kFactBM = 16, kFactWarps = 8, kFactNQ = 4;
+constexpr int kFactWarps = 8, kFactNQ = 4;  // cells per tile: BM = 16 (op.fact 1) or 32 (op.fact 2)
 constexpr int64_t kFactMinCells = 2048;
 
 struct FactSmem {
   size_t x, eb, lut, own, total;
 };
-__host__ __device__ inline FactSmem fact_a_layout(int kp) {
+__host__ __device__ inline FactSmem fact_a_layout(int kp, int bm) {
   FactSmem L;
   L.x = 0;
-  L.eb = L.x + sizeof(double) * (size_t)kFactBM * apply_x_stride(kp);
-  L.lut = L.eb + sizeof(int32_t) * kFactBM * 16;
+  L.eb = L.x + sizeof(double) * (size_t)bm * apply_x_stride(kp);
+  L.lut = L.eb + sizeof(int32_t) * bm * 16;
   L.own = L.lut + sizeof(uint16_t) * (size_t)((kp + 3) & ~3);
-  L.total = L.own + sizeof(uint16_t) * kFactBM;
+  L.total = L.own + sizeof(uint16_t) * bm;
   return L;
 }
 __host__ __device__ inline size_t fact_vs(int nfp) { return (size_t)nfp + 4; }  // V row stride (== 4 mod 16)
-__host__ __device__ inline FactSmem fact_b_layout(int kp, int nfp) {
+__host__ __device__ inline FactSmem fact_b_layout(int kp, int nfp, int bm) {
   FactSmem L;
-  L.x = 0;  // V [16][nfp + 4]
-  L.eb = L.x + sizeof(double) * (size_t)kFactBM * fact_vs(nfp);
-  L.lut = L.eb + sizeof(int32_t) * kFactBM * 16;
-  L.own = L.lut + sizeof(uint16_t) * (size_t)((kp + 3) & ~3);  // coefficients [16][n_mat <= 12] doubles
-  L.total = L.own + sizeof(double) * kFactBM * 12;
+  L.x = 0;  // V [bm][nfp + 4]
+  L.eb = L.x + sizeof(double) * (size_t)bm * fact_vs(nfp);
+  L.lut = L.eb + sizeof(int32_t) * bm * 16;
+  L.own = L.lut + sizeof(uint16_t) * (size_t)((kp + 3) & ~3);  // coefficients [bm][n_mat <= 12] doubles
+  L.total = L.own + sizeof(double) * bm * 12;
   return L;
 }
 
-template <bool PCG>
+template <int BM, bool PCG>
 __global__ void __launch_bounds__(kFactWarps * 32)
     fact_stage_a_kernel(DevOperator op, const double* __restrict__ x, const PcgScalars* guard, PcgScalars* sc,
                         double* pbuf0, double* pbuf1) {
   extern __shared__ __align__(128) unsigned char fsm_raw[];
   constexpr int NT = kFactWarps * 32;
   const int n = op.n_loc, kp = op.kp, XS = apply_x_stride(kp), nfp = op.nfp;
-  const FactSmem L = fact_a_layout(kp);
+  constexpr int MB = BM / 8;  // 8-row DMMA blocks per warp tile
+  const FactSmem L = fact_a_layout(kp, BM);
   double* X = reinterpret_cast<double*>(fsm_raw + L.x);
   int32_t* EB = reinterpret_cast<int32_t*>(fsm_raw + L.eb);
   uint16_t* LUT = reinterpret_cast<uint16_t*>(fsm_raw + L.lut);
   uint16_t* OWN = reinterpret_cast<uint16_t*>(fsm_raw + L.own);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g8 = lane >> 2, t4 = lane & 3;
-  const int64_t c0 = (int64_t)blockIdx.x * kFactBM;
-  const int nc = (int)min((int64_t)kFactBM, op.n_cells - c0);
+  const int64_t c0 = (int64_t)blockIdx.x * BM;
+  const int nc = (int)min((int64_t)BM, op.n_cells - c0);
   for (int i = tid; i < kp; i += NT) LUT[i] = i < n ? op.lut[i] : 0;
-  for (int e = tid; e < kFactBM * 16; e += NT) EB[e] = (e >> 4) < nc ? op.ebase[c0 * 16 + e] : -1;
-  for (int e = tid; e < kFactBM; e += NT) OWN[e] = e < nc ? op.own[c0 + e] : 0;
+  for (int e = tid; e < BM * 16; e += NT) EB[e] = (e >> 4) < nc ? op.ebase[c0 * 16 + e] : -1;
+  for (int e = tid; e < BM; e += NT) OWN[e] = e < nc ? op.own[c0 + e] : 0;
   pdl_wait();
   if (stopped(guard)) return;
   double beta = 0.0;
@@ -598,7 +599,7 @@ __global__ void __launch_bounds__(kFactWarps * 32)
   // a version issuing 8 elements' loads before any store measured slower:
   // profiles/round2/experiments/fact_apply_batched_gather_ab.jsonl)
   double zz = 0.0;
-  const int total = kFactBM * XS;
+  const int total = BM * XS;
   for (int e = tid; e < total; e += NT) {
     const int c = e / XS, j = e - c * XS;
     double v = 0.0;
@@ -621,32 +622,32 @@ __global__ void __launch_bounds__(kFactWarps * 32)
     X[e] = v;
   }
   __syncthreads();
-  // ---- stage A: U = X F, warp = 32-column block, 16 cells
-  const double* xr0 = X + g8 * XS + t4;
-  const double* xr1 = xr0 + 8 * XS;
+  // ---- stage A: U = X F, warp = 32-column block, BM cells
+  const double* xr = X + g8 * XS + t4;
   const int nblk = nfp / 32;
   for (int blk = warp; blk < nblk; blk += kFactWarps) {
-    double acc[2][kFactNQ][2];
+    double acc[MB][kFactNQ][2];
 #pragma unroll
-    for (int m = 0; m < 2; ++m)
+    for (int m = 0; m < MB; ++m)
 #pragma unroll
       for (int q = 0; q < kFactNQ; ++q) acc[m][q][0] = acc[m][q][1] = 0.0;
     const double* fb = op.F + (size_t)t4 * nfp + blk * 32 + g8;
 #pragma unroll 4
     for (int k0 = 0; k0 < kp; k0 += 4) {
-      const double a0 = xr0[k0], a1 = xr1[k0];
+      double a[MB];
+#pragma unroll
+      for (int m = 0; m < MB; ++m) a[m] = xr[m * 8 * XS + k0];
       const double* fr = fb + (size_t)k0 * nfp;
       double b[kFactNQ];
 #pragma unroll
       for (int q = 0; q < kFactNQ; ++q) b[q] = __ldg(fr + q * 8);
 #pragma unroll
-      for (int q = 0; q < kFactNQ; ++q) {
-        dmma884(acc[0][q][0], acc[0][q][1], a0, b[q]);
-        dmma884(acc[1][q][0], acc[1][q][1], a1, b[q]);
-      }
+      for (int q = 0; q < kFactNQ; ++q)
+#pragma unroll
+        for (int m = 0; m < MB; ++m) dmma884(acc[m][q][0], acc[m][q][1], a[m], b[q]);
     }
 #pragma unroll
-    for (int m = 0; m < 2; ++m) {
+    for (int m = 0; m < MB; ++m) {
       const int row = m * 8 + g8;
       if (row < nc) {
         double* ur = op.ubuf + (size_t)(c0 + row) * nfp + blk * 32 + 2 * t4;
@@ -704,28 +705,29 @@ __global__ void __launch_bounds__(kFactWarps * 32)
 // Gm_00, Gm_11, Gm_22, Gm_01, Gm_02, Gm_12; curl block: coef 6..11 likewise), p.Ap =
 // sum over the tile of u.v (PCG mode: into pq2 of the iteration stage A just ran), then
 // Y = V F^T and the scatter-add.
-template <bool PCG>
+template <int BM, bool PCG>
 __global__ void __launch_bounds__(kFactWarps * 32)
     fact_stage_b_kernel(DevOperator op, double* __restrict__ y, double* pq_acc, const PcgScalars* guard,
                         PcgScalars* sc) {
   extern __shared__ __align__(128) unsigned char fsm_raw[];
   constexpr int NT = kFactWarps * 32;
   const int n = op.n_loc, kp = op.kp, nfp = op.nfp, VS = (int)fact_vs(nfp);
-  const FactSmem L = fact_b_layout(kp, nfp);
+  constexpr int MB = BM / 8;
+  const FactSmem L = fact_b_layout(kp, nfp, BM);
   double* V = reinterpret_cast<double*>(fsm_raw + L.x);
   int32_t* EB = reinterpret_cast<int32_t*>(fsm_raw + L.eb);
   uint16_t* LUT = reinterpret_cast<uint16_t*>(fsm_raw + L.lut);
   double* C = reinterpret_cast<double*>(fsm_raw + L.own);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g8 = lane >> 2, t4 = lane & 3;
-  const int64_t c0 = (int64_t)blockIdx.x * kFactBM;
-  const int nc = (int)min((int64_t)kFactBM, op.n_cells - c0);
+  const int64_t c0 = (int64_t)blockIdx.x * BM;
+  const int nc = (int)min((int64_t)BM, op.n_cells - c0);
   for (int i = tid; i < kp; i += NT) LUT[i] = i < n ? op.lut[i] : 0;
-  for (int e = tid; e < kFactBM * 16; e += NT) EB[e] = (e >> 4) < nc ? op.ebase[c0 * 16 + e] : -1;
+  for (int e = tid; e < BM * 16; e += NT) EB[e] = (e >> 4) < nc ? op.ebase[c0 * 16 + e] : -1;
   const int nm = op.n_mat;
-  for (int e = tid; e < kFactBM * nm; e += NT) C[e] = e / nm < nc ? op.coef[c0 * nm + e] : 0.0;
+  for (int e = tid; e < BM * nm; e += NT) C[e] = e / nm < nc ? op.coef[c0 * nm + e] : 0.0;
   pdl_wait();
   if (stopped(guard)) return;
-  for (int e = tid; e < kFactBM * (nfp / 2); e += NT) {  // U tile -> smem (16-byte loads)
+  for (int e = tid; e < BM * (nfp / 2); e += NT) {  // U tile -> smem (16-byte loads)
     const int c = e / (nfp / 2), j = 2 * (e - c * (nfp / 2));
     const double2 u = c < nc ? *reinterpret_cast<const double2*>(op.ubuf + (size_t)(c0 + c) * nfp + j)
                              : make_double2(0.0, 0.0);
@@ -735,7 +737,7 @@ __global__ void __launch_bounds__(kFactWarps * 32)
   __syncthreads();
   double pq = 0.0;
   const int npm = op.nfm / 3, npk = (op.nf - op.nfm) / op.fck;
-  for (int e = tid; e < kFactBM * (npm + npk); e += NT) {
+  for (int e = tid; e < BM * (npm + npk); e += NT) {
     const int c = e / (npm + npk), k = e - c * (npm + npk);
     const bool val = k < npm;
     const int np3 = val ? npm : npk, off = val ? k : op.nfm + (k - npm);
@@ -757,14 +759,13 @@ __global__ void __launch_bounds__(kFactWarps * 32)
     pq = fma(u0, v0, fma(u1, v1, fma(u2, v2, pq)));
   }
   __syncthreads();
-  // ---- stage B: Y = V F^T, warp = 32 output columns, 16 cells
-  const double* vr0 = V + g8 * VS + t4;
-  const double* vr1 = vr0 + 8 * VS;
+  // ---- stage B: Y = V F^T, warp = 32 output columns, BM cells
+  const double* vrow = V + g8 * VS + t4;
   const int nblk = (kp + 31) / 32;
   for (int blk = warp; blk < nblk; blk += kFactWarps) {
-    double acc[2][kFactNQ][2];
+    double acc[MB][kFactNQ][2];
 #pragma unroll
-    for (int m = 0; m < 2; ++m)
+    for (int m = 0; m < MB; ++m)
 #pragma unroll
       for (int q = 0; q < kFactNQ; ++q) acc[m][q][0] = acc[m][q][1] = 0.0;
     int colr[kFactNQ];  // F row of this lane's B fragment column (clamped: rows >= kp read as zero)
@@ -775,18 +776,19 @@ __global__ void __launch_bounds__(kFactWarps * 32)
     for (int q = 0; q < kFactNQ; ++q) colok[q] = blk * 32 + q * 8 + g8 < kp;
 #pragma unroll 4
     for (int k0 = 0; k0 < op.nf; k0 += 4) {
-      const double a0 = vr0[k0], a1 = vr1[k0];
+      double a[MB];
+#pragma unroll
+      for (int m = 0; m < MB; ++m) a[m] = vrow[m * 8 * VS + k0];
       double b[kFactNQ];
 #pragma unroll
       for (int q = 0; q < kFactNQ; ++q) b[q] = colok[q] ? __ldg(op.F + (size_t)colr[q] * nfp + k0 + t4) : 0.0;
 #pragma unroll
-      for (int q = 0; q < kFactNQ; ++q) {
-        dmma884(acc[0][q][0], acc[0][q][1], a0, b[q]);
-        dmma884(acc[1][q][0], acc[1][q][1], a1, b[q]);
-      }
+      for (int q = 0; q < kFactNQ; ++q)
+#pragma unroll
+        for (int m = 0; m < MB; ++m) dmma884(acc[m][q][0], acc[m][q][1], a[m], b[q]);
     }
 #pragma unroll
-    for (int m = 0; m < 2; ++m) {
+    for (int m = 0; m < MB; ++m) {
       const int row = m * 8 + g8;
 #pragma unroll
       for (int q = 0; q < kFactNQ; ++q)
@@ -814,15 +816,21 @@ __global__ void __launch_bounds__(kFactWarps * 32)
   }
 }
 
+template <int BM, bool PCG>
+cudaError_t launch_fact_apply_bm(const DevOperator& op, const double* x, double* y, double* pq_acc,
+                                 const PcgScalars* guard, PcgScalars* sc, double* p0, double* p1, cudaStream_t s) {
+  const dim3 grid((unsigned)((op.n_cells + BM - 1) / BM)), block(kFactWarps * 32);
+  cudaError_t e = launch_k(fact_stage_a_kernel<BM, PCG>, grid, block, fact_a_layout(op.kp, BM).total, s, op, x, guard,
+                           sc, p0, p1);
+  if (e != cudaSuccess) return e;
+  return launch_k(fact_stage_b_kernel<BM, PCG>, grid, block, fact_b_layout(op.kp, op.nfp, BM).total, s, op, y, pq_acc,
+                  guard, sc);
+}
 template <bool PCG>
 cudaError_t launch_fact_apply(const DevOperator& op, const double* x, double* y, double* pq_acc,
                               const PcgScalars* guard, PcgScalars* sc, double* p0, double* p1, cudaStream_t s) {
-  const dim3 grid((unsigned)((op.n_cells + kFactBM - 1) / kFactBM)), block(kFactWarps * 32);
-  cudaError_t e = launch_k(fact_stage_a_kernel<PCG>, grid, block, fact_a_layout(op.kp).total, s, op, x, guard, sc, p0,
-                           p1);
-  if (e != cudaSuccess) return e;
-  return launch_k(fact_stage_b_kernel<PCG>, grid, block, fact_b_layout(op.kp, op.nfp).total, s, op, y, pq_acc, guard,
-                  sc);
+  return op.fact == 2 ? launch_fact_apply_bm<32, PCG>(op, x, y, pq_acc, guard, sc, p0, p1, s)
+                      : launch_fact_apply_bm<16, PCG>(op, x, y, pq_acc, guard, sc, p0, p1, s);
 }
 
 constexpr size_t kMaxSmem = 226 * 1024;  // 227 KB opt-in minus the static reduction scratch
@@ -2235,12 +2243,13 @@ int tune_fact(DevOperator& op, const double* x, double* y, PcgScalars* sc, doubl
   // Only meshes of >= kFactMinCells cells are considered: below that the two timings are
   // within noise, and a timing-dependent choice would make the rounding of small solves
   // (the iteration count of an ill-conditioned one) vary from setup to setup.
-  if (!fact_apply_fits(op) || op.n_cells < kFactMinCells) return 0;
+  if (!fact_apply_fits(op, 1) || op.n_cells < kFactMinCells) return 0;
   cudaEvent_t e0, e1;
   if (cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess) return -1;
-  float best[2] = {-1.f, -1.f};
+  float best[3] = {-1.f, -1.f, -1.f};  // DMMA apply, factored with 16 / 32 cells per tile
   for (int round = 0; round < 3; ++round)
-    for (int f = 0; f < 2; ++f) {
+    for (int f = 0; f < 3; ++f) {
+      if (f > 0 && !fact_apply_fits(op, f)) continue;
       DevOperator t = op;
       t.fact = f;
       if (launch_pcg_fused_apply(t, sc, x, p0, p1, y, s) != cudaSuccess) {
@@ -2258,12 +2267,16 @@ int tune_fact(DevOperator& op, const double* x, double* y, PcgScalars* sc, doubl
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   cudaGetLastError();
-  op.fact = best[1] >= 0.f && best[1] < best[0] ? 1 : 0;
+  int f = 0;
+  for (int k = 1; k < 3; ++k)
+    if (best[k] >= 0.f && best[k] < best[f]) f = k;
+  op.fact = f;
   return 0;
 }
 
-bool fact_apply_fits(const DevOperator& op) {
-  return op.F && fact_a_layout(op.kp).total <= kMaxSmem && fact_b_layout(op.kp, op.nfp).total <= kMaxSmem;
+bool fact_apply_fits(const DevOperator& op, int fact) {
+  const int bm = fact == 2 ? 32 : 16;
+  return op.F && fact_a_layout(op.kp, bm).total <= kMaxSmem && fact_b_layout(op.kp, op.nfp, bm).total <= kMaxSmem;
 }
 
 cudaError_t launch_pcg_update_jacobi(PcgScalars* sc, const DevPrecond& pc, const double* p0, const double* p1,
@@ -2295,10 +2308,14 @@ cudaError_t launch_dmma_peak(double* out, int n, int blocks, int threads, cudaSt
 
 namespace rdr {
 void configure_kernels() {  // errors here would surface as a later launch's cudaGetLastError
-  cudaFuncSetAttribute(fact_stage_a_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
-  cudaFuncSetAttribute(fact_stage_a_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
-  cudaFuncSetAttribute(fact_stage_b_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
-  cudaFuncSetAttribute(fact_stage_b_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
+  cudaFuncSetAttribute(fact_stage_a_kernel<16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
+  cudaFuncSetAttribute(fact_stage_a_kernel<16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
+  cudaFuncSetAttribute(fact_stage_b_kernel<16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
+  cudaFuncSetAttribute(fact_stage_b_kernel<16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
+  cudaFuncSetAttribute(fact_stage_a_kernel<32, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
+  cudaFuncSetAttribute(fact_stage_a_kernel<32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
+  cudaFuncSetAttribute(fact_stage_b_kernel<32, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
+  cudaFuncSetAttribute(fact_stage_b_kernel<32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
   cudaFuncSetAttribute(patch_ldg_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
   cudaFuncSetAttribute(patch_ldg_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
   int cnt = 0;

@@ -49,7 +49,7 @@ struct DevOperator {
   int av, ntiles, apply_grid, apply_slots;
   // factored apply (H(curl)): F [kp][nfp] (RefElement::F, zero-padded),
   // nf = its columns (nfm of them the value block), ubuf [n_cells][nfp] stage-A output;
-  // fact = 1: rdr_apply and the fused PCG run the two-stage factored kernels
+  // fact = 1 / 2: rdr_apply and the fused PCG run the two-stage factored kernels with 16 / 32 cells per tile
   const double* F;
   int nf, nfm, nfp, fact;
   int fck;                      // components of the second factor block: 3 (curls), 1 (divergence)
@@ -118,7 +118,7 @@ cudaError_t launch_pcg_direction(PcgScalars* sc, const double* z, double* p, dou
 // Fused PCG step (3 kernels per iteration for H(grad)): fused apply (direction
 // update + A p + ||z||^2 + stopping test), update + interior Jacobi, patches.
 bool fused_pcg_supported(const DevOperator& op);
-bool fact_apply_fits(const DevOperator& op);  // the factored apply's shared memory fits
+bool fact_apply_fits(const DevOperator& op, int fact);  // the factored apply's (op.fact = 1: 16, 2: 32 cells per tile) shared memory fits
 int tune_fact(DevOperator& op, const double* x, double* y, PcgScalars* sc, double* p0, double* p1, cudaStream_t s,
               int reps);
 // the apply's warp-layout variants (kernels.cu apply_variants): configure op for

@@ -1072,10 +1072,11 @@ int rdr_debug_set_apply_variant(rdr_handle* h, int variant) {
 int rdr_debug_set_apply_config(rdr_handle* h, int variant, int slots, int grid) {
   if (!h) return RDR_EINVAL;
   DevOperator t = h->op;
-  if (variant == -1) {  // the factored two-stage apply (H(curl))
-    if (!fact_apply_fits(t)) return RDR_EINVAL;
+  if (variant == -1 || variant == -2) {  // the factored two-stage apply, 16 / 32 cells per tile
+    const int f = -variant;
+    if (!fact_apply_fits(t, f)) return RDR_EINVAL;
     if (!t.fact && h->fused) h->launches_per_iter += 1;
-    t.fact = 1;
+    t.fact = f;
   } else {
     if (apply_configure_exact(t, variant, slots, grid)) return RDR_EINVAL;
     if (t.fact && h->fused) h->launches_per_iter -= 1;

@@ -431,25 +431,32 @@ def test_factored_apply(torch_cuda, space, p, n, perturb):
     S = rdr.Solver(c.vertices, c.tets, c.p, c.space, c.alpha, c.beta, c.mask, loop=rdr.LOOP_GRAPH)
     O = Oracle(c.vertices, c.tets, c.p, c.space, c.alpha, c.beta, c.mask)
     assert S.info["apply_factored"] == 0  # small meshes: setup never picks it (kFactMinCells)
-    assert S.set_apply_config(-1, 0, 0) and S.info["apply_factored"] == 1
     x = c.draw_vector(O.n_total)
     xt = torch.from_numpy(x).cuda()
     ya = O.apply(x)
-    assert rel(S.apply(xt).cpu().numpy(), ya) <= TOL
-    assert rel(S.debug_fused_apply(xt, torch.zeros_like(xt)).cpu().numpy(), O.apply(O.mask(x))) <= TOL
+    for v in (-1, -2):  # 16 and 32 cells per tile (the latter's shared memory does not fit at p >= 9)
+        if not S.set_apply_config(v, 0, 0):
+            assert v == -2 and p >= 9
+            continue
+        assert S.info["apply_factored"] == -v
+        assert rel(S.apply(xt).cpu().numpy(), ya) <= TOL, v
+        assert rel(S.debug_fused_apply(xt, torch.zeros_like(xt)).cpu().numpy(), O.apply(O.mask(x))) <= TOL, v
     # PCG with unit coefficients: with the 1e4 log-uniform contrast at p = 1 the iteration count
     # moves by 2 between two roundings of the same operator (DMMA 53, factored 52, oracle 54:
     # profiles/round2/experiments/fact_apply_rounding.txt), beyond the +-1 bar
     c = make_config(0, n=n, p=p, space=space, perturb=perturb, bc="x0", coeffs="one")
     S = rdr.Solver(c.vertices, c.tets, c.p, c.space, c.alpha, c.beta, c.mask, loop=rdr.LOOP_GRAPH)
     O = Oracle(c.vertices, c.tets, c.p, c.space, c.alpha, c.beta, c.mask)
-    assert S.set_apply_config(-1, 0, 0)
     b = c.draw_vector(O.n_total)
     hist = []
     xo, ito, _ = O.solve(b, rtol=1e-8, history=hist)
-    xg, it = S.solve(torch.from_numpy(b).cuda(), rtol=1e-8)
-    _check_iters(S, it, ito, lambda kk: hist[kk - 1] if 0 < kk <= len(hist) else None)
-    assert rel(xg.cpu().numpy(), xo) <= 1e-6
+    for v in (-1, -2):
+        if not S.set_apply_config(v, 0, 0):
+            assert v == -2 and p >= 9
+            continue
+        xg, it = S.solve(torch.from_numpy(b).cuda(), rtol=1e-8)
+        _check_iters(S, it, ito, lambda kk: hist[kk - 1] if 0 < kk <= len(hist) else None)
+        assert rel(xg.cpu().numpy(), xo) <= 1e-6, v
     # the factors behind it: sum_ab G_ab F_a F_b^T = the reference matrices to rounding
     lib = rdr._lib
     nl, nf, nfm = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()

@@ -148,8 +148,8 @@ struct rdr_info {
   int32_t apply_slots;         /* its TMA ring depth (reference-stack chunks of n_mat KB) */
   int32_t small_patch_grid;    /* > 0: all patches <= 128 dofs and setup's timing chose resident warps
                                   walking them (this many CTAs); 0: one warp per patch or CTA per patch */
-  int32_t apply_factored;      /* 1 / 2: the apply runs factored through orthonormal P_p / P_{p-1} bases
-                                  with 16 / 32 cells per tile
+  int32_t apply_factored;      /* 1 / 2 / 3: the apply runs factored through orthonormal P_p / P_{p-1} bases
+                                  with (16, 16) / (32, 32) / (32, 24) cells per tile of its two stages
                                   (two-stage kernels, H(curl) and H(div)), chosen by setup-time
                                   timing against the DMMA apply with the reference matrices */
 };
@@ -253,8 +253,8 @@ int rdr_debug_set_apply_variant(rdr_handle* h, int variant);
  * grid of resident CTAs) -- the three values rdr_info reports as apply_variant,
  * apply_slots and apply_grid -- so that a profiler run can reproduce the
  * configuration another setup's timing chose (scripts/prof_kernels.py --apply);
- * variant = -1 / -2 selects the factored two-stage apply with 16 / 32 cells per tile
- * (H(curl), H(div); rdr_info.apply_factored = 1 / 2; slots and grid ignored). RDR_EINVAL if it does not fit this operator. */
+ * variant = -1 / -2 / -3 selects the factored two-stage apply with (16, 16) / (32, 32) / (32, 24)
+ * cells per tile of its two stages (H(curl), H(div); rdr_info.apply_factored = 1 / 2 / 3; slots and grid ignored). RDR_EINVAL if it does not fit this operator. */
 int rdr_debug_set_apply_config(rdr_handle* h, int variant, int slots, int grid);
 
 /* Debugging entry point: run the small star patches (configurations whose

@@ -222,6 +222,11 @@ __global__ void __launch_bounds__((apply_mma_warps(BM, NQ, KS) + 1) * 32, MINB)
   constexpr int NT = NWARP * 32;
   constexpr int kChunk = apply_chunk_doubles(NM);
   constexpr uint32_t kChunkBytes = kChunk * sizeof(double);
+  // H(curl): the curl matrices (s >= NM0) vanish outside the leading ncb rows / columns of
+  // the lut_tc order, so chunks of rows >= ncb or groups of columns >= ncb carry, copy and
+  // multiply only the NM0 mass matrices (0.70 of the flops at p >= 8)
+  constexpr int NM0 = NM == 12 ? 6 : NM;
+  constexpr uint32_t kChunkBytes0 = apply_chunk_doubles(NM0) * sizeof(double);
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int n = op.n_loc, kp = op.kp;
   const int XS = apply_x_stride(kp);
@@ -250,7 +255,7 @@ __global__ void __launch_bounds__((apply_mma_warps(BM, NQ, KS) + 1) * 32, MINB)
     }
     mbar_fence_init();
   }
-  for (int i = threadIdx.x; i < kp; i += blockDim.x) LUT[i] = i < n ? op.lut[i] : 0;
+  for (int i = threadIdx.x; i < kp; i += blockDim.x) LUT[i] = i < n ? op.lut_tc[i] : 0;
   __syncthreads();
   const int prefilled = (int)min((int64_t)S, total_chunks);
   // producer cursor over the CTA's chunk sequence: unit group / chunk / ring slot,
@@ -258,8 +263,9 @@ __global__ void __launch_bounds__((apply_mma_warps(BM, NQ, KS) + 1) * 32, MINB)
   int p_grp = (int)(u0 % op.ngroups), p_c = 0, p_slot = 0;
   auto issue_next = [&]() {
     const double* src = op.Bsw + ((size_t)p_grp * nchunks + p_c) * kChunk;
-    mbar_expect_tx(&full[p_slot], kChunkBytes);
-    bulk_g2s(ring + p_slot * kChunk, src, kChunkBytes, &full[p_slot]);
+    const uint32_t bytes = (NM0 == NM || (4 * p_c < op.ncb && 32 * p_grp < op.ncb)) ? kChunkBytes : kChunkBytes0;
+    mbar_expect_tx(&full[p_slot], bytes);
+    bulk_g2s(ring + p_slot * kChunk, src, bytes, &full[p_slot]);
     if (++p_c == nchunks) {
       p_c = 0;
       if (++p_grp == op.ngroups) p_grp = 0;
@@ -390,12 +396,12 @@ __global__ void __launch_bounds__((apply_mma_warps(BM, NQ, KS) + 1) * 32, MINB)
       // ring position of this warp's first chunk of the unit (one division per unit)
       int slot = (int)((qbase + kg) % S);
       uint32_t par = (uint32_t)(((qbase + kg) / S) & 1);
+      const int cfull = (NM0 == NM || 32 * grp < op.ncb) ? op.ncb : 0;  // chunks c with 4 c < cfull: all NM
       for (int c = kg; c < nchunks; c += KS) {
         mbar_wait(&full[slot], par);
         const double* Bs = ring + slot * kChunk;
         const double x0 = xr0[4 * c], x1 = xr1[4 * c];
-#pragma unroll
-        for (int s = 0; s < NM; ++s) {
+        auto kstep = [&](const int s) {
           const double a0 = cs0[s] * x0, a1 = cs1[s] * x1;
           double b[NQ];
 #pragma unroll
@@ -405,6 +411,12 @@ __global__ void __launch_bounds__((apply_mma_warps(BM, NQ, KS) + 1) * 32, MINB)
             dmma884(acc[0][q][0], acc[0][q][1], a0, b[q]);
             dmma884(acc[1][q][0], acc[1][q][1], a1, b[q]);
           }
+        };
+#pragma unroll
+        for (int s = 0; s < NM0; ++s) kstep(s);
+        if (NM0 < NM && 4 * c < cfull) {
+#pragma unroll
+          for (int s = NM0; s < NM; ++s) kstep(s);
         }
         // every lane releases the slot after its own loads of it completed (DESIGN.md §6:
         // an arrive right behind the LDS let the TMA refill race the loads)
@@ -527,7 +539,11 @@ __global__ void __launch_bounds__((apply_mma_warps(BM, NQ, KS) + 1) * 32, MINB)
 // DMMA.8x8x4 with A from shared memory and B = F read through L1/L2 (op.F is
 // [kp][nfp], zero-padded, ~0.8 MB for Ned1_6). 8 warps, 16 cells per CTA, each warp
 // 16 cells x 32 columns per pass.
-constexpr int kFactWarps = 8, kFactNQ = 4;  // cells per tile: BM = 16 (op.fact 1) or 32 (op.fact 2)
+constexpr int kFactWarps = 8, kFactNQ = 4;
+// cells per tile of (stage A, stage B): op.fact 1 (16, 16), 2 (32, 32), 3 (32, 24: the V tile
+// of stage B small enough for two CTAs per SM up to Ned1_6 / RT_7)
+__host__ __device__ inline int fact_bm_a(int fact) { return fact == 1 ? 16 : 32; }
+__host__ __device__ inline int fact_bm_b(int fact) { return fact == 1 ? 16 : fact == 2 ? 32 : 24; }
 constexpr int64_t kFactMinCells = 2048;
 
 struct FactSmem {
@@ -816,21 +832,24 @@ __global__ void __launch_bounds__(kFactWarps * 32)
   }
 }
 
-template <int BM, bool PCG>
+template <int BMA, int BMB, bool PCG>
 cudaError_t launch_fact_apply_bm(const DevOperator& op, const double* x, double* y, double* pq_acc,
                                  const PcgScalars* guard, PcgScalars* sc, double* p0, double* p1, cudaStream_t s) {
-  const dim3 grid((unsigned)((op.n_cells + BM - 1) / BM)), block(kFactWarps * 32);
-  cudaError_t e = launch_k(fact_stage_a_kernel<BM, PCG>, grid, block, fact_a_layout(op.kp, BM).total, s, op, x, guard,
-                           sc, p0, p1);
+  const dim3 block(kFactWarps * 32);
+  cudaError_t e = launch_k(fact_stage_a_kernel<BMA, PCG>, dim3((unsigned)((op.n_cells + BMA - 1) / BMA)), block,
+                           fact_a_layout(op.kp, BMA).total, s, op, x, guard, sc, p0, p1);
   if (e != cudaSuccess) return e;
-  return launch_k(fact_stage_b_kernel<BM, PCG>, grid, block, fact_b_layout(op.kp, op.nfp, BM).total, s, op, y, pq_acc,
-                  guard, sc);
+  return launch_k(fact_stage_b_kernel<BMB, PCG>, dim3((unsigned)((op.n_cells + BMB - 1) / BMB)), block,
+                  fact_b_layout(op.kp, op.nfp, BMB).total, s, op, y, pq_acc, guard, sc);
 }
 template <bool PCG>
 cudaError_t launch_fact_apply(const DevOperator& op, const double* x, double* y, double* pq_acc,
                               const PcgScalars* guard, PcgScalars* sc, double* p0, double* p1, cudaStream_t s) {
-  return op.fact == 2 ? launch_fact_apply_bm<32, PCG>(op, x, y, pq_acc, guard, sc, p0, p1, s)
-                      : launch_fact_apply_bm<16, PCG>(op, x, y, pq_acc, guard, sc, p0, p1, s);
+  switch (op.fact) {
+    case 1: return launch_fact_apply_bm<16, 16, PCG>(op, x, y, pq_acc, guard, sc, p0, p1, s);
+    case 2: return launch_fact_apply_bm<32, 32, PCG>(op, x, y, pq_acc, guard, sc, p0, p1, s);
+    default: return launch_fact_apply_bm<32, 24, PCG>(op, x, y, pq_acc, guard, sc, p0, p1, s);
+  }
 }
 
 constexpr size_t kMaxSmem = 226 * 1024;  // 227 KB opt-in minus the static reduction scratch
@@ -2235,7 +2254,7 @@ cudaError_t launch_pcg_fused_apply(const DevOperator& op, PcgScalars* sc, const 
 }
 
 // Setup-time choice between the DMMA apply (op.fact = 0, its tuned layout) and the
-// factored two-stage apply (op.fact = 1): both timed on the PCG-mode kernels the solve
+// factored two-stage apply (op.fact = 1, 2, 3: its tile sizes): all timed on the PCG-mode kernels the solve
 // runs (scalars as in tune_apply), three interleaved rounds, best round each.
 int tune_fact(DevOperator& op, const double* x, double* y, PcgScalars* sc, double* p0, double* p1, cudaStream_t s,
               int reps) {
@@ -2246,9 +2265,10 @@ int tune_fact(DevOperator& op, const double* x, double* y, PcgScalars* sc, doubl
   if (!fact_apply_fits(op, 1) || op.n_cells < kFactMinCells) return 0;
   cudaEvent_t e0, e1;
   if (cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess) return -1;
-  float best[3] = {-1.f, -1.f, -1.f};  // DMMA apply, factored with 16 / 32 cells per tile
+  constexpr int kNF = 4;
+  float best[kNF] = {-1.f, -1.f, -1.f, -1.f};  // DMMA apply, factored with op.fact = 1, 2, 3
   for (int round = 0; round < 3; ++round)
-    for (int f = 0; f < 3; ++f) {
+    for (int f = 0; f < kNF; ++f) {
       if (f > 0 && !fact_apply_fits(op, f)) continue;
       DevOperator t = op;
       t.fact = f;
@@ -2268,15 +2288,15 @@ int tune_fact(DevOperator& op, const double* x, double* y, PcgScalars* sc, doubl
   cudaEventDestroy(e1);
   cudaGetLastError();
   int f = 0;
-  for (int k = 1; k < 3; ++k)
+  for (int k = 1; k < kNF; ++k)
     if (best[k] >= 0.f && best[k] < best[f]) f = k;
   op.fact = f;
   return 0;
 }
 
 bool fact_apply_fits(const DevOperator& op, int fact) {
-  const int bm = fact == 2 ? 32 : 16;
-  return op.F && fact_a_layout(op.kp, bm).total <= kMaxSmem && fact_b_layout(op.kp, op.nfp, bm).total <= kMaxSmem;
+  return op.F && fact >= 1 && fact <= 3 && fact_a_layout(op.kp, fact_bm_a(fact)).total <= kMaxSmem &&
+         fact_b_layout(op.kp, op.nfp, fact_bm_b(fact)).total <= kMaxSmem;
 }
 
 cudaError_t launch_pcg_update_jacobi(PcgScalars* sc, const DevPrecond& pc, const double* p0, const double* p1,
@@ -2315,6 +2335,8 @@ void configure_kernels() {  // errors here would surface as a later launch's cud
   cudaFuncSetAttribute(fact_stage_a_kernel<32, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
   cudaFuncSetAttribute(fact_stage_a_kernel<32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
   cudaFuncSetAttribute(fact_stage_b_kernel<32, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
+  cudaFuncSetAttribute(fact_stage_b_kernel<24, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
+  cudaFuncSetAttribute(fact_stage_b_kernel<24, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
   cudaFuncSetAttribute(fact_stage_b_kernel<32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
   cudaFuncSetAttribute(patch_ldg_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
   cudaFuncSetAttribute(patch_ldg_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);

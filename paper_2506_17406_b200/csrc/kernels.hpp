@@ -44,12 +44,17 @@ struct DevOperator {
   int ngroups;                  // ceil(n_loc / 32) column groups
   const double* Bsw;            // [ngroups][kp/4][n_mat][4][32]: the reference matrices stacked j-major
                                 // (chunk j4 = rows 4 j4 .. 4 j4 + 3 of every R_s), columns swizzled (kernels.cu
-                                // apply_tc_kernel)
+                                // apply_tc_kernel), in the local order of lut_tc
+  const uint16_t* lut_tc;       // [n_loc] lut in the DMMA apply's local order: H(curl) puts the ncb dofs whose
+                                // curl is not zero first (gradient dofs have curl 0, Eq. 3.14)
+  int ncb;                      // H(curl): the curl matrices R_6..R_11 vanish outside rows / columns [0, ncb)
+                                // of that order; n_loc otherwise
   // launch configuration (configure_apply): warp-layout variant, cell tiles, persistent grid
   int av, ntiles, apply_grid, apply_slots;
   // factored apply (H(curl)): F [kp][nfp] (RefElement::F, zero-padded),
   // nf = its columns (nfm of them the value block), ubuf [n_cells][nfp] stage-A output;
-  // fact = 1 / 2: rdr_apply and the fused PCG run the two-stage factored kernels with 16 / 32 cells per tile
+  // fact = 1 / 2 / 3: rdr_apply and the fused PCG run the two-stage factored kernels with (stage A, stage B)
+  // tiles of (16, 16) / (32, 32) / (32, 24) cells
   const double* F;
   int nf, nfm, nfp, fact;
   int fck;                      // components of the second factor block: 3 (curls), 1 (divergence)
@@ -118,7 +123,7 @@ cudaError_t launch_pcg_direction(PcgScalars* sc, const double* z, double* p, dou
 // Fused PCG step (3 kernels per iteration for H(grad)): fused apply (direction
 // update + A p + ||z||^2 + stopping test), update + interior Jacobi, patches.
 bool fused_pcg_supported(const DevOperator& op);
-bool fact_apply_fits(const DevOperator& op, int fact);  // the factored apply's (op.fact = 1: 16, 2: 32 cells per tile) shared memory fits
+bool fact_apply_fits(const DevOperator& op, int fact);  // the factored apply's (op.fact = 1, 2, 3) shared memory fits
 int tune_fact(DevOperator& op, const double* x, double* y, PcgScalars* sc, double* p0, double* p1, cudaStream_t s,
               int reps);
 // the apply's warp-layout variants (kernels.cu apply_variants): configure op for

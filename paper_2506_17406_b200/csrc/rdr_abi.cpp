@@ -328,9 +328,39 @@ static int setup_impl(rdr_handle* h, const double* vertices, int64_t nv, const i
   op.kp = (el.n + 3) / 4 * 4;
   op.ngroups = (el.n + 31) / 32;
   {
+    // The DMMA apply's local order. H(curl): the curl matrices R_6..R_11 (K^ab) are zero
+    // on the gradient dofs (curl grad = 0; Eq. 3.14 splits every entity's Ned1 dofs into
+    // gradients of H(grad) bubbles and the rest), up to rounding of the extended-precision
+    // build (<= 1e-16 of max |K^ab|): those dofs go last, the ncb others first, and the
+    // apply skips the curl matrices on chunks / column groups beyond ncb (kernels.cu).
+    std::vector<int> perm(el.n);
+    for (int i = 0; i < el.n; ++i) perm[i] = i;
+    op.ncb = el.n;
+    if (space == RDR_HCURL) {
+      const size_t nn = (size_t)el.n * el.n;
+      double mx = 0.0;
+      for (int s = 6; s < el.n_mat; ++s)
+        for (size_t k = 0; k < nn; ++k) mx = std::max(mx, std::fabs(el.R[s * nn + k]));
+      std::vector<char> curl(el.n, 0);
+      for (int s = 6; s < el.n_mat; ++s)
+        for (int i = 0; i < el.n; ++i)
+          for (int j = 0; j < el.n; ++j)
+            if (std::fabs(el.R[s * nn + (size_t)i * el.n + j]) > 1e-12 * mx) curl[i] = curl[j] = 1;
+      int k = 0;
+      for (int i = 0; i < el.n; ++i)
+        if (curl[i]) perm[k++] = i;
+      op.ncb = k;
+      for (int i = 0; i < el.n; ++i)
+        if (!curl[i]) perm[k++] = i;
+    }
+    std::vector<uint16_t> lut_tc(el.n);
+    for (int i = 0; i < el.n; ++i) lut_tc[i] = em.lut[perm[i]];
+    uint16_t* d_lut_tc;
+    if ((st = h->own_upload(&d_lut_tc, lut_tc))) return st;
+    op.lut_tc = d_lut_tc;
     // reference matrices stacked j-major in 32-column groups: group g, chunk j4,
-    // matrix s, row t holds R_s[4 j4 + t][32 g + c] at column c ^ (t << 2) (the
-    // shared-memory swizzle of apply_tc_kernel's B fragments)
+    // matrix s, row t holds R_s[4 j4 + t][32 g + c] (local order perm) at column
+    // c ^ (t << 2) (the shared-memory swizzle of apply_tc_kernel's B fragments)
     const int nm = el.n_mat, nj4 = op.kp / 4;
     std::vector<double> B((size_t)op.ngroups * nj4 * nm * 4 * 32, 0.0);
     for (int g = 0; g < op.ngroups; ++g)
@@ -342,7 +372,8 @@ static int setup_impl(rdr_handle* h, const double* vertices, int64_t nv, const i
             const size_t row = (((size_t)g * nj4 + j4) * nm + s) * 4 + t;
             for (int c = 0; c < 32; ++c) {
               const int col = 32 * g + c;
-              if (col < el.n) B[row * 32 + (c ^ (t << 2))] = el.R[((size_t)s * el.n + j) * el.n + col];
+              if (col < el.n && (s < 6 || (j < op.ncb && col < op.ncb)))
+                B[row * 32 + (c ^ (t << 2))] = el.R[((size_t)s * el.n + perm[j]) * el.n + perm[col]];
             }
           }
     double* d_B;
@@ -1072,7 +1103,7 @@ int rdr_debug_set_apply_variant(rdr_handle* h, int variant) {
 int rdr_debug_set_apply_config(rdr_handle* h, int variant, int slots, int grid) {
   if (!h) return RDR_EINVAL;
   DevOperator t = h->op;
-  if (variant == -1 || variant == -2) {  // the factored two-stage apply, 16 / 32 cells per tile
+  if (variant <= -1 && variant >= -3) {  // the factored two-stage apply, tile sizes op.fact = -variant
     const int f = -variant;
     if (!fact_apply_fits(t, f)) return RDR_EINVAL;
     if (!t.fact && h->fused) h->launches_per_iter += 1;

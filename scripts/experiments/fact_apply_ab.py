@@ -24,7 +24,8 @@ for spec in sys.argv[1:]:
            "layout": [i["apply_variant"], i["apply_slots"], i["apply_grid"]], "flops_12mat": i["flops_apply"]}
     b = torch.from_numpy(c.draw_vector(S.n_total)).cuda()
     tuned = (i["apply_variant"], i["apply_slots"], i["apply_grid"])
-    for name, cfgv in (("dmma", tuned), ("factored", (-1, 0, 0)), ("factored32", (-2, 0, 0))):
+    for name, cfgv in (("dmma", tuned), ("factored", (-1, 0, 0)), ("factored32", (-2, 0, 0)),
+                       ("factored32_24", (-3, 0, 0))):
         if not S.set_apply_config(*cfgv):
             continue
         k = min((S.time_kernels(b, b, reps=10) for _ in range(3)), key=lambda v: v[3])

@@ -243,7 +243,7 @@ void rdr_destroy(rdr_handle* h);
 const char* rdr_strerror(int code);
 
 /* Debugging entry point: run the operator apply (and the solves) with warp
- * layout `variant` (0 <= variant < 12; kernels.cu apply_variants) instead of the
+ * layout `variant` (0 <= variant < 18; kernels.cu apply_variants) instead of the
  * one setup's autotuning chose; RDR_EINVAL if it does not fit this operator.
  * The GPU tests use it to check every layout against the oracle. */
 int rdr_debug_set_apply_variant(rdr_handle* h, int variant);

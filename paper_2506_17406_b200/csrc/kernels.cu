@@ -214,7 +214,7 @@ __device__ __forceinline__ void mma_bar_sync(int nthreads) {  // named barrier 1
 // p.(Ap). In PCG mode the gather also forms p_k = z_k + beta_k p_{k-1}, which
 // the owner cell of each entity writes once (the CTA holding the tile's
 // column group 0), and the last CTA performs the stopping test (R-A16).
-template <int BM, int NQ, int KS, int NM, int MINB, bool PCG>
+template <int BM, int NQ, int KS, int NM, int NM0, int MINB, bool PCG>
 __global__ void __launch_bounds__((apply_mma_warps(BM, NQ, KS) + 1) * 32, MINB)
     apply_tc_kernel(DevOperator op, int S, const double* __restrict__ x, double* __restrict__ y, double* pq_acc,
                     const PcgScalars* guard, PcgScalars* sc, double* pbuf0, double* pbuf1) {
@@ -222,10 +222,10 @@ __global__ void __launch_bounds__((apply_mma_warps(BM, NQ, KS) + 1) * 32, MINB)
   constexpr int NT = NWARP * 32;
   constexpr int kChunk = apply_chunk_doubles(NM);
   constexpr uint32_t kChunkBytes = kChunk * sizeof(double);
-  // H(curl): the curl matrices (s >= NM0) vanish outside the leading ncb rows / columns of
-  // the lut_tc order, so chunks of rows >= ncb or groups of columns >= ncb carry, copy and
-  // multiply only the NM0 mass matrices (0.70 of the flops at p >= 8)
-  constexpr int NM0 = NM == 12 ? 6 : NM;
+  // H(curl) / H(div) (NM0 = 6 < NM): the curl (div-div) matrices s >= NM0 vanish outside the
+  // leading ncb rows / columns of the lut_tc order, so chunks of rows >= ncb or groups of
+  // columns >= ncb carry, copy and multiply only the NM0 mass matrices (0.70 of the flops
+  // for H(curl) at p >= 8, 0.87 for H(div)); H(grad): NM0 = NM
   constexpr uint32_t kChunkBytes0 = apply_chunk_doubles(NM0) * sizeof(double);
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int n = op.n_loc, kp = op.kp;
@@ -544,7 +544,6 @@ constexpr int kFactWarps = 8, kFactNQ = 4;
 // of stage B small enough for two CTAs per SM up to Ned1_6 / RT_7)
 __host__ __device__ inline int fact_bm_a(int fact) { return fact == 1 ? 16 : 32; }
 __host__ __device__ inline int fact_bm_b(int fact) { return fact == 1 ? 16 : fact == 2 ? 32 : 24; }
-constexpr int64_t kFactMinCells = 2048;
 
 struct FactSmem {
   size_t x, eb, lut, own, total;
@@ -854,17 +853,18 @@ cudaError_t launch_fact_apply(const DevOperator& op, const double* x, double* y,
 
 constexpr size_t kMaxSmem = 226 * 1024;  // 227 KB opt-in minus the static reduction scratch
 
-// The warp layouts built (BM, NQ, KS), each for NM = 7 (H(grad), H(div)) and 12
-// (H(curl)). The ring depth is sized per operator (apply_configure_variant).
+// The warp layouts built (BM, NQ, KS), each for NM = 7, NM0 = 7 (H(grad)), NM = 12,
+// NM0 = 6 (H(curl)) and NM = 7, NM0 = 6 (H(div)). The ring depth is sized per operator
+// (apply_configure_variant).
 struct ApplyVariant {
-  int bm, nq, ks, nm;
+  int bm, nq, ks, nm, nm0;
   const void* fn[2];  // plain, PCG
 };
-template <int BM, int NQ, int KS, int NM, int MINB = 1>
+template <int BM, int NQ, int KS, int NM, int MINB = 1, int NM0 = (NM == 12 ? 6 : NM)>
 ApplyVariant apply_variant() {
-  return {BM, NQ, KS, NM,
-          {(const void*)apply_tc_kernel<BM, NQ, KS, NM, MINB, false>,
-           (const void*)apply_tc_kernel<BM, NQ, KS, NM, MINB, true>}};
+  return {BM, NQ, KS, NM, NM0,
+          {(const void*)apply_tc_kernel<BM, NQ, KS, NM, NM0, MINB, false>,
+           (const void*)apply_tc_kernel<BM, NQ, KS, NM, NM0, MINB, true>}};
 }
 const ApplyVariant* apply_variants(int* count) {
   static const ApplyVariant v[] = {
@@ -874,6 +874,9 @@ const ApplyVariant* apply_variants(int* count) {
       apply_variant<16, 4, 4, 7>(),  apply_variant<16, 4, 4, 12>(),   // 4 MMA warps, 16 cells per unit
       apply_variant<32, 4, 4, 7, 2>(), apply_variant<32, 4, 4, 12, 2>(),  // 8 MMA warps, registers for 2 CTAs/SM
       apply_variant<16, 2, 4, 7>(),  apply_variant<16, 2, 4, 12>(),   // 8 MMA warps, 16 cells (large n_loc)
+      // the same six layouts for H(div) (the div-div matrix skipped beyond ncb)
+      apply_variant<32, 4, 2, 7, 1, 6>(), apply_variant<32, 4, 4, 7, 1, 6>(), apply_variant<32, 2, 2, 7, 1, 6>(),
+      apply_variant<16, 4, 4, 7, 1, 6>(), apply_variant<32, 4, 4, 7, 2, 6>(), apply_variant<16, 2, 4, 7, 1, 6>(),
   };
   *count = (int)(sizeof(v) / sizeof(v[0]));
   return v;
@@ -2068,7 +2071,7 @@ bool fused_pcg_supported(const DevOperator& op) { return op.Bsw && op.own; }
 int apply_configure_variant_ring(DevOperator& op, int k, int ring) {
   int cnt = 0;
   const ApplyVariant* vs = apply_variants(&cnt);
-  if (k < 0 || k >= cnt || vs[k].nm != op.n_mat) return -1;
+  if (k < 0 || k >= cnt || vs[k].nm != op.n_mat || vs[k].nm0 != op.nm0) return -1;
   const ApplyVariant& v = vs[k];
   // Ring depth: each K group consumes every KS-th chunk, so the ring holds S / KS
   // chunks ahead per group; take the deepest ring (up to 4 per group) that keeps
@@ -2255,9 +2258,10 @@ cudaError_t launch_pcg_fused_apply(const DevOperator& op, PcgScalars* sc, const 
 
 // Setup-time choice between the DMMA apply (op.fact = 0, its tuned layout) and the
 // factored two-stage apply (op.fact = 1, 2, 3: its tile sizes): all timed on the PCG-mode kernels the solve
-// runs (scalars as in tune_apply), three interleaved rounds, best round each.
-int tune_fact(DevOperator& op, const double* x, double* y, PcgScalars* sc, double* p0, double* p1, cudaStream_t s,
-              int reps) {
+// runs (scalars as in tune_apply), each behind the patch solves, three interleaved rounds,
+// best round each (the patch time is common to all candidates).
+int tune_fact(DevOperator& op, const DevPrecond& pc, const double* x, double* y, double* z, PcgScalars* sc, double* p0,
+              double* p1, cudaStream_t s, int reps) {
   op.fact = 0;
   // Only meshes of >= kFactMinCells cells are considered: below that the two timings are
   // within noise, and a timing-dependent choice would make the rounding of small solves
@@ -2276,8 +2280,15 @@ int tune_fact(DevOperator& op, const double* x, double* y, PcgScalars* sc, doubl
         cudaGetLastError();
         continue;
       }
+      // each apply behind the patch solves, as in the solve: they stream the patch
+      // inverses through L2, and the factored stages lost up to 0.15 ms per apply to
+      // that which a loop of applies alone did not show (RT_9: 0.345 ms alone, 0.499 ms
+      // in the solve; experiments/fact_in_solve.jsonl)
       cudaEventRecord(e0, s);
-      for (int r = 0; r < reps; ++r) launch_pcg_fused_apply(t, sc, x, p0, p1, y, s);
+      for (int r = 0; r < reps; ++r) {
+        launch_precond(pc, x, z, nullptr, nullptr, s);
+        launch_pcg_fused_apply(t, sc, x, p0, p1, y, s);
+      }
       cudaEventRecord(e1, s);
       if (cudaEventSynchronize(e1) != cudaSuccess) continue;
       float ms = 0.f;

@@ -45,10 +45,11 @@ struct DevOperator {
   const double* Bsw;            // [ngroups][kp/4][n_mat][4][32]: the reference matrices stacked j-major
                                 // (chunk j4 = rows 4 j4 .. 4 j4 + 3 of every R_s), columns swizzled (kernels.cu
                                 // apply_tc_kernel), in the local order of lut_tc
-  const uint16_t* lut_tc;       // [n_loc] lut in the DMMA apply's local order: H(curl) puts the ncb dofs whose
-                                // curl is not zero first (gradient dofs have curl 0, Eq. 3.14)
-  int ncb;                      // H(curl): the curl matrices R_6..R_11 vanish outside rows / columns [0, ncb)
-                                // of that order; n_loc otherwise
+  const uint16_t* lut_tc;       // [n_loc] lut in the DMMA apply's local order: H(curl) (H(div)) puts the ncb dofs
+                                // whose curl (divergence) is not zero first
+  int ncb;                      // H(curl) / H(div): the curl (div-div) matrices R_s, s >= nm0, vanish outside
+                                // rows / columns [0, ncb) of that order; n_loc for H(grad)
+  int nm0;                      // 6 (H(curl), H(div)) or n_mat (H(grad)): the DMMA apply variants built for it
   // launch configuration (configure_apply): warp-layout variant, cell tiles, persistent grid
   int av, ntiles, apply_grid, apply_slots;
   // factored apply (H(curl)): F [kp][nfp] (RefElement::F, zero-padded),
@@ -60,6 +61,13 @@ struct DevOperator {
   int fck;                      // components of the second factor block: 3 (curls), 1 (divergence)
   double* ubuf;
 };
+
+// Meshes below this many cells keep the reference element's own rounding of the
+// operator: setup does not consider the factored apply there, nor the skipped zero
+// blocks of the DMMA apply (both gain nothing on such launch-bound meshes, and with a 1e4
+// coefficient contrast two roundings of the same operator can move a PCG count by 2,
+// profiles/round2/experiments/fact_apply_rounding.txt, skip_rounding_small.txt).
+constexpr int64_t kFactMinCells = 2048;
 
 struct DevPrecond {
   int64_t n_total, off3;        // interior dofs are [off3, n_total)
@@ -124,8 +132,8 @@ cudaError_t launch_pcg_direction(PcgScalars* sc, const double* z, double* p, dou
 // update + A p + ||z||^2 + stopping test), update + interior Jacobi, patches.
 bool fused_pcg_supported(const DevOperator& op);
 bool fact_apply_fits(const DevOperator& op, int fact);  // the factored apply's (op.fact = 1, 2, 3) shared memory fits
-int tune_fact(DevOperator& op, const double* x, double* y, PcgScalars* sc, double* p0, double* p1, cudaStream_t s,
-              int reps);
+int tune_fact(DevOperator& op, const DevPrecond& pc, const double* x, double* y, double* z, PcgScalars* sc, double* p0,
+              double* p1, cudaStream_t s, int reps);
 // the apply's warp-layout variants (kernels.cu apply_variants): configure op for
 // variant k (0, or -1 if it does not fit this operator), and setup-time
 // autotuning over all that fit (x, y: device scratch of length n_total)

@@ -333,10 +333,14 @@ static int setup_impl(rdr_handle* h, const double* vertices, int64_t nv, const i
     // gradients of H(grad) bubbles and the rest), up to rounding of the extended-precision
     // build (<= 1e-16 of max |K^ab|): those dofs go last, the ncb others first, and the
     // apply skips the curl matrices on chunks / column groups beyond ncb (kernels.cu).
+    // H(div) likewise: the div-div matrix R_6 is zero on the divergence-free RT dofs
+    // (curls of Ned1 bubbles, §3.4.3), 0.87 of the flops. Meshes below
+    // kFactMinCells cells keep the element order and every entry (kernels.hpp).
     std::vector<int> perm(el.n);
     for (int i = 0; i < el.n; ++i) perm[i] = i;
     op.ncb = el.n;
-    if (space == RDR_HCURL) {
+    op.nm0 = space == RDR_HGRAD ? el.n_mat : 6;
+    if (space != RDR_HGRAD && nt >= kFactMinCells) {  // H(div): R_6 likewise on the div-free dofs
       const size_t nn = (size_t)el.n * el.n;
       double mx = 0.0;
       for (int s = 6; s < el.n_mat; ++s)
@@ -607,7 +611,7 @@ static int setup_impl(rdr_handle* h, const double* vertices, int64_t nv, const i
     h->h_sc->maxit = 1 << 30;
     CK(cudaMemcpy(h->d_sc, h->h_sc, sizeof(PcgScalars), cudaMemcpyHostToDevice));
     if (tune_apply(op, h->d_b, h->d_q, h->d_sc, h->d_p, h->d_p2, 0, 5)) return RDR_ECUDA;
-    if (tune_fact(op, h->d_b, h->d_q, h->d_sc, h->d_p, h->d_p2, 0, 5)) return RDR_ECUDA;
+    if (tune_fact(op, pc, h->d_b, h->d_q, h->d_z, h->d_sc, h->d_p, h->d_p2, 0, 5)) return RDR_ECUDA;
     if (op.fact && h->fused) h->launches_per_iter += 1;  // two stage kernels instead of one apply
     CK(cudaMemset(h->d_p, 0, vb));
     CK(cudaMemset(h->d_p2, 0, vb));

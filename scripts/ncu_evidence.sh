@@ -25,7 +25,9 @@ for spec in "$@"; do
   for k in ${KERNELS:-apply patch update}; do
     case $k in
       apply) sel='-k regex:apply_tc_kernel.*bool\)1 -s 1 -c 1' ;;
-      patch) sel='-k regex:patch_(ldg|warp)_kernel -s 1 -c 1' ;;
+      patch) sel='-k regex:patch_(ldg|warp|warp_loop)_kernel -s 1 -c 1' ;;
+      facta) sel='-k regex:fact_stage_a_kernel.*bool\)1 -s 1 -c 1' ;;
+      factb) sel='-k regex:fact_stage_b_kernel.*bool\)1 -s 1 -c 1' ;;
       update) sel='-k regex:pcg_update_jacobi -s 1 -c 1' ;;
     esac
     rep=/tmp/${TAG}_${name}_${k}

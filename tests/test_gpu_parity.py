@@ -403,7 +403,7 @@ def test_every_apply_layout(torch_cuda, space, p):
     hist = []
     _, ito, _ = O.solve(b, rtol=1e-8, history=hist)
     ran = 0
-    for k in range(12):
+    for k in range(18):  # 6 layouts x (H(grad), H(curl), H(div))
         if not S.set_apply_variant(k):
             continue
         ran += 1

@@ -95,7 +95,8 @@ enum { RDR_SETUP_DEVICE = 0, RDR_SETUP_HOST = 1 };
  *   RDR_LOOP_GRAPH -- one CUDA graph whose conditional WHILE node repeats a body
  *                of 8 iterations (3 kernels each: fused apply with the stopping
  *                test, update + Jacobi, patches) until the test fires (the
- *                hybrid preconditioner's unfused path uses RDR_LOOP_HOST);
+ *                hybrid preconditioner: a body of one unfused iteration, its
+ *                sweep included, so nothing runs past convergence);
  *   RDR_LOOP_PERSISTENT -- the whole solve in one persistent cooperative kernel
  *                (grid barriers between the phases of each iteration; CUDA-core
  *                apply with the reference matrices in shared memory, one warp

@@ -853,13 +853,17 @@ static int build_graph(rdr_handle* h, int iters) {
   return RDR_OK;
 }
 
-// Device-side PCG loop (fused path): one graph whose while node repeats a body
-// of kWhileUnroll iterations until the fused apply's stopping test clears the
-// condition, so a whole solve is one graph launch and one host
-// synchronisation. (A body per iteration measured ~3 us/iteration slower
-// than the host-driven 8-iteration graphs: the conditional node's body launch
-// is not free, so it is amortised over several iterations.)
+// Device-side PCG loop: one graph whose while node repeats a body of
+// while_unroll(h) iterations until the stopping test (inside the fused apply;
+// pcg_finish_kernel on the unfused path) clears the condition, so a whole
+// solve is one graph launch and one host synchronisation. (Fused path: a body
+// per iteration measured ~3 us/iteration slower than the host-driven
+// 8-iteration graphs: the conditional node's body launch is not free, so it is
+// amortised over several iterations. The hybrid sweep is 20+ launches per
+// iteration and converges in 10-25 iterations, so its body is one iteration:
+// nothing runs past the iteration that converged.)
 constexpr int kWhileUnroll = 8;
+static int while_unroll(const rdr_handle* h) { return h->fused ? kWhileUnroll : h->pc.hybrid ? 1 : 4; }
 static int build_while_graph(rdr_handle* h) {
   if (h->wgraph) return RDR_OK;
   cudaGraph_t g;
@@ -876,7 +880,7 @@ static int build_while_graph(rdr_handle* h) {
   cudaGraph_t body = params.conditional.phGraph_out[0];
   CK(cudaStreamBeginCaptureToGraph(h->cap_stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
   int st = RDR_OK;
-  for (int k = 0; k < kWhileUnroll && st == RDR_OK; ++k) st = enqueue_iteration(h, h->cap_stream);
+  for (int k = 0; k < while_unroll(h) && st == RDR_OK; ++k) st = enqueue_iteration(h, h->cap_stream);
   if (st == RDR_OK) {
     cudaError_t ce = launch_pcg_loop_condition(h->d_sc, loop, h->cap_stream);
     if (ce != cudaSuccess) st = cuda_status(ce);
@@ -933,8 +937,8 @@ static int fetch_scalars(rdr_handle* h, cudaStream_t s) {
 
 // One PCG solve. rdr_options.loop: RDR_LOOP_DEVICE -- one graph whose while node
 // repeats 8-iteration bodies until the device-side stopping test fires (one host
-// synchronisation per solve; fused path; the unfused hybrid path falls back to
-// RDR_LOOP_HOST); RDR_LOOP_HOST -- graphs of 8 iterations relaunched by the host
+// synchronisation per solve; the hybrid preconditioner's unfused iteration with a
+// one-iteration body); RDR_LOOP_HOST -- graphs of 8 iterations relaunched by the host
 // until done; RDR_LOOP_EAGER -- every kernel launched on the stream, the host
 // checking the stop flag after each iteration (no graphs: profilers see every
 // launch).
@@ -957,13 +961,17 @@ static int solve_device(rdr_handle* h, const double* b, double rtol, int maxit, 
   if (st) return st;
   // the unfused path tests before each iteration, the fused one inside its apply
   const bool test_first = !h->fused;
-  if (h->fused && (h->loop == RDR_LOOP_DEVICE || h->loop == RDR_LOOP_GRAPH)) {
+  if (h->loop == RDR_LOOP_DEVICE || h->loop == RDR_LOOP_GRAPH) {
     if ((st = build_while_graph(h))) return st;
     CK(cudaGraphLaunch(h->wgraph, s));
     if ((st = fetch_scalars(h, s))) return st;
-    // bodies of kWhileUnroll iterations (+ the condition kernel) ran until the one that detected convergence
-    const int64_t bodies = (h->h_sc->k + kWhileUnroll - 1) / kWhileUnroll;
-    launches += bodies * (kWhileUnroll * h->launches_per_iter + 1);
+    // bodies of U iterations (+ the condition kernel) ran until the one that detected convergence
+    // (fused: k counts the fused applies; unfused: the first body always runs, its kernels
+    // returning at once when the start already set the stop flag)
+    const int U = while_unroll(h);
+    const int64_t steps = h->fused ? h->h_sc->k : std::max(h->h_sc->iters, 1);
+    const int64_t bodies = (steps + U - 1) / U;
+    launches += bodies * ((int64_t)U * h->launches_per_iter + 1);
   } else if (h->loop == RDR_LOOP_EAGER) {
     for (;;) {
       if (test_first) {

@@ -2257,18 +2257,26 @@ cudaError_t launch_pcg_fused_apply(const DevOperator& op, PcgScalars* sc, const 
 }
 
 // Setup-time choice between the DMMA apply (op.fact = 0, its tuned layout) and the
-// factored two-stage apply (op.fact = 1, 2, 3: its tile sizes): all timed on the PCG-mode kernels the solve
-// runs (scalars as in tune_apply), each behind the patch solves, three interleaved rounds,
-// best round each (the patch time is common to all candidates).
-int tune_fact(DevOperator& op, const DevPrecond& pc, const double* x, double* y, double* z, PcgScalars* sc, double* p0,
-              double* p1, cudaStream_t s, int reps) {
+// factored two-stage apply (op.fact = 1, 2, 3: its tile sizes), timed on the iteration the
+// solve runs: for each candidate a PCG on b is started (x = 0, r = b, z = P^-1 r; sc_init:
+// the scalars with rtol 0 and a huge maxit, so the stopping test never fires) and `reps`
+// whole iterations (fused apply, update + Jacobi, patch solves) are timed after a warm-up
+// one, in three interleaved rounds, best round each. The factored stages lose up to
+// 0.15 ms per apply inside the iteration which a loop of applies alone does not show (RT_9:
+// 0.345 ms alone, 0.499 ms in the solve; experiments/fact_in_solve.jsonl), and a loop of
+// patch solves + apply without the vector update reproduced only part of that: on close
+// calls (RT_9, Ned1_5) it picked the slower iteration in some setups.
+int tune_fact(DevOperator& op, const DevPrecond& pc, const double* b, const uint8_t* cons, double* x, double* r,
+              double* z, double* q, PcgScalars* sc, const PcgScalars* sc_init, double* p0, double* p1,
+              cudaStream_t s, int reps) {
   op.fact = 0;
   // Only meshes of >= kFactMinCells cells are considered: below that the two timings are
   // within noise, and a timing-dependent choice would make the rounding of small solves
   // (the iteration count of an ill-conditioned one) vary from setup to setup.
-  if (!fact_apply_fits(op, 1) || op.n_cells < kFactMinCells) return 0;
+  if (!fact_apply_fits(op, 1) || op.n_cells < kFactMinCells || !fused_pcg_supported(op)) return 0;
   cudaEvent_t e0, e1;
   if (cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess) return -1;
+  const int64_t n = pc.n_total;
   constexpr int kNF = 4;
   float best[kNF] = {-1.f, -1.f, -1.f, -1.f};  // DMMA apply, factored with op.fact = 1, 2, 3
   for (int round = 0; round < 3; ++round)
@@ -2276,19 +2284,23 @@ int tune_fact(DevOperator& op, const DevPrecond& pc, const double* x, double* y,
       if (f > 0 && !fact_apply_fits(op, f)) continue;
       DevOperator t = op;
       t.fact = f;
-      if (launch_pcg_fused_apply(t, sc, x, p0, p1, y, s) != cudaSuccess) {
+      auto iteration = [&]() {
+        cudaError_t e = launch_pcg_fused_apply(t, sc, z, p0, p1, q, s);
+        if (e == cudaSuccess) e = launch_pcg_update_jacobi(sc, pc, p0, p1, q, x, r, z, s);
+        if (e == cudaSuccess) e = launch_precond_part(1, pc, r, z, &sc->rz_acc, sc, s);
+        return e;
+      };
+      bool ok = cudaMemcpyAsync(sc, sc_init, sizeof(PcgScalars), cudaMemcpyHostToDevice, s) == cudaSuccess &&
+                cudaMemsetAsync(p0, 0, sizeof(double) * n, s) == cudaSuccess &&
+                cudaMemsetAsync(p1, 0, sizeof(double) * n, s) == cudaSuccess &&
+                launch_pcg_init(b, cons, n, x, r, q, s) == cudaSuccess &&
+                launch_precond(pc, r, z, &sc->rz_acc, nullptr, s) == cudaSuccess && iteration() == cudaSuccess;
+      if (!ok) {
         cudaGetLastError();
         continue;
       }
-      // each apply behind the patch solves, as in the solve: they stream the patch
-      // inverses through L2, and the factored stages lost up to 0.15 ms per apply to
-      // that which a loop of applies alone did not show (RT_9: 0.345 ms alone, 0.499 ms
-      // in the solve; experiments/fact_in_solve.jsonl)
       cudaEventRecord(e0, s);
-      for (int r = 0; r < reps; ++r) {
-        launch_precond(pc, x, z, nullptr, nullptr, s);
-        launch_pcg_fused_apply(t, sc, x, p0, p1, y, s);
-      }
+      for (int k = 0; k < reps; ++k) iteration();
       cudaEventRecord(e1, s);
       if (cudaEventSynchronize(e1) != cudaSuccess) continue;
       float ms = 0.f;
@@ -2300,7 +2312,7 @@ int tune_fact(DevOperator& op, const DevPrecond& pc, const double* x, double* y,
   cudaGetLastError();
   int f = 0;
   for (int k = 1; k < kNF; ++k)
-    if (best[k] >= 0.f && best[k] < best[f]) f = k;
+    if (best[k] >= 0.f && (best[f] < 0.f || best[k] < best[f])) f = k;
   op.fact = f;
   return 0;
 }

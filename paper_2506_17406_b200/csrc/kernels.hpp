@@ -132,8 +132,11 @@ cudaError_t launch_pcg_direction(PcgScalars* sc, const double* z, double* p, dou
 // update + A p + ||z||^2 + stopping test), update + interior Jacobi, patches.
 bool fused_pcg_supported(const DevOperator& op);
 bool fact_apply_fits(const DevOperator& op, int fact);  // the factored apply's (op.fact = 1, 2, 3) shared memory fits
-int tune_fact(DevOperator& op, const DevPrecond& pc, const double* x, double* y, double* z, PcgScalars* sc, double* p0,
-              double* p1, cudaStream_t s, int reps);
+// setup-time choice of op.fact, timed on whole PCG iterations (b: right-hand side, cons: constrained flags,
+// x, r, z, q, p0, p1: the solve's vectors, sc_init: host scalars with rtol 0 and a huge maxit)
+int tune_fact(DevOperator& op, const DevPrecond& pc, const double* b, const uint8_t* cons, double* x, double* r,
+              double* z, double* q, PcgScalars* sc, const PcgScalars* sc_init, double* p0, double* p1,
+              cudaStream_t s, int reps);
 // the apply's warp-layout variants (kernels.cu apply_variants): configure op for
 // variant k (0, or -1 if it does not fit this operator), and setup-time
 // autotuning over all that fit (x, y: device scratch of length n_total)

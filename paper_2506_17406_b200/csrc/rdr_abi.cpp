@@ -611,7 +611,8 @@ static int setup_impl(rdr_handle* h, const double* vertices, int64_t nv, const i
     h->h_sc->maxit = 1 << 30;
     CK(cudaMemcpy(h->d_sc, h->h_sc, sizeof(PcgScalars), cudaMemcpyHostToDevice));
     if (tune_apply(op, h->d_b, h->d_q, h->d_sc, h->d_p, h->d_p2, 0, 5)) return RDR_ECUDA;
-    if (tune_fact(op, pc, h->d_b, h->d_q, h->d_z, h->d_sc, h->d_p, h->d_p2, 0, 5)) return RDR_ECUDA;
+    if (tune_fact(op, pc, h->d_b, h->d_cons, h->d_x, h->d_r, h->d_z, h->d_q, h->d_sc, h->h_sc, h->d_p, h->d_p2, 0, 5))
+      return RDR_ECUDA;
     if (op.fact && h->fused) h->launches_per_iter += 1;  // two stage kernels instead of one apply
     CK(cudaMemset(h->d_p, 0, vb));
     CK(cudaMemset(h->d_p2, 0, vb));

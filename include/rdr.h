@@ -153,6 +153,8 @@ struct rdr_info {
                                   with (16, 16) / (32, 32) / (32, 24) cells per tile of its two stages
                                   (two-stage kernels, H(curl) and H(div)), chosen by setup-time
                                   timing against the DMMA apply with the reference matrices */
+  int32_t apply_fact_split_a;  /* factored apply: CTAs per cell tile in stage A (each a share of the 32-column */
+  int32_t apply_fact_split_b;  /* blocks of U) and in stage B (of Y), chosen by the same timing; 0 if not factored */
 };
 
 /* Build the operator and the preconditioner (host setup once, then upload).
@@ -224,6 +226,18 @@ int rdr_last_solve(const rdr_handle* h, struct rdr_solve_stats* out);
 int rdr_profile_solve(rdr_handle* h, const double* b, double rtol, int maxit, int* iters, double* ms,
                       void* stream);
 
+/* Measurement helper: the SM clock the fused apply runs at, inside the PCG
+ * iteration and alone. A PCG on b (device, n_total) is run for `iters` timed
+ * iterations with rtol 0 (stream launches, no host synchronisation in
+ * between), with a one-thread probe kernel behind each fused apply that spins
+ * 10 us of %globaltimer and reads clock64; then the fused apply is launched
+ * `iters` times back to back with the same probe. out[4] (host): out[0] mean
+ * SM MHz behind the apply in the iteration, out[1] the same for the apply
+ * alone, out[2] ms per iteration (probe time subtracted), out[3] ms per apply
+ * alone. Additive preconditioner only (RDR_EINVAL otherwise). Synchronizes
+ * `stream`; the handle's solve vectors are overwritten. */
+int rdr_debug_profile_clocks(rdr_handle* h, const double* b, int iters, double* out, void* stream);
+
 /* Measurement helper (bench.py roofline): launch each hot-path kernel `reps`
  * times back to back on `stream` between CUDA events and return the average
  * device time per launch in ms: ms[0] operator apply (gather-contract-scatter),
@@ -255,7 +269,9 @@ int rdr_debug_set_apply_variant(rdr_handle* h, int variant);
  * apply_slots and apply_grid -- so that a profiler run can reproduce the
  * configuration another setup's timing chose (scripts/prof_kernels.py --apply);
  * variant = -1 / -2 / -3 selects the factored two-stage apply with (16, 16) / (32, 32) / (32, 24)
- * cells per tile of its two stages (H(curl), H(div); rdr_info.apply_factored = 1 / 2 / 3; slots and grid ignored). RDR_EINVAL if it does not fit this operator. */
+ * cells per tile of its two stages (H(curl), H(div); rdr_info.apply_factored = 1 / 2 / 3), with
+ * `slots` / `grid` (0..8, 0 = 1) CTAs per cell tile in stage A / stage B (rdr_info.apply_fact_split_a / _b).
+ * RDR_EINVAL if it does not fit this operator. */
 int rdr_debug_set_apply_config(rdr_handle* h, int variant, int slots, int grid);
 
 /* Debugging entry point: run the small star patches (configurations whose

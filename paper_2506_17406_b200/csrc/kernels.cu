@@ -582,6 +582,9 @@ __global__ void __launch_bounds__(kFactWarps * 32)
   uint16_t* LUT = reinterpret_cast<uint16_t*>(fsm_raw + L.lut);
   uint16_t* OWN = reinterpret_cast<uint16_t*>(fsm_raw + L.own);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g8 = lane >> 2, t4 = lane & 3;
+  // gridDim.y column splits per cell tile (op.fact_nsa): split sp takes the 32-column blocks
+  // sp, sp + ns, ... of U; every split gathers the tile, split 0 writes the direction
+  const int ns = gridDim.y, sp = blockIdx.y;
   const int64_t c0 = (int64_t)blockIdx.x * BM;
   const int nc = (int)min((int64_t)BM, op.n_cells - c0);
   for (int i = tid; i < kp; i += NT) LUT[i] = i < n ? op.lut[i] : 0;
@@ -627,7 +630,7 @@ __global__ void __launch_bounds__(kFactWarps * 32)
         v = xv;
         if (PCG) {
           v = fma(beta, p_old[g], xv);
-          if ((OWN[c] >> (l >> kLutShift)) & 1) {
+          if (sp == 0 && ((OWN[c] >> (l >> kLutShift)) & 1)) {
             p_new[g] = v;
             zz = fma(xv, xv, zz);
           }
@@ -640,7 +643,7 @@ __global__ void __launch_bounds__(kFactWarps * 32)
   // ---- stage A: U = X F, warp = 32-column block, BM cells
   const double* xr = X + g8 * XS + t4;
   const int nblk = nfp / 32;
-  for (int blk = warp; blk < nblk; blk += kFactWarps) {
+  for (int blk = sp + ns * warp; blk < nblk; blk += ns * kFactWarps) {
     double acc[MB][kFactNQ][2];
 #pragma unroll
     for (int m = 0; m < MB; ++m)
@@ -679,7 +682,7 @@ __global__ void __launch_bounds__(kFactWarps * 32)
     if (tid == 0) {
       atomicAdd(&sc->zz, szz);
       __threadfence();
-      last = atomicAdd(&sc->ticket, 1u) == gridDim.x - 1;
+      last = atomicAdd(&sc->ticket, 1u) == gridDim.x * gridDim.y - 1;
     }
     __syncthreads();
     if (last && tid == 0) {
@@ -734,6 +737,9 @@ __global__ void __launch_bounds__(kFactWarps * 32)
   uint16_t* LUT = reinterpret_cast<uint16_t*>(fsm_raw + L.lut);
   double* C = reinterpret_cast<double*>(fsm_raw + L.own);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g8 = lane >> 2, t4 = lane & 3;
+  // gridDim.y column splits per cell tile (op.fact_nsb): split sp takes the 32-column blocks
+  // sp, sp + ns, ... of Y; every split loads and mixes the U tile, split 0 accumulates p.Ap
+  const int ns = gridDim.y, sp = blockIdx.y;
   const int64_t c0 = (int64_t)blockIdx.x * BM;
   const int nc = (int)min((int64_t)BM, op.n_cells - c0);
   for (int i = tid; i < kp; i += NT) LUT[i] = i < n ? op.lut[i] : 0;
@@ -774,10 +780,11 @@ __global__ void __launch_bounds__(kFactWarps * 32)
     pq = fma(u0, v0, fma(u1, v1, fma(u2, v2, pq)));
   }
   __syncthreads();
+  if (sp != 0) pq = 0.0;
   // ---- stage B: Y = V F^T, warp = 32 output columns, BM cells
   const double* vrow = V + g8 * VS + t4;
   const int nblk = (kp + 31) / 32;
-  for (int blk = warp; blk < nblk; blk += kFactWarps) {
+  for (int blk = sp + ns * warp; blk < nblk; blk += ns * kFactWarps) {
     double acc[MB][kFactNQ][2];
 #pragma unroll
     for (int m = 0; m < MB; ++m)
@@ -835,10 +842,11 @@ template <int BMA, int BMB, bool PCG>
 cudaError_t launch_fact_apply_bm(const DevOperator& op, const double* x, double* y, double* pq_acc,
                                  const PcgScalars* guard, PcgScalars* sc, double* p0, double* p1, cudaStream_t s) {
   const dim3 block(kFactWarps * 32);
-  cudaError_t e = launch_k(fact_stage_a_kernel<BMA, PCG>, dim3((unsigned)((op.n_cells + BMA - 1) / BMA)), block,
+  const unsigned nsa = (unsigned)std::max(1, op.fact_nsa), nsb = (unsigned)std::max(1, op.fact_nsb);
+  cudaError_t e = launch_k(fact_stage_a_kernel<BMA, PCG>, dim3((unsigned)((op.n_cells + BMA - 1) / BMA), nsa), block,
                            fact_a_layout(op.kp, BMA).total, s, op, x, guard, sc, p0, p1);
   if (e != cudaSuccess) return e;
-  return launch_k(fact_stage_b_kernel<BMB, PCG>, dim3((unsigned)((op.n_cells + BMB - 1) / BMB)), block,
+  return launch_k(fact_stage_b_kernel<BMB, PCG>, dim3((unsigned)((op.n_cells + BMB - 1) / BMB), nsb), block,
                   fact_b_layout(op.kp, op.nfp, BMB).total, s, op, y, pq_acc, guard, sc);
 }
 template <bool PCG>
@@ -2277,13 +2285,27 @@ int tune_fact(DevOperator& op, const DevPrecond& pc, const double* b, const uint
   cudaEvent_t e0, e1;
   if (cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess) return -1;
   const int64_t n = pc.n_total;
-  constexpr int kNF = 4;
-  float best[kNF] = {-1.f, -1.f, -1.f, -1.f};  // DMMA apply, factored with op.fact = 1, 2, 3
+  // candidates: the DMMA apply, the factored apply with op.fact = 1, 2, 3 and, for the 32-cell
+  // tiles, column splits (stage A, stage B) that leave every CTA >= 3 column blocks (the stages
+  // launch one CTA per cell tile otherwise: 96 and 128 CTAs on the 8^3 x 6 mesh, 1.1 and 1.5
+  // waves on config 4; experiments/fact_split_in_solve.jsonl)
+  struct Cand {
+    int f, nsa, nsb;
+  };
+  std::vector<Cand> cand = {{0, 1, 1}, {1, 1, 1}};
+  const int nblk_a = op.nfp / 32, nblk_b = (op.kp + 31) / 32;
+  for (int f = 2; f <= 3; ++f)
+    for (const Cand& c : {Cand{f, 1, 1}, Cand{f, 2, 1}, Cand{f, 2, 2}, Cand{f, 3, 1}, Cand{f, 3, 2}, Cand{f, 4, 2}})
+      if ((c.nsa == 1 || nblk_a / c.nsa >= 3) && (c.nsb == 1 || nblk_b / c.nsb >= 3)) cand.push_back(c);
+  const int kNF = (int)cand.size();
+  std::vector<float> best(kNF, -1.f);
   for (int round = 0; round < 3; ++round)
     for (int f = 0; f < kNF; ++f) {
-      if (f > 0 && !fact_apply_fits(op, f)) continue;
+      if (cand[f].f > 0 && !fact_apply_fits(op, cand[f].f)) continue;
       DevOperator t = op;
-      t.fact = f;
+      t.fact = cand[f].f;
+      t.fact_nsa = cand[f].nsa;
+      t.fact_nsb = cand[f].nsb;
       auto iteration = [&]() {
         cudaError_t e = launch_pcg_fused_apply(t, sc, z, p0, p1, q, s);
         if (e == cudaSuccess) e = launch_pcg_update_jacobi(sc, pc, p0, p1, q, x, r, z, s);
@@ -2313,7 +2335,9 @@ int tune_fact(DevOperator& op, const DevPrecond& pc, const double* b, const uint
   int f = 0;
   for (int k = 1; k < kNF; ++k)
     if (best[k] >= 0.f && (best[f] < 0.f || best[k] < best[f])) f = k;
-  op.fact = f;
+  op.fact = cand[f].f;
+  op.fact_nsa = cand[f].nsa;
+  op.fact_nsb = cand[f].nsb;
   return 0;
 }
 
@@ -2340,6 +2364,24 @@ __global__ void dmma_peak_kernel(double* out, int n) {
     dmma884(f0, f1, a, b);
   }
   if (c0 + d0 + e0 + f0 + c1 + d1 + e1 + f1 == 1.2345) out[0] = 1.0;
+}
+
+// SM clock probe (rdr_debug_profile_clocks): one thread spins `ns` nanoseconds of the
+// global timer and adds the SM cycles per microsecond it saw (MHz) to acc[0], 1 to acc[1]
+__global__ void sm_clock_probe_kernel(double* acc, unsigned ns) {
+  unsigned long long t0, t1;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  const long long c0 = clock64();
+  do {
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+  } while (t1 - t0 < ns);
+  const long long c1 = clock64();
+  acc[0] += (double)(c1 - c0) * 1e3 / (double)(t1 - t0);
+  acc[1] += 1.0;
+}
+cudaError_t launch_sm_clock_probe(double* acc, unsigned ns, cudaStream_t s) {
+  sm_clock_probe_kernel<<<1, 1, 0, s>>>(acc, ns);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_dmma_peak(double* out, int n, int blocks, int threads, cudaStream_t s) {

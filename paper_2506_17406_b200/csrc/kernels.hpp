@@ -58,6 +58,7 @@ struct DevOperator {
   // tiles of (16, 16) / (32, 32) / (32, 24) cells
   const double* F;
   int nf, nfm, nfp, fact;
+  int fact_nsa, fact_nsb;       // column splits of a cell tile over CTAs in stage A / stage B (grid.y; 0 = 1)
   int fck;                      // components of the second factor block: 3 (curls), 1 (divergence)
   double* ubuf;
 };
@@ -172,5 +173,6 @@ size_t max_kernel_smem();                           // per-CTA dynamic shared-me
 void configure_kernels();                            // shared-memory opt-ins (call once, outside capture)
 // DMMA.8x8x4 issue-bound loop: n iterations x 4 chains x 512 flop per warp
 cudaError_t launch_dmma_peak(double* out, int n, int blocks, int threads, cudaStream_t s);
+cudaError_t launch_sm_clock_probe(double* acc, unsigned ns, cudaStream_t s);  // acc[0] += MHz, acc[1] += 1
 
 }  // namespace rdr

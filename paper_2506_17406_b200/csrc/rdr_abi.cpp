@@ -386,6 +386,7 @@ static int setup_impl(rdr_handle* h, const double* vertices, int64_t nv, const i
   }
   op.F = nullptr;
   op.nf = op.nfm = op.nfp = op.fact = 0;
+  op.fact_nsa = op.fact_nsb = 1;
   op.fck = space == RDR_HDIV ? 1 : 3;
   op.ubuf = nullptr;
   if (el.nf > 0) {  // factored apply: F [kp][nfp] zero-padded, stage-A buffer
@@ -646,6 +647,8 @@ static int setup_impl(rdr_handle* h, const double* vertices, int64_t nv, const i
   in.apply_slots = op.apply_slots;
   in.small_patch_grid = pc.small_grid;
   in.apply_factored = op.fact;
+  in.apply_fact_split_a = op.fact ? op.fact_nsa : 0;
+  in.apply_fact_split_b = op.fact ? op.fact_nsb : 0;
   in.patch_setup_flops = 0;
   for (int32_t n : P.n) {  // lower tiles I >= J, I, J != K: nb(nb-1)/2 per K; panel: nb-1 per K
     const double nb = (n + 63) / 64;
@@ -1103,6 +1106,7 @@ int rdr_debug_set_apply_variant(rdr_handle* h, int variant) {
   if (t.fact && h->fused) h->launches_per_iter -= 1;
   t.fact = 0;
   h->info.apply_factored = 0;
+  h->info.apply_fact_split_a = h->info.apply_fact_split_b = 0;
   h->op = t;
   if (h->graph) cudaGraphExecDestroy(h->graph);
   if (h->wgraph) cudaGraphExecDestroy(h->wgraph);
@@ -1119,14 +1123,19 @@ int rdr_debug_set_apply_config(rdr_handle* h, int variant, int slots, int grid) 
   if (variant <= -1 && variant >= -3) {  // the factored two-stage apply, tile sizes op.fact = -variant
     const int f = -variant;
     if (!fact_apply_fits(t, f)) return RDR_EINVAL;
+    if (slots < 0 || slots > 8 || grid < 0 || grid > 8) return RDR_EINVAL;
     if (!t.fact && h->fused) h->launches_per_iter += 1;
     t.fact = f;
+    t.fact_nsa = std::max(1, slots);  // factored: slots / grid carry the column splits of stage A / B
+    t.fact_nsb = std::max(1, grid);
   } else {
     if (apply_configure_exact(t, variant, slots, grid)) return RDR_EINVAL;
     if (t.fact && h->fused) h->launches_per_iter -= 1;
     t.fact = 0;
   }
   h->info.apply_factored = t.fact;
+  h->info.apply_fact_split_a = t.fact ? t.fact_nsa : 0;
+  h->info.apply_fact_split_b = t.fact ? t.fact_nsb : 0;
   h->op = t;
   if (h->graph) cudaGraphExecDestroy(h->graph);
   if (h->wgraph) cudaGraphExecDestroy(h->wgraph);
@@ -1214,6 +1223,54 @@ int rdr_profile_solve(rdr_handle* h, const double* b, double rtol, int maxit, in
   ms[3] = acc[3] / n_full;
   *iters = h->h_sc->iters;
   return h->h_sc->converged ? RDR_OK : RDR_ENOCONV;
+}
+
+int rdr_debug_profile_clocks(rdr_handle* h, const double* b, int iters, double* out, void* stream) {
+  if (!h || !b || !out || iters < 1 || !h->fused) return RDR_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  double* d_acc = nullptr;
+  CK(cudaMalloc((void**)&d_acc, 4 * sizeof(double)));
+  CK(cudaMemsetAsync(d_acc, 0, 4 * sizeof(double), s));
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  constexpr unsigned kProbeNs = 10000;
+  float t[2] = {0.f, 0.f};
+  int st = RDR_OK;
+  for (int mode = 0; mode < 2 && st == RDR_OK; ++mode) {
+    // mode 0: the PCG iteration (rtol 0: `iters` + 2 iterations whatever the residual), a probe
+    // behind each fused apply; mode 1: the fused apply alone, back to back, a probe behind each
+    pcg_begin(h, b, 0.0, 1 << 30, s, &st);
+    if (st) break;
+    auto step = [&]() -> int {
+      CK(launch_pcg_fused_apply(h->op, h->d_sc, h->d_z, h->d_p, h->d_p2, h->d_q, s));
+      CK(launch_sm_clock_probe(d_acc + 2 * mode, kProbeNs, s));
+      if (mode == 0) {
+        CK(launch_pcg_update_jacobi(h->d_sc, h->pc, h->d_p, h->d_p2, h->d_q, h->d_x, h->d_r, h->d_z, s));
+        CK(launch_precond_part(1, h->pc, h->d_r, h->d_z, &h->d_sc->rz_acc, h->d_sc, s));
+      }
+      return RDR_OK;
+    };
+    for (int k = 0; k < 2 && st == RDR_OK; ++k) st = step();  // warm-up
+    if (st) break;
+    CK(cudaMemsetAsync(d_acc + 2 * mode, 0, 2 * sizeof(double), s));
+    CK(cudaEventRecord(e0, s));
+    for (int k = 0; k < iters && st == RDR_OK; ++k) st = step();
+    CK(cudaEventRecord(e1, s));
+    CK(cudaEventSynchronize(e1));
+    CK(cudaEventElapsedTime(&t[mode], e0, e1));
+  }
+  double acc[4] = {0, 0, 0, 0};
+  if (st == RDR_OK) CK(cudaMemcpy(acc, d_acc, sizeof(acc), cudaMemcpyDeviceToHost));
+  cudaFree(d_acc);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (st) return st;
+  out[0] = acc[1] > 0 ? acc[0] / acc[1] : 0.0;
+  out[1] = acc[3] > 0 ? acc[2] / acc[3] : 0.0;
+  out[2] = t[0] / iters - kProbeNs * 1e-6;
+  out[3] = t[1] / iters - kProbeNs * 1e-6;
+  return RDR_OK;
 }
 
 int rdr_time_kernels(rdr_handle* h, const double* x, double* y, const double* r, double* z, int reps, double* ms,

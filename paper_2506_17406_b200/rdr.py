@@ -48,7 +48,8 @@ class Info(ctypes.Structure):
                 ("patch_kernel_seconds", ctypes.c_double), ("patch_setup_flops", ctypes.c_double),
                 ("apply_variant", ctypes.c_int32), ("apply_grid", ctypes.c_int32),
                 ("persistent_loop", ctypes.c_int32), ("apply_slots", ctypes.c_int32),
-                ("small_patch_grid", ctypes.c_int32), ("apply_factored", ctypes.c_int32)]
+                ("small_patch_grid", ctypes.c_int32), ("apply_factored", ctypes.c_int32),
+                ("apply_fact_split_a", ctypes.c_int32), ("apply_fact_split_b", ctypes.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -77,6 +78,7 @@ def _load():
         "rdr_time_kernels": (ctypes.c_int, [P, P, P, P, P, ctypes.c_int, P, P]),
         "rdr_measure_fp64_peak": (ctypes.c_int, [ctypes.POINTER(D), P]),
         "rdr_debug_fused_apply": (ctypes.c_int, [P, P, P, P]),
+        "rdr_debug_profile_clocks": (ctypes.c_int, [P, P, ctypes.c_int, P, P]),
         "rdr_debug_set_apply_variant": (ctypes.c_int, [P, ctypes.c_int]),
         "rdr_debug_set_small_patch_kernel": (ctypes.c_int, [P, ctypes.c_int]),
         "rdr_debug_set_apply_config": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_int, ctypes.c_int]),
@@ -250,6 +252,14 @@ class Solver:
             _check(code, "rdr_profile_solve")
         self.converged = code == RDR_OK
         return it.value, ms
+
+    def profile_clocks(self, b, iters=20, stream=None):
+        """[SM MHz behind the fused apply in the PCG iteration, the same for the apply alone,
+        ms per iteration, ms per apply alone] (rdr_debug_profile_clocks)."""
+        out = np.zeros(4)
+        _check(_lib.rdr_debug_profile_clocks(self._h, _ptr(b), int(iters), _ptr(out), _stream(stream)),
+               "rdr_debug_profile_clocks")
+        return out
 
     def set_apply_variant(self, variant: int) -> bool:
         """Debugging: force the apply's warp layout; False if it does not fit this operator."""

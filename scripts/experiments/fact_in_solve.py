@@ -24,7 +24,10 @@ for spec in sys.argv[1:]:
     tuned = (i["apply_variant"], i["apply_slots"], i["apply_grid"])
     out = {"cfg": cfg, "p": c.p, "chosen_factored": i["apply_factored"]}
     b = torch.from_numpy(c.draw_vector(S.n_total)).cuda()
-    for name, cfgv in (("dmma", tuned), ("fact1", (-1, 0, 0)), ("fact2", (-2, 0, 0)), ("fact3", (-3, 0, 0))):
+    out["chosen_split"] = (i["apply_fact_split_a"], i["apply_fact_split_b"])
+    for name, cfgv in (("dmma", tuned), ("fact1", (-1, 0, 0)), ("fact2", (-2, 0, 0)), ("fact3", (-3, 0, 0)),
+                       ("fact3_s21", (-3, 2, 1)), ("fact3_s22", (-3, 2, 2)), ("fact3_s32", (-3, 3, 2)),
+                       ("fact3_s42", (-3, 4, 2)), ("fact2_s22", (-2, 2, 2))):
         if not S.set_apply_config(*cfgv):
             continue
         S.solve(b)

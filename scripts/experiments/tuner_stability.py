@@ -26,6 +26,7 @@ for spec in sys.argv[1:]:
     e1.record()
     torch.cuda.synchronize()
     print(json.dumps({"cfg": cfg, "p": c.p, "apply_factored": i["apply_factored"],
+                      "split": (i["apply_fact_split_a"], i["apply_fact_split_b"]),
                       "ms_per_iter": round(e0.elapsed_time(e1) / its, 4), "apply_variant": i["apply_variant"], "apply_slots": i["apply_slots"],
                       "apply_grid": i["apply_grid"], "setup_s": i["setup_seconds"]}), flush=True)
     S.close()

@@ -441,6 +441,13 @@ def test_factored_apply(torch_cuda, space, p, n, perturb):
         assert S.info["apply_factored"] == -v
         assert rel(S.apply(xt).cpu().numpy(), ya) <= TOL, v
         assert rel(S.debug_fused_apply(xt, torch.zeros_like(xt)).cpu().numpy(), O.apply(O.mask(x))) <= TOL, v
+        # each cell tile's column blocks split over (stage A, stage B) CTAs
+        for nsa, nsb in ((2, 1), (3, 2), (8, 5)):
+            assert S.set_apply_config(v, nsa, nsb)
+            assert (S.info["apply_fact_split_a"], S.info["apply_fact_split_b"]) == (nsa, nsb)
+            assert rel(S.apply(xt).cpu().numpy(), ya) <= TOL, (v, nsa, nsb)
+            assert rel(S.debug_fused_apply(xt, torch.zeros_like(xt)).cpu().numpy(), O.apply(O.mask(x))) <= TOL
+        assert not S.set_apply_config(v, 9, 1)
     # PCG with unit coefficients: with the 1e4 log-uniform contrast at p = 1 the iteration count
     # moves by 2 between two roundings of the same operator (DMMA 53, factored 52, oracle 54:
     # profiles/round2/experiments/fact_apply_rounding.txt), beyond the +-1 bar
@@ -450,8 +457,8 @@ def test_factored_apply(torch_cuda, space, p, n, perturb):
     b = c.draw_vector(O.n_total)
     hist = []
     xo, ito, _ = O.solve(b, rtol=1e-8, history=hist)
-    for v in (-1, -2, -3):
-        if not S.set_apply_config(v, 0, 0):
+    for v, nsa, nsb in ((-1, 0, 0), (-2, 0, 0), (-3, 0, 0), (-1, 2, 2), (-3, 3, 2)):
+        if not S.set_apply_config(v, nsa, nsb):
             assert v in (-2, -3) and p >= 9
             continue
         xg, it = S.solve(torch.from_numpy(b).cuda(), rtol=1e-8)

@@ -373,6 +373,27 @@ def test_loop_modes_and_profile(torch_cuda, space):
         assert rel(xl, x0) <= 1e-8
 
 
+def test_profile_clocks(torch_cuda):
+    """rdr_debug_profile_clocks: the probe behind the fused apply reads a plausible SM
+    clock inside the iteration and alone, times are positive, and the solver still
+    solves afterwards (the call overwrites the solve vectors); hybrid: RDR_EINVAL."""
+    from paper_2506_17406_b200 import rdr
+    torch = torch_cuda
+    c = make_config(0, n=3, p=3, space=HGRAD, perturb=True, bc="x0", coeffs="loguniform")
+    S = rdr.Solver(c.vertices, c.tets, c.p, c.space, c.alpha, c.beta, c.mask, loop=rdr.LOOP_GRAPH)
+    b = torch.from_numpy(c.draw_vector(S.n_total)).cuda()
+    x0, it0 = S.solve(b)
+    mhz_in, mhz_alone, ms_iter, ms_apply = S.profile_clocks(b, iters=20)
+    assert 300 <= mhz_in <= 3000 and 300 <= mhz_alone <= 3000
+    assert ms_iter > 0 and ms_apply > 0 and ms_apply < ms_iter
+    x1, it1 = S.solve(b)
+    assert it1 == it0 and rel(x1.cpu().numpy(), x0.cpu().numpy()) <= 1e-8
+    H = rdr.Solver(c.vertices, c.tets, c.p, c.space, c.alpha, c.beta, c.mask, preconditioner=rdr.HYBRID)
+    with pytest.raises(rdr.RdrError) as e:
+        H.profile_clocks(b)
+    assert e.value.code == -1
+
+
 def test_persistent_loop_not_eligible(torch_cuda):
     """RDR_LOOP_PERSISTENT needs star patches of at most 256 dofs: H(grad) p = 6
     (431-dof vertex stars) is RDR_EINVAL; the default loop then uses the graph."""

@@ -1,6 +1,8 @@
 """The fused PCG iteration with the direction update folded into the apply's gather
 (3 kernels) against a separate direction kernel in front of the plain apply (4 kernels,
 rdr_info.separate_direction): graph-solve ms per iteration, per config, with setup's choice.
+Needs profiles/round2/experiments/separate_direction_kernel.diff applied (measured and not
+kept: the two forms are within 1 %, separate_direction_ab.jsonl).
 
     python scripts/experiments/direction_ab.py 3 4 6 7:9 7:10 8:9 8:10 5:10 5:12 2
 """

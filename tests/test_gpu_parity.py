@@ -728,6 +728,37 @@ def test_hybrid_preconditioner(torch_cuda, space, p, bc, n):
         assert ng <= ne + max(itg, 1), (ng, ne, itg)
 
 
+def _hybrid_golden():
+    return [(e["cfg"], e["p"]) for e in json.load(open(GOLDEN)).get("hybrid_entries", [])]
+
+
+@pytest.mark.parametrize("cfg,p", _hybrid_golden())
+def test_hybrid_full_size_golden(torch_cuda, cfg, p):
+    """NEXT-1 at the sizes DESIGN.md section 10b reports (config 2; the H(grad), H(curl) and
+    H(div) p-sweeps on the 8^3 x 6 mesh): the library's weights rho_m equal the oracle's, PCG
+    iterations within +-1 of oracle/hybrid.py's count (tests/golden, written by
+    scripts/oracle_golden.py --hybrid, oracle/ only), and the GPU's own exit satisfies R-A16."""
+    from paper_2506_17406_b200 import rdr
+    torch = torch_cuda
+    g = [e for e in json.load(open(GOLDEN))["hybrid_entries"] if (e["cfg"], e["p"]) == (cfg, p)][0]
+    c = make_config(cfg, p=p) if cfg in (5, 7, 8) else make_config(cfg)
+    S = rdr.Solver(c.vertices, c.tets, c.p, c.space, c.alpha, c.beta, c.mask, preconditioner=rdr.HYBRID)
+    assert S.n_total == g["n_total"] and S.info["n_free"] == g["n_free"]
+    assert np.allclose(S.weights, g["rho"], rtol=1e-9, atol=0), (S.weights, g["rho"])
+    b = c.draw_vector(S.n_total)   # the config's rhs (first draw), as scripts/oracle_golden.py
+    x, it = S.solve(torch.from_numpy(b).cuda(), rtol=1e-8)
+    st = S.last_stats()
+    assert st["converged"] == 1 and st["z_last"] <= 1e-8 * st["z0"]
+    assert abs(it - g["iters"]) <= 1, (it, g["iters"])
+    # true residual of the GPU's x through the library's own operator: the same order as the oracle's
+    bm = torch.from_numpy(b).cuda()
+    r = S.apply(x) - bm
+    free = x != 0  # x is exactly zero on the constrained dofs (and nowhere else, generically)
+    assert int(free.sum()) == g["n_free"]
+    rel_res = float(r[free].norm() / bm[free].norm())
+    assert rel_res <= max(10 * g["true_rel_res"], 1e-6), (rel_res, g["true_rel_res"])
+
+
 def test_tet_vertex_order_invariance(torch_cuda):
     """rdr_setup accepts tets in any vertex order (it sorts, R-A3): shuffling
     every tet's vertices (and the mask columns with them) changes nothing."""

@@ -12,7 +12,9 @@ A step = one full PCG solve (every hot-path row of SURVEY §8(a): operator
 apply, interior Jacobi, star-patch solves, PCG vector ops) on a fresh rhs
 already resident in HBM. value = PCG iterations/s over the whole job.
 The line also carries "sweep": config 2 and the config-5 p-sweep (p = 1..12),
-each measured the same way (the metric's "vs p"); --no-sweep skips it.
+each measured the same way (the metric's "vs p"), and "hybrid": the bench workload solved
+with the paper's hybrid Schwarz preconditioner (iterations, time to solution); --no-sweep
+skips both.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--config 3] [--p 6]
 
@@ -296,6 +298,36 @@ def measure_point(rdr, torch, cfg, p, dev, solves, fp64_peak, hbm, seed=0):
     return out
 
 
+def measure_hybrid(rdr, torch, cfg, p, dev, solves, seed=0):
+    """The bench workload with the paper's own preconditioner (NEXT-1: symmetric hybrid
+    Schwarz with the Whitney coarse space) beside the headline's one-level
+    additive one: iterations and time to solution of `solves` solves after a warm-up one."""
+    c = make_cfg(cfg, p, seed)
+    S = rdr.Solver(c.vertices, c.tets, c.p, c.space, c.alpha, c.beta, c.mask, preconditioner=rdr.HYBRID)
+    n = S.n_total
+    rhs = [torch.from_numpy(c.draw_vector(n)).to(dev) for _ in range(solves + 1)]
+    x = torch.empty(n, dtype=torch.float64, device=dev)
+    S.solve(rhs[0], x, rtol=1e-8)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    iters, nonconv = [], 0
+    e0.record()
+    for k in range(solves):
+        _, it = S.solve(rhs[1 + k], x, rtol=1e-8)
+        iters.append(it)
+        nonconv += not S.converged
+    e1.record()
+    e1.synchronize()
+    ms = e0.elapsed_time(e1)
+    out = {"workload": workload_name(cfg, c.p), "preconditioner": "hybrid Schwarz: Jacobi, star patches, exact "
+           "Whitney coarse solve, patches, Jacobi (rho_m from 10 CG-Lanczos steps)",
+           "rho": [float(v) for v in S.weights], "iters": float(np.mean(iters)), "nonconverged": nonconv,
+           "time_to_solution_ms": ms / solves, "ms_per_iter": ms / max(1, sum(iters)),
+           "pcg_iters_per_s": sum(iters) / (ms / 1e3), "setup_s": S.info["setup_seconds"]}
+    S.close()
+    return out
+
+
 def run(args):
     import torch
     ws, rank, local = dist_env()
@@ -436,6 +468,10 @@ def run(args):
     if not args.no_sweep and ws == 1:
         pts = [(2, None)] + [(5, p) for p in range(1, 13)]
         line["sweep"] = [measure_point(rdr, torch, cf, p, dev, 3, fp64_peak, hbm) for cf, p in pts]
+        try:  # the same workload with the paper's hybrid preconditioner (extra key, not the headline)
+            line["hybrid"] = measure_hybrid(rdr, torch, cfg, c.p if cfg in (5, 7, 8) else None, dev, 3)
+        except Exception as e:  # noqa: BLE001  (never lose the headline line to the extra key)
+            line["hybrid"] = {"error": f"{type(e).__name__}: {e}"}
     if not args.no_cpu:
         ips, per_step, desc, det = oracle_sample(cfg, c.p, args.cpu_steps, 1, args.ref_iters)
         line["cpu_baseline"] = {"value": ips, "unit": "PCG iters/s", "kind": "oracle", "sample": desc,

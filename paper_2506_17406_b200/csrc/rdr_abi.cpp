@@ -1225,23 +1225,18 @@ int rdr_profile_solve(rdr_handle* h, const double* b, double rtol, int maxit, in
   return h->h_sc->converged ? RDR_OK : RDR_ENOCONV;
 }
 
-int rdr_debug_profile_clocks(rdr_handle* h, const double* b, int iters, double* out, void* stream) {
-  if (!h || !b || !out || iters < 1 || !h->fused) return RDR_EINVAL;
-  cudaStream_t s = (cudaStream_t)stream;
-  double* d_acc = nullptr;
-  CK(cudaMalloc((void**)&d_acc, 4 * sizeof(double)));
-  CK(cudaMemsetAsync(d_acc, 0, 4 * sizeof(double), s));
-  cudaEvent_t e0, e1;
-  CK(cudaEventCreate(&e0));
-  CK(cudaEventCreate(&e1));
+// body of rdr_debug_profile_clocks (the caller owns d_acc and the events)
+static int profile_clocks(rdr_handle* h, const double* b, int iters, double* out, cudaStream_t s, double* d_acc,
+                          cudaEvent_t e0, cudaEvent_t e1) {
   constexpr unsigned kProbeNs = 10000;
+  CK(cudaMemsetAsync(d_acc, 0, 4 * sizeof(double), s));
   float t[2] = {0.f, 0.f};
-  int st = RDR_OK;
-  for (int mode = 0; mode < 2 && st == RDR_OK; ++mode) {
+  for (int mode = 0; mode < 2; ++mode) {
     // mode 0: the PCG iteration (rtol 0: `iters` + 2 iterations whatever the residual), a probe
     // behind each fused apply; mode 1: the fused apply alone, back to back, a probe behind each
+    int st;
     pcg_begin(h, b, 0.0, 1 << 30, s, &st);
-    if (st) break;
+    if (st) return st;
     auto step = [&]() -> int {
       CK(launch_pcg_fused_apply(h->op, h->d_sc, h->d_z, h->d_p, h->d_p2, h->d_q, s));
       CK(launch_sm_clock_probe(d_acc + 2 * mode, kProbeNs, s));
@@ -1251,26 +1246,37 @@ int rdr_debug_profile_clocks(rdr_handle* h, const double* b, int iters, double* 
       }
       return RDR_OK;
     };
-    for (int k = 0; k < 2 && st == RDR_OK; ++k) st = step();  // warm-up
-    if (st) break;
+    for (int k = 0; k < 2; ++k)  // warm-up
+      if ((st = step())) return st;
     CK(cudaMemsetAsync(d_acc + 2 * mode, 0, 2 * sizeof(double), s));
     CK(cudaEventRecord(e0, s));
-    for (int k = 0; k < iters && st == RDR_OK; ++k) st = step();
+    for (int k = 0; k < iters; ++k)
+      if ((st = step())) return st;
     CK(cudaEventRecord(e1, s));
     CK(cudaEventSynchronize(e1));
     CK(cudaEventElapsedTime(&t[mode], e0, e1));
   }
   double acc[4] = {0, 0, 0, 0};
-  if (st == RDR_OK) CK(cudaMemcpy(acc, d_acc, sizeof(acc), cudaMemcpyDeviceToHost));
-  cudaFree(d_acc);
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
-  if (st) return st;
+  CK(cudaMemcpy(acc, d_acc, sizeof(acc), cudaMemcpyDeviceToHost));
   out[0] = acc[1] > 0 ? acc[0] / acc[1] : 0.0;
   out[1] = acc[3] > 0 ? acc[2] / acc[3] : 0.0;
   out[2] = t[0] / iters - kProbeNs * 1e-6;
   out[3] = t[1] / iters - kProbeNs * 1e-6;
   return RDR_OK;
+}
+
+int rdr_debug_profile_clocks(rdr_handle* h, const double* b, int iters, double* out, void* stream) {
+  if (!h || !b || !out || iters < 1 || !h->fused) return RDR_EINVAL;
+  double* d_acc = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  int st = RDR_ECUDA;
+  if (cudaMalloc((void**)&d_acc, 4 * sizeof(double)) == cudaSuccess && cudaEventCreate(&e0) == cudaSuccess &&
+      cudaEventCreate(&e1) == cudaSuccess)
+    st = profile_clocks(h, b, iters, out, (cudaStream_t)stream, d_acc, e0, e1);
+  if (e0) cudaEventDestroy(e0);
+  if (e1) cudaEventDestroy(e1);
+  cudaFree(d_acc);
+  return st;
 }
 
 int rdr_time_kernels(rdr_handle* h, const double* x, double* y, const double* r, double* z, int reps, double* ms,

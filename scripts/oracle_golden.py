@@ -65,7 +65,9 @@ def run_hybrid(cfg, p):
 def main():
     data = json.load(open(OUT)) if os.path.exists(OUT) else {"note": "", "entries": []}
     data["note"] = ("Oracle PCG iteration counts (oracle/solver.py, R-A16, rtol 1e-8) on BASELINE.json configs "
-                    "with the seeded rhs; written by scripts/oracle_golden.py (oracle/ only).")
+                    "with the seeded rhs; written by scripts/oracle_golden.py (oracle/ only). "
+                    "hybrid_entries: the same with oracle/hybrid.py (hybrid Schwarz with the Whitney coarse "
+                    "space, P:2399-2455), with its weights rho_m.")
     lean = "--lean" in sys.argv
     hybrid = "--hybrid" in sys.argv
     key = "hybrid_entries" if hybrid else "entries"

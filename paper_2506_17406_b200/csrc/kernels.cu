@@ -1625,13 +1625,23 @@ __global__ void pcg_update_kernel(PcgScalars* sc, const double* __restrict__ p, 
   }
 }
 
-__global__ void pcg_finish_kernel(PcgScalars* sc, const double* __restrict__ z, int64_t n) {
+// r != nullptr (hybrid preconditioner, which does not accumulate r.z itself): r.z into
+// sc->rz_new in the same pass, each block before it takes its ticket
+__global__ void pcg_finish_kernel(PcgScalars* sc, const double* __restrict__ z, const double* __restrict__ r,
+                                  int64_t n) {
   if (stopped(sc)) return;
-  double part = 0;
+  double part = 0, rz = 0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
     double zi = z[i];
     part = fma(zi, zi, part);
+    if (r) rz = fma(r[i], zi, rz);
+  }
+  if (r) {
+    __shared__ double shr[32];
+    const double s = block_sum(rz, shr);
+    if (threadIdx.x == 0) atomicAdd(&sc->rz_new, s);
+    __syncthreads();
   }
   if (last_block(sc, part) && threadIdx.x == 0) {
     __threadfence();
@@ -2060,8 +2070,8 @@ cudaError_t launch_pcg_update(PcgScalars* sc, const double* p, const double* q, 
   pcg_update_kernel<<<vec_grid(n), kVecThreads, 0, s>>>(sc, p, q, x, r, n);
   return cudaGetLastError();
 }
-cudaError_t launch_pcg_finish(PcgScalars* sc, const double* z, int64_t n, cudaStream_t s) {
-  pcg_finish_kernel<<<vec_grid(n), kVecThreads, 0, s>>>(sc, z, n);
+cudaError_t launch_pcg_finish(PcgScalars* sc, const double* z, const double* r, int64_t n, cudaStream_t s) {
+  pcg_finish_kernel<<<vec_grid(n), kVecThreads, 0, s>>>(sc, z, r, n);
   return cudaGetLastError();
 }
 cudaError_t launch_pcg_direction(PcgScalars* sc, const double* z, double* p, double* q, int64_t n, cudaStream_t s) {

@@ -126,7 +126,8 @@ cudaError_t launch_pcg_start(PcgScalars* sc, const double* z, double* p, int64_t
                              cudaStream_t s);
 cudaError_t launch_pcg_update(PcgScalars* sc, const double* p, const double* q, double* x, double* r, int64_t n,
                               cudaStream_t s);
-cudaError_t launch_pcg_finish(PcgScalars* sc, const double* z, int64_t n, cudaStream_t s);
+// r != nullptr: also r.z into sc->rz_new (the hybrid preconditioner does not accumulate it)
+cudaError_t launch_pcg_finish(PcgScalars* sc, const double* z, const double* r, int64_t n, cudaStream_t s);
 cudaError_t launch_pcg_direction(PcgScalars* sc, const double* z, double* p, double* q, int64_t n, cudaStream_t s);
 
 // Fused PCG step (3 kernels per iteration for H(grad)): fused apply (direction

@@ -600,7 +600,7 @@ static int setup_impl(rdr_handle* h, const double* vertices, int64_t nv, const i
       cudaGetLastError();
   }
   h->launches_per_iter = h->fused ? 1 + count_precond_launches(pc)
-                                  : 4 + (hybrid ? count_hybrid_launches(pc) + 1 : count_precond_launches(pc));
+                                  : 4 + (hybrid ? count_hybrid_launches(pc) : count_precond_launches(pc));
   // one warm-up apply/precond on zero vectors: kernel attributes get configured
   // here, outside any later stream capture
   CK(cudaMemset(h->d_p, 0, vb));
@@ -830,13 +830,12 @@ static int enqueue_iteration(rdr_handle* h, cudaStream_t s) {
   }
   CK(launch_apply(h->op, h->d_p, h->d_q, &h->d_sc->pq, h->d_sc, s));
   CK(launch_pcg_update(h->d_sc, h->d_p, h->d_q, h->d_x, h->d_r, n, s));
-  if (h->pc.hybrid) {
+  if (h->pc.hybrid) {  // r.z of the new z in the finish kernel's pass over z
     CK(launch_precond_hybrid(h->op, h->pc, h->d_r, h->d_z, h->d_sc, s));
-    CK(launch_pcg_rz(h->d_sc, h->d_r, h->d_z, n, s));
   } else {
     CK(launch_precond(h->pc, h->d_r, h->d_z, &h->d_sc->rz_new, h->d_sc, s));
   }
-  CK(launch_pcg_finish(h->d_sc, h->d_z, n, s));
+  CK(launch_pcg_finish(h->d_sc, h->d_z, h->pc.hybrid ? h->d_r : nullptr, n, s));
   CK(launch_pcg_direction(h->d_sc, h->d_z, h->d_p, h->d_q, n, s));
   return RDR_OK;
 }
